@@ -1,0 +1,164 @@
+// fs_device.cuh -- device-side program view, random streams and small helpers shared by the
+// sm_100a engines.  See DESIGN.md for the data layout and stream definitions.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/fs_sampler.h"
+
+namespace fs {
+
+constexpr double kInvSqrt2 = 0.70710678118654757;  // 1/math.sqrt(2.0), runtime.py:46
+constexpr double kBranchFloor = 1e-12;               // runtime.py:47
+constexpr int kSmall = 8;                            // runtime.py:48 (selects the reduction formula)
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// Device copy of the serialized program (include/fs_sampler.h).  All tables live in one
+// device allocation; the struct is passed by value as a kernel parameter.
+struct DevProg {
+  int n, k_max, num_instrs, R, U, D, O, E, num_slots, has_psel;
+  const int* __restrict__ instrs;  // [N][8]
+  const int* __restrict__ schedule;
+  const double* __restrict__ fparams;
+  const uint32_t* __restrict__ gates;
+  const uint32_t* __restrict__ paulis;
+  const int* __restrict__ reclists;
+  const double* __restrict__ site_prob;
+  const int* __restrict__ site_case_off;
+  const double* __restrict__ case_cum;
+  const int* __restrict__ case_pauli_off;
+  const double* __restrict__ cum_hazard;
+  const int* __restrict__ plans;
+  const int* __restrict__ record_out;
+  const int* __restrict__ bit_slot;
+};
+
+struct RunArgs {
+  uint64_t seed, shot0, nshots;
+  uint32_t flags;
+  uint32_t W;          // output words = ceil(nshots/32)
+  uint32_t* meas;      // [U][W]
+  uint32_t* det;       // [D][W]
+  uint32_t* obs;       // [O][W]
+  uint32_t* accepted;  // [W]
+  uint32_t* error;     // [W]
+  int* status;         // max FS_ERR_SHOT_* seen
+  int prezeroed;       // outputs memset to 0 => a warp whose shots all halted may stop early
+  // trace mode
+  const int16_t* fault_modes;  // [nshots][E]
+  const int8_t* forced;        // [nshots][R]
+  int stop;                    // instructions to execute
+  uint8_t* t_fx;
+  uint8_t* t_fz;
+  double* t_gamma;
+  double* t_amps;
+  uint32_t* t_draws;
+  // general engine: per-resident-warp array storage when it does not fit in shared memory
+  double2* scratch;
+  int arr_log2;  // log2 capacity (k_max)
+};
+
+// ------------------------------------------------------------------ random streams
+enum : uint32_t { TAG_COIN = 1, TAG_BORN = 2, TAG_NOISE = 3, TAG_FORCED = 4 };
+
+__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint64_t seed) {
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    c1 = lo1;
+    c3 = lo0;
+    c0 = n0;
+    c2 = n2;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+__device__ __forceinline__ double u64_to_unit(uint64_t x) {
+  return __dmul_rn(__ull2double_rn(x), 5.421010862427522e-20);
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+// reference ShotRng (rng.py:24-71): key = mix(mix(seed) ^ shot); draw c = mix(key + c*golden)
+struct SplitMix {
+  uint64_t key;
+  uint32_t count;
+  __device__ __forceinline__ void reset(uint64_t seed, uint64_t shot) {
+    key = mix64(mix64(seed) ^ shot);
+    count = 0;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    uint64_t c = count++;
+    return mix64(key + c * 0x9E3779B97F4A7C15ULL);
+  }
+  __device__ __forceinline__ double uniform() { return u64_to_unit(next()); }
+  __device__ __forceinline__ int bit() { return (int)(next() >> 63); }
+};
+
+// per-(shot|word, instruction, tag) Philox stream: draw j uses block j/2, half j%2
+struct PhiloxStream {
+  uint64_t seed, ctr;
+  uint32_t instr, tag, j;
+  uint4 blk;
+  __device__ __forceinline__ void init(uint64_t s, uint64_t c, uint32_t i, uint32_t t) {
+    seed = s; ctr = c; instr = i; tag = t; j = 0;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    if ((j & 1) == 0) blk = philox((uint32_t)ctr, (uint32_t)(ctr >> 32), instr, (tag << 24) | (j >> 1), seed);
+    uint64_t r = (j & 1) ? (((uint64_t)blk.w << 32) | blk.z) : (((uint64_t)blk.y << 32) | blk.x);
+    j++;
+    return r;
+  }
+  __device__ __forceinline__ double uniform() { return u64_to_unit(next()); }
+};
+
+// ------------------------------------------------------------------ complex helpers
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
+// python complex * float (runtime.py: `buf[i] * scale`): real-scaled, no FMA contraction
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(__dmul_rn(a.x, s), __dmul_rn(a.y, s)); }
+__device__ __forceinline__ double cnorm2(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
+
+// insert a 0 bit at position a (Retire / MeasCollapse gather, backend.py:436-441)
+__device__ __forceinline__ uint32_t ins0(uint32_t i, int a) {
+  uint32_t lowmask = (1u << a) - 1u;
+  return ((i & ~lowmask) << 1) | (i & lowmask);
+}
+
+// ------------------------------------------------------------------ noise helpers
+__device__ __forceinline__ int bisect_right(const double* __restrict__ S, double x, int lo, int hi) {
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (x < __ldg(S + mid)) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// _pick_case (runtime.py:702-707) with a supplied uniform
+__device__ __forceinline__ int pick_case(const DevProg& P, int site, double u) {
+  int c0 = __ldg(P.site_case_off + site), nc = __ldg(P.site_case_off + site + 1) - c0;
+  double x = u * __ldg(P.site_prob + site);
+  int c = bisect_right(P.case_cum + c0, x, 0, nc);
+  return c0 + (c < nc - 1 ? c : nc - 1);
+}
+
+__device__ __forceinline__ int num_cases(const DevProg& P, int site) {
+  return __ldg(P.site_case_off + site + 1) - __ldg(P.site_case_off + site);
+}
+
+}  // namespace fs

@@ -1,0 +1,564 @@
+// fs_general.cuh -- the general engine: one warp executes one 32-shot word, lane = shot.
+//
+// Every opcode of the reference VM (runtime.py:130-641) is implemented.  State per warp:
+//   * Pauli frame bit-sliced across the warp's 32 shots: smem word fx[q], fz[q] (bit = lane);
+//     word-level updates are issued by lane 0 and published with __syncwarp;
+//   * record / detector bits that a later instruction reads: smem slot words (program.py slot
+//     allocation), every other record goes straight to the output words;
+//   * per-lane dense active array of 2^k complex128, interleaved [i][lane] so a warp-wide
+//     access is one coalesced 512 B row, in shared memory when 32*2^k_max*16 B fits, else in a
+//     per-resident-warp HBM scratch slab;
+//   * per-lane gamma, random stream and trace inputs.
+#pragma once
+#include "fs_device.cuh"
+
+namespace fs {
+
+constexpr int kGenWarps = 4;  // warps per block of the general engine
+
+__device__ __forceinline__ void word_gate(uint32_t* fx, uint32_t* fz, uint32_t g) {
+  int a = FS_GATE_A(g), b = FS_GATE_B(g);
+  uint32_t t;
+  switch (FS_GATE_G(g)) {
+    case FS_G_H: t = fx[a]; fx[a] = fz[a]; fz[a] = t; break;
+    case FS_G_S:
+    case FS_G_SDAG: fz[a] ^= fx[a]; break;
+    case FS_G_CX: fx[b] ^= fx[a]; fz[a] ^= fz[b]; break;
+    case FS_G_CZ: fz[b] ^= fx[a]; fz[a] ^= fx[b]; break;
+    case FS_G_SWAP:
+      t = fx[a]; fx[a] = fx[b]; fx[b] = t;
+      t = fz[a]; fz[a] = fz[b]; fz[b] = t;
+      break;
+    default: break;
+  }
+}
+
+// XOR the Pauli list [off, off+cnt) into frame words with `bits` (lane-0 writer or atomics)
+template <bool ATOMIC>
+__device__ __forceinline__ void xor_paulis(const DevProg& P, uint32_t* fx, uint32_t* fz, int off, int cnt,
+                                           uint32_t bits) {
+  for (int j = 0; j < cnt; j++) {
+    uint32_t e = __ldg(P.paulis + off + j);
+    uint32_t* f = FS_PAULI_Z(e) ? fz : fx;
+    if (ATOMIC) atomicXor(f + FS_PAULI_Q(e), bits);
+    else f[FS_PAULI_Q(e)] ^= bits;
+  }
+}
+
+__device__ __forceinline__ void xor_case(const DevProg& P, uint32_t* fx, uint32_t* fz, int c, uint32_t bits,
+                                         bool atomic) {
+  int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
+  if (atomic) xor_paulis<true>(P, fx, fz, off, end - off, bits);
+  else xor_paulis<false>(P, fx, fz, off, end - off, bits);
+}
+
+// Word-level flattened hazard process (Philox stream): one Exp(1) jump per
+// realised fault over the concatenation of the 32 lanes' hazard intervals.  Called by one lane;
+// returns nothing, XORs every fault (lane l, site, case) into bit l of the frame words.
+// `stride` = 1 for a warp-owned word, 32 for the frame engine's lane-interleaved layout.
+__device__ void philox_noise_word(const DevProg& P, uint32_t* fx, uint32_t* fz, int stride, uint64_t seed,
+                                  uint64_t word, int instr, const int* ins) {
+  const double* S = P.cum_hazard;
+  PhiloxStream ps;
+  ps.init(seed, word, (uint32_t)instr, TAG_NOISE);
+  const int plan_off = ins[3], plan_cnt = ins[4];
+  for (int pi = 0; pi < plan_cnt; pi++) {
+    int a = __ldg(P.plans + 2 * (plan_off + pi)), b = __ldg(P.plans + 2 * (plan_off + pi) + 1);
+    if (a < 0) {  // certain site (p = 1): every lane fires; cases drawn lane by lane
+      int site = b;
+      int nc = num_cases(P, site);
+      for (int l = 0; l < 32; l++) {
+        int c = __ldg(P.site_case_off + site);
+        if (nc > 1) c = pick_case(P, site, ps.uniform());
+        int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
+        for (int j = off; j < end; j++) {
+          uint32_t e = __ldg(P.paulis + j);
+          uint32_t* f = FS_PAULI_Z(e) ? fz : fx;
+          f[FS_PAULI_Q(e) * stride] ^= 1u << l;
+        }
+      }
+      continue;
+    }
+    const double Sa = __ldg(S + a);
+    const double H = __dsub_rn(__ldg(S + b), Sa);
+    if (!(H > 0.0)) continue;
+    const double total = __dmul_rn(32.0, H);
+    double t = 0.0;
+    for (;;) {
+      t = __dadd_rn(t, -log1p(-ps.uniform()));
+      if (!(t < total)) break;
+      int l = (int)__ddiv_rn(t, H);
+      if (l > 31) break;
+      double local = __dadd_rn(Sa, __dsub_rn(t, __dmul_rn((double)l, H)));
+      int idx = bisect_right(S, local, a + 1, b + 1);
+      if (idx > b) { t = __dmul_rn((double)(l + 1), H); continue; }
+      int site = idx - 1;
+      int c = __ldg(P.site_case_off + site);
+      if (num_cases(P, site) > 1) c = pick_case(P, site, ps.uniform());
+      int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
+      for (int j = off; j < end; j++) {
+        uint32_t e = __ldg(P.paulis + j);
+        uint32_t* f = FS_PAULI_Z(e) ? fz : fx;
+        f[FS_PAULI_Q(e) * stride] ^= 1u << l;
+      }
+      t = __dadd_rn(__dmul_rn((double)l, H), __dsub_rn(__ldg(S + site + 1), Sa));
+    }
+  }
+}
+
+// Reference hazard skipping for one shot (runtime.py:564-586 / :675-699), draw for draw.
+template <class Draw>
+__device__ void hazard_shot(const DevProg& P, uint32_t* fx, uint32_t* fz, uint32_t bit, const int* ins, Draw& rng) {
+  const double* S = P.cum_hazard;
+  const int plan_off = ins[3], plan_cnt = ins[4];
+  for (int pi = 0; pi < plan_cnt; pi++) {
+    int a = __ldg(P.plans + 2 * (plan_off + pi)), b = __ldg(P.plans + 2 * (plan_off + pi) + 1);
+    if (a < 0) {
+      int site = b, c = __ldg(P.site_case_off + site);
+      if (num_cases(P, site) > 1) c = pick_case(P, site, rng.uniform());
+      xor_case(P, fx, fz, c, bit, true);
+      continue;
+    }
+    int i = a;
+    while (i < b) {
+      double target = __dadd_rn(__ldg(S + i), -log1p(-rng.uniform()));
+      int idx = bisect_right(S, target, i + 1, b + 1);
+      if (idx > b) break;
+      int site = idx - 1, c = __ldg(P.site_case_off + site);
+      if (num_cases(P, site) > 1) c = pick_case(P, site, rng.uniform());
+      xor_case(P, fx, fz, c, bit, true);
+      i = site + 1;
+    }
+  }
+}
+
+// Forced fault modes for one shot (runtime.py:587-601).
+template <class Draw>
+__device__ void forced_faults_shot(const DevProg& P, uint32_t* fx, uint32_t* fz, uint32_t bit, const int* ins,
+                                   const int16_t* modes, Draw& rng, int stride) {
+  for (int site = ins[1]; site < ins[2]; site++) {
+    int mode = modes[site];
+    if (mode == 2) continue;
+    int nc = num_cases(P, site);
+    int c = __ldg(P.site_case_off + site);
+    if (mode == 0) {
+      if (nc == 0) continue;
+      if (rng.uniform() >= __ldg(P.site_prob + site)) continue;
+      if (nc > 1) c = pick_case(P, site, rng.uniform());
+    } else if (mode == 1) {
+      if (nc > 1) c = pick_case(P, site, rng.uniform());
+    } else {
+      c += mode - 3;
+    }
+    int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
+    for (int j = off; j < end; j++) {
+      uint32_t e = __ldg(P.paulis + j);
+      uint32_t* f = FS_PAULI_Z(e) ? fz : fx;
+      if (stride == 1) atomicXor(f + FS_PAULI_Q(e), bit);
+      else f[FS_PAULI_Q(e) * stride] ^= bit;
+    }
+  }
+}
+
+// per-shot draw source for the general engine: SplitMix (reference) or Philox (per shot/instr)
+struct ShotDraws {
+  bool splitmix;
+  SplitMix sm;
+  PhiloxStream ph;
+  uint64_t seed, shot;
+  __device__ __forceinline__ void begin(int instr, uint32_t tag) {
+    if (!splitmix) ph.init(seed, shot, (uint32_t)instr, tag);
+  }
+  __device__ __forceinline__ double uniform() { return splitmix ? sm.uniform() : ph.uniform(); }
+};
+
+template <bool SPLITMIX, bool ARR_SMEM>
+__global__ void __launch_bounds__(kGenWarps * 32)
+general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const uint32_t lanebit = 1u << lane;
+  uint32_t* wsm = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wib * smem_words_per_warp;
+  uint32_t* fx = wsm;
+  uint32_t* fz = fx + P.n;
+  uint32_t* slots = fz + P.n;
+  uint32_t* obsw = slots + P.num_slots;
+  const size_t cap = (size_t)1 << A.arr_log2;
+  double2* arr;
+  if (ARR_SMEM) {
+    unsigned char* abase = smem_raw + (size_t)kGenWarps * smem_words_per_warp * 4;
+    abase = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(abase) + 15) & ~uintptr_t(15));
+    arr = reinterpret_cast<double2*>(abase) + (size_t)wib * cap * 32;
+  } else {
+    const size_t gwarp = (size_t)blockIdx.x * kGenWarps + wib;
+    arr = A.scratch + gwarp * cap * 32;
+  }
+#define AMP(i) arr[(size_t)(i) * 32 + lane]
+  const bool renorm = !(A.flags & FS_NO_RENORM);
+  const uint64_t word0 = A.shot0 >> 5;
+  const int stop = A.stop;
+
+  for (uint32_t w = blockIdx.x * kGenWarps + wib; w < A.W; w += gridDim.x * kGenWarps) {
+    const uint64_t si = (uint64_t)w * 32 + lane;  // shot index within the call
+    const bool valid = si < A.nshots;
+    const uint64_t shot = A.shot0 + si;
+    const uint64_t wabs = word0 + w;
+    const uint32_t validmask = __ballot_sync(kFull, valid);
+    uint32_t alive = validmask;
+    uint32_t errmask = 0;
+    int errcode = 0;
+    for (int q = lane; q < 2 * P.n + P.num_slots + P.O; q += 32) wsm[q] = 0;
+    AMP(0) = make_double2(1.0, 0.0);
+    double2 gamma = make_double2(1.0, 0.0);
+    ShotDraws rng;
+    rng.splitmix = SPLITMIX;
+    rng.seed = A.seed;
+    rng.shot = shot;
+    if (SPLITMIX) rng.sm.reset(A.seed, shot);
+    const int16_t* fmodes = A.fault_modes ? A.fault_modes + (valid ? si : 0) * (size_t)P.E : nullptr;
+    const int8_t* forced = A.forced ? A.forced + (valid ? si : 0) * (size_t)P.R : nullptr;
+    int branch = 0;
+    __syncwarp();
+
+    // write one record word to its output column and/or slot
+    auto put_record = [&](int r, uint32_t word) {
+      if (lane == 0) {
+        int col = __ldg(P.record_out + r);
+        if (col >= 0) A.meas[(size_t)col * A.W + w] = word & alive;
+        int sl = __ldg(P.bit_slot + r);
+        if (sl >= 0) slots[sl] = word;
+      }
+    };
+    auto fail = [&](bool bad, int code) {
+      uint32_t b = __ballot_sync(kFull, bad);
+      if (b) {
+        errmask |= b;
+        alive &= ~b;
+        errcode = code;
+      }
+    };
+
+    for (int i = 0; i < stop; i++) {
+      if (alive == 0 && A.prezeroed) break;
+      const int4 I0 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i);
+      const int4 I1 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i + 1);
+      const int ins[8] = {I0.x, I0.y, I0.z, I0.w, I1.x, I1.y, I1.z, I1.w};
+      const int op = FS_OPCODE(I0.x);
+      const uint32_t flipw = FS_FLIP(I0.x) ? kFull : 0u;
+      const bool me = (alive >> lane) & 1;
+      switch (op) {
+        case FS_OP_FRAME: {
+          if (lane == 0)
+            for (int j = 0; j < ins[2]; j++) word_gate(fx, fz, __ldg(P.gates + ins[1] + j));
+          __syncwarp();
+          break;
+        }
+        case FS_OP_ARRAY_GATE: {
+          const int g = ins[1], va = ins[2], vb = ins[3], a = ins[4], b = ins[5];
+          const uint32_t size = 1u << ins[6];
+          if (lane == 0) {
+            uint32_t t;
+            switch (g) {
+              case FS_G_S: case FS_G_SDAG: fz[va] ^= fx[va]; break;
+              case FS_G_H: t = fx[va]; fx[va] = fz[va]; fz[va] = t; break;
+              case FS_G_CX: fx[vb] ^= fx[va]; fz[va] ^= fz[vb]; break;
+              case FS_G_CZ: fz[vb] ^= fx[va]; fz[va] ^= fx[vb]; break;
+            }
+          }
+          if (me) {
+            if (g == FS_G_S || g == FS_G_SDAG) {
+              const double2 ph = make_double2(0.0, g == FS_G_S ? 1.0 : -1.0);
+              for (uint32_t j = 0; j < size / 2; j++) {
+                uint32_t idx = ins0(j, a) | (1u << a);
+                AMP(idx) = cmul(AMP(idx), ph);
+              }
+            } else if (g == FS_G_H) {
+              const uint32_t st = 1u << a;
+              for (uint32_t j = 0; j < size / 2; j++) {
+                uint32_t i0 = ins0(j, a);
+                double2 lo = AMP(i0), hi = AMP(i0 + st);
+                AMP(i0) = cscale(cadd(lo, hi), kInvSqrt2);
+                AMP(i0 + st) = cscale(csub(lo, hi), kInvSqrt2);
+              }
+            } else if (g == FS_G_CX) {
+              const int lo_ax = a < b ? a : b, hi_ax = a < b ? b : a;
+              for (uint32_t j = 0; j < size / 4; j++) {
+                uint32_t idx = ins0(ins0(j, lo_ax), hi_ax) | (1u << a);
+                uint32_t jdx = idx | (1u << b);
+                double2 t0 = AMP(idx);
+                AMP(idx) = AMP(jdx);
+                AMP(jdx) = t0;
+              }
+            } else if (g == FS_G_CZ) {
+              const int lo_ax = a < b ? a : b, hi_ax = a < b ? b : a;
+              for (uint32_t j = 0; j < size / 4; j++) {
+                uint32_t idx = ins0(ins0(j, lo_ax), hi_ax) | (1u << a) | (1u << b);
+                double2 v = AMP(idx);
+                AMP(idx) = make_double2(-v.x, -v.y);
+              }
+            }
+          }
+          __syncwarp();
+          break;
+        }
+        case FS_OP_EXPAND: {
+          const int par = (fx[ins[1]] >> lane) & 1;
+          const double* f = P.fparams + ins[5] + 4 * par;
+          const double2 ph0 = make_double2(__ldg(f), __ldg(f + 1)), ph1 = make_double2(__ldg(f + 2), __ldg(f + 3));
+          const uint32_t size = 1u << ins[6];
+          if (me)
+            for (uint32_t j = 0; j < size; j++) {
+              double2 v = AMP(j);
+              AMP(j) = cmul(v, ph0);
+              AMP(size + j) = cmul(v, ph1);
+            }
+          break;
+        }
+        case FS_OP_GAMMA_ROT: {
+          const int par = (fx[ins[1]] >> lane) & 1;
+          const double* f = P.fparams + ins[5] + 2 * par;
+          gamma = cmul(gamma, make_double2(__ldg(f), __ldg(f + 1)));
+          break;
+        }
+        case FS_OP_ARRAY_ROT: {
+          const int par = (fx[ins[1]] >> lane) & 1;
+          const int a = ins[2];
+          const double* f = P.fparams + ins[5];
+          const double2 e0 = make_double2(__ldg(f), __ldg(f + 1)), e1 = make_double2(__ldg(f + 2), __ldg(f + 3));
+          const double2 ph0 = par ? e1 : e0, ph1 = par ? e0 : e1;
+          const uint32_t size = 1u << ins[6];
+          if (me)
+            for (uint32_t j = 0; j < size; j++) AMP(j) = cmul(AMP(j), ((j >> a) & 1) ? ph1 : ph0);
+          break;
+        }
+        case FS_OP_MEAS_DSTATIC: {
+          const int virt = ins[1], rec = ins[3];
+          const uint32_t bitw = fx[virt] ^ flipw;
+          if (forced) {
+            int fo = forced[rec];
+            fail(me && fo >= 0 && fo != (int)((bitw >> lane) & 1), FS_ERR_SHOT_FORCED);
+          }
+          put_record(rec, bitw);
+          __syncwarp();
+          break;
+        }
+        case FS_OP_MEAS_DRANDOM: {
+          const int virt = ins[1], rec = ins[3];
+          const uint32_t pw = fz[virt];
+          const int pbit = (pw >> lane) & 1;
+          const int fo = forced ? forced[rec] : -1;
+          int coin;
+          if (SPLITMIX) {
+            coin = (fo >= 0) ? (fo ^ pbit ^ (int)(flipw & 1)) : (me ? rng.sm.bit() : 0);
+          } else {
+            uint32_t cw = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), (uint32_t)i, TAG_COIN << 24, A.seed).x;
+            coin = (fo >= 0) ? (fo ^ pbit ^ (int)(flipw & 1)) : (int)((cw >> lane) & 1);
+          }
+          const uint32_t coinw = __ballot_sync(kFull, coin);
+          __syncwarp();
+          if (lane == 0) {
+            uint32_t t = fx[virt];
+            fx[virt] = fz[virt] ^ coinw;
+            fz[virt] = t;
+          }
+          gamma = cscale(gamma, kInvSqrt2);
+          put_record(rec, coinw ^ pw ^ flipw);
+          __syncwarp();
+          break;
+        }
+        case FS_OP_MEAS_ACTIVE:
+        case FS_OP_MEAS_COLLAPSE: {
+          const int virt = ins[1], a = ins[2], rec = ins[3];
+          const uint32_t size = 1u << ins[6], half = size >> 1, st = 1u << a;
+          const bool collapse = op == FS_OP_MEAS_COLLAPSE;
+          double2 u00 = make_double2(1, 0), u01 = make_double2(0, 0), u10 = make_double2(0, 0), u11 = make_double2(1, 0);
+          if (collapse) {
+            const double* f = P.fparams + ins[5];
+            u00 = make_double2(__ldg(f), __ldg(f + 1));
+            u01 = make_double2(__ldg(f + 2), __ldg(f + 3));
+            u10 = make_double2(__ldg(f + 4), __ldg(f + 5));
+            u11 = make_double2(__ldg(f + 6), __ldg(f + 7));
+            if (lane == 0) {
+              const int po = ins[4] >> 8, pc = ins[4] & 0xFF;
+              for (int j = 0; j < pc; j++) word_gate(fx, fz, __ldg(P.gates + po + j));
+            }
+            __syncwarp();
+          }
+          const int parity = (fx[virt] >> lane) & 1;
+          int recbit = 0, brbit = 0;
+          bool bad = false;
+          int badcode = 0;
+          if (me) {
+            double p1 = 0.0, p_all = 0.0;
+            if (collapse) {
+              if (size == 2) {
+                double2 a0 = AMP(0), a1 = AMP(1);
+                double2 b0 = cadd(cmul(u00, a0), cmul(u01, a1));
+                double2 b1 = cadd(cmul(u10, a0), cmul(u11, a1));
+                p1 = cnorm2(b1);
+                p_all = __dadd_rn(p1, cnorm2(b0));
+              } else if (size <= 2 * kSmall) {
+                for (uint32_t j = 0; j < half; j++) {
+                  uint32_t i0 = ins0(j, a);
+                  double2 a0 = AMP(i0), a1 = AMP(i0 + st);
+                  double q1 = cnorm2(cadd(cmul(u10, a0), cmul(u11, a1)));
+                  double2 b0 = cadd(cmul(u00, a0), cmul(u01, a1));
+                  p1 = __dadd_rn(p1, q1);
+                  p_all = __dadd_rn(p_all, __dadd_rn(q1, cnorm2(b0)));
+                }
+              } else {
+                for (uint32_t j = 0; j < half; j++) {
+                  uint32_t i0 = ins0(j, a);
+                  p1 = __dadd_rn(p1, cnorm2(cadd(cmul(AMP(i0), u10), cmul(u11, AMP(i0 + st)))));
+                }
+                for (uint32_t j = 0; j < size; j++) p_all = __dadd_rn(p_all, cnorm2(AMP(j)));
+              }
+              if (p1 != p1) { bad = true; badcode = FS_ERR_SHOT_NAN; }
+              p1 = p_all > 0 ? __ddiv_rn(p1, p_all) : 0.0;
+            } else {
+              if (size == 2) p1 = cnorm2(AMP(1));
+              else
+                for (uint32_t j = 0; j < half; j++) p1 = __dadd_rn(p1, cnorm2(AMP(ins0(j, a) | st)));
+              if (p1 != p1) { bad = true; badcode = FS_ERR_SHOT_NAN; }
+              if (!renorm) {
+                double norm2 = 0.0;
+                for (uint32_t j = 0; j < size; j++) norm2 = __dadd_rn(norm2, cnorm2(AMP(j)));
+                p1 = norm2 > 0 ? __ddiv_rn(p1, norm2) : 0.0;
+              }
+            }
+            if (!bad) {
+              if (p1 < 0.0) p1 = 0.0;
+              else if (p1 > 1.0) p1 = 1.0;
+              const int fo = forced ? forced[rec] : -1;
+              double pb;
+              if (fo < 0) {
+                rng.begin(i, TAG_BORN);
+                brbit = rng.uniform() < p1 ? 1 : 0;
+                pb = brbit ? p1 : __dsub_rn(1.0, p1);
+                if (pb < kBranchFloor) { brbit ^= 1; pb = __dsub_rn(1.0, pb); }
+              } else {
+                brbit = fo ^ parity ^ FS_FLIP(I0.x);
+                pb = brbit ? p1 : __dsub_rn(1.0, p1);
+                if (pb < kBranchFloor) { bad = true; badcode = FS_ERR_SHOT_FORCED; }
+              }
+              if (!bad) {
+                recbit = brbit ^ parity ^ FS_FLIP(I0.x);
+                if (collapse) {
+                  const double scale = renorm ? __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(pb, p_all))) : 1.0;
+                  const double2 k0 = brbit == 0 ? cscale(u00, scale) : cscale(u10, scale);
+                  const double2 k1 = brbit == 0 ? cscale(u01, scale) : cscale(u11, scale);
+                  for (uint32_t j = 0; j < half; j++) {
+                    uint32_t i0 = ins0(j, a);
+                    AMP(j) = cadd(cmul(k0, AMP(i0)), cmul(k1, AMP(i0 + st)));
+                  }
+                } else {
+                  const double scale = renorm ? __ddiv_rn(1.0, __dsqrt_rn(pb)) : 1.0;
+                  const uint32_t dead = 1u - brbit;
+                  for (uint32_t j = 0; j < size; j++) {
+                    if (((j >> a) & 1) == dead) AMP(j) = make_double2(0.0, 0.0);
+                    else if (renorm) AMP(j) = cscale(AMP(j), scale);
+                  }
+                }
+                if (renorm) gamma = cscale(gamma, __dsqrt_rn(pb));
+              }
+            }
+          }
+          fail(bad, badcode);
+          branch = brbit;
+          const uint32_t recw = __ballot_sync(kFull, recbit);
+          if (collapse) {
+            const uint32_t brw = __ballot_sync(kFull, brbit);
+            if (lane == 0) fx[virt] ^= brw;
+          }
+          put_record(rec, recw);
+          __syncwarp();
+          break;
+        }
+        case FS_OP_RETIRE: {
+          const int virt = ins[1], a = ins[2];
+          const uint32_t half = (1u << ins[6]) >> 1;
+          if (me)
+            for (uint32_t j = 0; j < half; j++) AMP(j) = AMP(ins0(j, a) + ((uint32_t)branch << a));
+          const uint32_t brw = __ballot_sync(kFull, me && branch);
+          if (lane == 0) fx[virt] ^= brw;
+          __syncwarp();
+          break;
+        }
+        case FS_OP_COND_FRAME: {
+          const uint32_t rw = slots[__ldg(P.bit_slot + ins[3])];
+          if (lane == 0 && rw) xor_paulis<false>(P, fx, fz, ins[1], ins[2], rw);
+          __syncwarp();
+          break;
+        }
+        case FS_OP_NOISE: {
+          if (fmodes) {
+            if (me) {
+              ShotDraws& d = rng;
+              d.begin(i, TAG_FORCED);
+              forced_faults_shot(P, fx, fz, lanebit, ins, fmodes, d, 1);
+            }
+          } else if (SPLITMIX) {
+            if (me) hazard_shot(P, fx, fz, lanebit, ins, rng.sm);
+          } else {
+            if (lane == 0) philox_noise_word(P, fx, fz, 1, A.seed, wabs, i, ins);
+          }
+          __syncwarp();
+          break;
+        }
+        case FS_OP_DETECTOR:
+        case FS_OP_OBSERVABLE: {
+          if (lane == 0) {
+            uint32_t wv = 0;
+            for (int j = 0; j < ins[3]; j++) wv ^= slots[__ldg(P.bit_slot + __ldg(P.reclists + ins[2] + j))];
+            if (op == FS_OP_DETECTOR) {
+              A.det[(size_t)ins[1] * A.W + w] = wv & alive;
+              int sl = __ldg(P.bit_slot + P.R + ins[1]);
+              if (sl >= 0) slots[sl] = wv;
+            } else {
+              obsw[ins[1]] ^= wv & alive;
+            }
+          }
+          __syncwarp();
+          break;
+        }
+        case FS_OP_POSTSELECT: {
+          const int bid = ins[1] == 0 ? P.R + ins[2] : ins[2];
+          const uint32_t bw = slots[__ldg(P.bit_slot + bid)];
+          alive &= ~((bw ^ (ins[3] ? kFull : 0u)) & alive);
+          break;
+        }
+        default: break;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (int o = 0; o < P.O; o++) A.obs[(size_t)o * A.W + w] = obsw[o] & validmask;
+      A.accepted[w] = alive & validmask;
+      A.error[w] = errmask;
+      if (errmask) atomicMax(A.status, errcode);
+    }
+    if (valid) {
+      if (A.t_fx)
+        for (int q = 0; q < P.n; q++) {
+          A.t_fx[si * P.n + q] = (fx[q] >> lane) & 1;
+          A.t_fz[si * P.n + q] = (fz[q] >> lane) & 1;
+        }
+      if (A.t_gamma) { A.t_gamma[2 * si] = gamma.x; A.t_gamma[2 * si + 1] = gamma.y; }
+      if (A.t_draws) A.t_draws[si] = SPLITMIX ? rng.sm.count : 0u;
+      if (A.t_amps) {
+        const int kst = stop > 0 ? __ldg(P.schedule + stop - 1) : 0;
+        const uint32_t sz = 1u << kst;
+        for (uint32_t j = 0; j < sz; j++) {
+          double2 v = AMP(j);
+          A.t_amps[(si * sz + j) * 2] = v.x;
+          A.t_amps[(si * sz + j) * 2 + 1] = v.y;
+        }
+      }
+    }
+    __syncwarp();
+  }
+#undef AMP
+}
+
+}  // namespace fs

@@ -1,0 +1,240 @@
+"""Generate golden fixtures from the REFERENCE implementation (run in the build container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Imports the reference ``framesim`` package from /root/reference (read-only),
+compiles circuits with the reference compiler, serializes the programs with
+``paper_2604_27058_b200.program.serialize`` and records what the REFERENCE VM
+(``framesim.runtime``) produces:
+
+* free sampling with the reference SplitMix64 stream (``sample(prog, S, seed)``):
+  measurement / detector / observable bits and ``accepted`` per shot;
+* trace mode (SURVEY §8(d) recipe): a per-shot fault plan (2 = off, 3+c = case c,
+  drawn with numpy at rate site_prob x boost), the outcomes of every random
+  measurement record of a free ``run_shot`` under that plan, then a second
+  ``run_shot`` under another seed/shot with both supplied -- its records,
+  detectors, observables, accepted flag, frames, gamma and active array (at the
+  end and at checkpoints via ``trace``) are stored;
+* config programs (BASELINE.json configs 0-4) for bench.py.
+
+Nothing here is imported by the tests: they read the .npz files.
+"""
+from __future__ import annotations
+
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from framesim.backend import compile_circuit  # noqa: E402  (reference)
+from framesim.circuit import parse_circuit  # noqa: E402
+from framesim.runtime import ShotState, run_shot, sample  # noqa: E402
+from framesim import testing as ftest  # noqa: E402
+
+from paper_2604_27058_b200.configs import CONFIGS, config_text  # noqa: E402
+from paper_2604_27058_b200.program import serialize  # noqa: E402
+
+OUT = ROOT / "tests" / "golden"
+PROGS = ROOT / "paper_2604_27058_b200" / "programs"
+RANDOM_KINDS = ("MeasDormantRandom", "MeasActive", "MeasCollapse")
+
+# irreducible peak dimension 10 (same construction as the reference's performance smoke,
+# test_acceptance.py criterion 10): rotation layer, global parity readout, X readouts
+_K10 = "\n".join([f"R_Y(0.7) {q}" for q in range(10)] + [f"CX {q} {q + 1}" for q in range(9)]
+                 + ["M 9"] + [f"CX {q} {q + 1}" for q in range(8, -1, -1)]
+                 + ["MX " + " ".join(str(q) for q in range(10))]) + "\n"
+
+
+def free_golden(prog, shots, seed):
+    recs = list(sample(prog, shots, seed=seed))
+    U, D, O = len(prog.user_records), prog.num_detectors, prog.num_observables
+    meas = np.array([r.measurements for r in recs], dtype=np.uint8).reshape(shots, U)
+    det = np.array([r.detectors for r in recs], dtype=np.uint8).reshape(shots, D)
+    obs = np.array([r.observables for r in recs], dtype=np.uint8).reshape(shots, O)
+    acc = np.array([r.accepted for r in recs], dtype=np.uint8)
+    return meas, det, obs, acc
+
+
+def trace_golden(prog, shots, seed, boost, rng, checkpoints=()):
+    E = len(prog.sites)
+    R = prog.record_count
+    rand_records = {ins.record for ins in prog.instrs if type(ins).__name__ in RANDOM_KINDS}
+    modes = np.full((shots, E), 2, dtype=np.int16)
+    forced = np.full((shots, R), -1, dtype=np.int8)
+    rows = {k: [] for k in ("meas", "det", "obs", "acc", "fx", "fz", "gamma", "k", "amps", "draws")}
+    cps = {c: {"fx": [], "fz": [], "gamma": [], "amps": []} for c in checkpoints}
+    for s in range(shots):
+        for site, tab in enumerate(prog.sites):
+            if tab.case_cum and rng.random() < min(1.0, tab.prob * boost):
+                modes[s, site] = 3 + int(rng.integers(0, len(tab.case_cum)))
+        st = ShotState(prog, seed=seed + 17)
+        run_shot(prog, st, shot=1000 + s, forced_faults=modes[s])
+        for r in rand_records:
+            forced[s, r] = int(st.records[r])
+        snap = {}
+
+        def tr(state, ins, _idx=[0]):
+            i = _idx[0]
+            _idx[0] += 1
+            if i in cps:
+                snap[i] = (state.frame_x.copy(), state.frame_z.copy(), complex(state.gamma),
+                           state.active_view().copy())
+
+        st2 = ShotState(prog, seed=seed)
+        fo = {int(r): int(forced[s, r]) for r in rand_records}
+        rec = run_shot(prog, st2, shot=s, forced_faults=modes[s], forced_outcomes=fo,
+                       trace=tr if checkpoints else None)
+        rows["meas"].append(rec.measurements.astype(np.uint8))
+        rows["det"].append(rec.detectors.astype(np.uint8))
+        rows["obs"].append(rec.observables.astype(np.uint8))
+        rows["acc"].append(int(rec.accepted))
+        rows["fx"].append(st2.frame_x.copy())
+        rows["fz"].append(st2.frame_z.copy())
+        rows["gamma"].append(complex(st2.gamma))
+        rows["k"].append(st2.k)
+        rows["amps"].append(st2.active_view().copy())
+        rows["draws"].append(st2.rng.draws)
+        for c in checkpoints:
+            if c in snap:
+                fx, fz, g, a = snap[c]
+            else:  # shot halted before the checkpoint
+                fx = fz = np.zeros(prog.n, np.uint8)
+                g, a = complex("nan"), np.full(1 << prog.active_schedule[c], np.nan + 0j)
+            cps[c]["fx"].append(fx)
+            cps[c]["fz"].append(fz)
+            cps[c]["gamma"].append(g)
+            cps[c]["amps"].append(a)
+    U, D, O = len(prog.user_records), prog.num_detectors, prog.num_observables
+    out = {
+        "t_modes": modes, "t_forced": forced,
+        "t_meas": np.array(rows["meas"], np.uint8).reshape(shots, U),
+        "t_det": np.array(rows["det"], np.uint8).reshape(shots, D),
+        "t_obs": np.array(rows["obs"], np.uint8).reshape(shots, O),
+        "t_acc": np.array(rows["acc"], np.uint8),
+        "t_fx": np.array(rows["fx"], np.uint8), "t_fz": np.array(rows["fz"], np.uint8),
+        "t_gamma": np.array(rows["gamma"], np.complex128), "t_k": np.array(rows["k"], np.int32),
+        "t_draws": np.array(rows["draws"], np.int64),
+    }
+    ks = set(rows["k"])
+    if len(ks) == 1:  # every shot ends at the same k unless some halted
+        out["t_amps"] = np.array(rows["amps"], np.complex128)
+    out["t_seed"] = np.array([seed])
+    if checkpoints:
+        out["cp_index"] = np.array(checkpoints, np.int32)
+        for c in checkpoints:
+            out[f"cp{c}_fx"] = np.array(cps[c]["fx"], np.uint8)
+            out[f"cp{c}_fz"] = np.array(cps[c]["fz"], np.uint8)
+            out[f"cp{c}_gamma"] = np.array(cps[c]["gamma"], np.complex128)
+            out[f"cp{c}_amps"] = np.array(cps[c]["amps"], np.complex128)
+    return out
+
+
+def write_case(name, prog, text, *, free_shots=256, free_seed=3, trace_shots=16, boost=20.0,
+               checkpoints=(), rng=None, meta=None):
+    t0 = time.time()
+    rng = rng or np.random.default_rng(abs(hash(name)) % (2 ** 32))
+    P = serialize(prog, name=name, meta=meta or {})
+    payload = {"program": np.frombuffer(P.to_npz_bytes(), dtype=np.uint8),
+               "circuit": np.array(text)}
+    if free_shots:
+        m, d, o, a = free_golden(prog, free_shots, free_seed)
+        payload.update(f_meas=m, f_det=d, f_obs=o, f_acc=a, f_seed=np.array([free_seed]))
+    if trace_shots:
+        payload.update(trace_golden(prog, trace_shots, seed=11, boost=boost, rng=rng,
+                                    checkpoints=checkpoints))
+    np.savez_compressed(OUT / f"{name}.npz", **payload)
+    print(f"{name:28s} k_max={prog.k_max:2d} instrs={len(prog.instrs):4d} "
+          f"({time.time() - t0:.1f}s)", flush=True)
+
+
+def main(which=("configs", "random", "toys")):
+    OUT.mkdir(exist_ok=True)
+    PROGS.mkdir(exist_ok=True)
+    if "toys" in which:
+        toys = {
+            "toy_htm": ("H 0\nT 0\nH 0\nM 0\n", {}),
+            "toy_noise_twice": ("H 0\nT 0\nH 0\nM 0\nDEPOLARIZE1(0.3) 0\nM 0\n", {}),
+            "toy_mirror": ("H 0\nT 0\nT 0\nT 0\nCX 0 1\nCX 0 1\nS_DAG 0\nT_DAG 0\nH 0\nM 0 1\n", {}),
+            "toy_worked": ("H 0\nT 0\nT 0\nT 0\nCX 0 1\nDEPOLARIZE1(0.001) 0 1\nCX 0 1\nT_DAG 0\nH 0\nM 0 1\n", {}),
+            "toy_postselect": ("H 0\nM 0\nPOSTSELECT rec[-1]\nH 1\nT 1\nH 1\nM 1\nDEPOLARIZE1(0.5) 1\nM 1\n", {}),
+            "toy_postselect1": ("H 0\nM 0\nPOSTSELECT(1) rec[-1]\nM 0\n", {}),
+            "toy_certain": ("X_ERROR(1.0) 0\nX_ERROR(0.5) 1\nX_ERROR(0.0) 2\nDEPOLARIZE1(1.0) 3\nM 0 1 2 3\n",
+                            {"optimize": False}),
+            "toy_unopt_active": ("H 0\nT 0\nH 1\nT 1\nCX 0 1\nH 0\nM 0\nH 1\nM 1\nR_X(0.3) 2\nMX 2\n",
+                                 {"optimize": False}),
+            "toy_feedforward": ("H 0\nT 0\nH 0\nM 0\nCX rec[-1] 1\nX_ERROR(0.3) 1\nM 1\nDETECTOR rec[-1] rec[-2]\n"
+                                "OBSERVABLE_INCLUDE(0) rec[-1]\nOBSERVABLE_INCLUDE(0) rec[-2]\n", {}),
+            "toy_repetition": (str(ftest.repetition_code_circuit(3, 5, 0.05)), {}),
+            "toy_pad200": ("R_Y(0.7) 0\nR_Y(0.7) 1\nCX 0 1\nM 1\nCX 0 1\nMX 0 1\nZ 199\n", {}),
+            "toy_k10": (_K10, {}),
+            "toy_k10_pad200": (_K10 + "Z 199\n", {}),
+        }
+        for name, (text, kw) in toys.items():
+            prog = compile_circuit(text, optimize=kw.get("optimize", True))
+            write_case(name, prog, text, free_shots=512, trace_shots=12,
+                       checkpoints=tuple(range(min(len(prog.instrs), 6))))
+    if "random" in which:
+        rng = np.random.default_rng(20261019)
+        for i in range(24):
+            n = int(rng.integers(2, 9))
+            kw = dict(p_noise=float(rng.choice([0.0, 0.05, 0.3])),
+                      measure_rate=float(rng.uniform(0.1, 0.3)),
+                      rot_rate=float(rng.uniform(0.1, 0.35)),
+                      reset_rate=float(rng.choice([0.0, 0.05])),
+                      feedforward_rate=float(rng.choice([0.0, 0.08])),
+                      measure_all=bool(rng.random() < 0.6),
+                      max_noncliff=int(rng.integers(3, 11)))
+            circ = ftest.random_circuit(rng, n, int(rng.integers(8, 40)), **kw)
+            text = str(circ)
+            opt = bool(rng.random() < 0.8)
+            prog = compile_circuit(text, optimize=opt)
+            cps = tuple(sorted(set(int(x) for x in rng.integers(0, len(prog.instrs), size=3))))
+            write_case(f"rand{i:02d}", prog, text, free_shots=256, trace_shots=10,
+                       checkpoints=cps, rng=rng, meta={"optimize": opt, **kw})
+        from paper_2604_27058_b200.configs import random_near_clifford
+        for i in range(8):  # rotation-heavy: larger active dimension (config-0-like, own sizes)
+            n = int(rng.integers(6, 12))
+            text = random_near_clifford(n, int(rng.integers(4, 9)), t_cells=int(rng.integers(5, 11)),
+                                        seed=int(rng.integers(0, 2 ** 31)))
+            lines = text.strip().split("\n")
+            if i % 2:  # keep the final active array alive: measure only half the qubits
+                lines[-1] = "M " + " ".join(str(q) for q in range(0, n, 2))
+            if i % 4 >= 2:  # sprinkle noise
+                lines = [x for ln in lines for x in (ln, f"DEPOLARIZE1(0.02) {rng.integers(0, n)}")]
+            text = "\n".join(lines) + "\n"
+            prog = compile_circuit(text)
+            cps = tuple(sorted(set(int(x) for x in rng.integers(0, len(prog.instrs), size=3))))
+            write_case(f"bigk{i:02d}", prog, text, free_shots=128, trace_shots=6, checkpoints=cps,
+                       rng=rng)
+        for i in range(6):
+            circ = ftest.random_mirror_circuit(rng, int(rng.integers(2, 7)), int(rng.integers(1, 8)))
+            text = str(circ)
+            write_case(f"mirror{i:02d}", compile_circuit(text), text, free_shots=512, trace_shots=4, rng=rng)
+    if "configs" in which:
+        for i in range(5):
+            text, ps = config_text(i)
+            t0 = time.time()
+            prog = compile_circuit(text, postselect_detectors=ps)
+            ct = time.time() - t0
+            meta = {"config": i, "compile_s": round(ct, 2), "shots": CONFIGS[i]["shots"],
+                    "desc": CONFIGS[i]["desc"]}
+            P = serialize(prog, name=CONFIGS[i]["name"], meta=meta)
+            P.save(PROGS / f"c{i}.npz")
+            # reference outputs: bounded by the reference's speed (config 3: ~25 s/shot)
+            if i == 3:
+                write_case(f"config{i}", prog, "", free_shots=0, trace_shots=1, boost=1.0, meta=meta)
+            elif i == 4:
+                write_case(f"config{i}", prog, "", free_shots=512, trace_shots=12, boost=20.0, meta=meta,
+                           checkpoints=(40, 120))
+            else:
+                write_case(f"config{i}", prog, "", free_shots=256, trace_shots=12, boost=20.0, meta=meta,
+                           checkpoints=(len(prog.instrs) // 3, len(prog.instrs) // 2))
+
+
+if __name__ == "__main__":
+    main(tuple(sys.argv[1:]) or ("toys", "random", "configs"))

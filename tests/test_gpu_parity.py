@@ -1,0 +1,141 @@
+"""GPU parity: the CUDA engines (through the C ABI) against the reference goldens and the oracle.
+
+* trace mode (all random choices supplied): records / detectors / observables /
+  accepted / frames bit-exact vs the REFERENCE; gamma and active amplitudes
+  within 1e-10 relative (complex128, north_star);
+* free sampling with the reference stream (FS_RNG_SPLITMIX): bit-exact vs the
+  reference's own ``sample()`` output;
+* free sampling with the Philox stream: bit-exact vs the oracle's restatement
+  of that stream; frame engine == general engine on frame-only programs.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from goldens import case_names, load, rel_err
+from paper_2604_27058_b200._abi import FS_FORCE_GENERAL, FS_RNG_PHILOX, FS_RNG_SPLITMIX
+
+pytestmark = pytest.mark.gpu
+ALL = case_names()
+# programs whose active array lives in HBM (k_max >= 16) go through the large-k engine tests
+CASES = [c for c in ALL if load(c)["prog"].k_max < 16]
+AMP_TOL = 1e-10
+
+
+def _dev(P):
+    from paper_2604_27058_b200.engine import DeviceProgram
+
+    return DeviceProgram(P)
+
+
+def _same(a, b):
+    np.testing.assert_array_equal(a.measurements(), b.measurements())
+    np.testing.assert_array_equal(a.detectors(), b.detectors())
+    np.testing.assert_array_equal(a.observables(), b.observables())
+    np.testing.assert_array_equal(a.accepted_bits(), b.accepted_bits())
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if "t_modes" in load(c)])
+@pytest.mark.parametrize("flags", [FS_RNG_SPLITMIX, FS_RNG_PHILOX])
+def test_gpu_trace_matches_reference(cuda, name, flags):
+    g = load(name)
+    P = g["prog"]
+    dp = _dev(P)
+    n = g["t_modes"].shape[0]
+    st, out, tb = dp.sample_host(n, seed=int(g["t_seed"][0]), flags=flags, fault_modes=g["t_modes"],
+                                 forced=g["t_forced"], want_state=True)
+    assert st == 0
+    np.testing.assert_array_equal(out.measurements(), g["t_meas"])
+    np.testing.assert_array_equal(out.detectors(), g["t_det"])
+    np.testing.assert_array_equal(out.observables(), g["t_obs"])
+    np.testing.assert_array_equal(out.accepted_bits(), g["t_acc"])
+    np.testing.assert_array_equal(tb.frame_x[:, :P.n], g["t_fx"])
+    np.testing.assert_array_equal(tb.frame_z[:, :P.n], g["t_fz"])
+    assert rel_err(tb.gamma_c(), g["t_gamma"]) < AMP_TOL
+    if "t_amps" in g and g["t_acc"].all():
+        assert rel_err(tb.amps_c(), g["t_amps"]) < AMP_TOL
+    if flags == FS_RNG_SPLITMIX:
+        np.testing.assert_array_equal(tb.draws, g["t_draws"])
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if "t_modes" in load(c) and load(c)["prog"].k_max == 0])
+def test_gpu_frame_engine_trace_matches_reference(cuda, name):
+    """Frame-only programs through the bit-sliced frame engine (no state outputs requested)."""
+    g = load(name)
+    P = g["prog"]
+    dp = _dev(P)
+    assert dp.engine(FS_RNG_PHILOX) == "frame"
+    n = g["t_modes"].shape[0]
+    st, out, tb = dp.sample_host(n, seed=int(g["t_seed"][0]), flags=FS_RNG_PHILOX,
+                                 fault_modes=g["t_modes"], forced=g["t_forced"])
+    assert st == 0
+    np.testing.assert_array_equal(out.measurements(), g["t_meas"])
+    np.testing.assert_array_equal(out.detectors(), g["t_det"])
+    np.testing.assert_array_equal(out.observables(), g["t_obs"])
+    np.testing.assert_array_equal(out.accepted_bits(), g["t_acc"])
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if "cp_index" in load(c)])
+def test_gpu_checkpoints_match_reference(cuda, name):
+    g = load(name)
+    P = g["prog"]
+    dp = _dev(P)
+    n = g["t_modes"].shape[0]
+    for c in g["cp_index"].tolist():
+        st, out, tb = dp.sample_host(n, seed=int(g["t_seed"][0]), flags=FS_RNG_SPLITMIX,
+                                     fault_modes=g["t_modes"], forced=g["t_forced"], stop=c + 1,
+                                     want_state=True)
+        ok = ~np.isnan(g[f"cp{c}_gamma"])
+        np.testing.assert_array_equal(tb.frame_x[ok, :P.n], g[f"cp{c}_fx"][ok])
+        np.testing.assert_array_equal(tb.frame_z[ok, :P.n], g[f"cp{c}_fz"][ok])
+        assert rel_err(tb.gamma_c()[ok], g[f"cp{c}_gamma"][ok]) < AMP_TOL
+        assert rel_err(tb.amps_c()[ok], g[f"cp{c}_amps"][ok]) < AMP_TOL
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if "f_meas" in load(c)])
+def test_gpu_free_reference_stream_matches_reference(cuda, name):
+    g = load(name)
+    P = g["prog"]
+    dp = _dev(P)
+    n = g["f_meas"].shape[0]
+    st, out, _ = dp.sample_host(n, seed=int(g["f_seed"][0]), flags=FS_RNG_SPLITMIX)
+    assert st == 0
+    np.testing.assert_array_equal(out.measurements(), g["f_meas"])
+    np.testing.assert_array_equal(out.detectors(), g["f_det"])
+    np.testing.assert_array_equal(out.observables(), g["f_obs"])
+    np.testing.assert_array_equal(out.accepted_bits(), g["f_acc"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_gpu_free_philox_matches_oracle(cuda, name):
+    P = load(name)["prog"]
+    n = 2048 if P.k_max < 12 else 256
+    dp = _dev(P)
+    _, gout, _ = dp.sample_host(n, seed=77, shot0=64, flags=FS_RNG_PHILOX)
+    _, oout, _ = oracle.sample(P, n, seed=77, shot0=64, flags=FS_RNG_PHILOX)
+    _same(gout, oout)
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if load(c)["prog"].k_max == 0])
+def test_gpu_frame_engine_equals_general_engine(cuda, name):
+    P = load(name)["prog"]
+    dp = _dev(P)
+    n = 5000
+    _, a, _ = dp.sample_host(n, seed=5, flags=FS_RNG_PHILOX)
+    _, b, _ = dp.sample_host(n, seed=5, flags=FS_RNG_PHILOX | FS_FORCE_GENERAL)
+    _same(a, b)
+
+
+def test_gpu_accumulate_matches_samples(cuda):
+    P = load("config2")["prog"] if "config2" in CASES else load("toy_repetition")["prog"]
+    dp = _dev(P)
+    n = 100_000
+    acc = dp.accumulate(n, seed=9)
+    _, out, _ = dp.sample_host(n, seed=9)
+    a = out.accepted_bits().astype(bool)
+    assert acc["accepted"] == int(a.sum())
+    np.testing.assert_array_equal(acc["measurements"], out.measurements()[a].sum(0))
+    np.testing.assert_array_equal(acc["detectors"], out.detectors()[a].sum(0))
+    np.testing.assert_array_equal(acc["observables"], out.observables()[a].sum(0))
