@@ -43,7 +43,7 @@ frame_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  uint32_t* base = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wib * smem_words_per_warp + lane;
+  uint32_t* base = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wib * smem_words_per_warp * 32 + lane;
   uint32_t* fx = base;
   uint32_t* fz = base + P.n * 32;
   uint32_t* slots = fz + P.n * 32;
@@ -58,6 +58,17 @@ frame_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
     uint32_t alive = validmask, errmask = 0;
     int errcode = 0;
     for (int q = 0; q < nwords_smem; q++) base[q * 32] = 0;
+    uint32_t dumped = 0;
+    auto dump_frames = [&](uint32_t mask) {
+      for (int j = 0; j < 32; j++) {
+        if (!((mask >> j) & 1)) continue;
+        const uint64_t si = (uint64_t)w * 32 + j;
+        for (int q = 0; q < P.n; q++) {
+          A.t_fx[si * P.n + q] = (fx[q * 32] >> j) & 1;
+          A.t_fz[si * P.n + q] = (fz[q * 32] >> j) & 1;
+        }
+      }
+    };
 
     for (int i = 0; i < A.stop; i++) {
       const int4 I0 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i);
@@ -150,7 +161,12 @@ frame_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
         case FS_OP_POSTSELECT: {
           const int bid = I0.y == 0 ? P.R + I0.z : I0.z;
           const uint32_t bw = slots[__ldg(P.bit_slot + bid) * 32];
-          alive &= ~((bw ^ (I0.w ? kFull : 0u)) & alive);
+          const uint32_t rej = (bw ^ (I0.w ? kFull : 0u)) & alive;
+          alive &= ~rej;
+          if (TRACE && rej && A.t_fx) {  // a rejected shot's frame freezes at its halt point
+            dump_frames(rej);
+            dumped |= rej;
+          }
           break;
         }
         default: break;  // GammaRot: global phase only, no observable effect
@@ -160,16 +176,7 @@ frame_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
     A.accepted[w] = alive & validmask;
     A.error[w] = errmask;
     if (errmask) atomicMax(A.status, errcode);
-    if (TRACE && A.t_fx) {
-      for (int j = 0; j < 32; j++) {
-        if (!((validmask >> j) & 1)) continue;
-        const uint64_t si = (uint64_t)w * 32 + j;
-        for (int q = 0; q < P.n; q++) {
-          A.t_fx[si * P.n + q] = (fx[q * 32] >> j) & 1;
-          A.t_fz[si * P.n + q] = (fz[q * 32] >> j) & 1;
-        }
-      }
-    }
+    if (TRACE && A.t_fx) dump_frames(validmask & ~dumped);
   }
 }
 

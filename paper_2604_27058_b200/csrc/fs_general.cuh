@@ -239,6 +239,30 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
       }
     };
 
+    // trace state of shots in `mask` as of now (a post-selected shot freezes at its halt point,
+    // runtime.py:632-641, while the warp keeps executing for the others)
+    uint32_t dumped = 0;
+    auto dump_trace = [&](uint32_t mask, int upto) {
+      if (!((mask >> lane) & 1)) return;
+      if (A.t_fx)
+        for (int q = 0; q < P.n; q++) {
+          A.t_fx[si * P.n + q] = (fx[q] >> lane) & 1;
+          A.t_fz[si * P.n + q] = (fz[q] >> lane) & 1;
+        }
+      if (A.t_gamma) { A.t_gamma[2 * si] = gamma.x; A.t_gamma[2 * si + 1] = gamma.y; }
+      if (A.t_draws) A.t_draws[si] = SPLITMIX ? rng.sm.count : 0u;
+      if (A.t_amps) {
+        const int kst = stop > 0 ? __ldg(P.schedule + stop - 1) : 0;
+        const int kcur = upto > 0 ? __ldg(P.schedule + upto - 1) : 0;
+        const uint32_t sz = 1u << kst, cur = 1u << kcur;
+        for (uint32_t j = 0; j < sz; j++) {
+          double2 v = j < cur ? AMP(j) : make_double2(0.0, 0.0);
+          A.t_amps[(si * sz + j) * 2] = v.x;
+          A.t_amps[(si * sz + j) * 2 + 1] = v.y;
+        }
+      }
+    };
+
     for (int i = 0; i < stop; i++) {
       if (alive == 0 && A.prezeroed) break;
       const int4 I0 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i);
@@ -525,7 +549,12 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
         case FS_OP_POSTSELECT: {
           const int bid = ins[1] == 0 ? P.R + ins[2] : ins[2];
           const uint32_t bw = slots[__ldg(P.bit_slot + bid)];
-          alive &= ~((bw ^ (ins[3] ? kFull : 0u)) & alive);
+          const uint32_t rej = (bw ^ (ins[3] ? kFull : 0u)) & alive;
+          alive &= ~rej;
+          if (rej && (A.t_fx || A.t_gamma || A.t_amps || A.t_draws)) {
+            dump_trace(rej, i);
+            dumped |= rej;
+          }
           break;
         }
         default: break;
@@ -538,24 +567,7 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
       A.error[w] = errmask;
       if (errmask) atomicMax(A.status, errcode);
     }
-    if (valid) {
-      if (A.t_fx)
-        for (int q = 0; q < P.n; q++) {
-          A.t_fx[si * P.n + q] = (fx[q] >> lane) & 1;
-          A.t_fz[si * P.n + q] = (fz[q] >> lane) & 1;
-        }
-      if (A.t_gamma) { A.t_gamma[2 * si] = gamma.x; A.t_gamma[2 * si + 1] = gamma.y; }
-      if (A.t_draws) A.t_draws[si] = SPLITMIX ? rng.sm.count : 0u;
-      if (A.t_amps) {
-        const int kst = stop > 0 ? __ldg(P.schedule + stop - 1) : 0;
-        const uint32_t sz = 1u << kst;
-        for (uint32_t j = 0; j < sz; j++) {
-          double2 v = AMP(j);
-          A.t_amps[(si * sz + j) * 2] = v.x;
-          A.t_amps[(si * sz + j) * 2 + 1] = v.y;
-        }
-      }
-    }
+    dump_trace(validmask & ~dumped, stop);
     __syncwarp();
   }
 #undef AMP
