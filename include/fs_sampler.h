@@ -105,6 +105,7 @@ typedef struct fs_prog_desc {
 #define FS_RNG_SPLITMIX 1u   /* reference stream: framesim ShotRng draw for draw (rng.py:24-71) */
 #define FS_NO_RENORM    2u   /* renormalize=False (runtime.py:355-366, :389-404) */
 #define FS_FORCE_GENERAL 4u  /* testing: force the general per-shot-lane interpreter */
+#define FS_FORCE_HBM    8u   /* testing: force the large-k (HBM-resident array) engine */
 
 /* trace mode: every random choice may be supplied (SURVEY §8(d) "trace mode") */
 typedef struct fs_trace_in {
@@ -146,7 +147,8 @@ typedef struct fs_prog fs_prog;
 /* Copies the program to the current CUDA device; chooses the execution engine. */
 int fs_program_create(const fs_prog_desc* desc, fs_prog** out);
 void fs_program_destroy(fs_prog* prog);
-/* engine chosen for a flag set: 0 = general (lane = shot), 1 = bit-sliced frame engine */
+/* engine chosen for a flag set: 0 = general (lane = shot), 1 = bit-sliced frame engine,
+   2 = large-k engine (active arrays in HBM) */
 int fs_program_engine(const fs_prog* prog, uint32_t flags);
 
 /* shot0 must be a multiple of 32 (shot words are absolute).  Returns FS_OK, or

@@ -140,6 +140,11 @@ __device__ __forceinline__ uint32_t ins0(uint32_t i, int a) {
   return ((i & ~lowmask) << 1) | (i & lowmask);
 }
 
+__device__ __forceinline__ uint64_t ins0_64(uint64_t i, int a) {
+  const uint64_t lowmask = (1ull << a) - 1ull;
+  return ((i & ~lowmask) << 1) | (i & lowmask);
+}
+
 // ------------------------------------------------------------------ noise helpers
 __device__ __forceinline__ int bisect_right(const double* __restrict__ S, double x, int lo, int hi) {
   while (lo < hi) {

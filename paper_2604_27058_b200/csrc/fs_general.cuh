@@ -107,8 +107,21 @@ __device__ void philox_noise_word(const DevProg& P, uint32_t* fx, uint32_t* fz, 
 }
 
 // Reference hazard skipping for one shot (runtime.py:564-586 / :675-699), draw for draw.
+// Frame words are `stride` apart; `atomic` when several lanes share the words.
+__device__ __forceinline__ void xor_case_strided(const DevProg& P, uint32_t* fx, uint32_t* fz, int c, uint32_t bit,
+                                                 int stride, bool atomic) {
+  int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
+  for (int j = off; j < end; j++) {
+    uint32_t e = __ldg(P.paulis + j);
+    uint32_t* f = (FS_PAULI_Z(e) ? fz : fx) + (size_t)FS_PAULI_Q(e) * stride;
+    if (atomic) atomicXor(f, bit);
+    else *f ^= bit;
+  }
+}
+
 template <class Draw>
-__device__ void hazard_shot(const DevProg& P, uint32_t* fx, uint32_t* fz, uint32_t bit, const int* ins, Draw& rng) {
+__device__ void hazard_shot(const DevProg& P, uint32_t* fx, uint32_t* fz, uint32_t bit, const int* ins, Draw& rng,
+                            int stride = 1, bool atomic = true) {
   const double* S = P.cum_hazard;
   const int plan_off = ins[3], plan_cnt = ins[4];
   for (int pi = 0; pi < plan_cnt; pi++) {
@@ -116,7 +129,7 @@ __device__ void hazard_shot(const DevProg& P, uint32_t* fx, uint32_t* fz, uint32
     if (a < 0) {
       int site = b, c = __ldg(P.site_case_off + site);
       if (num_cases(P, site) > 1) c = pick_case(P, site, rng.uniform());
-      xor_case(P, fx, fz, c, bit, true);
+      xor_case_strided(P, fx, fz, c, bit, stride, atomic);
       continue;
     }
     int i = a;
@@ -126,16 +139,16 @@ __device__ void hazard_shot(const DevProg& P, uint32_t* fx, uint32_t* fz, uint32
       if (idx > b) break;
       int site = idx - 1, c = __ldg(P.site_case_off + site);
       if (num_cases(P, site) > 1) c = pick_case(P, site, rng.uniform());
-      xor_case(P, fx, fz, c, bit, true);
+      xor_case_strided(P, fx, fz, c, bit, stride, atomic);
       i = site + 1;
     }
   }
 }
 
-// Forced fault modes for one shot (runtime.py:587-601).
+// Forced fault modes for one shot (runtime.py:587-601).  stride==1 => words shared by lanes (atomic).
 template <class Draw>
 __device__ void forced_faults_shot(const DevProg& P, uint32_t* fx, uint32_t* fz, uint32_t bit, const int* ins,
-                                   const int16_t* modes, Draw& rng, int stride) {
+                                   const int16_t* modes, Draw& rng, int stride, bool atomic = false) {
   for (int site = ins[1]; site < ins[2]; site++) {
     int mode = modes[site];
     if (mode == 2) continue;
@@ -150,13 +163,7 @@ __device__ void forced_faults_shot(const DevProg& P, uint32_t* fx, uint32_t* fz,
     } else {
       c += mode - 3;
     }
-    int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
-    for (int j = off; j < end; j++) {
-      uint32_t e = __ldg(P.paulis + j);
-      uint32_t* f = FS_PAULI_Z(e) ? fz : fx;
-      if (stride == 1) atomicXor(f + FS_PAULI_Q(e), bit);
-      else f[FS_PAULI_Q(e) * stride] ^= bit;
-    }
+    xor_case_strided(P, fx, fz, c, bit, stride, atomic);
   }
 }
 
@@ -520,7 +527,7 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
             if (me) {
               ShotDraws& d = rng;
               d.begin(i, TAG_FORCED);
-              forced_faults_shot(P, fx, fz, lanebit, ins, fmodes, d, 1);
+              forced_faults_shot(P, fx, fz, lanebit, ins, fmodes, d, 1, true);
             }
           } else if (SPLITMIX) {
             if (me) hazard_shot(P, fx, fz, lanebit, ins, rng.sm);

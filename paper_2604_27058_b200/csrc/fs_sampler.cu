@@ -15,6 +15,7 @@
 
 #include "fs_frame.cuh"
 #include "fs_general.cuh"
+#include "fs_hbm.cuh"
 
 namespace {
 
@@ -36,6 +37,18 @@ constexpr size_t kSmemBudget = 200 * 1024;  // per block, leaves room for L1
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+struct Stage {  // carve-out of one device allocation
+  size_t off = 0;
+  unsigned char* base = nullptr;
+  template <class T>
+  T* take(size_t count) {
+    if (!count) return nullptr;
+    T* r = reinterpret_cast<T*>(base + off);
+    off = align_up(off + count * sizeof(T), 256);
+    return r;
+  }
+};
+
 }  // namespace
 
 struct fs_prog {
@@ -54,7 +67,18 @@ struct fs_prog {
   size_t stage_bytes = 0;
   int64_t* d_counts = nullptr;
   size_t counts_len = 0;
+  // host copies used by the large-k engine's host-side walk
+  std::vector<int32_t> h_instrs, h_sched;
+  std::vector<double> h_fparams;
+  // large-k engine state
+  void* hbm = nullptr;
+  size_t hbm_bytes = 0;
+  uint64_t hbm_B = 0;
 };
+
+namespace {
+constexpr int kLargeK = 16;  // k_max at which active arrays move to the HBM engine
+}
 
 extern "C" int fs_abi_version(void) { return FS_ABI_VERSION; }
 extern "C" const char* fs_last_error(void) { return g_last_error.c_str(); }
@@ -128,6 +152,9 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   dp.plans = reinterpret_cast<const int*>(b + o_pl);
   dp.record_out = reinterpret_cast<const int*>(b + o_ro);
   dp.bit_slot = reinterpret_cast<const int*>(b + o_bs);
+  p->h_instrs.assign(d->instrs, d->instrs + (size_t)FS_INS_WORDS * d->num_instrs);
+  p->h_sched.assign(d->schedule, d->schedule + d->num_instrs);
+  if (d->num_fparams) p->h_fparams.assign(d->fparams, d->fparams + d->num_fparams);
   // pointers of the creator's arrays are not retained
   p->desc.instrs = nullptr;
   *out = p;
@@ -141,8 +168,11 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->d_status);
   cudaFree(p->stage);
   cudaFree(p->d_counts);
+  cudaFree(p->hbm);
   delete p;
 }
+
+static bool wants_hbm(const fs_prog* p, uint32_t flags) { return p->dp.k_max >= kLargeK || (flags & FS_FORCE_HBM); }
 
 static bool wants_general(const fs_prog* p, uint32_t flags, const fs_trace_out* tout) {
   if (p->dp.k_max > 0) return true;
@@ -153,6 +183,7 @@ static bool wants_general(const fs_prog* p, uint32_t flags, const fs_trace_out* 
 
 extern "C" int fs_program_engine(const fs_prog* p, uint32_t flags) {
   if (!p) return set_error(FS_ERR_ARG, "null program");
+  if (wants_hbm(p, flags)) return 2;
   return wants_general(p, flags, nullptr) ? 0 : 1;
 }
 
@@ -163,6 +194,211 @@ int occupancy_blocks(K kernel, int threads, size_t smem) {
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem) != cudaSuccess) return 1;
   return std::max(nb, 1);
+}
+
+
+// ------------------------------------------------------------------ large-k engine driver
+int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
+  const fs::DevProg& dp = p->dp;
+  const uint64_t cap = 1ull << dp.k_max;
+  const size_t per_shot = cap * sizeof(double2);
+  const int n = dp.n, S = dp.num_slots, O = dp.O, N = dp.num_instrs;
+  const int nblk = 64;
+  size_t free_b = 0, total_b = 0;
+  FS_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  auto state_bytes = [&](uint64_t B) {
+    const uint64_t Wm = (B + 31) / 32;
+    size_t b = 0;
+    b += align_up(B * per_shot, 256);
+    b += align_up(4 * Wm * (2 * (size_t)n + S + O + 5 + (size_t)N), 256);
+    b += align_up(B * (16 + 4 + 2 * nblk * 8 + 16 + 32), 256);
+    return b + 4096;
+  };
+  uint64_t want = (a.nshots + 31) / 32 * 32;
+  const size_t budget = std::min<size_t>((size_t)((double)(free_b + p->hbm_bytes) * 0.80), (size_t)140 << 30);
+  uint64_t B = want;
+  while (B > 32 && state_bytes(B) > budget) B = std::max<uint64_t>(32, (B / 2) / 32 * 32);
+  if (state_bytes(B) > budget) {
+    if (a.nshots <= 1 && state_bytes(1) <= budget) B = 1;
+    else return set_error(FS_ERR_ARG, "active array too large for device memory");
+  }
+  if (state_bytes(B) > p->hbm_bytes) {
+    cudaFree(p->hbm);
+    p->hbm = nullptr;
+    p->hbm_bytes = 0;
+    FS_CUDA_TRY(cudaMalloc(&p->hbm, state_bytes(B)));
+    p->hbm_bytes = state_bytes(B);
+  }
+  const uint64_t Wm = (B + 31) / 32;
+  fs::HbmState H{};
+  {
+    Stage st;
+    st.base = static_cast<unsigned char*>(p->hbm);
+    H.amps = st.take<double2>(B * cap);
+    H.fx = st.take<uint32_t>(Wm * n + 1);
+    H.fz = st.take<uint32_t>(Wm * n + 1);
+    H.slots = st.take<uint32_t>(Wm * S + 1);
+    H.obs = st.take<uint32_t>(Wm * O + 1);
+    H.alive = st.take<uint32_t>(Wm);
+    H.err = st.take<uint32_t>(Wm);
+    H.brw = st.take<uint32_t>(Wm);
+    H.frozen = st.take<uint32_t>(Wm);
+    H.par = st.take<uint32_t>(Wm * N + 1);
+    H.gamma = st.take<double2>(B);
+    H.smcount = st.take<uint32_t>(B);
+    H.red = st.take<double>(B * 2 * nblk);
+    H.p1 = st.take<double>(B);
+    H.pall = st.take<double>(B);
+    H.kco = st.take<double2>(2 * B);
+    H.cap = cap;
+    H.nblk = nblk;
+  }
+  // all output words are written by the scalar kernel unless a batch halts early
+  if (dp.U) FS_CUDA_TRY(cudaMemsetAsync(a.meas, 0, sizeof(uint32_t) * dp.U * (size_t)a.W, stream));
+  if (dp.D) FS_CUDA_TRY(cudaMemsetAsync(a.det, 0, sizeof(uint32_t) * dp.D * (size_t)a.W, stream));
+  const bool splitmix = a.flags & FS_RNG_SPLITMIX;
+  auto scalar = [&](int i0, int i1, int init, uint64_t batch0, uint32_t W) -> int {
+    dim3 g((W + 127) / 128);
+    if (splitmix) fs::hbm_scalar_kernel<true><<<g, 128, 0, stream>>>(dp, a, H, i0, i1, init, batch0, W);
+    else fs::hbm_scalar_kernel<false><<<g, 128, 0, stream>>>(dp, a, H, i0, i1, init, batch0, W);
+    FS_CUDA_TRY(cudaGetLastError());
+    return FS_OK;
+  };
+  const int* ins_all = p->h_instrs.data();
+  const double* fpar = p->h_fparams.data();
+  for (uint64_t batch0 = 0; batch0 < a.nshots; batch0 += B) {
+    const uint64_t nb = std::min<uint64_t>(B, a.nshots - batch0);
+    const uint32_t W = (uint32_t)((nb + 31) / 32);
+    int rc = scalar(0, 0, 1, batch0, W);
+    if (rc) return rc;
+    fs::hbm_init_amps_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, stream>>>(H, (uint32_t)nb);
+    std::vector<int> live;  // logical axis -> physical position
+    auto dead_list = [&](std::initializer_list<int> extra) {
+      fs::DeadBits d{};
+      int top = -1;
+      for (int x : live) top = std::max(top, x);
+      for (int x : extra) top = std::max(top, x);
+      std::vector<int> pos;
+      for (int q = 0; q <= top; q++) {
+        bool isl = std::find(live.begin(), live.end(), q) != live.end();
+        bool ise = std::find(extra.begin(), extra.end(), q) != extra.end();
+        if (!isl || ise) pos.push_back(q);
+      }
+      std::sort(pos.begin(), pos.end());
+      pos.erase(std::unique(pos.begin(), pos.end()), pos.end());
+      d.n = (int)pos.size();
+      for (int t = 0; t < d.n; t++) d.pos[t] = (int8_t)pos[t];
+      return d;
+    };
+    auto lowest_dead = [&]() {
+      for (int q = 0; q < dp.k_max; q++)
+        if (std::find(live.begin(), live.end(), q) == live.end()) return q;
+      return -1;
+    };
+    auto run_op = [&](fs::ArrOp& o, uint64_t count) -> int {
+      if (count == 0) return FS_OK;
+      const uint64_t want_x = (count + 255) / 256;
+      const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(want_x, std::max<uint64_t>(1, 16384 / nb)));
+      fs::hbm_array_kernel<<<dim3((unsigned)gx, (unsigned)nb), 256, 0, stream>>>(o, H, count, W);
+      FS_CUDA_TRY(cudaGetLastError());
+      return FS_OK;
+    };
+    auto cpx = [&](int off) { return make_double2(fpar[off], fpar[off + 1]); };
+    int i = 0;
+    const int stop = a.stop;
+    while (i < stop) {
+      int j = i;
+      while (j < stop) {
+        const int op = FS_OPCODE(ins_all[(size_t)j * FS_INS_WORDS]);
+        if (op == FS_OP_MEAS_ACTIVE || op == FS_OP_MEAS_COLLAPSE) break;
+        j++;
+      }
+      if (j > i && (rc = scalar(i, j, 0, batch0, W))) return rc;
+      for (int t = i; t < j; t++) {
+        const int* I = ins_all + (size_t)t * FS_INS_WORDS;
+        const int op = FS_OPCODE(I[0]);
+        fs::ArrOp o{};
+        o.instr = t;
+        if (op == FS_OP_ARRAY_GATE) {
+          const int g = I[1], k = I[6];
+          o.pa = live[I[4]];
+          if (g == FS_G_CX || g == FS_G_CZ) {
+            o.pb = live[I[5]];
+            o.kind = g == FS_G_CX ? fs::HA_CX : fs::HA_CZ;
+            o.dead = dead_list({o.pa, o.pb});
+            if ((rc = run_op(o, 1ull << (k - 2)))) return rc;
+          } else {
+            o.kind = g == FS_G_H ? fs::HA_H : (g == FS_G_S ? fs::HA_S : fs::HA_SDAG);
+            o.dead = dead_list({o.pa});
+            if ((rc = run_op(o, 1ull << (k - 1)))) return rc;
+          }
+        } else if (op == FS_OP_EXPAND) {
+          const int kb = I[6];
+          o.kind = fs::HA_EXPAND;
+          o.pa = lowest_dead();
+          o.dead = dead_list({o.pa});
+          o.c0 = cpx(I[5]); o.c1 = cpx(I[5] + 2); o.c2 = cpx(I[5] + 4); o.c3 = cpx(I[5] + 6);
+          if ((rc = run_op(o, 1ull << kb))) return rc;
+          live.push_back(o.pa);
+        } else if (op == FS_OP_ARRAY_ROT) {
+          const int k = I[6];
+          o.kind = fs::HA_ROT;
+          o.pa = live[I[2]];
+          o.dead = dead_list({o.pa});
+          o.c0 = cpx(I[5]); o.c1 = cpx(I[5] + 2);
+          if ((rc = run_op(o, 1ull << (k - 1)))) return rc;
+        } else if (op == FS_OP_RETIRE) {
+          const int k = I[6];
+          o.kind = fs::HA_RETIRE;
+          o.pa = live[I[2]];
+          o.dead = dead_list({o.pa});
+          if ((rc = run_op(o, 1ull << (k - 1)))) return rc;
+          live.erase(live.begin() + I[2]);
+        }
+      }
+      if (j >= stop) { i = j; break; }
+      // measurement j: reduction -> decision -> collapse
+      const int* I = ins_all + (size_t)j * FS_INS_WORDS;
+      const int op = FS_OPCODE(I[0]);
+      const int k = I[6];
+      fs::ArrOp o{};
+      o.instr = j;
+      o.pa = live[I[2]];
+      o.dead = dead_list({o.pa});
+      const uint64_t pairs = 1ull << (k - 1);
+      const bool collapse = op == FS_OP_MEAS_COLLAPSE;
+      double2 u10 = make_double2(0, 0), u11 = make_double2(1, 0);
+      if (collapse) { u10 = cpx(I[5] + 4); u11 = cpx(I[5] + 6); }
+      const int nbu = (int)std::max<uint64_t>(1, std::min<uint64_t>(nblk, (pairs + 2047) / 2048));
+      fs::hbm_reduce_kernel<<<dim3(nbu, (unsigned)nb), 256, 0, stream>>>(o, H, pairs, collapse ? 1 : 0, u10, u11);
+      fs::hbm_reduce_final_kernel<<<(unsigned)((nb + 127) / 128), 128, 0, stream>>>(H, (uint32_t)nb, nbu);
+      FS_CUDA_TRY(cudaGetLastError());
+      if ((rc = scalar(j, j + 1, 0, batch0, W))) return rc;
+      if (collapse) {
+        o.kind = fs::HA_COLLAPSE;
+        if ((rc = run_op(o, pairs))) return rc;
+        live.erase(live.begin() + I[2]);
+      } else {
+        o.kind = fs::HA_ACTIVE_ZERO;
+        o.c0 = make_double2((a.flags & FS_NO_RENORM) ? 0.0 : 1.0, 0.0);
+        if ((rc = run_op(o, pairs))) return rc;
+      }
+      i = j + 1;
+    }
+    fs::hbm_finish_kernel<<<(W + 127) / 128, 128, 0, stream>>>(dp, a, H, batch0, W);
+    FS_CUDA_TRY(cudaGetLastError());
+    if (a.t_amps) {
+      const int kst = stop > 0 ? p->h_sched[stop - 1] : 0;
+      if ((int)live.size() != kst) return set_error(FS_ERR_ARG, "internal: axis map out of sync with schedule");
+      fs::DevAxisMap m{};
+      for (int b = 0; b < kst; b++) m.phys[b] = (int8_t)live[b];
+      const uint64_t sz = 1ull << kst;
+      const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>((sz + 255) / 256, 1024));
+      fs::hbm_gather_kernel<<<dim3((unsigned)gx, (unsigned)nb), 256, 0, stream>>>(dp, a, H, batch0, (uint32_t)nb, kst, m);
+      FS_CUDA_TRY(cudaGetLastError());
+    }
+  }
+  return FS_OK;
 }
 
 int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t flags, const fs_trace_in* tin,
@@ -202,6 +438,7 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
   }
   a.arr_log2 = dp.k_max;
   if (!out->status) FS_CUDA_TRY(cudaMemsetAsync(p->d_status, 0, sizeof(int), stream));
+  if (wants_hbm(p, flags)) return launch_hbm(p, a, stream);
   const size_t W = a.W;
   a.prezeroed = 0;
   if (dp.has_psel) {  // halted warps may stop early: their remaining output words must read 0
@@ -291,19 +528,6 @@ extern "C" int fs_sample(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nsh
   return launch(p, seed, shot0, nshots, flags, tin, out, tout, static_cast<cudaStream_t>(stream));
 }
 
-namespace {
-struct Stage {  // device staging carve-out for fs_sample_host
-  size_t off = 0;
-  unsigned char* base = nullptr;
-  template <class T>
-  T* take(size_t count) {
-    if (!count) return nullptr;
-    T* r = reinterpret_cast<T*>(base + off);
-    off = align_up(off + count * sizeof(T), 256);
-    return r;
-  }
-};
-}  // namespace
 
 extern "C" int fs_sample_host(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t flags,
                               const fs_trace_in* tin, const fs_sample_out* out, const fs_trace_out* tout) {

@@ -56,7 +56,7 @@ class DeviceProgram:
             pass
 
     def engine(self, flags: int = 0) -> str:
-        return "frame" if self._lib.fs_program_engine(self._h, flags) == 1 else "general"
+        return {0: "general", 1: "frame", 2: "hbm"}[self._lib.fs_program_engine(self._h, flags)]
 
     # -- host buffers (C-ABI does H2D/D2H) ----------------------------------------------
     def sample_host(self, nshots: int, seed: int = 0, shot0: int = 0, flags: int = 0,

@@ -15,7 +15,7 @@ import pytest
 
 import oracle
 from goldens import case_names, load, rel_err
-from paper_2604_27058_b200._abi import FS_FORCE_GENERAL, FS_RNG_PHILOX, FS_RNG_SPLITMIX
+from paper_2604_27058_b200._abi import FS_FORCE_GENERAL, FS_FORCE_HBM, FS_RNG_PHILOX, FS_RNG_SPLITMIX
 
 pytestmark = pytest.mark.gpu
 ALL = case_names()
@@ -37,8 +37,8 @@ def _same(a, b):
     np.testing.assert_array_equal(a.accepted_bits(), b.accepted_bits())
 
 
-@pytest.mark.parametrize("name", [c for c in CASES if "t_modes" in load(c)])
-@pytest.mark.parametrize("flags", [FS_RNG_SPLITMIX, FS_RNG_PHILOX])
+@pytest.mark.parametrize("name", [c for c in ALL if "t_modes" in load(c)])
+@pytest.mark.parametrize("flags", [FS_RNG_SPLITMIX, FS_RNG_PHILOX, FS_RNG_SPLITMIX | FS_FORCE_HBM])
 def test_gpu_trace_matches_reference(cuda, name, flags):
     g = load(name)
     P = g["prog"]
@@ -56,7 +56,7 @@ def test_gpu_trace_matches_reference(cuda, name, flags):
     assert rel_err(tb.gamma_c(), g["t_gamma"]) < AMP_TOL
     if "t_amps" in g and g["t_acc"].all():
         assert rel_err(tb.amps_c(), g["t_amps"]) < AMP_TOL
-    if flags == FS_RNG_SPLITMIX:
+    if flags & FS_RNG_SPLITMIX:
         np.testing.assert_array_equal(tb.draws, g["t_draws"])
 
 
@@ -78,13 +78,14 @@ def test_gpu_frame_engine_trace_matches_reference(cuda, name):
 
 
 @pytest.mark.parametrize("name", [c for c in CASES if "cp_index" in load(c)])
-def test_gpu_checkpoints_match_reference(cuda, name):
+@pytest.mark.parametrize("engine_flag", [0, FS_FORCE_HBM])
+def test_gpu_checkpoints_match_reference(cuda, name, engine_flag):
     g = load(name)
     P = g["prog"]
     dp = _dev(P)
     n = g["t_modes"].shape[0]
     for c in g["cp_index"].tolist():
-        st, out, tb = dp.sample_host(n, seed=int(g["t_seed"][0]), flags=FS_RNG_SPLITMIX,
+        st, out, tb = dp.sample_host(n, seed=int(g["t_seed"][0]), flags=FS_RNG_SPLITMIX | engine_flag,
                                      fault_modes=g["t_modes"], forced=g["t_forced"], stop=c + 1,
                                      want_state=True)
         ok = ~np.isnan(g[f"cp{c}_gamma"])
@@ -95,12 +96,13 @@ def test_gpu_checkpoints_match_reference(cuda, name):
 
 
 @pytest.mark.parametrize("name", [c for c in CASES if "f_meas" in load(c)])
-def test_gpu_free_reference_stream_matches_reference(cuda, name):
+@pytest.mark.parametrize("engine_flag", [0, FS_FORCE_HBM])
+def test_gpu_free_reference_stream_matches_reference(cuda, name, engine_flag):
     g = load(name)
     P = g["prog"]
     dp = _dev(P)
     n = g["f_meas"].shape[0]
-    st, out, _ = dp.sample_host(n, seed=int(g["f_seed"][0]), flags=FS_RNG_SPLITMIX)
+    st, out, _ = dp.sample_host(n, seed=int(g["f_seed"][0]), flags=FS_RNG_SPLITMIX | engine_flag)
     assert st == 0
     np.testing.assert_array_equal(out.measurements(), g["f_meas"])
     np.testing.assert_array_equal(out.detectors(), g["f_det"])
@@ -109,11 +111,12 @@ def test_gpu_free_reference_stream_matches_reference(cuda, name):
 
 
 @pytest.mark.parametrize("name", CASES)
-def test_gpu_free_philox_matches_oracle(cuda, name):
+@pytest.mark.parametrize("engine_flag", [0, FS_FORCE_HBM])
+def test_gpu_free_philox_matches_oracle(cuda, name, engine_flag):
     P = load(name)["prog"]
     n = 2048 if P.k_max < 12 else 256
     dp = _dev(P)
-    _, gout, _ = dp.sample_host(n, seed=77, shot0=64, flags=FS_RNG_PHILOX)
+    _, gout, _ = dp.sample_host(n, seed=77, shot0=64, flags=FS_RNG_PHILOX | engine_flag)
     _, oout, _ = oracle.sample(P, n, seed=77, shot0=64, flags=FS_RNG_PHILOX)
     _same(gout, oout)
 
@@ -139,3 +142,13 @@ def test_gpu_accumulate_matches_samples(cuda):
     np.testing.assert_array_equal(acc["measurements"], out.measurements()[a].sum(0))
     np.testing.assert_array_equal(acc["detectors"], out.detectors()[a].sum(0))
     np.testing.assert_array_equal(acc["observables"], out.observables()[a].sum(0))
+
+
+def test_gpu_large_k_config3_philox_matches_oracle(cuda):
+    """Config 3 (k = 22, HBM engine) free sampling vs the oracle restatement, 2 shots."""
+    P = load("config3")["prog"]
+    dp = _dev(P)
+    assert dp.engine(0) == "hbm"
+    _, gout, _ = dp.sample_host(2, seed=3, flags=FS_RNG_PHILOX)
+    _, oout, _ = oracle.sample(P, 2, seed=3, flags=FS_RNG_PHILOX)
+    _same(gout, oout)
