@@ -1,0 +1,291 @@
+"""Drop-in mirror of the reference per-shot API (``framesim/runtime.py``), executed on the GPU.
+
+Same names, arguments and error behaviour as the reference:
+
+* ``sample(prog, shots, seed=0, workers=1, renormalize=True, stratum=None,
+  keep_rejected=True)`` -> iterator of :class:`ShotRecord`  (runtime.py:777-795)
+* ``sample_accumulate(prog, shots, seed=0, stratum=None)`` -> dict (runtime.py:836-867)
+* ``run_shot(prog, state=None, shot=0, seed=0, forced_faults=None,
+  forced_outcomes=None, weight=1.0, trace=None)`` -> ShotRecord (runtime.py:731-751)
+* ``ShotState``, ``ShotRecord``, ``ShotError``, ``BRANCH_FLOOR``
+
+``prog`` is either the reference compiler's ``BytecodeProgram`` (serialized on
+first use and cached on the object) or a :class:`~.program.Program`.
+
+Random stream: ``rng="reference"`` (default here) reproduces framesim's
+SplitMix64 ``ShotRng`` draw for draw, so ``sample(prog, n, seed)`` returns the
+same records as the reference; ``rng="philox"`` is the engine's native
+Philox4x32-10 stream (same law, different realisation), which unlocks the
+bit-sliced frame engine and is what ``bench.py`` measures.
+
+Batched entry points (``sample_batch``) return the shot-bit-word arrays
+directly; they are the throughput path (the per-shot ``ShotRecord`` objects are
+a host-side convenience and cost Python time per shot).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterator
+
+import numpy as np
+
+from . import _abi
+from .engine import DeviceProgram, ShotError
+from .program import OP_NAMES, Program, as_program
+
+BRANCH_FLOOR = 1e-12  # runtime.py:47
+_CHUNK = 1 << 20      # shots per device call in the record iterator
+
+__all__ = ["BRANCH_FLOOR", "ShotError", "ShotRecord", "ShotState", "run_shot", "sample",
+           "sample_accumulate", "sample_batch", "Sampler", "compile_circuit"]
+
+
+@dataclass(slots=True)
+class ShotRecord:
+    """runtime.py:59-65"""
+
+    measurements: np.ndarray
+    detectors: np.ndarray
+    observables: np.ndarray
+    accepted: bool
+    weight: float
+
+
+def _flags(rng: str, renormalize: bool = True) -> int:
+    if rng not in ("reference", "philox"):
+        raise ValueError(f"unknown rng {rng!r} (expected 'reference' or 'philox')")
+    f = _abi.FS_RNG_SPLITMIX if rng == "reference" else _abi.FS_RNG_PHILOX
+    if not renormalize:
+        f |= _abi.FS_NO_RENORM
+    return f
+
+
+def _device_program(prog) -> DeviceProgram:
+    """One resident DeviceProgram per program object (cached like the reference's closures)."""
+    d = getattr(prog, "__dict__", None)
+    if d is not None:
+        cached = d.get("_fs_b200_device")
+        if cached is not None:
+            return cached
+    dp = DeviceProgram(as_program(prog))
+    if d is not None:
+        d["_fs_b200_device"] = dp
+    return dp
+
+
+def compile_circuit(circuit_or_text, optimize: bool = True, postselect_detectors=()):
+    """The host compiler stays the reference's (backend.py:599); re-exported for convenience."""
+    try:
+        from framesim.backend import compile_circuit as _cc
+    except ImportError as exc:  # pragma: no cover - depends on the user's install
+        raise ImportError("compile_circuit needs the reference compiler package `framesim` "
+                          "(the GPU engine consumes its BytecodeProgram)") from exc
+    return _cc(circuit_or_text, optimize=optimize, postselect_detectors=postselect_detectors)
+
+
+class Sampler:
+    """A compiled program resident on the GPU (the ``_compiled(prog)`` analogue, runtime.py:663)."""
+
+    def __init__(self, prog, rng: str = "philox", renormalize: bool = True):
+        self.prog = prog
+        self.dp = _device_program(prog)
+        self.flags = _flags(rng, renormalize)
+
+    @property
+    def program(self) -> Program:
+        return self.dp.prog
+
+    def sample_batch(self, shots: int, seed: int = 0, shot0: int = 0) -> dict:
+        """All outputs of shots [shot0, shot0+shots) as uint8 arrays [shots, ...]."""
+        if shots < 1:
+            raise ValueError("shots must be >= 1")
+        if shot0 % 32:
+            raise ValueError("shot0 must be a multiple of 32")
+        _, out, _ = self.dp.sample_host(shots, seed=seed, shot0=shot0, flags=self.flags)
+        return {"measurements": out.measurements(), "detectors": out.detectors(),
+                "observables": out.observables(), "accepted": out.accepted_bits().astype(bool)}
+
+    def sample_packed(self, shots: int, seed: int = 0, shot0: int = 0):
+        """Raw shot-bit words (include/fs_sampler.h layout): HostOutputs."""
+        _, out, _ = self.dp.sample_host(shots, seed=seed, shot0=shot0, flags=self.flags)
+        return out
+
+    def accumulate(self, shots: int, seed: int = 0) -> dict:
+        acc = self.dp.accumulate(shots, seed=seed, flags=self.flags)
+        acc["weight_sum"] = float(acc["accepted"])
+        return acc
+
+
+def sample_batch(prog, shots: int, seed: int = 0, rng: str = "reference", renormalize: bool = True) -> dict:
+    return Sampler(prog, rng=rng, renormalize=renormalize).sample_batch(shots, seed=seed)
+
+
+def sample(prog, shots: int, seed: int = 0, workers: int = 1, renormalize: bool = True,
+           stratum=None, keep_rejected: bool = True, rng: str = "reference") -> Iterator[ShotRecord]:
+    """Yield ShotRecords for shots 0..shots-1 in order (runtime.py:777-795).
+
+    ``workers`` is accepted for signature compatibility; the GPU executes every
+    shot of a chunk concurrently and the output does not depend on it.
+    """
+    if shots < 1:
+        raise ValueError("shots must be >= 1")
+    if stratum is not None:
+        raise NotImplementedError("stratified importance sampling (runtime.py:873-945) is not on "
+                                  "the GPU path yet; use framesim.runtime.importance_sample")
+    s = Sampler(prog, rng=rng, renormalize=renormalize)
+    return _iter_records(s, shots, seed, keep_rejected)
+
+
+def _iter_records(s: Sampler, shots: int, seed: int, keep_rejected: bool):
+    for c0 in range(0, shots, _CHUNK):
+        n = min(_CHUNK, shots - c0)
+        b = s.sample_batch(n, seed=seed, shot0=c0)
+        m, d, o, a = b["measurements"], b["detectors"], b["observables"], b["accepted"]
+        for i in range(n):
+            if a[i] or keep_rejected:
+                yield ShotRecord(m[i], d[i], o[i], bool(a[i]), 1.0)
+
+
+def sample_accumulate(prog, shots: int, seed: int = 0, stratum=None, rng: str = "reference") -> dict:
+    """Bit sums over accepted shots (runtime.py:836-867), reduced on the device."""
+    if stratum is not None:
+        raise NotImplementedError("stratified importance sampling is not on the GPU path yet")
+    if shots < 1:
+        return {"shots": shots, "accepted": 0, "weight_sum": 0.0,
+                "measurements": np.zeros(as_program(prog).num_user_records, np.int64),
+                "detectors": np.zeros(as_program(prog).num_detectors, np.int64),
+                "observables": np.zeros(as_program(prog).num_observables, np.int64)}
+    return Sampler(prog, rng=rng).accumulate(shots, seed=seed)
+
+
+class ShotState:
+    """Host view of one shot's factored state after ``run_shot`` (runtime.py:71-122).
+
+    The authoritative state lives on the GPU during execution; ``run_shot``
+    copies the frames, gamma, active array and record bits back here.
+    """
+
+    def __init__(self, prog, seed: int = 0, renormalize: bool = True):
+        P = as_program(prog)
+        self.prog = prog
+        self.n = P.n
+        self.k_max = P.k_max
+        self.seed = seed
+        self.renormalize = renormalize
+        self.frame_x = np.zeros(P.n, np.uint8)
+        self.frame_z = np.zeros(P.n, np.uint8)
+        self.records = np.zeros(P.record_count, np.uint8)
+        self.detectors = np.zeros(P.num_detectors, np.uint8)
+        self.observables = np.zeros(P.num_observables, np.uint8)
+        self.buf = np.zeros(1 << P.k_max, np.complex128)
+        self.buf[0] = 1.0
+        self.gamma = 1.0 + 0.0j
+        self.k = 0
+        self.weight = 1.0
+        self.accepted = True
+        self.draws = 0
+        self.forced_faults = None
+        self.forced_outcomes = None
+
+    def active_view(self) -> np.ndarray:
+        return self.buf[: 1 << self.k]
+
+
+def _fault_modes(P: Program, forced_faults) -> np.ndarray | None:
+    """Reference encoding (runtime.py:587-601): dict site->mode (default 0) or an array."""
+    if forced_faults is None:
+        return None
+    if isinstance(forced_faults, dict):
+        modes = np.zeros(P.num_sites, np.int16)
+        for k, v in forced_faults.items():
+            modes[int(k)] = int(v)
+        return modes[None, :]
+    arr = np.asarray(forced_faults, dtype=np.int16).reshape(1, -1)
+    if arr.shape[1] != P.num_sites:
+        raise ValueError("forced_faults array length must equal the number of noise sites")
+    return arr
+
+
+def _forced(P: Program, forced_outcomes) -> np.ndarray | None:
+    if forced_outcomes is None:
+        return None
+    f = np.full((1, P.record_count), -1, np.int8)
+    for r, b in forced_outcomes.items():
+        f[0, int(r)] = int(b)
+    return f
+
+
+def run_shot(prog, state: ShotState | None = None, shot: int = 0, seed: int = 0, forced_faults=None,
+             forced_outcomes=None, weight: float = 1.0, trace=None, rng: str = "reference") -> ShotRecord:
+    """Execute one shot on the GPU; ``state`` receives its final state (runtime.py:731-751).
+
+    ``trace(state, ins)`` is called after every instruction like the reference;
+    each call re-executes the program prefix on the device (the engine does
+    not stop mid-kernel), so traced runs are for validation, not speed.
+    """
+    if state is None:
+        state = ShotState(prog, seed=seed)
+    dp = _device_program(prog)
+    P = dp.prog
+    flags = _flags(rng, state.renormalize)
+    fm = _fault_modes(P, forced_faults)
+    fo = _forced(P, forced_outcomes)
+    base = (shot // 32) * 32
+    lane = shot - base
+    state.forced_faults = forced_faults
+    state.forced_outcomes = forced_outcomes
+    state.weight = weight
+
+    def run(stop: int):
+        # a 1-shot call at absolute shot index `shot`: pad the word so the Philox word matches
+        n = lane + 1
+        fmn = None if fm is None else np.repeat(fm, n, axis=0)
+        fon = None if fo is None else np.repeat(fo, n, axis=0)
+        if fon is not None:
+            fon[:lane] = -1
+        st, out, tb = dp.sample_host(n, seed=state.seed, shot0=base, flags=flags,
+                                     fault_modes=fmn, forced=fon, stop=stop, want_state=True, check=False)
+        if st not in (0,) and st > 0:
+            # errors of padding lanes are impossible (no forced outcomes there); ours raises
+            if out.error_bits()[lane]:
+                from .engine import raise_for_status
+
+                raise_for_status(st)
+        _copy_state(state, P, out, tb, lane, stop)
+        return out
+
+    if trace is None:
+        out = run(-1)
+    else:
+        instrs = getattr(prog, "instrs", None)
+        names = {v: k for k, v in OP_NAMES.items()}
+        out = None
+        for i in range(P.num_instrs):
+            out = run(i + 1)
+            ins = instrs[i] if instrs is not None else names[int(P.instrs[i, 0] & 0xFF)]
+            if not state.accepted:
+                break  # the halting post-select raises before its trace callback (runtime.py:749)
+            trace(state, ins)
+        if out is None:
+            out = run(-1)
+    return ShotRecord(measurements=out.measurements()[lane].copy(),
+                      detectors=out.detectors()[lane].copy(),
+                      observables=out.observables()[lane].copy(),
+                      accepted=bool(out.accepted_bits()[lane]), weight=weight)
+
+
+def _copy_state(state: ShotState, P: Program, out, tb, lane: int, stop: int) -> None:
+    state.frame_x[:] = tb.frame_x[lane, : P.n]
+    state.frame_z[:] = tb.frame_z[lane, : P.n]
+    state.gamma = complex(tb.gamma_c()[lane])
+    state.k = tb.k_stop
+    state.buf[: 1 << tb.k_stop] = tb.amps_c()[lane]
+    state.accepted = bool(out.accepted_bits()[lane])
+    state.draws = int(tb.draws[lane])
+    meas = out.measurements()[lane]
+    state.records[:] = 0
+    state.records[P.user_records] = meas
+    if P.num_detectors:
+        state.detectors[:] = out.detectors()[lane]
+    if P.num_observables:
+        state.observables[:] = out.observables()[lane]
