@@ -32,7 +32,9 @@
 #ifndef FS_SAMPLER_H
 #define FS_SAMPLER_H
 
+#ifndef __CUDACC_RTC__
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -49,7 +51,7 @@ enum fs_opcode {
   FS_OP_GAMMA_ROT = 3,    /* GammaRot             backend.py:137   w1=virt w5=fp(4) */
   FS_OP_ARRAY_ROT = 4,    /* ArrayRot             backend.py:145   w1=virt w2=axis w5=fp(4) w6=k */
   FS_OP_MEAS_DSTATIC = 5, /* MeasDormantStatic    backend.py:155   w1=virt w3=record, flip in w0 */
-  FS_OP_MEAS_DRANDOM = 6, /* MeasDormantRandom    backend.py:162   w1=virt w3=record, flip in w0 */
+  FS_OP_MEAS_DRANDOM = 6, /* MeasDormantRandom    backend.py:162   w1=virt w2=coin ordinal w3=record */
   FS_OP_MEAS_ACTIVE = 7,  /* MeasActive           backend.py:169   w1=virt w2=axis w3=record w6=k */
   FS_OP_MEAS_COLLAPSE = 8,/* MeasCollapse         backend.py:189   w1..w3,w6 as above, w4=pre_off<<8|pre_cnt w5=fp(8) */
   FS_OP_RETIRE = 9,       /* Retire               backend.py:178   w1=virt w2=axis w6=k */
@@ -106,6 +108,7 @@ typedef struct fs_prog_desc {
 #define FS_NO_RENORM    2u   /* renormalize=False (runtime.py:355-366, :389-404) */
 #define FS_FORCE_GENERAL 4u  /* testing: force the general per-shot-lane interpreter */
 #define FS_FORCE_HBM    8u   /* testing: force the large-k (HBM-resident array) engine */
+#define FS_NO_JIT       16u  /* testing: frame engine interpreter instead of the program-specialised kernel */
 
 /* trace mode: every random choice may be supplied (SURVEY §8(d) "trace mode") */
 typedef struct fs_trace_in {
@@ -139,6 +142,7 @@ typedef struct fs_sample_out {
 #define FS_ERR_SHOT_NAN 1        /* "NaN amplitude encountered at an active measurement" */
 #define FS_ERR_SHOT_FORCED 2     /* "forced outcome ... has probability ..." */
 
+#ifndef __CUDACC_RTC__ /* host entry points (not visible to NVRTC-compiled device code) */
 int fs_abi_version(void);
 const char* fs_last_error(void);
 
@@ -163,6 +167,7 @@ int fs_sample_host(fs_prog* prog, uint64_t seed, uint64_t shot0, uint64_t nshots
  * (runtime.py:857-865) */
 int fs_accumulate(fs_prog* prog, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t flags,
                   int64_t* counts, void* stream);
+#endif
 
 #ifdef __cplusplus
 }

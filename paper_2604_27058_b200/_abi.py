@@ -16,6 +16,7 @@ FS_RNG_SPLITMIX = 1
 FS_NO_RENORM = 2
 FS_FORCE_GENERAL = 4
 FS_FORCE_HBM = 8
+FS_NO_JIT = 16
 
 FS_OK = 0
 FS_ERR_ARG = -1

@@ -1,8 +1,19 @@
 // fs_device.cuh -- device-side program view, random streams and small helpers shared by the
 // sm_100a engines.  See DESIGN.md for the data layout and stream definitions.
 #pragma once
+#ifdef __CUDACC_RTC__  // NVRTC (program-specialised kernels, fs_jit.cuh): no host headers
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef unsigned long long uint64_t;
+typedef unsigned char uint8_t;
+typedef signed char int8_t;
+typedef short int16_t;
+typedef unsigned short uint16_t;
+typedef unsigned long long uintptr_t;
+#else
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 #include "../../include/fs_sampler.h"
 
@@ -77,6 +88,13 @@ __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, u
     k1 += 0xBB67AE85u;
   }
   return make_uint4(c0, c1, c2, c3);
+}
+
+// coin word of MeasDormantRandom number `ord` for 32-shot word `wabs`: 4 coin words per block
+__device__ __forceinline__ uint32_t coin_word(uint64_t seed, uint64_t wabs, int ord) {
+  const uint4 b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), (uint32_t)(ord >> 2), TAG_COIN << 24, seed);
+  const int j = ord & 3;
+  return j == 0 ? b.x : (j == 1 ? b.y : (j == 2 ? b.z : b.w));
 }
 
 __device__ __forceinline__ double u64_to_unit(uint64_t x) {

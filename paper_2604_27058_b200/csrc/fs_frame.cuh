@@ -98,7 +98,7 @@ frame_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
             }
           } else {
             const uint32_t pw = fz[virt * 32];
-            uint32_t coinw = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), (uint32_t)i, TAG_COIN << 24, A.seed).x;
+            uint32_t coinw = coin_word(A.seed, wabs, I0.z);
             if (TRACE && A.forced) {
               for (int j = 0; j < 32; j++) {
                 if (!((validmask >> j) & 1)) continue;

@@ -383,7 +383,7 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
           if (SPLITMIX) {
             coin = (fo >= 0) ? (fo ^ pbit ^ (int)(flipw & 1)) : (me ? rng.sm.bit() : 0);
           } else {
-            uint32_t cw = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), (uint32_t)i, TAG_COIN << 24, A.seed).x;
+            uint32_t cw = coin_word(A.seed, wabs, ins[2]);
             coin = (fo >= 0) ? (fo ^ pbit ^ (int)(flipw & 1)) : (int)((cw >> lane) & 1);
           }
           const uint32_t coinw = __ballot_sync(kFull, coin);

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(128) hbm_scalar_kernel(DevProg P, RunArgs A, H
         } else {
           const uint32_t pw = FZ(virt);
           uint32_t coinw = 0;
-          if (!SPLITMIX) coinw = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), (uint32_t)i, TAG_COIN << 24, A.seed).x;
+          if (!SPLITMIX) coinw = coin_word(A.seed, wabs, ins[2]);
           for (int j = 0; j < 32; j++) {
             if (!((validmask >> j) & 1)) continue;
             const int fo = A.forced ? A.forced[(si0 + j) * P.R + rec] : -1;

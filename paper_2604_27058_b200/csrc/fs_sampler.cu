@@ -16,6 +16,7 @@
 #include "fs_frame.cuh"
 #include "fs_general.cuh"
 #include "fs_hbm.cuh"
+#include "fs_jit.cuh"
 
 namespace {
 
@@ -67,9 +68,17 @@ struct fs_prog {
   size_t stage_bytes = 0;
   int64_t* d_counts = nullptr;
   size_t counts_len = 0;
-  // host copies used by the large-k engine's host-side walk
+  // host copies used by the large-k engine's host-side walk and the JIT generator
   std::vector<int32_t> h_instrs, h_sched;
   std::vector<double> h_fparams;
+  std::vector<uint32_t> h_gates, h_paulis;
+  std::vector<int32_t> h_reclists, h_record_out, h_bit_slot, h_plans, h_case_pauli_off, h_site_case_off;
+  // program-specialised frame kernel (fs_jit.cuh); built on first use
+  int jit_state = 0;  // 0 not tried, 1 ready, -1 failed (interpreter is used)
+  std::string jit_error;
+  fsjit::Compiled jit;
+  uint16_t* d_pslot = nullptr;
+  int jit_nslots = 0;
   // large-k engine state
   void* hbm = nullptr;
   size_t hbm_bytes = 0;
@@ -155,6 +164,14 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   p->h_instrs.assign(d->instrs, d->instrs + (size_t)FS_INS_WORDS * d->num_instrs);
   p->h_sched.assign(d->schedule, d->schedule + d->num_instrs);
   if (d->num_fparams) p->h_fparams.assign(d->fparams, d->fparams + d->num_fparams);
+  p->h_gates.assign(d->gates, d->gates + d->num_gates);
+  p->h_paulis.assign(d->paulis, d->paulis + d->num_paulis);
+  p->h_reclists.assign(d->reclists, d->reclists + d->num_reclists);
+  p->h_record_out.assign(d->record_out, d->record_out + R);
+  p->h_bit_slot.assign(d->bit_slot, d->bit_slot + R + D);
+  p->h_plans.assign(d->plans, d->plans + 2 * d->num_plans);
+  p->h_case_pauli_off.assign(d->case_pauli_off, d->case_pauli_off + d->num_cases + 1);
+  p->h_site_case_off.assign(d->site_case_off, d->site_case_off + E + 1);
   // pointers of the creator's arrays are not retained
   p->desc.instrs = nullptr;
   *out = p;
@@ -169,6 +186,8 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->stage);
   cudaFree(p->d_counts);
   cudaFree(p->hbm);
+  cudaFree(p->d_pslot);
+  if (p->jit.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->jit.mod);
   delete p;
 }
 
@@ -179,6 +198,35 @@ static bool wants_general(const fs_prog* p, uint32_t flags, const fs_trace_out* 
   if (flags & (FS_RNG_SPLITMIX | FS_FORCE_GENERAL)) return true;
   if (tout && (tout->gamma || tout->amps || tout->draws)) return true;
   return false;
+}
+
+// Diagnostics (not part of include/fs_sampler.h): source of the program-specialised frame kernel
+// and the state of its compilation.  Used by tests/test_host.py to compile the generated
+// kernel with NVRTC on a CPU-only host.
+extern "C" int fs_debug_jit_source(const fs_prog_desc* d, char* buf, size_t len) {
+  if (!d) return -1;
+  const int R = d->record_count, D = d->num_detectors, E = d->num_sites;
+  std::vector<int32_t> ins(d->instrs, d->instrs + (size_t)FS_INS_WORDS * d->num_instrs);
+  std::vector<uint32_t> g(d->gates, d->gates + d->num_gates), pa(d->paulis, d->paulis + d->num_paulis);
+  std::vector<int32_t> rl(d->reclists, d->reclists + d->num_reclists), ro(d->record_out, d->record_out + R);
+  std::vector<int32_t> bs(d->bit_slot, d->bit_slot + R + D), pl(d->plans, d->plans + 2 * d->num_plans);
+  std::vector<int32_t> cpo(d->case_pauli_off, d->case_pauli_off + d->num_cases + 1);
+  std::vector<int32_t> sco(d->site_case_off, d->site_case_off + E + 1);
+  fsjit::FrameKernelSource K = fsjit::gen_frame_kernel(*d, ins, g, pa, rl, ro, bs, pl, cpo, sco);
+  if (buf && len) {
+    size_t m = std::min(len - 1, K.src.size());
+    std::memcpy(buf, K.src.data(), m);
+    buf[m] = 0;
+  }
+  return (int)K.src.size();
+}
+
+extern "C" const char* fs_debug_jit_status(fs_prog* p) {
+  static thread_local std::string s;
+  if (!p) return "null";
+  s = p->jit_state == 1 ? "ready compile_bytes=" + std::to_string(p->jit.cubin_bytes)
+                        : (p->jit_state == 0 ? "not built" : "failed: " + p->jit_error);
+  return s.c_str();
 }
 
 extern "C" int fs_program_engine(const fs_prog* p, uint32_t flags) {
@@ -196,6 +244,30 @@ int occupancy_blocks(K kernel, int threads, size_t smem) {
   return std::max(nb, 1);
 }
 
+
+// ------------------------------------------------------------------ program-specialised kernel
+int ensure_jit(fs_prog* p) {
+  if (p->jit_state == 1) return FS_OK;
+  if (p->jit_state == -1) return set_error(FS_ERR_ARG, p->jit_error);
+  p->jit_state = -1;
+  fsjit::FrameKernelSource K = fsjit::gen_frame_kernel(p->desc, p->h_instrs, p->h_gates, p->h_paulis, p->h_reclists,
+                                                       p->h_record_out, p->h_bit_slot, p->h_plans,
+                                                       p->h_case_pauli_off, p->h_site_case_off);
+  const size_t smem = (size_t)4 * K.nslots * 32 * sizeof(uint32_t);
+  if (smem > kSmemBudget) { p->jit_error = "frame too large for the specialised kernel"; return FS_ERR_ARG; }
+  std::string err = fsjit::compile(K.src, fsjit::self_dir() + "/../csrc", p->jit);
+  if (!err.empty()) { p->jit_error = err; return set_error(FS_ERR_ARG, err); }
+  fsjit::Api& J = fsjit::api();
+  if (J.cuFuncSetAttribute(p->jit.fn, 8 /* MAX_DYNAMIC_SHARED_SIZE_BYTES */, (int)smem) != 0) {
+    p->jit_error = "cuFuncSetAttribute failed";
+    return FS_ERR_ARG;
+  }
+  FS_CUDA_TRY(cudaMalloc(&p->d_pslot, sizeof(uint16_t) * K.pslot.size()));
+  FS_CUDA_TRY(cudaMemcpy(p->d_pslot, K.pslot.data(), sizeof(uint16_t) * K.pslot.size(), cudaMemcpyHostToDevice));
+  p->jit_nslots = K.nslots;
+  p->jit_state = 1;
+  return FS_OK;
+}
 
 // ------------------------------------------------------------------ large-k engine driver
 int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
@@ -447,6 +519,24 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     a.prezeroed = 1;
   }
   const bool general = wants_general(p, flags, tout);
+  const bool trace_in = tin && (tin->fault_modes || tin->forced);
+  if (!general && !trace_in && !(tout && tout->frame_x) && !(flags & FS_NO_JIT) && a.stop == dp.num_instrs) {
+    int rc = ensure_jit(p);
+    if (rc == FS_OK) {
+      fsjit::Api& J = fsjit::api();
+      const size_t smem = (size_t)4 * p->jit_nslots * 32 * sizeof(uint32_t);
+      int occ = 1;
+      J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->jit.fn, 128, smem);
+      const size_t groups = (W + 127) / 128;
+      const size_t grid = std::min<size_t>(groups, (size_t)p->num_sms * std::max(occ, 1));
+      fs::DevProg dpv = dp;
+      const uint16_t* ps = p->d_pslot;
+      void* args[] = {&dpv, &a, &ps};
+      int r = J.cuLaunchKernel(p->jit.fn, (unsigned)grid, 1, 1, 128, 1, 1, (unsigned)smem, stream, args, nullptr);
+      if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_jit_frame) failed: " + std::to_string(r));
+      return FS_OK;
+    }
+  }
   if (!general) {
     const int words_per_warp = 2 * dp.n + dp.num_slots + dp.O;
     const size_t smem = (size_t)fs::kFrameWarps * words_per_warp * 32 * sizeof(uint32_t);

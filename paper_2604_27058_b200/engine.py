@@ -55,6 +55,13 @@ class DeviceProgram:
         except Exception:
             pass
 
+    def jit_status(self) -> str:
+        """State of the program-specialised frame kernel ("ready ...", "not built", "failed: ...")."""
+        f = self._lib.fs_debug_jit_status
+        f.restype = C.c_char_p
+        f.argtypes = [C.c_void_p]
+        return f(self._h).decode()
+
     def engine(self, flags: int = 0) -> str:
         return {0: "general", 1: "frame", 2: "hbm"}[self._lib.fs_program_engine(self._h, flags)]
 

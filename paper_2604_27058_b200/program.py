@@ -220,6 +220,7 @@ def serialize(prog, name: str = "", meta: dict | None = None) -> Program:
         return off
 
     sites = prog.sites
+    n_coins = 0
     for i, ins in enumerate(prog.instrs):
         kind = type(ins).__name__
         if kind not in OP_NAMES:
@@ -267,6 +268,9 @@ def serialize(prog, name: str = "", meta: dict | None = None) -> Program:
             w[0] |= int(ins.flip) << 8
             w[1] = int(ins.virt)
             w[3] = int(ins.record)
+            if op == OP_MEAS_DRANDOM:  # coin ordinal: 4 coin words per Philox block
+                w[2] = n_coins
+                n_coins += 1
             wrote(int(ins.record), i)
         elif op in (OP_MEAS_ACTIVE, OP_MEAS_COLLAPSE):
             w[0] |= int(ins.flip) << 8

@@ -15,7 +15,7 @@ import pytest
 
 import oracle
 from goldens import case_names, load, rel_err
-from paper_2604_27058_b200._abi import FS_FORCE_GENERAL, FS_FORCE_HBM, FS_RNG_PHILOX, FS_RNG_SPLITMIX
+from paper_2604_27058_b200._abi import FS_FORCE_GENERAL, FS_FORCE_HBM, FS_NO_JIT, FS_RNG_PHILOX, FS_RNG_SPLITMIX
 
 pytestmark = pytest.mark.gpu
 ALL = case_names()
@@ -152,3 +152,15 @@ def test_gpu_large_k_config3_philox_matches_oracle(cuda):
     _, gout, _ = dp.sample_host(2, seed=3, flags=FS_RNG_PHILOX)
     _, oout, _ = oracle.sample(P, 2, seed=3, flags=FS_RNG_PHILOX)
     _same(gout, oout)
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if load(c)["prog"].k_max == 0])
+def test_gpu_jit_equals_interpreter(cuda, name):
+    """Program-specialised frame kernel (NVRTC) == frame interpreter, bit for bit."""
+    P = load(name)["prog"]
+    dp = _dev(P)
+    n = 70_000
+    _, a, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX)
+    _, b, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX | FS_NO_JIT)
+    _same(a, b)
+    assert dp.jit_status().startswith("ready"), dp.jit_status()
