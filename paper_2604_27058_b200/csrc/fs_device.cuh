@@ -42,6 +42,12 @@ struct DevProg {
   const int* __restrict__ plans;
   const int* __restrict__ record_out;
   const int* __restrict__ bit_slot;
+  // Philox noise runs (host-computed): maximal runs of consecutive sites with equal 0<p<1
+  // (run_len > 0, run_lp = log1p(-p)) or a single certain site (run_len == 0)
+  int num_runs;
+  const int* __restrict__ run_start;
+  const int* __restrict__ run_len;
+  const double* __restrict__ run_lp;
 };
 
 struct RunArgs {

@@ -58,6 +58,8 @@ frame_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
     uint32_t alive = validmask, errmask = 0;
     int errcode = 0;
     for (int q = 0; q < nwords_smem; q++) base[q * 32] = 0;
+    FaultBuffer<kFaultCap> fbuf;
+    if (!(TRACE && A.fault_modes)) fbuf.init(P, A.seed, wabs);
     uint32_t dumped = 0;
     auto dump_frames = [&](uint32_t mask) {
       for (int j = 0; j < 32; j++) {
@@ -141,7 +143,13 @@ frame_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
               forced_faults_shot(P, fx, fz, 1u << j, ins, A.fault_modes + si * P.E, d, 32);
             }
           } else {
-            philox_noise_word(P, fx, fz, 32, A.seed, wabs, i, ins);
+            fbuf.apply_until(P, I0.z, [&](int c, int l) {
+              const int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
+              for (int j = off; j < end; j++) {
+                const uint32_t e = __ldg(P.paulis + j);
+                (FS_PAULI_Z(e) ? fz : fx)[FS_PAULI_Q(e) * 32] ^= 1u << l;
+              }
+            });
           }
           break;
         }

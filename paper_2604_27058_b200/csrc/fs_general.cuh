@@ -52,59 +52,93 @@ __device__ __forceinline__ void xor_case(const DevProg& P, uint32_t* fx, uint32_
   else xor_paulis<false>(P, fx, fz, off, end - off, bits);
 }
 
-// Word-level flattened hazard process (Philox stream): one Exp(1) jump per
-// realised fault over the concatenation of the 32 lanes' hazard intervals.  Called by one lane;
-// returns nothing, XORs every fault (lane l, site, case) into bit l of the frame words.
-// `stride` = 1 for a warp-owned word, 32 for the frame engine's lane-interleaved layout.
-__device__ void philox_noise_word(const DevProg& P, uint32_t* fx, uint32_t* fz, int stride, uint64_t seed,
-                                  uint64_t word, int instr, const int* ins) {
-  const double* S = P.cum_hazard;
+// Philox noise stream: one geometric-skip process per 32-shot word over the
+// whole program (runs of equal-probability sites, site-major (site, lane) cells), generated
+// lazily into a small per-thread buffer and consumed in site order by the NoiseBlocks.
+struct WordFaultGen {
   PhiloxStream ps;
-  ps.init(seed, word, (uint32_t)instr, TAG_NOISE);
-  const int plan_off = ins[3], plan_cnt = ins[4];
-  for (int pi = 0; pi < plan_cnt; pi++) {
-    int a = __ldg(P.plans + 2 * (plan_off + pi)), b = __ldg(P.plans + 2 * (plan_off + pi) + 1);
-    if (a < 0) {  // certain site (p = 1): every lane fires; cases drawn lane by lane
-      int site = b;
-      int nc = num_cases(P, site);
-      for (int l = 0; l < 32; l++) {
-        int c = __ldg(P.site_case_off + site);
-        if (nc > 1) c = pick_case(P, site, ps.uniform());
-        int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
-        for (int j = off; j < end; j++) {
-          uint32_t e = __ldg(P.paulis + j);
-          uint32_t* f = FS_PAULI_Z(e) ? fz : fx;
-          f[FS_PAULI_Q(e) * stride] ^= 1u << l;
+  int run;
+  int cl;    // next lane of a certain site
+  double c;  // current cell of a geometric run
+  __device__ __forceinline__ void init(uint64_t seed, uint64_t wabs) {
+    ps.init(seed, wabs, 0u, TAG_NOISE);
+    run = 0;
+    cl = 0;
+    c = -1.0;
+  }
+  // next fault (site, lane, absolute case id); false when the word has no more faults
+  __device__ __forceinline__ bool next(const DevProg& P, int& site, int& lane, int& cs) {
+    while (run < P.num_runs) {
+      const int start = __ldg(P.run_start + run), len = __ldg(P.run_len + run);
+      if (len == 0) {  // certain site: every lane fires, case drawn lane by lane
+        if (cl < 32) {
+          site = start;
+          lane = cl++;
+          cs = __ldg(P.site_case_off + site);
+          if (num_cases(P, site) > 1) cs = pick_case(P, site, ps.uniform());
+          return true;
         }
+        run++;
+        cl = 0;
+        continue;
       }
-      continue;
+      const double g = floor(__ddiv_rn(log1p(-ps.uniform()), __ldg(P.run_lp + run)));
+      c = __dadd_rn(__dadd_rn(c, 1.0), g);
+      if (c < (double)(32 * len)) {
+        const long long ci = (long long)c;
+        lane = (int)(ci & 31);
+        site = start + (int)(ci >> 5);
+        cs = __ldg(P.site_case_off + site);
+        if (num_cases(P, site) > 1) cs = pick_case(P, site, ps.uniform());
+        return true;
+      }
+      run++;
+      c = -1.0;
     }
-    const double Sa = __ldg(S + a);
-    const double H = __dsub_rn(__ldg(S + b), Sa);
-    if (!(H > 0.0)) continue;
-    const double total = __dmul_rn(32.0, H);
-    double t = 0.0;
-    for (;;) {
-      t = __dadd_rn(t, -log1p(-ps.uniform()));
-      if (!(t < total)) break;
-      int l = (int)__ddiv_rn(t, H);
-      if (l > 31) break;
-      double local = __dadd_rn(Sa, __dsub_rn(t, __dmul_rn((double)l, H)));
-      int idx = bisect_right(S, local, a + 1, b + 1);
-      if (idx > b) { t = __dmul_rn((double)(l + 1), H); continue; }
-      int site = idx - 1;
-      int c = __ldg(P.site_case_off + site);
-      if (num_cases(P, site) > 1) c = pick_case(P, site, ps.uniform());
-      int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
-      for (int j = off; j < end; j++) {
-        uint32_t e = __ldg(P.paulis + j);
-        uint32_t* f = FS_PAULI_Z(e) ? fz : fx;
-        f[FS_PAULI_Q(e) * stride] ^= 1u << l;
-      }
-      t = __dadd_rn(__dmul_rn((double)l, H), __dsub_rn(__ldg(S + site + 1), Sa));
+    return false;
+  }
+};
+
+template <int CAP>
+struct FaultBuffer {
+  WordFaultGen gen;
+  int cnt, cur;
+  bool more;
+  int fsite[CAP];
+  uint32_t fent[CAP];  // absolute case << 5 | lane
+  __device__ __forceinline__ void refill(const DevProg& P) {
+    cnt = 0;
+    cur = 0;
+    int site, lane, cs;
+    while (cnt < CAP) {
+      if (!gen.next(P, site, lane, cs)) { more = false; return; }
+      fsite[cnt] = site;
+      fent[cnt] = ((uint32_t)cs << 5) | (uint32_t)lane;
+      cnt++;
     }
   }
-}
+  __device__ __forceinline__ void init(const DevProg& P, uint64_t seed, uint64_t wabs) {
+    gen.init(seed, wabs);
+    more = true;
+    refill(P);
+  }
+  // apply (via fn(case, lane)) every buffered fault with site < hi
+  template <class Fn>
+  __device__ __forceinline__ void apply_until(const DevProg& P, int hi, Fn&& fn) {
+    for (;;) {
+      if (cur == cnt) {
+        if (!more) return;
+        refill(P);
+        if (cnt == 0) return;
+      }
+      if (fsite[cur] >= hi) return;
+      const uint32_t e = fent[cur++];
+      fn((int)(e >> 5), (int)(e & 31));
+    }
+  }
+};
+
+constexpr int kFaultCap = 48;
 
 // Reference hazard skipping for one shot (runtime.py:564-586 / :675-699), draw for draw.
 // Frame words are `stride` apart; `atomic` when several lanes share the words.
@@ -226,6 +260,8 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
     const int16_t* fmodes = A.fault_modes ? A.fault_modes + (valid ? si : 0) * (size_t)P.E : nullptr;
     const int8_t* forced = A.forced ? A.forced + (valid ? si : 0) * (size_t)P.R : nullptr;
     int branch = 0;
+    FaultBuffer<kFaultCap> fbuf;
+    if (!SPLITMIX && !fmodes && lane == 0) fbuf.init(P, A.seed, wabs);
     __syncwarp();
 
     // write one record word to its output column and/or slot
@@ -531,8 +567,14 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
             }
           } else if (SPLITMIX) {
             if (me) hazard_shot(P, fx, fz, lanebit, ins, rng.sm);
-          } else {
-            if (lane == 0) philox_noise_word(P, fx, fz, 1, A.seed, wabs, i, ins);
+          } else if (lane == 0) {
+            fbuf.apply_until(P, ins[2], [&](int c, int l) {
+              const int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
+              for (int j = off; j < end; j++) {
+                const uint32_t e = __ldg(P.paulis + j);
+                (FS_PAULI_Z(e) ? fz : fx)[FS_PAULI_Q(e)] ^= 1u << l;
+              }
+            });
           }
           __syncwarp();
           break;

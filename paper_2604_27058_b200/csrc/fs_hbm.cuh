@@ -326,7 +326,18 @@ __global__ void __launch_bounds__(128) hbm_scalar_kernel(DevProg P, RunArgs A, H
             }
           }
         } else {
-          philox_noise_word(P, fx, fz, (int)W, A.seed, wabs, i, ins);
+          // the word's fault generator state persists in HBM between launches: regenerate
+          // and skip the sites before this block (cheap: the HBM engine is array-bound)
+          FaultBuffer<kFaultCap> fb;
+          fb.init(P, A.seed, wabs);
+          fb.apply_until(P, ins[1], [&](int, int) {});
+          fb.apply_until(P, ins[2], [&](int c, int l) {
+            const int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
+            for (int jj = off; jj < end; jj++) {
+              const uint32_t e = __ldg(P.paulis + jj);
+              (FS_PAULI_Z(e) ? fz : fx)[(size_t)FS_PAULI_Q(e) * W] ^= 1u << l;
+            }
+          });
         }
         break;
       }

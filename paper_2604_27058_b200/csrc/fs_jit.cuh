@@ -141,6 +141,7 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   for (int s = 0; s < d.num_slots; s++) o << "    uint32_t r" << s << " = 0u;\n";
   for (int j = 0; j < d.num_observables; j++) o << "    uint32_t ob" << j << " = 0u;\n";
   o << "    uint4 cb = make_uint4(0u, 0u, 0u, 0u);\n";
+  o << "    fs::FaultBuffer<fs::kFaultCap> fbuf;\n    fbuf.init(P, seed, wabs);\n";
   auto put_record = [&](int rec, const std::string& expr) {
     const int col = record_out[rec], sl = bit_slot[rec];
     o << "    { const uint32_t rw = " << expr << ";";
@@ -213,7 +214,7 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
               const int q = FS_PAULI_Q(e);
               K.pslot[j] = (uint16_t)(FS_PAULI_Z(e) ? Z(q) : X(q));
             }
-        o << "    fs::jit_noise_block(P, F, pslot, seed, wabs, " << i << ", " << I[3] << ", " << I[4] << ");\n";
+        o << "    fs::jit_noise_block(P, F, pslot, fbuf, " << I[2] << ");\n";
         break;
       }
       case FS_OP_DETECTOR:

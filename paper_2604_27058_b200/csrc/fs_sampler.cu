@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -129,6 +130,30 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   size_t o_pl = add(d->plans, sizeof(int32_t) * 2 * d->num_plans);
   size_t o_ro = add(d->record_out, sizeof(int32_t) * R);
   size_t o_bs = add(d->bit_slot, sizeof(int32_t) * (R + D));
+  // Philox noise runs: maximal runs of consecutive sites with equal 0<p<1,
+  // single certain sites (p >= 1); p = 0 / caseless sites never fire
+  std::vector<int32_t> run_start, run_len;
+  std::vector<double> run_lp;
+  for (int site = 0; site < E;) {
+    const double prob = d->site_prob[site];
+    const int nc = d->site_case_off[site + 1] - d->site_case_off[site];
+    if (!(prob > 0.0) || nc == 0) { site++; continue; }
+    if (prob >= 1.0) {
+      run_start.push_back(site); run_len.push_back(0); run_lp.push_back(0.0);
+      site++;
+      continue;
+    }
+    int len = 1;
+    while (site + len < E && d->site_prob[site + len] == prob &&
+           d->site_case_off[site + len + 1] - d->site_case_off[site + len] > 0)
+      len++;
+    run_start.push_back(site); run_len.push_back(len); run_lp.push_back(log1p(-prob));
+    site += len;
+  }
+  const int nruns = (int)run_start.size();
+  size_t o_rs = add(run_start.data(), sizeof(int32_t) * nruns);
+  size_t o_rl2 = add(run_len.data(), sizeof(int32_t) * nruns);
+  size_t o_rlp = add(run_lp.data(), sizeof(double) * nruns);
   std::vector<unsigned char> host(total, 0);
   for (auto& s : secs)
     if (s.src && s.bytes) std::memcpy(host.data() + s.off, s.src, s.bytes);
@@ -161,6 +186,10 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   dp.plans = reinterpret_cast<const int*>(b + o_pl);
   dp.record_out = reinterpret_cast<const int*>(b + o_ro);
   dp.bit_slot = reinterpret_cast<const int*>(b + o_bs);
+  dp.num_runs = nruns;
+  dp.run_start = reinterpret_cast<const int*>(b + o_rs);
+  dp.run_len = reinterpret_cast<const int*>(b + o_rl2);
+  dp.run_lp = reinterpret_cast<const double*>(b + o_rlp);
   p->h_instrs.assign(d->instrs, d->instrs + (size_t)FS_INS_WORDS * d->num_instrs);
   p->h_sched.assign(d->schedule, d->schedule + d->num_instrs);
   if (d->num_fparams) p->h_fparams.assign(d->fparams, d->fparams + d->num_fparams);

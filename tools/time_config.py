@@ -4,7 +4,7 @@ sys.path.insert(0, '.')
 import torch
 from paper_2604_27058_b200.program import Program
 from paper_2604_27058_b200.engine import DeviceProgram
-cfg = int(sys.argv[1]); shots = int(sys.argv[2]) if len(sys.argv) > 2 else None; steps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+cfg = int(sys.argv[1]); shots = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] else None; steps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 from paper_2604_27058_b200.configs import CONFIGS
 shots = shots or CONFIGS[cfg]['shots']
 P = Program.load(f'paper_2604_27058_b200/programs/c{cfg}.npz')
