@@ -43,11 +43,12 @@ struct DevProg {
   const int* __restrict__ record_out;
   const int* __restrict__ bit_slot;
   // Philox noise runs (host-computed): maximal runs of consecutive sites with equal 0<p<1
-  // (run_len > 0, run_lp = log1p(-p)) or a single certain site (run_len == 0)
+  // (run_len > 0, run_lp = 1/log1p(-q)) or a single certain site (run_len == 0)
   int num_runs;
   const int* __restrict__ run_start;
   const int* __restrict__ run_len;
   const double* __restrict__ run_lp;
+  const double* __restrict__ site_acc;  // p_site / q of its run (thinning), 1.0 when equal
 };
 
 struct RunArgs {

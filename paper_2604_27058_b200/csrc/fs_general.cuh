@@ -56,46 +56,45 @@ __device__ __forceinline__ void xor_case(const DevProg& P, uint32_t* fx, uint32_
 // whole program (runs of equal-probability sites, site-major (site, lane) cells), generated
 // lazily into a small per-thread buffer and consumed in site order by the NoiseBlocks.
 struct WordFaultGen {
-  PhiloxStream ps;
+  uint64_t seed, wabs;
+  uint32_t step_no;
   int run;
   int cl;    // next lane of a certain site
   double c;  // current cell of a geometric run
-  __device__ __forceinline__ void init(uint64_t seed, uint64_t wabs) {
-    ps.init(seed, wabs, 0u, TAG_NOISE);
+  __device__ __forceinline__ void init(uint64_t s, uint64_t w) {
+    seed = s;
+    wabs = w;
+    step_no = 0;
     run = 0;
     cl = 0;
     c = -1.0;
   }
-  // next fault (site, lane, absolute case id); false when the word has no more faults
-  __device__ __forceinline__ bool next(const DevProg& P, int& site, int& lane, int& cs) {
-    while (run < P.num_runs) {
-      const int start = __ldg(P.run_start + run), len = __ldg(P.run_len + run);
-      if (len == 0) {  // certain site: every lane fires, case drawn lane by lane
-        if (cl < 32) {
-          site = start;
-          lane = cl++;
-          cs = __ldg(P.site_case_off + site);
-          if (num_cases(P, site) > 1) cs = pick_case(P, site, ps.uniform());
-          return true;
-        }
-        run++;
-        cl = 0;
-        continue;
-      }
-      const double g = floor(__ddiv_rn(log1p(-ps.uniform()), __ldg(P.run_lp + run)));
-      c = __dadd_rn(__dadd_rn(c, 1.0), g);
-      if (c < (double)(32 * len)) {
-        const long long ci = (long long)c;
-        lane = (int)(ci & 31);
-        site = start + (int)(ci >> 5);
-        cs = __ldg(P.site_case_off + site);
-        if (num_cases(P, site) > 1) cs = pick_case(P, site, ps.uniform());
-        return true;
-      }
-      run++;
-      c = -1.0;
+  // One step = one Philox block: 0 nothing emitted, 1 fault (site, lane, case), 2 exhausted.
+  __device__ __forceinline__ int step(const DevProg& P, int& site, int& lane, int& cs) {
+    if (run >= P.num_runs) return 2;
+    const int start = __ldg(P.run_start + run), len = __ldg(P.run_len + run);
+    const uint4 b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), 0u, (TAG_NOISE << 24) | step_no++, seed);
+    const double u2 = u64_to_unit(((uint64_t)b.w << 32) | b.z);
+    if (len == 0) {  // certain site: lane cl fires
+      site = start;
+      lane = cl++;
+      if (cl == 32) { run++; cl = 0; }
+      cs = __ldg(P.site_case_off + site);
+      if (num_cases(P, site) > 1) cs = pick_case(P, site, u2);
+      return 1;
     }
-    return false;
+    const double u1 = u64_to_unit(((uint64_t)b.y << 32) | b.x);
+    const double g = floor(__dmul_rn(log1p(-u1), __ldg(P.run_lp + run)));
+    c = __dadd_rn(__dadd_rn(c, 1.0), g);
+    if (!(c < (double)(32 * len))) { run++; c = -1.0; return 0; }
+    const long long ci = (long long)c;
+    lane = (int)(ci & 31);
+    site = start + (int)(ci >> 5);
+    const double acc = __ldg(P.site_acc + site);
+    if (!(u2 < acc)) return 0;  // thinning: p_site < q
+    cs = __ldg(P.site_case_off + site);
+    if (num_cases(P, site) > 1) cs = pick_case(P, site, acc < 1.0 ? __ddiv_rn(u2, acc) : u2);
+    return 1;
   }
 };
 
@@ -109,12 +108,15 @@ struct FaultBuffer {
   __device__ __forceinline__ void refill(const DevProg& P) {
     cnt = 0;
     cur = 0;
-    int site, lane, cs;
-    while (cnt < CAP) {
-      if (!gen.next(P, site, lane, cs)) { more = false; return; }
-      fsite[cnt] = site;
-      fent[cnt] = ((uint32_t)cs << 5) | (uint32_t)lane;
-      cnt++;
+    int site = 0, lane = 0, cs = 0;
+    for (;;) {  // one Philox block per iteration: keeps the lanes of a warp in lock step
+      const int r = gen.step(P, site, lane, cs);
+      if (r == 2) { more = false; return; }
+      if (r == 1) {
+        fsite[cnt] = site;
+        fent[cnt] = ((uint32_t)cs << 5) | (uint32_t)lane;
+        if (++cnt == CAP) return;
+      }
     }
   }
   __device__ __forceinline__ void init(const DevProg& P, uint64_t seed, uint64_t wabs) {

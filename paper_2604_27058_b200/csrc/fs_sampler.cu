@@ -130,10 +130,11 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   size_t o_pl = add(d->plans, sizeof(int32_t) * 2 * d->num_plans);
   size_t o_ro = add(d->record_out, sizeof(int32_t) * R);
   size_t o_bs = add(d->bit_slot, sizeof(int32_t) * (R + D));
-  // Philox noise runs: maximal runs of consecutive sites with equal 0<p<1,
-  // single certain sites (p >= 1); p = 0 / caseless sites never fire
+  // Philox noise runs: consecutive sites whose probabilities agree to 1e-9
+  // (relative) share one geometric process at q = max p, thinned by p/q per candidate; certain
+  // sites (p >= 1) are single runs; p = 0 / caseless sites never fire
   std::vector<int32_t> run_start, run_len;
-  std::vector<double> run_lp;
+  std::vector<double> run_lp, site_acc(E > 0 ? E : 1, 1.0);
   for (int site = 0; site < E;) {
     const double prob = d->site_prob[site];
     const int nc = d->site_case_off[site + 1] - d->site_case_off[site];
@@ -144,16 +145,23 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
       continue;
     }
     int len = 1;
-    while (site + len < E && d->site_prob[site + len] == prob &&
-           d->site_case_off[site + len + 1] - d->site_case_off[site + len] > 0)
-      len++;
-    run_start.push_back(site); run_len.push_back(len); run_lp.push_back(log1p(-prob));
+    double lo = prob, hi = prob;
+    while (site + len < E) {
+      const double pn = d->site_prob[site + len];
+      if (!(pn > 0.0) || pn >= 1.0 || d->site_case_off[site + len + 1] - d->site_case_off[site + len] == 0) break;
+      const double nlo = std::min(pn, lo), nhi = std::max(pn, hi);
+      if (!(nhi <= nlo * (1.0 + 1e-9))) break;
+      lo = nlo; hi = nhi; len++;
+    }
+    for (int t = site; t < site + len; t++) site_acc[t] = d->site_prob[t] / hi;
+    run_start.push_back(site); run_len.push_back(len); run_lp.push_back(1.0 / log1p(-hi));
     site += len;
   }
   const int nruns = (int)run_start.size();
   size_t o_rs = add(run_start.data(), sizeof(int32_t) * nruns);
   size_t o_rl2 = add(run_len.data(), sizeof(int32_t) * nruns);
   size_t o_rlp = add(run_lp.data(), sizeof(double) * nruns);
+  size_t o_sacc = add(site_acc.data(), sizeof(double) * site_acc.size());
   std::vector<unsigned char> host(total, 0);
   for (auto& s : secs)
     if (s.src && s.bytes) std::memcpy(host.data() + s.off, s.src, s.bytes);
@@ -190,6 +198,7 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   dp.run_start = reinterpret_cast<const int*>(b + o_rs);
   dp.run_len = reinterpret_cast<const int*>(b + o_rl2);
   dp.run_lp = reinterpret_cast<const double*>(b + o_rlp);
+  dp.site_acc = reinterpret_cast<const double*>(b + o_sacc);
   p->h_instrs.assign(d->instrs, d->instrs + (size_t)FS_INS_WORDS * d->num_instrs);
   p->h_sched.assign(d->schedule, d->schedule + d->num_instrs);
   if (d->num_fparams) p->h_fparams.assign(d->fparams, d->fparams + d->num_fparams);
