@@ -14,6 +14,8 @@
 #pragma once
 #include <dlfcn.h>
 
+#include <cstdlib>
+
 #include <sstream>
 #include <string>
 #include <vector>
@@ -125,7 +127,8 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   };
   const int R = d.record_count;
   o << "#include \"fs_jit_kernels.cuh\"\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(128) fs_jit_frame(fs::DevProg P, fs::RunArgs A, "
+  const char* mb = getenv("FS_JIT_MINBLOCKS");
+  o << "extern \"C\" __global__ void __launch_bounds__(128, " << (mb ? atoi(mb) : 2) << ") fs_jit_frame(fs::DevProg P, fs::RunArgs A, "
        "const uint16_t* __restrict__ pslot) {\n";
   o << "  extern __shared__ uint32_t smem[];\n";
   o << "  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;\n";
