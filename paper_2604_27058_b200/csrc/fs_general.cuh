@@ -215,9 +215,35 @@ struct ShotDraws {
   __device__ __forceinline__ double uniform() { return splitmix ? sm.uniform() : ph.uniform(); }
 };
 
-template <bool SPLITMIX, bool ARR_SMEM>
+// Segmented mode (programs with PostSelect): the program is cut after every PostSelect; each
+// segment runs over the list of shots still alive, 32 per warp (lanes carry arbitrary shot
+// ids), and the survivors' state is compacted into a store for the next segment.
+struct StateStore {
+  uint32_t* frame;    // [slot][nfw]  packed x bits (q) then z bits (n+q)
+  uint32_t* slotbits; // [slot][nsw]
+  uint32_t* obsbits;  // [slot][now]
+  double2* gamma;     // [slot]
+  uint32_t* smcount;  // [slot]
+  uint32_t* gen_i;    // [slot][6]: step_no, run, cl, pend_site, pend_lane, pend_case
+  double* gen_c;      // [slot]
+  double2* amps;      // [slot/32][cap][32]
+  uint32_t* shot;     // [slot] shot index within the call
+};
+
+struct SegArgs {
+  int seg_begin, seg_end;  // instruction range of this segment
+  int first, last;         // initialise / finalise
+  uint32_t n_in;
+  uint64_t chunk0;         // first shot (within the call) of the chunk (identity list)
+  uint32_t* n_out;         // survivors counter
+  StateStore in, out;
+  int k_in, k_out;         // active dimension at the segment boundaries
+  int nfw, nsw, now;
+};
+
+template <bool SPLITMIX, bool ARR_SMEM, bool SEG>
 __global__ void __launch_bounds__(kGenWarps * 32)
-general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
+general_kernel(DevProg P, RunArgs A, int smem_words_per_warp, SegArgs S) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -241,12 +267,26 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
   const bool renorm = !(A.flags & FS_NO_RENORM);
   const uint64_t word0 = A.shot0 >> 5;
   const int stop = A.stop;
+  const int i_begin = SEG ? S.seg_begin : 0;
+  const int i_end = SEG ? S.seg_end : stop;
+  const uint32_t nunits = SEG ? (S.n_in + 31) / 32 : A.W;
 
-  for (uint32_t w = blockIdx.x * kGenWarps + wib; w < A.W; w += gridDim.x * kGenWarps) {
-    const uint64_t si = (uint64_t)w * 32 + lane;  // shot index within the call
-    const bool valid = si < A.nshots;
+  for (uint32_t w = blockIdx.x * kGenWarps + wib; w < nunits; w += gridDim.x * kGenWarps) {
+    const uint32_t idx = w * 32 + lane;  // SEG: input slot of this lane
+    uint64_t si;                          // shot index within the call
+    bool valid;
+    if (SEG) {
+      valid = idx < S.n_in;
+      si = S.first ? S.chunk0 + idx : (valid ? S.in.shot[idx] : 0);
+      valid = valid && si < A.nshots;
+    } else {
+      si = (uint64_t)w * 32 + lane;
+      valid = si < A.nshots;
+    }
     const uint64_t shot = A.shot0 + si;
-    const uint64_t wabs = word0 + w;
+    const uint64_t wabs = SEG ? (shot >> 5) : word0 + w;  // SEG: the lane's own 32-shot word
+    const uint32_t wout = SEG ? (uint32_t)((S.chunk0 >> 5) + w) : w;  // output word (aligned)
+    const bool aligned = !SEG || S.first;  // lanes == consecutive shots of one output word
     const uint32_t validmask = __ballot_sync(kFull, valid);
     uint32_t alive = validmask;
     uint32_t errmask = 0;
@@ -263,15 +303,62 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
     const int8_t* forced = A.forced ? A.forced + (valid ? si : 0) * (size_t)P.R : nullptr;
     int branch = 0;
     FaultBuffer<kFaultCap> fbuf;
-    if (!SPLITMIX && !fmodes && lane == 0) fbuf.init(P, A.seed, wabs);
+    if (!SEG && !SPLITMIX && !fmodes && lane == 0) fbuf.init(P, A.seed, wabs);
+    // SEG + Philox: every lane runs its own word's generator lazily, keeping one pending fault
+    WordFaultGen lgen;
+    int pend_site = -1, pend_lane = 0, pend_case = 0;
+    if (SEG && !SPLITMIX) lgen.init(A.seed, wabs);
     __syncwarp();
+    if (SEG && !S.first) {  // restore the survivor state saved by the previous segment
+      const StateStore& I = S.in;
+      for (int b = 0; b < 2 * P.n; b++) {
+        const int bit = valid ? (int)((I.frame[(size_t)idx * S.nfw + (b >> 5)] >> (b & 31)) & 1) : 0;
+        const uint32_t wv = __ballot_sync(kFull, bit);
+        if (lane == 0) { if (b < P.n) fx[b] = wv; else fz[b - P.n] = wv; }
+      }
+      for (int b = 0; b < P.num_slots; b++) {
+        const int bit = valid ? (int)((I.slotbits[(size_t)idx * S.nsw + (b >> 5)] >> (b & 31)) & 1) : 0;
+        const uint32_t wv = __ballot_sync(kFull, bit);
+        if (lane == 0) slots[b] = wv;
+      }
+      for (int b = 0; b < P.O; b++) {
+        const int bit = valid ? (int)((I.obsbits[(size_t)idx * S.now + (b >> 5)] >> (b & 31)) & 1) : 0;
+        const uint32_t wv = __ballot_sync(kFull, bit);
+        if (lane == 0) obsw[b] = wv;
+      }
+      if (valid) {
+        gamma = I.gamma[idx];
+        if (SPLITMIX) rng.sm.count = I.smcount[idx];
+        else {
+          lgen.step_no = I.gen_i[(size_t)idx * 6];
+          lgen.run = (int)I.gen_i[(size_t)idx * 6 + 1];
+          lgen.cl = (int)I.gen_i[(size_t)idx * 6 + 2];
+          pend_site = (int)I.gen_i[(size_t)idx * 6 + 3];
+          pend_lane = (int)I.gen_i[(size_t)idx * 6 + 4];
+          pend_case = (int)I.gen_i[(size_t)idx * 6 + 5];
+          lgen.c = I.gen_c[idx];
+        }
+        const uint32_t sz = 1u << S.k_in;
+        const double2* src = I.amps + (size_t)(idx >> 5) * ((size_t)sz * 32) + (idx & 31);
+        for (uint32_t j = 0; j < sz; j++) AMP(j) = src[(size_t)j * 32];
+      }
+      __syncwarp();
+    }
 
     // write one record word to its output column and/or slot
+    // one output bit row: whole word when the lanes are one output word, else per-lane bits
+    auto put_out = [&](uint32_t* row, uint32_t word) {
+      if (aligned) {
+        if (lane == 0) row[wout] = word & alive;
+      } else if (((word & alive) >> lane) & 1) {
+        atomicOr(row + (si >> 5), 1u << (si & 31));
+      }
+    };
     auto put_record = [&](int r, uint32_t word) {
+      const int col = __ldg(P.record_out + r);
+      if (col >= 0) put_out(A.meas + (size_t)col * A.W, word);
       if (lane == 0) {
-        int col = __ldg(P.record_out + r);
-        if (col >= 0) A.meas[(size_t)col * A.W + w] = word & alive;
-        int sl = __ldg(P.bit_slot + r);
+        const int sl = __ldg(P.bit_slot + r);
         if (sl >= 0) slots[sl] = word;
       }
     };
@@ -308,7 +395,7 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
       }
     };
 
-    for (int i = 0; i < stop; i++) {
+    for (int i = i_begin; i < i_end; i++) {
       if (alive == 0 && A.prezeroed) break;
       const int4 I0 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i);
       const int4 I1 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i + 1);
@@ -421,8 +508,9 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
           if (SPLITMIX) {
             coin = (fo >= 0) ? (fo ^ pbit ^ (int)(flipw & 1)) : (me ? rng.sm.bit() : 0);
           } else {
-            uint32_t cw = coin_word(A.seed, wabs, ins[2]);
-            coin = (fo >= 0) ? (fo ^ pbit ^ (int)(flipw & 1)) : (int)((cw >> lane) & 1);
+            const uint32_t cw = coin_word(A.seed, wabs, ins[2]);
+            const int cbit = SEG ? (int)(shot & 31) : lane;
+            coin = (fo >= 0) ? (fo ^ pbit ^ (int)(flipw & 1)) : (int)((cw >> cbit) & 1);
           }
           const uint32_t coinw = __ballot_sync(kFull, coin);
           __syncwarp();
@@ -569,6 +657,22 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
             }
           } else if (SPLITMIX) {
             if (me) hazard_shot(P, fx, fz, lanebit, ins, rng.sm);
+          } else if (SEG) {
+            if (me) {  // own word's generator; keep only this shot's faults
+              const int hi = ins[2], mylane = (int)(shot & 31);
+              for (;;) {
+                if (pend_site < 0) {
+                  int st_, ln_, cs_;
+                  const int r = lgen.step(P, st_, ln_, cs_);
+                  if (r == 2) { pend_site = 0x7FFFFFFF; break; }
+                  if (r == 0) continue;
+                  pend_site = st_; pend_lane = ln_; pend_case = cs_;
+                }
+                if (pend_site >= hi) break;
+                if (pend_lane == mylane) xor_case_strided(P, fx, fz, pend_case, lanebit, 1, true);
+                pend_site = -1;
+              }
+            }
           } else if (lane == 0) {
             fbuf.apply_until(P, ins[2], [&](int c, int l) {
               const int off = __ldg(P.case_pauli_off + c), end = __ldg(P.case_pauli_off + c + 1);
@@ -583,16 +687,17 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
         }
         case FS_OP_DETECTOR:
         case FS_OP_OBSERVABLE: {
-          if (lane == 0) {
-            uint32_t wv = 0;
-            for (int j = 0; j < ins[3]; j++) wv ^= slots[__ldg(P.bit_slot + __ldg(P.reclists + ins[2] + j))];
-            if (op == FS_OP_DETECTOR) {
-              A.det[(size_t)ins[1] * A.W + w] = wv & alive;
-              int sl = __ldg(P.bit_slot + P.R + ins[1]);
+          uint32_t wv = 0;
+          for (int j = 0; j < ins[3]; j++) wv ^= slots[__ldg(P.bit_slot + __ldg(P.reclists + ins[2] + j))];
+          __syncwarp();
+          if (op == FS_OP_DETECTOR) {
+            put_out(A.det + (size_t)ins[1] * A.W, wv);
+            if (lane == 0) {
+              const int sl = __ldg(P.bit_slot + P.R + ins[1]);
               if (sl >= 0) slots[sl] = wv;
-            } else {
-              obsw[ins[1]] ^= wv & alive;
             }
+          } else if (lane == 0) {
+            obsw[ins[1]] ^= wv & alive;
           }
           __syncwarp();
           break;
@@ -612,13 +717,63 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp) {
       }
     }
     __syncwarp();
-    if (lane == 0) {
-      for (int o = 0; o < P.O; o++) A.obs[(size_t)o * A.W + w] = obsw[o] & validmask;
-      A.accepted[w] = alive & validmask;
-      A.error[w] = errmask;
-      if (errmask) atomicMax(A.status, errcode);
+    if (!SEG) {
+      if (lane == 0) {
+        for (int o = 0; o < P.O; o++) A.obs[(size_t)o * A.W + w] = obsw[o] & validmask;
+        A.accepted[w] = alive & validmask;
+        A.error[w] = errmask;
+        if (errmask) atomicMax(A.status, errcode);
+      }
+      dump_trace(validmask & ~dumped, stop);
+    } else {
+      // shots that ended in this segment (halted, errored, or the program finished)
+      const uint32_t ended = S.last ? validmask : (validmask & ~alive);
+      if ((ended >> lane) & 1) {
+        for (int o = 0; o < P.O; o++)
+          if ((obsw[o] >> lane) & 1) atomicOr(A.obs + (size_t)o * A.W + (si >> 5), 1u << (si & 31));
+        if ((alive >> lane) & 1) atomicOr(A.accepted + (si >> 5), 1u << (si & 31));
+        if ((errmask >> lane) & 1) atomicOr(A.error + (si >> 5), 1u << (si & 31));
+      }
+      if (lane == 0 && errmask) atomicMax(A.status, errcode);
+      if (!S.last) {  // compact the survivors into the output store
+        const uint32_t surv = alive & validmask;
+        uint32_t base = 0;
+        if (lane == 0 && surv) base = atomicAdd(S.n_out, (uint32_t)__popc(surv));
+        base = __shfl_sync(kFull, base, 0);
+        if ((surv >> lane) & 1) {
+          const uint32_t slot = base + __popc(surv & ((1u << lane) - 1u));
+          const StateStore& O = S.out;
+          O.shot[slot] = (uint32_t)si;
+          for (int j = 0; j < S.nfw; j++) {
+            uint32_t v = 0;
+            for (int b = 32 * j; b < 32 * j + 32 && b < 2 * P.n; b++)
+              v |= (((b < P.n ? fx[b] : fz[b - P.n]) >> lane) & 1u) << (b & 31);
+            O.frame[(size_t)slot * S.nfw + j] = v;
+          }
+          for (int j = 0; j < S.nsw; j++) {
+            uint32_t v = 0;
+            for (int b = 32 * j; b < 32 * j + 32 && b < P.num_slots; b++) v |= ((slots[b] >> lane) & 1u) << (b & 31);
+            O.slotbits[(size_t)slot * S.nsw + j] = v;
+          }
+          for (int j = 0; j < S.now; j++) {
+            uint32_t v = 0;
+            for (int b = 32 * j; b < 32 * j + 32 && b < P.O; b++) v |= ((obsw[b] >> lane) & 1u) << (b & 31);
+            O.obsbits[(size_t)slot * S.now + j] = v;
+          }
+          O.gamma[slot] = gamma;
+          if (SPLITMIX) O.smcount[slot] = rng.sm.count;
+          else {
+            uint32_t* gi = O.gen_i + (size_t)slot * 6;
+            gi[0] = lgen.step_no; gi[1] = (uint32_t)lgen.run; gi[2] = (uint32_t)lgen.cl;
+            gi[3] = (uint32_t)pend_site; gi[4] = (uint32_t)pend_lane; gi[5] = (uint32_t)pend_case;
+            O.gen_c[slot] = lgen.c;
+          }
+          const uint32_t sz = 1u << S.k_out;
+          double2* dst = O.amps + (size_t)(slot >> 5) * ((size_t)sz * 32) + (slot & 31);
+          for (uint32_t j = 0; j < sz; j++) dst[(size_t)j * 32] = AMP(j);
+        }
+      }
     }
-    dump_trace(validmask & ~dumped, stop);
     __syncwarp();
   }
 #undef AMP

@@ -80,6 +80,9 @@ struct fs_prog {
   fsjit::Compiled jit;
   uint16_t* d_pslot = nullptr;
   int jit_nslots = 0;
+  // segmented general engine: ping-pong survivor state stores
+  void* seg_pool[2] = {nullptr, nullptr};
+  size_t seg_bytes[2] = {0, 0};
   // large-k engine state
   void* hbm = nullptr;
   size_t hbm_bytes = 0;
@@ -224,6 +227,8 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->stage);
   cudaFree(p->d_counts);
   cudaFree(p->hbm);
+  cudaFree(p->seg_pool[0]);
+  cudaFree(p->seg_pool[1]);
   cudaFree(p->d_pslot);
   if (p->jit.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->jit.mod);
   delete p;
@@ -304,6 +309,147 @@ int ensure_jit(fs_prog* p) {
   FS_CUDA_TRY(cudaMemcpy(p->d_pslot, K.pslot.data(), sizeof(uint16_t) * K.pslot.size(), cudaMemcpyHostToDevice));
   p->jit_nslots = K.nslots;
   p->jit_state = 1;
+  return FS_OK;
+}
+
+
+// one general-engine launch (array capacity 2^karr per lane; `units` = 32-shot groups)
+int launch_general_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, bool seg, int karr, size_t units,
+                          cudaStream_t stream) {
+  const fs::DevProg& dp = p->dp;
+  const bool splitmix = a.flags & FS_RNG_SPLITMIX;
+  const int words_per_warp = (int)align_up(2 * dp.n + dp.num_slots + dp.O, 4);
+  const size_t words_bytes = (size_t)fs::kGenWarps * words_per_warp * 4;
+  const size_t arr_bytes_warp = ((size_t)32 << karr) * sizeof(double2);
+  const bool arr_smem = words_bytes + 16 + fs::kGenWarps * arr_bytes_warp <= kSmemBudget;
+  const size_t smem = words_bytes + (arr_smem ? 16 + fs::kGenWarps * arr_bytes_warp : 0);
+  if (words_bytes > kSmemBudget) return set_error(FS_ERR_ARG, "program too large for the general engine");
+  void (*kern)(fs::DevProg, fs::RunArgs, int, fs::SegArgs);
+#define FS_PICK(SM, AS, SG) kern = fs::general_kernel<SM, AS, SG>
+  if (seg) {
+    if (splitmix) { if (arr_smem) FS_PICK(true, true, true); else FS_PICK(true, false, true); }
+    else { if (arr_smem) FS_PICK(false, true, true); else FS_PICK(false, false, true); }
+  } else {
+    if (splitmix) { if (arr_smem) FS_PICK(true, true, false); else FS_PICK(true, false, false); }
+    else { if (arr_smem) FS_PICK(false, true, false); else FS_PICK(false, false, false); }
+  }
+#undef FS_PICK
+  FS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int threads = fs::kGenWarps * 32;
+  const size_t blocks_needed = std::max<size_t>(1, (units + fs::kGenWarps - 1) / fs::kGenWarps);
+  const int occ = occupancy_blocks(kern, threads, smem);
+  size_t grid = std::min<size_t>(blocks_needed, (size_t)p->num_sms * occ);
+  a.arr_log2 = karr;
+  if (!arr_smem) {
+    // HBM slab per resident warp; cap the footprint at ~48 GiB
+    const size_t per_block = fs::kGenWarps * arr_bytes_warp;
+    const size_t cap_blocks = std::max<size_t>(1, ((size_t)48 << 30) / per_block);
+    grid = std::min(grid, cap_blocks);
+    const size_t need = grid * per_block;
+    if (need > p->scratch_bytes) {
+      cudaFree(p->scratch);
+      p->scratch = nullptr;
+      p->scratch_bytes = 0;
+      FS_CUDA_TRY(cudaMalloc(&p->scratch, need));
+      p->scratch_bytes = need;
+    }
+    a.scratch = p->scratch;
+  }
+  kern<<<(unsigned)grid, threads, smem, stream>>>(p->dp, a, words_per_warp, S);
+  FS_CUDA_TRY(cudaGetLastError());
+  return FS_OK;
+}
+
+// state store carve-out for `slots` survivors with arrays of 2^k
+size_t store_bytes(const fs::DevProg& dp, const fs::SegArgs& S, size_t slots, int k) {
+  const size_t sl = align_up(slots, 32);
+  return align_up(sl * 4 * (S.nfw + S.nsw + S.now + 2 + 6), 256) + align_up(sl * 24, 256) +
+         align_up(sl * 16 * ((size_t)1 << k), 256) + 4096;
+}
+
+fs::StateStore carve_store(void* base, const fs::SegArgs& S, size_t slots, int k) {
+  Stage st;
+  st.base = static_cast<unsigned char*>(base);
+  const size_t sl = align_up(slots, 32);
+  fs::StateStore o{};
+  o.frame = st.take<uint32_t>(sl * S.nfw + 1);
+  o.slotbits = st.take<uint32_t>(sl * S.nsw + 1);
+  o.obsbits = st.take<uint32_t>(sl * S.now + 1);
+  o.smcount = st.take<uint32_t>(sl);
+  o.shot = st.take<uint32_t>(sl);
+  o.gen_i = st.take<uint32_t>(sl * 6);
+  o.gen_c = st.take<double>(sl);
+  o.gamma = st.take<double2>(sl);
+  o.amps = st.take<double2>(sl * ((size_t)1 << k));
+  return o;
+}
+
+// Segmented general engine for programs with PostSelect (config 4): cut after every
+// PostSelect, run each segment over the surviving shots only, compact survivors in between.
+int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
+  const fs::DevProg& dp = p->dp;
+  const int* I = p->h_instrs.data();
+  const int* sched = p->h_sched.data();
+  std::vector<int> bounds{0};
+  for (int i = 0; i < dp.num_instrs; i++)
+    if (FS_OPCODE(I[(size_t)i * FS_INS_WORDS]) == FS_OP_POSTSELECT && i + 1 < dp.num_instrs) bounds.push_back(i + 1);
+  bounds.push_back(dp.num_instrs);
+  const int nseg = (int)bounds.size() - 1;
+  // outputs are OR-ed bit by bit once shots are compacted
+  const size_t W = a.W;
+  if (dp.U) FS_CUDA_TRY(cudaMemsetAsync(a.meas, 0, 4 * dp.U * W, stream));
+  if (dp.D) FS_CUDA_TRY(cudaMemsetAsync(a.det, 0, 4 * dp.D * W, stream));
+  if (dp.O) FS_CUDA_TRY(cudaMemsetAsync(a.obs, 0, 4 * dp.O * W, stream));
+  FS_CUDA_TRY(cudaMemsetAsync(a.accepted, 0, 4 * W, stream));
+  FS_CUDA_TRY(cudaMemsetAsync(a.error, 0, 4 * W, stream));
+  a.prezeroed = 1;
+  fs::SegArgs S{};
+  S.nfw = (2 * dp.n + 31) / 32;
+  S.nsw = (dp.num_slots + 31) / 32;
+  S.now = (dp.O + 31) / 32;
+  const uint64_t chunk = (uint64_t)1 << 22;
+  if (!p->d_counts) FS_CUDA_TRY(cudaMalloc(&p->d_counts, 64));
+  uint32_t* d_nout = reinterpret_cast<uint32_t*>(p->d_counts);
+  for (uint64_t c0 = 0; c0 < a.nshots; c0 += chunk) {
+    uint32_t n_in = (uint32_t)std::min<uint64_t>(chunk, a.nshots - c0);
+    int cur = 0;  // which pool holds the input store
+    for (int sgi = 0; sgi < nseg; sgi++) {
+      const int b = bounds[sgi], e = bounds[sgi + 1];
+      S.seg_begin = b;
+      S.seg_end = e;
+      S.first = sgi == 0;
+      S.last = sgi == nseg - 1;
+      S.n_in = n_in;
+      S.chunk0 = c0;
+      S.k_in = b > 0 ? sched[b - 1] : 0;
+      S.k_out = sched[e - 1];
+      int karr = S.k_in;
+      for (int i = b; i < e; i++) karr = std::max(karr, sched[i]);
+      if (!S.last) {
+        const size_t need = store_bytes(dp, S, n_in, S.k_out);
+        if (need > p->seg_bytes[1 - cur]) {
+          cudaFree(p->seg_pool[1 - cur]);
+          p->seg_pool[1 - cur] = nullptr;
+          p->seg_bytes[1 - cur] = 0;
+          FS_CUDA_TRY(cudaMalloc(&p->seg_pool[1 - cur], need));
+          p->seg_bytes[1 - cur] = need;
+        }
+        S.out = carve_store(p->seg_pool[1 - cur], S, n_in, S.k_out);
+        FS_CUDA_TRY(cudaMemsetAsync(d_nout, 0, 4, stream));
+      }
+      S.n_out = d_nout;
+      int rc = launch_general_kernel(p, a, S, true, karr, (n_in + 31) / 32, stream);
+      if (rc) return rc;
+      if (S.last) break;
+      uint32_t n_out = 0;
+      FS_CUDA_TRY(cudaMemcpyAsync(&n_out, d_nout, 4, cudaMemcpyDeviceToHost, stream));
+      FS_CUDA_TRY(cudaStreamSynchronize(stream));
+      if (n_out == 0) break;
+      S.in = S.out;
+      cur = 1 - cur;
+      n_in = n_out;
+    }
+  }
   return FS_OK;
 }
 
@@ -591,39 +737,10 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     return FS_OK;
   }
   // general engine
-  const bool splitmix = flags & FS_RNG_SPLITMIX;
-  const int words_per_warp = (int)align_up(2 * dp.n + dp.num_slots + dp.O, 4);
-  const size_t words_bytes = (size_t)fs::kGenWarps * words_per_warp * 4;
-  const size_t arr_bytes_warp = ((size_t)32 << dp.k_max) * sizeof(double2);
-  const bool arr_smem = words_bytes + 16 + fs::kGenWarps * arr_bytes_warp <= kSmemBudget;
-  const size_t smem = words_bytes + (arr_smem ? 16 + fs::kGenWarps * arr_bytes_warp : 0);
-  if (words_bytes > kSmemBudget) return set_error(FS_ERR_ARG, "program too large for the general engine");
-  void (*kern)(fs::DevProg, fs::RunArgs, int);
-  if (splitmix) kern = arr_smem ? fs::general_kernel<true, true> : fs::general_kernel<true, false>;
-  else kern = arr_smem ? fs::general_kernel<false, true> : fs::general_kernel<false, false>;
-  FS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int threads = fs::kGenWarps * 32;
-  const size_t blocks_needed = (W + fs::kGenWarps - 1) / fs::kGenWarps;
-  const int occ = occupancy_blocks(kern, threads, smem);
-  size_t grid = std::min<size_t>(blocks_needed, (size_t)p->num_sms * occ);
-  if (!arr_smem) {
-    // HBM slab per resident warp; cap the footprint at ~48 GiB
-    const size_t per_block = fs::kGenWarps * arr_bytes_warp;
-    const size_t cap_blocks = std::max<size_t>(1, ((size_t)48 << 30) / per_block);
-    grid = std::min(grid, cap_blocks);
-    const size_t need = grid * per_block;
-    if (need > p->scratch_bytes) {
-      cudaFree(p->scratch);
-      p->scratch = nullptr;
-      p->scratch_bytes = 0;
-      FS_CUDA_TRY(cudaMalloc(&p->scratch, need));
-      p->scratch_bytes = need;
-    }
-    a.scratch = p->scratch;
-  }
-  kern<<<(unsigned)grid, threads, smem, stream>>>(dp, a, words_per_warp);
-  FS_CUDA_TRY(cudaGetLastError());
-  return FS_OK;
+  const bool trace = (tin && (tin->fault_modes || tin->forced)) || tout;
+  if (dp.has_psel && !trace && a.stop == dp.num_instrs) return launch_segmented(p, a, stream);
+  fs::SegArgs none{};
+  return launch_general_kernel(p, a, none, false, dp.k_max, a.W, stream);
 }
 
 // popcount reduction of one sampling chunk into counts (sums over accepted shots)
