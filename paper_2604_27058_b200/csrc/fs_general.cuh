@@ -226,9 +226,15 @@ struct StateStore {
   uint32_t* smcount;  // [slot]
   uint32_t* gen_i;    // [slot][6]: step_no, run, cl, pend_site, pend_lane, pend_case
   double* gen_c;      // [slot]
-  double2* amps;      // [slot/32][cap][32]
+  double2* amps;      // [slot/32][cap][32] (interleaved) or [slot][cap] (shot_major)
   uint32_t* shot;     // [slot] shot index within the call
+  int shot_major;     // layout chosen for the consuming engine
 };
+
+// amplitude j of store slot `slot`: interleaved [slot/32][j][32] or shot-major [slot][j]
+__device__ __forceinline__ size_t store_amp_index(uint32_t slot, uint32_t j, uint32_t cap, int shot_major) {
+  return shot_major ? (size_t)slot * cap + j : (size_t)(slot >> 5) * ((size_t)cap * 32) + (size_t)j * 32 + (slot & 31);
+}
 
 struct SegArgs {
   int seg_begin, seg_end;  // instruction range of this segment
@@ -339,8 +345,7 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp, SegArgs S) {
           lgen.c = I.gen_c[idx];
         }
         const uint32_t sz = 1u << S.k_in;
-        const double2* src = I.amps + (size_t)(idx >> 5) * ((size_t)sz * 32) + (idx & 31);
-        for (uint32_t j = 0; j < sz; j++) AMP(j) = src[(size_t)j * 32];
+        for (uint32_t j = 0; j < sz; j++) AMP(j) = I.amps[store_amp_index(idx, j, sz, I.shot_major)];
       }
       __syncwarp();
     }
@@ -769,8 +774,7 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp, SegArgs S) {
             O.gen_c[slot] = lgen.c;
           }
           const uint32_t sz = 1u << S.k_out;
-          double2* dst = O.amps + (size_t)(slot >> 5) * ((size_t)sz * 32) + (slot & 31);
-          for (uint32_t j = 0; j < sz; j++) dst[(size_t)j * 32] = AMP(j);
+          for (uint32_t j = 0; j < sz; j++) O.amps[store_amp_index(slot, j, sz, O.shot_major)] = AMP(j);
         }
       }
     }

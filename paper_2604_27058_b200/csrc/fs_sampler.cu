@@ -17,6 +17,7 @@
 #include "fs_frame.cuh"
 #include "fs_general.cuh"
 #include "fs_hbm.cuh"
+#include "fs_block.cuh"
 #include "fs_jit.cuh"
 
 namespace {
@@ -91,6 +92,7 @@ struct fs_prog {
 
 namespace {
 constexpr int kLargeK = 16;  // k_max at which active arrays move to the HBM engine
+constexpr int kBlockK = 6;   // segment active dimension at which a shot gets a whole CTA
 }
 
 extern "C" int fs_abi_version(void) { return FS_ABI_VERSION; }
@@ -360,6 +362,22 @@ int launch_general_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, bool seg, 
   return FS_OK;
 }
 
+// CTA-per-shot launch for a segment with a large active array (fs_block.cuh)
+int launch_block_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cudaStream_t stream) {
+  const fs::DevProg& dp = p->dp;
+  const size_t smem = ((size_t)16 << karr) + (size_t)4 * (2 * dp.n + dp.num_slots + dp.O + 4);
+  if (smem > kSmemBudget) return set_error(FS_ERR_ARG, "active array too large for the block engine");
+  const int nt = std::min(256, std::max(64, 1 << std::max(0, karr - 2)));
+  void (*kern)(fs::DevProg, fs::RunArgs, fs::SegArgs, int) =
+      (a.flags & FS_RNG_SPLITMIX) ? fs::block_kernel<true> : fs::block_kernel<false>;
+  FS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int occ = occupancy_blocks(kern, nt, smem);
+  const size_t grid = std::max<size_t>(1, std::min<size_t>(S.n_in, (size_t)p->num_sms * occ));
+  kern<<<(unsigned)grid, nt, smem, stream>>>(dp, a, S, karr);
+  FS_CUDA_TRY(cudaGetLastError());
+  return FS_OK;
+}
+
 // state store carve-out for `slots` survivors with arrays of 2^k
 size_t store_bytes(const fs::DevProg& dp, const fs::SegArgs& S, size_t slots, int k) {
   const size_t sl = align_up(slots, 32);
@@ -425,6 +443,12 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
       S.k_out = sched[e - 1];
       int karr = S.k_in;
       for (int i = b; i < e; i++) karr = std::max(karr, sched[i]);
+      // engine of the NEXT segment decides the survivor store layout
+      int karr_next = 0;
+      if (!S.last) {
+        karr_next = S.k_out;
+        for (int i = e; i < bounds[sgi + 2]; i++) karr_next = std::max(karr_next, sched[i]);
+      }
       if (!S.last) {
         const size_t need = store_bytes(dp, S, n_in, S.k_out);
         if (need > p->seg_bytes[1 - cur]) {
@@ -435,10 +459,12 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
           p->seg_bytes[1 - cur] = need;
         }
         S.out = carve_store(p->seg_pool[1 - cur], S, n_in, S.k_out);
+        S.out.shot_major = karr_next >= kBlockK ? 1 : 0;
         FS_CUDA_TRY(cudaMemsetAsync(d_nout, 0, 4, stream));
       }
       S.n_out = d_nout;
-      int rc = launch_general_kernel(p, a, S, true, karr, (n_in + 31) / 32, stream);
+      int rc = karr >= kBlockK ? launch_block_kernel(p, a, S, karr, stream)
+                               : launch_general_kernel(p, a, S, true, karr, (n_in + 31) / 32, stream);
       if (rc) return rc;
       if (S.last) break;
       uint32_t n_out = 0;
