@@ -10,22 +10,33 @@
 
 namespace fs {
 
-template <bool SPLITMIX>
-__global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArgs S, int karr) {
+// G threads per shot: G = 32 (warp per shot, several shots per CTA) or G = 256 (CTA per shot)
+template <bool SPLITMIX, int G>
+__global__ void __launch_bounds__(256, 4) block_kernel(DevProg P, RunArgs A, SegArgs S, int karr, int group_bytes) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t cap = 1u << karr;
-  double2* amp = reinterpret_cast<double2*>(smem_raw);
+  const int group = threadIdx.x / G, ngroups = blockDim.x / G;
+  double2* amp = reinterpret_cast<double2*>(smem_raw + (size_t)group * group_bytes);
   uint32_t* fx = reinterpret_cast<uint32_t*>(amp + cap);  // one shot: values 0/1
   uint32_t* fz = fx + P.n;
   uint32_t* slots = fz + P.n;
   uint32_t* obsb = slots + P.num_slots;
-  __shared__ double red1[256], red2[256];
-  __shared__ double2 sh_k0, sh_k1;
-  __shared__ int sh_alive, sh_branch, sh_err;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double red1s[256], red2s[256];
+  __shared__ double2 sh_k0s[8], sh_k1s[8];
+  __shared__ int sh_alives[8], sh_branchs[8], sh_errs[8];
+  __shared__ uint32_t sh_slots[8];
+  double2& sh_k0 = sh_k0s[group];
+  double2& sh_k1 = sh_k1s[group];
+  int& sh_alive = sh_alives[group];
+  int& sh_branch = sh_branchs[group];
+  int& sh_err = sh_errs[group];
+  double* red1 = red1s + group * G;
+  double* red2 = red2s + group * G;
+  const int tid = threadIdx.x % G, nt = G;
   const bool renorm = !(A.flags & FS_NO_RENORM);
+#define FS_BAR() do { if (G == 32) __syncwarp(); else __syncthreads(); } while (0)
 
-  for (uint32_t idx = blockIdx.x; idx < S.n_in; idx += gridDim.x) {
+  for (uint32_t idx = blockIdx.x * ngroups + group; idx < S.n_in; idx += gridDim.x * ngroups) {
     const uint64_t si = S.first ? S.chunk0 + idx : S.in.shot[idx];
     if (si >= A.nshots) continue;  // uniform over the block
     const uint64_t shot = A.shot0 + si;
@@ -68,10 +79,101 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
         }
       }
     }
-    __syncthreads();
+    FS_BAR();
     auto out_bit = [&](uint32_t* row) { atomicOr(row + (si >> 5), 1u << (si & 31)); };
+    // one scalar instruction of this shot (thread 0 only)
+    auto scalar_step = [&](int i) {
+      const int4 I0 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i);
+      const int4 I1 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i + 1);
+      const int ins[8] = {I0.x, I0.y, I0.z, I0.w, I1.x, I1.y, I1.z, I1.w};
+      const int op = FS_OPCODE(I0.x);
+      const int flip = FS_FLIP(I0.x);
+            switch (op) {
+        case FS_OP_FRAME:
+          for (int j = 0; j < ins[2]; j++) word_gate(fx, fz, __ldg(P.gates + ins[1] + j));
+          break;
+        case FS_OP_GAMMA_ROT: {
+          const int par = fx[ins[1]] & 1;
+          const double* f = P.fparams + ins[5] + 2 * par;
+          gamma = cmul(gamma, make_double2(__ldg(f), __ldg(f + 1)));
+          break;
+        }
+        case FS_OP_MEAS_DSTATIC:
+        case FS_OP_MEAS_DRANDOM: {
+          const int virt = ins[1], rec = ins[3];
+          uint32_t bit;
+          if (op == FS_OP_MEAS_DSTATIC) {
+            bit = fx[virt] ^ (uint32_t)flip;
+          } else {
+            const uint32_t pz = fz[virt];
+            uint32_t coin = SPLITMIX ? (uint32_t)sm.bit() : ((coin_word(A.seed, wabs, ins[2]) >> mylane) & 1u);
+            bit = coin ^ pz ^ (uint32_t)flip;
+            const uint32_t t = fx[virt];
+            fx[virt] = fz[virt] ^ coin;
+            fz[virt] = t;
+            gamma = cscale(gamma, kInvSqrt2);
+          }
+          const int col = __ldg(P.record_out + rec);
+          if (col >= 0 && bit) out_bit(A.meas + (size_t)col * A.W);
+          const int sl = __ldg(P.bit_slot + rec);
+          if (sl >= 0) slots[sl] = bit;
+          break;
+        }
+        case FS_OP_COND_FRAME:
+          if (slots[__ldg(P.bit_slot + ins[3])]) xor_paulis<false>(P, fx, fz, ins[1], ins[2], 1u);
+          break;
+        case FS_OP_NOISE:
+          if (SPLITMIX) {
+            hazard_shot(P, fx, fz, 1u, ins, sm, 1, false);
+          } else {
+            const int hi = ins[2];
+            for (;;) {
+              if (pend_site < 0) {
+                int st_, ln_, cs_;
+                const int r = gen.step(P, st_, ln_, cs_);
+                if (r == 2) { pend_site = 0x7FFFFFFF; break; }
+                if (r == 0) continue;
+                pend_site = st_; pend_lane = ln_; pend_case = cs_;
+              }
+              if (pend_site >= hi) break;
+              if (pend_lane == mylane) xor_case_strided(P, fx, fz, pend_case, 1u, 1, false);
+              pend_site = -1;
+            }
+          }
+          break;
+        case FS_OP_DETECTOR:
+        case FS_OP_OBSERVABLE: {
+          uint32_t v = 0;
+          for (int j = 0; j < ins[3]; j++) v ^= slots[__ldg(P.bit_slot + __ldg(P.reclists + ins[2] + j))];
+          if (op == FS_OP_DETECTOR) {
+            if (v) out_bit(A.det + (size_t)ins[1] * A.W);
+            const int sl = __ldg(P.bit_slot + P.R + ins[1]);
+            if (sl >= 0) slots[sl] = v;
+          } else {
+            obsb[ins[1]] ^= v;
+          }
+          break;
+        }
+        case FS_OP_POSTSELECT: {
+          const int bid = ins[1] == 0 ? P.R + ins[2] : ins[2];
+          if ((int)slots[__ldg(P.bit_slot + bid)] != ins[3]) sh_alive = 0;
+          break;
+        }
+        default: break;
+      }
+    };
     for (int i = S.seg_begin; i < S.seg_end; i++) {
       if (!sh_alive) break;
+      {  // a run of scalar instructions executes on thread 0 with one barrier at its end
+        const int j = min(__ldg(P.next_array + i), S.seg_end);
+        if (j > i) {
+          if (tid == 0)
+            for (int t = i; t < j && sh_alive; t++) scalar_step(t);
+          FS_BAR();
+          i = j - 1;
+          continue;
+        }
+      }
       const int4 I0 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i);
       const int4 I1 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i + 1);
       const int ins[8] = {I0.x, I0.y, I0.z, I0.w, I1.x, I1.y, I1.z, I1.w};
@@ -120,7 +222,7 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
               case FS_G_CZ: fz[vb] ^= fx[va]; fz[va] ^= fx[vb]; break;
             }
           }
-          __syncthreads();
+          FS_BAR();
           break;
         }
         case FS_OP_EXPAND: {
@@ -133,7 +235,7 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
             amp[j] = cmul(v, ph0);
             amp[size + j] = cmul(v, ph1);
           }
-          __syncthreads();
+          FS_BAR();
           break;
         }
         case FS_OP_ARRAY_ROT: {
@@ -143,7 +245,7 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
           const double2 ph0 = par ? e1 : e0, ph1 = par ? e0 : e1;
           const uint32_t size = 1u << ins[6];
           for (uint32_t j = tid; j < size; j += nt) amp[j] = cmul(amp[j], ((j >> a) & 1) ? ph1 : ph0);
-          __syncthreads();
+          FS_BAR();
           break;
         }
         case FS_OP_MEAS_ACTIVE:
@@ -173,13 +275,13 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
           }
           red1[tid] = s1;
           red2[tid] = sa;
-          __syncthreads();
+          FS_BAR();
           for (int w = nt >> 1; w; w >>= 1) {
             if (tid < w) {
               red1[tid] = __dadd_rn(red1[tid], red1[tid + w]);
               red2[tid] = __dadd_rn(red2[tid], red2[tid + w]);
             }
-            __syncthreads();
+            FS_BAR();
           }
           if (tid == 0) {
             if (collapse) {
@@ -223,7 +325,7 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
               if (renorm) gamma = cscale(gamma, __dsqrt_rn(pb));
             }
           }
-          __syncthreads();
+          FS_BAR();
           if (!sh_alive) break;
           branch = sh_branch;
           if (collapse) {  // compaction: gather sources first (in-place, different threads)
@@ -234,7 +336,7 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
               const uint32_t i0 = ins0(j, a);
               v[nv] = cadd(cmul(k0, amp[i0]), cmul(k1, amp[i0 + st]));
             }
-            __syncthreads();
+            FS_BAR();
             nv = 0;
             for (uint32_t j = tid; j < half && nv < 16; j += nt, nv++) amp[j] = v[nv];
           } else {
@@ -245,7 +347,7 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
               else if (renorm) amp[j] = cscale(amp[j], s);
             }
           }
-          __syncthreads();
+          FS_BAR();
           break;
         }
         case FS_OP_RETIRE: {
@@ -255,95 +357,18 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
           double2 v[16];
           int nv = 0;
           for (uint32_t j = tid; j < half && nv < 16; j += nt, nv++) v[nv] = amp[ins0(j, a) + ((uint32_t)br << a)];
-          __syncthreads();
+          FS_BAR();
           nv = 0;
           for (uint32_t j = tid; j < half && nv < 16; j += nt, nv++) amp[j] = v[nv];
           if (tid == 0) fx[virt] ^= (uint32_t)br;
-          __syncthreads();
+          FS_BAR();
           break;
         }
-        default: {  // scalar instruction: thread 0
-          if (tid == 0) {
-            switch (op) {
-              case FS_OP_FRAME:
-                for (int j = 0; j < ins[2]; j++) word_gate(fx, fz, __ldg(P.gates + ins[1] + j));
-                break;
-              case FS_OP_GAMMA_ROT: {
-                const int par = fx[ins[1]] & 1;
-                const double* f = P.fparams + ins[5] + 2 * par;
-                gamma = cmul(gamma, make_double2(__ldg(f), __ldg(f + 1)));
-                break;
-              }
-              case FS_OP_MEAS_DSTATIC:
-              case FS_OP_MEAS_DRANDOM: {
-                const int virt = ins[1], rec = ins[3];
-                uint32_t bit;
-                if (op == FS_OP_MEAS_DSTATIC) {
-                  bit = fx[virt] ^ (uint32_t)flip;
-                } else {
-                  const uint32_t pz = fz[virt];
-                  uint32_t coin = SPLITMIX ? (uint32_t)sm.bit() : ((coin_word(A.seed, wabs, ins[2]) >> mylane) & 1u);
-                  bit = coin ^ pz ^ (uint32_t)flip;
-                  const uint32_t t = fx[virt];
-                  fx[virt] = fz[virt] ^ coin;
-                  fz[virt] = t;
-                  gamma = cscale(gamma, kInvSqrt2);
-                }
-                const int col = __ldg(P.record_out + rec);
-                if (col >= 0 && bit) out_bit(A.meas + (size_t)col * A.W);
-                const int sl = __ldg(P.bit_slot + rec);
-                if (sl >= 0) slots[sl] = bit;
-                break;
-              }
-              case FS_OP_COND_FRAME:
-                if (slots[__ldg(P.bit_slot + ins[3])]) xor_paulis<false>(P, fx, fz, ins[1], ins[2], 1u);
-                break;
-              case FS_OP_NOISE:
-                if (SPLITMIX) {
-                  hazard_shot(P, fx, fz, 1u, ins, sm, 1, false);
-                } else {
-                  const int hi = ins[2];
-                  for (;;) {
-                    if (pend_site < 0) {
-                      int st_, ln_, cs_;
-                      const int r = gen.step(P, st_, ln_, cs_);
-                      if (r == 2) { pend_site = 0x7FFFFFFF; break; }
-                      if (r == 0) continue;
-                      pend_site = st_; pend_lane = ln_; pend_case = cs_;
-                    }
-                    if (pend_site >= hi) break;
-                    if (pend_lane == mylane) xor_case_strided(P, fx, fz, pend_case, 1u, 1, false);
-                    pend_site = -1;
-                  }
-                }
-                break;
-              case FS_OP_DETECTOR:
-              case FS_OP_OBSERVABLE: {
-                uint32_t v = 0;
-                for (int j = 0; j < ins[3]; j++) v ^= slots[__ldg(P.bit_slot + __ldg(P.reclists + ins[2] + j))];
-                if (op == FS_OP_DETECTOR) {
-                  if (v) out_bit(A.det + (size_t)ins[1] * A.W);
-                  const int sl = __ldg(P.bit_slot + P.R + ins[1]);
-                  if (sl >= 0) slots[sl] = v;
-                } else {
-                  obsb[ins[1]] ^= v;
-                }
-                break;
-              }
-              case FS_OP_POSTSELECT: {
-                const int bid = ins[1] == 0 ? P.R + ins[2] : ins[2];
-                if ((int)slots[__ldg(P.bit_slot + bid)] != ins[3]) sh_alive = 0;
-                break;
-              }
-              default: break;
-            }
-          }
-          __syncthreads();
+        default:
           break;
-        }
       }
     }
-    __syncthreads();
+    FS_BAR();
     const bool alive = sh_alive != 0;
     const bool errored = sh_err != 0;
     if (tid == 0) {
@@ -358,10 +383,9 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
       }
     }
     if (!S.last && alive) {  // survivor: compact into the output store
-      __shared__ uint32_t sh_slot;
-      if (tid == 0) sh_slot = atomicAdd(S.n_out, 1u);
-      __syncthreads();
-      const uint32_t slot = sh_slot;
+      if (tid == 0) sh_slots[group] = atomicAdd(S.n_out, 1u);
+      FS_BAR();
+      const uint32_t slot = sh_slots[group];
       const StateStore& O = S.out;
       for (int j = tid; j < S.nfw; j += nt) {
         uint32_t v = 0;
@@ -392,8 +416,9 @@ __global__ void __launch_bounds__(256) block_kernel(DevProg P, RunArgs A, SegArg
         }
       }
     }
-    __syncthreads();
+    FS_BAR();
   }
+#undef FS_BAR
 }
 
 }  // namespace fs

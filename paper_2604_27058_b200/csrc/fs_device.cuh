@@ -49,6 +49,7 @@ struct DevProg {
   const int* __restrict__ run_len;
   const double* __restrict__ run_lp;
   const double* __restrict__ site_acc;  // p_site / q of its run (thinning), 1.0 when equal
+  const int* __restrict__ next_array;   // [N] first array instruction >= i (N if none)
 };
 
 struct RunArgs {

@@ -167,6 +167,14 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   size_t o_rl2 = add(run_len.data(), sizeof(int32_t) * nruns);
   size_t o_rlp = add(run_lp.data(), sizeof(double) * nruns);
   size_t o_sacc = add(site_acc.data(), sizeof(double) * site_acc.size());
+  std::vector<int32_t> next_array(d->num_instrs + 1, d->num_instrs);
+  for (int i = d->num_instrs - 1; i >= 0; i--) {
+    const int op = FS_OPCODE(d->instrs[(size_t)i * FS_INS_WORDS]);
+    const bool arr = op == FS_OP_ARRAY_GATE || op == FS_OP_EXPAND || op == FS_OP_ARRAY_ROT ||
+                     op == FS_OP_MEAS_ACTIVE || op == FS_OP_MEAS_COLLAPSE || op == FS_OP_RETIRE;
+    next_array[i] = arr ? i : next_array[i + 1];
+  }
+  size_t o_na = add(next_array.data(), sizeof(int32_t) * next_array.size());
   std::vector<unsigned char> host(total, 0);
   for (auto& s : secs)
     if (s.src && s.bytes) std::memcpy(host.data() + s.off, s.src, s.bytes);
@@ -204,6 +212,7 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   dp.run_len = reinterpret_cast<const int*>(b + o_rl2);
   dp.run_lp = reinterpret_cast<const double*>(b + o_rlp);
   dp.site_acc = reinterpret_cast<const double*>(b + o_sacc);
+  dp.next_array = reinterpret_cast<const int*>(b + o_na);
   p->h_instrs.assign(d->instrs, d->instrs + (size_t)FS_INS_WORDS * d->num_instrs);
   p->h_sched.assign(d->schedule, d->schedule + d->num_instrs);
   if (d->num_fparams) p->h_fparams.assign(d->fparams, d->fparams + d->num_fparams);
@@ -362,18 +371,24 @@ int launch_general_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, bool seg, 
   return FS_OK;
 }
 
-// CTA-per-shot launch for a segment with a large active array (fs_block.cuh)
+// shot-per-warp (k <= 10) or shot-per-CTA launch for a segment with a large active array
 int launch_block_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cudaStream_t stream) {
   const fs::DevProg& dp = p->dp;
-  const size_t smem = ((size_t)16 << karr) + (size_t)4 * (2 * dp.n + dp.num_slots + dp.O + 4);
-  if (smem > kSmemBudget) return set_error(FS_ERR_ARG, "active array too large for the block engine");
-  const int nt = std::min(256, std::max(64, 1 << std::max(0, karr - 2)));
-  void (*kern)(fs::DevProg, fs::RunArgs, fs::SegArgs, int) =
-      (a.flags & FS_RNG_SPLITMIX) ? fs::block_kernel<true> : fs::block_kernel<false>;
+  const size_t group_bytes = align_up(((size_t)16 << karr) + (size_t)4 * (2 * dp.n + dp.num_slots + dp.O + 4), 16);
+  if (group_bytes > kSmemBudget) return set_error(FS_ERR_ARG, "active array too large for the block engine");
+  const bool warp_mode = karr <= 10;
+  const int ngroups = warp_mode ? (int)std::max<size_t>(1, std::min<size_t>(8, kSmemBudget / group_bytes)) : 1;
+  const int nt = warp_mode ? 32 * ngroups : 256;
+  const size_t smem = group_bytes * ngroups;
+  void (*kern)(fs::DevProg, fs::RunArgs, fs::SegArgs, int, int);
+  const bool sm = a.flags & FS_RNG_SPLITMIX;
+  if (warp_mode) kern = sm ? fs::block_kernel<true, 32> : fs::block_kernel<false, 32>;
+  else kern = sm ? fs::block_kernel<true, 256> : fs::block_kernel<false, 256>;
   FS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int occ = occupancy_blocks(kern, nt, smem);
-  const size_t grid = std::max<size_t>(1, std::min<size_t>(S.n_in, (size_t)p->num_sms * occ));
-  kern<<<(unsigned)grid, nt, smem, stream>>>(dp, a, S, karr);
+  const size_t blocks_needed = (S.n_in + ngroups - 1) / ngroups;
+  const size_t grid = std::max<size_t>(1, std::min<size_t>(blocks_needed, (size_t)p->num_sms * occ));
+  kern<<<(unsigned)grid, nt, smem, stream>>>(dp, a, S, karr, (int)group_bytes);
   FS_CUDA_TRY(cudaGetLastError());
   return FS_OK;
 }
