@@ -102,6 +102,8 @@ struct FrameKernelSource {
   std::string src;
   std::vector<uint16_t> pslot;  // per Pauli entry: physical slot under the renaming at its block
   int nslots = 0;               // physical frame slots (2n)
+  std::vector<int32_t> site_block;  // NoiseBlock ordinal of every site
+  int nblocks = 0;
 };
 
 // Generate the specialised frame kernel for a frame-only program.
@@ -128,8 +130,8 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   const int R = d.record_count;
   o << "#include \"fs_jit_kernels.cuh\"\n";
   const char* mb = getenv("FS_JIT_MINBLOCKS");
-  o << "extern \"C\" __global__ void __launch_bounds__(128, " << (mb ? atoi(mb) : 2) << ") fs_jit_frame(fs::DevProg P, fs::RunArgs A, "
-       "const uint16_t* __restrict__ pslot) {\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(128, " << (mb ? atoi(mb) : 3) << ") fs_jit_frame(fs::DevProg P, fs::RunArgs A, "
+       "const uint16_t* __restrict__ pslot, const uint32_t* __restrict__ flips, const uint32_t* __restrict__ bcount) {\n";
   o << "  extern __shared__ uint32_t smem[];\n";
   o << "  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;\n";
   o << "  uint32_t* F = smem + wib * " << K.nslots * 32 << " + lane;\n";
@@ -144,7 +146,10 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   for (int s = 0; s < d.num_slots; s++) o << "    uint32_t r" << s << " = 0u;\n";
   for (int j = 0; j < d.num_observables; j++) o << "    uint32_t ob" << j << " = 0u;\n";
   o << "    uint4 cb = make_uint4(0u, 0u, 0u, 0u);\n";
-  o << "    fs::FaultBuffer<fs::kFaultCap> fbuf;\n    fbuf.init(P, seed, wabs);\n";
+  // faults come from the pre-generated per-word list (noise_list_kernel); an overflowed list
+  // (count == ~0) falls back to generating the word's stream in place
+  o << "    const bool fover = bcount[w] == 0xFFFFFFFFu;\n    uint32_t fcur = 0;\n";
+  o << "    fs::FaultBuffer<fs::kFaultCap> fbuf;\n    if (fover) fbuf.init(P, seed, wabs);\n";
   auto put_record = [&](int rec, const std::string& expr) {
     const int col = record_out[rec], sl = bit_slot[rec];
     o << "    { const uint32_t rw = " << expr << ";";
@@ -153,6 +158,14 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
     o << " }\n";
   };
   int coin_blk = -1;
+  int nblk = 0;  // NoiseBlock ordinal
+  K.site_block.assign(d.num_sites + 1, 0);
+  for (int i = 0, b = 0; i < d.num_instrs; i++)
+    if (FS_OPCODE(ins_all[(size_t)i * FS_INS_WORDS]) == FS_OP_NOISE) {
+      for (int s2 = ins_all[(size_t)i * FS_INS_WORDS + 1]; s2 < ins_all[(size_t)i * FS_INS_WORDS + 2]; s2++) K.site_block[s2] = b;
+      b++;
+      K.nblocks = b;
+    }
   for (int i = 0; i < d.num_instrs; i++) {
     const int* I = ins_all.data() + (size_t)i * FS_INS_WORDS;
     const int op = FS_OPCODE(I[0]);
@@ -217,7 +230,9 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
               const int q = FS_PAULI_Q(e);
               K.pslot[j] = (uint16_t)(FS_PAULI_Z(e) ? Z(q) : X(q));
             }
-        o << "    fs::jit_noise_block(P, F, pslot, fbuf, " << I[2] << ");\n";
+        o << "    if (!fover) fs::jit_apply_flips(F, flips, A.W, w, fcur, bcount[(size_t)" << nblk
+          << " * A.W + w]); else fs::jit_noise_block(P, F, pslot, fbuf, " << I[2] << ");\n";
+        nblk++;
         break;
       }
       case FS_OP_DETECTOR:

@@ -19,6 +19,7 @@
 #include "fs_hbm.cuh"
 #include "fs_block.cuh"
 #include "fs_jit.cuh"
+#include "fs_jit_kernels.cuh"
 
 namespace {
 
@@ -75,12 +76,18 @@ struct fs_prog {
   std::vector<double> h_fparams;
   std::vector<uint32_t> h_gates, h_paulis;
   std::vector<int32_t> h_reclists, h_record_out, h_bit_slot, h_plans, h_case_pauli_off, h_site_case_off;
+  std::vector<double> h_site_prob;
   // program-specialised frame kernel (fs_jit.cuh); built on first use
   int jit_state = 0;  // 0 not tried, 1 ready, -1 failed (interpreter is used)
   std::string jit_error;
   fsjit::Compiled jit;
   uint16_t* d_pslot = nullptr;
   int jit_nslots = 0;
+  void* flist = nullptr;  // per-word fault lists for the specialised kernel
+  size_t flist_bytes = 0;
+  uint32_t flist_cap = 0;
+  int* d_site_block = nullptr;
+  int jit_nblocks = 0;
   // segmented general engine: ping-pong survivor state stores
   void* seg_pool[2] = {nullptr, nullptr};
   size_t seg_bytes[2] = {0, 0};
@@ -224,6 +231,7 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   p->h_plans.assign(d->plans, d->plans + 2 * d->num_plans);
   p->h_case_pauli_off.assign(d->case_pauli_off, d->case_pauli_off + d->num_cases + 1);
   p->h_site_case_off.assign(d->site_case_off, d->site_case_off + E + 1);
+  p->h_site_prob.assign(d->site_prob, d->site_prob + E);
   // pointers of the creator's arrays are not retained
   p->desc.instrs = nullptr;
   *out = p;
@@ -241,6 +249,8 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->seg_pool[0]);
   cudaFree(p->seg_pool[1]);
   cudaFree(p->d_pslot);
+  cudaFree(p->flist);
+  cudaFree(p->d_site_block);
   if (p->jit.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->jit.mod);
   delete p;
 }
@@ -301,6 +311,10 @@ int occupancy_blocks(K kernel, int threads, size_t smem) {
 
 // ------------------------------------------------------------------ program-specialised kernel
 int ensure_jit(fs_prog* p) {
+  {
+    cudaError_t pre = cudaGetLastError();
+    if (pre != cudaSuccess) return set_error(FS_ERR_CUDA, std::string("before ensure_jit: ") + cudaGetErrorString(pre));
+  }
   if (p->jit_state == 1) return FS_OK;
   if (p->jit_state == -1) return set_error(FS_ERR_ARG, p->jit_error);
   p->jit_state = -1;
@@ -319,7 +333,25 @@ int ensure_jit(fs_prog* p) {
   FS_CUDA_TRY(cudaMalloc(&p->d_pslot, sizeof(uint16_t) * K.pslot.size()));
   FS_CUDA_TRY(cudaMemcpy(p->d_pslot, K.pslot.data(), sizeof(uint16_t) * K.pslot.size(), cudaMemcpyHostToDevice));
   p->jit_nslots = K.nslots;
+  // flip capacity per 32-shot word: mean + 8 sigma + 64 (overflow falls back in-kernel)
+  double mu = 0.0;
+  for (int s = 0; s < p->desc.num_sites; s++) {
+    const int c0 = p->h_site_case_off[s], c1 = p->h_site_case_off[s + 1];
+    double wsum = 0.0;
+    for (int c = c0; c < c1; c++) wsum += p->h_case_pauli_off[c + 1] - p->h_case_pauli_off[c];
+    const double avgw = c1 > c0 ? wsum / (c1 - c0) : 0.0;
+    mu += 32.0 * std::min(1.0, p->h_site_prob[s]) * std::max(1.0, avgw);
+  }
+  p->flist_cap = (uint32_t)std::min(1.0e6, mu + 8.0 * std::sqrt(mu) + 64.0);
+  if (const char* fc = getenv("FS_JIT_FLIPCAP")) p->flist_cap = (uint32_t)atoi(fc);  // testing
+  p->jit_nblocks = K.nblocks;
+  FS_CUDA_TRY(cudaMalloc(&p->d_site_block, sizeof(int) * K.site_block.size()));
+  FS_CUDA_TRY(cudaMemcpy(p->d_site_block, K.site_block.data(), sizeof(int) * K.site_block.size(), cudaMemcpyHostToDevice));
   p->jit_state = 1;
+  {
+    cudaError_t pre = cudaGetLastError();
+    if (pre != cudaSuccess) return set_error(FS_ERR_CUDA, std::string("end of ensure_jit: ") + cudaGetErrorString(pre));
+  }
   return FS_OK;
 }
 
@@ -754,9 +786,36 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
       J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->jit.fn, 128, smem);
       const size_t groups = (W + 127) / 128;
       const size_t grid = std::min<size_t>(groups, (size_t)p->num_sms * std::max(occ, 1));
+      // 1) per-word noise flips (high-occupancy generator kernel)
+      const uint32_t cap = p->flist_cap;
+      const int nb = std::max(1, p->jit_nblocks);
+      const size_t need = align_up((size_t)cap * W * 4, 256) + (size_t)nb * W * 4 + 256;
+      if (need > p->flist_bytes) {
+        cudaFree(p->flist);
+        p->flist = nullptr;
+        p->flist_bytes = 0;
+        FS_CUDA_TRY(cudaMalloc(&p->flist, need));
+        p->flist_bytes = need;
+      }
+      uint32_t* flips = static_cast<uint32_t*>(p->flist);
+      uint32_t* bcount = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(p->flist) + align_up((size_t)cap * W * 4, 256));
+      {
+        cudaError_t pre = cudaGetLastError();
+        if (pre != cudaSuccess) return set_error(FS_ERR_CUDA, std::string("before noise_flip_kernel: ") + cudaGetErrorString(pre));
+      }
+      fs::noise_flip_kernel<<<(unsigned)((W + 255) / 256), 256, 0, stream>>>(dp, a.seed, a.shot0 >> 5, (uint32_t)W,
+                                                                             p->d_pslot, p->d_site_block, nb,
+                                                                             flips, bcount, cap);
+      {
+        cudaError_t e2 = cudaGetLastError();
+        if (e2 != cudaSuccess) return set_error(FS_ERR_CUDA, std::string("noise_flip_kernel launch: ") + cudaGetErrorString(e2));
+      }
+      // 2) the program-specialised frame kernel
       fs::DevProg dpv = dp;
       const uint16_t* ps = p->d_pslot;
-      void* args[] = {&dpv, &a, &ps};
+      const uint32_t* fl = flips;
+      const uint32_t* fc = bcount;
+      void* args[] = {&dpv, &a, &ps, &fl, &fc};
       int r = J.cuLaunchKernel(p->jit.fn, (unsigned)grid, 1, 1, 128, 1, 1, (unsigned)smem, stream, args, nullptr);
       if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_jit_frame) failed: " + std::to_string(r));
       return FS_OK;
