@@ -14,6 +14,7 @@
 #pragma once
 #include <dlfcn.h>
 
+#include <cmath>
 #include <cstdlib>
 
 #include <sstream>
@@ -21,6 +22,8 @@
 #include <vector>
 
 namespace fsjit {
+
+constexpr int kJitStage = 64;  // staged fault entries per word (more -> in-place generation)
 
 typedef int CUresult;
 typedef void* CUmodule;
@@ -104,6 +107,8 @@ struct FrameKernelSource {
   int nslots = 0;               // physical frame slots (2n)
   std::vector<int32_t> site_block;  // NoiseBlock ordinal of every site
   int nblocks = 0;
+  std::vector<int32_t> block_hi, block_cap, row_off;  // flip rows per NoiseBlock
+  int rows = 0, capmax = 0;
 };
 
 // Generate the specialised frame kernel for a frame-only program.
@@ -112,10 +117,32 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
                                           const std::vector<int32_t>& reclists, const std::vector<int32_t>& record_out,
                                           const std::vector<int32_t>& bit_slot, const std::vector<int32_t>& plans,
                                           const std::vector<int32_t>& case_pauli_off,
-                                          const std::vector<int32_t>& site_case_off) {
+                                          const std::vector<int32_t>& site_case_off,
+                                          const std::vector<double>& site_prob) {
   FrameKernelSource K;
   const int n = d.n;
   K.nslots = 2 * n;
+  K.site_block.assign(d.num_sites + 1, 0);
+  for (int i = 0, b = 0; i < d.num_instrs; i++)
+    if (FS_OPCODE(ins_all[(size_t)i * FS_INS_WORDS]) == FS_OP_NOISE) {
+      const int lo = ins_all[(size_t)i * FS_INS_WORDS + 1], hi = ins_all[(size_t)i * FS_INS_WORDS + 2];
+      double mu = 0.0;  // expected flips per 32-shot word in this block
+      for (int s2 = lo; s2 < hi; s2++) {
+        K.site_block[s2] = b;
+        const int c0 = site_case_off[s2], c1 = site_case_off[s2 + 1];
+        double wsum = 0.0;
+        for (int c = c0; c < c1; c++) wsum += case_pauli_off[c + 1] - case_pauli_off[c];
+        mu += 32.0 * std::min(1.0, site_prob[s2]) * (c1 > c0 ? wsum / (c1 - c0) : 0.0);
+      }
+      const int cap = (int)std::ceil(mu + 8.0 * std::sqrt(mu) + 16.0);
+      K.block_hi.push_back(hi);
+      K.block_cap.push_back(cap);
+      K.row_off.push_back(K.rows);
+      K.rows += cap;
+      K.capmax = std::max(K.capmax, cap);
+      b++;
+      K.nblocks = b;
+    }
   K.pslot.assign(paulis.size() + 1, 0);
   std::vector<int> phys(2 * n);
   for (int v = 0; v < 2 * n; v++) phys[v] = v;
@@ -131,10 +158,12 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   o << "#include \"fs_jit_kernels.cuh\"\n";
   const char* mb = getenv("FS_JIT_MINBLOCKS");
   o << "extern \"C\" __global__ void __launch_bounds__(128, " << (mb ? atoi(mb) : 3) << ") fs_jit_frame(fs::DevProg P, fs::RunArgs A, "
-       "const uint16_t* __restrict__ pslot, const uint32_t* __restrict__ flips, const uint32_t* __restrict__ bcount) {\n";
+       "const uint16_t* __restrict__ pslot, const uint32_t* __restrict__ fent, const uint32_t* __restrict__ bcount, "
+       "const uint32_t* __restrict__ ntot) {\n";
   o << "  extern __shared__ uint32_t smem[];\n";
   o << "  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;\n";
-  o << "  uint32_t* F = smem + wib * " << K.nslots * 32 << " + lane;\n";
+  o << "  uint32_t* F = smem + wib * " << (K.nslots + kJitStage) * 32 << " + lane;\n";
+  o << "  uint32_t* stage = smem + wib * " << (K.nslots + kJitStage) * 32 << " + " << K.nslots * 32 << ";\n";
   o << "  const uint64_t word0 = A.shot0 >> 5;\n";
   o << "  const uint64_t seed = A.seed;\n";
   o << "  for (uint32_t w = (blockIdx.x * 4 + wib) * 32 + lane; w < A.W; w += gridDim.x * 4 * 32) {\n";
@@ -148,8 +177,17 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   o << "    uint4 cb = make_uint4(0u, 0u, 0u, 0u);\n";
   // faults come from the pre-generated per-word list (noise_list_kernel); an overflowed list
   // (count == ~0) falls back to generating the word's stream in place
-  o << "    const bool fover = bcount[w] == 0xFFFFFFFFu;\n    uint32_t fcur = 0;\n";
+  // stage the word's fault entries into shared memory with full-row loads (all lanes read
+  // entry row t together), and prefetch the per-block counts
+  o << "    const uint32_t nt_ = ntot[w];\n    const bool fover = nt_ == 0xFFFFFFFFu;\n";
   o << "    fs::FaultBuffer<fs::kFaultCap> fbuf;\n    if (fover) fbuf.init(P, seed, wabs);\n";
+  o << "    uint32_t fcur = 0;\n";
+  o << "    {\n      const uint32_t mine = fover ? 0u : min(nt_, " << kJitStage << "u);\n";
+  o << "      uint32_t tmax = mine;\n";
+  o << "      for (int o_ = 16; o_; o_ >>= 1) tmax = max(tmax, __shfl_xor_sync(__activemask(), tmax, o_));\n";
+  o << "      for (uint32_t t = 0; t < tmax; t++) if (t < mine) stage[t * 32 + lane] = __ldg(fent + (size_t)t * A.W + w);\n";
+  o << "    }\n";
+  for (int b = 0; b < K.nblocks; b++) o << "    const uint32_t nbk" << b << " = fover ? 0u : __ldg(bcount + (size_t)" << b << " * A.W + w);\n";
   auto put_record = [&](int rec, const std::string& expr) {
     const int col = record_out[rec], sl = bit_slot[rec];
     o << "    { const uint32_t rw = " << expr << ";";
@@ -159,13 +197,6 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   };
   int coin_blk = -1;
   int nblk = 0;  // NoiseBlock ordinal
-  K.site_block.assign(d.num_sites + 1, 0);
-  for (int i = 0, b = 0; i < d.num_instrs; i++)
-    if (FS_OPCODE(ins_all[(size_t)i * FS_INS_WORDS]) == FS_OP_NOISE) {
-      for (int s2 = ins_all[(size_t)i * FS_INS_WORDS + 1]; s2 < ins_all[(size_t)i * FS_INS_WORDS + 2]; s2++) K.site_block[s2] = b;
-      b++;
-      K.nblocks = b;
-    }
   for (int i = 0; i < d.num_instrs; i++) {
     const int* I = ins_all.data() + (size_t)i * FS_INS_WORDS;
     const int op = FS_OPCODE(I[0]);
@@ -230,8 +261,8 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
               const int q = FS_PAULI_Q(e);
               K.pslot[j] = (uint16_t)(FS_PAULI_Z(e) ? Z(q) : X(q));
             }
-        o << "    if (!fover) fs::jit_apply_flips(F, flips, A.W, w, fcur, bcount[(size_t)" << nblk
-          << " * A.W + w]); else fs::jit_noise_block(P, F, pslot, fbuf, " << I[2] << ");\n";
+        o << "    if (!fover) fs::jit_apply_faults(F, stage, pslot, lane, fcur, nbk" << nblk
+          << "); else fs::jit_noise_block(P, F, pslot, fbuf, " << I[2] << ");\n";
         nblk++;
         break;
       }

@@ -20,16 +20,17 @@ __device__ __noinline__ void jit_noise_block(const DevProg& P, uint32_t* F, cons
   });
 }
 
-// Pre-expanded noise flips for the specialised frame kernel.  noise_flip_kernel generates the
-// word's faults (WordFaultGen, the engine stream) and expands every fault into its frame flips
-// (physical slot under the renaming at its NoiseBlock, lane bit): flips[i][W] = slot << 5 | lane,
-// grouped by NoiseBlock with bcount[b][W] flips per block.  bcount[0][w] == ~0 marks a word whose
-// flips overflowed `cap`; the frame kernel then regenerates that word's stream in place.
-__global__ void __launch_bounds__(256) noise_flip_kernel(DevProg P, uint64_t seed, uint64_t word0, uint32_t W,
-                                                        const uint16_t* __restrict__ pslot,
+// Noise for the specialised frame kernel.  fault_list_kernel generates each 32-shot word's
+// faults (WordFaultGen: the engine stream; lane = word) and writes one entry per fault,
+// ent[i][W] = pauli_off << 10 | pauli_cnt << 5 | shot_bit, plus per-NoiseBlock counts
+// bcount[b][W] and the total ntot[W].  The frame kernel copies a warp's entries into shared
+// memory with full-row (coalesced) loads once per word and applies them from there.  A word
+// with more than `cap` faults, or a fault with more than 31 Pauli entries, is marked
+// ntot = ~0 and regenerates its stream in place (identical results).
+__global__ void __launch_bounds__(256) fault_list_kernel(DevProg P, uint64_t seed, uint64_t word0, uint32_t W,
                                                         const int* __restrict__ site_block, int nblocks,
-                                                        uint32_t* __restrict__ flips, uint32_t* __restrict__ bcount,
-                                                        uint32_t cap) {
+                                                        uint32_t* __restrict__ ent, uint32_t* __restrict__ bcount,
+                                                        uint32_t* __restrict__ ntot, uint32_t cap) {
   const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= W) return;
   WordFaultGen gen;
@@ -43,41 +44,35 @@ __global__ void __launch_bounds__(256) noise_flip_kernel(DevProg P, uint64_t see
     if (r == 2) break;
     if (r == 0) continue;
     const int b = __ldg(site_block + site);
-    while (blk < b) {  // close the blocks before this fault's block
+    for (; blk < b; blk++) {
       bcount[(size_t)blk * W + w] = nb;
       nb = 0;
-      blk++;
     }
-    const int off = __ldg(P.case_pauli_off + cs), end = __ldg(P.case_pauli_off + cs + 1);
-    if (n + (uint32_t)(end - off) > cap) { over = true; break; }
-    for (int j = off; j < end; j++) flips[(size_t)(n++) * W + w] = ((uint32_t)__ldg(pslot + j) << 5) | (uint32_t)lane;
-    nb += (uint32_t)(end - off);
+    const int off = __ldg(P.case_pauli_off + cs), cnt = __ldg(P.case_pauli_off + cs + 1) - off;
+    if (n == cap || cnt > 31 || off >= (1 << 22)) { over = true; break; }
+    ent[(size_t)n * W + w] = ((uint32_t)off << 10) | ((uint32_t)cnt << 5) | (uint32_t)lane;
+    n++;
+    nb++;
   }
   if (over) {
-    bcount[w] = 0xFFFFFFFFu;
+    ntot[w] = 0xFFFFFFFFu;
     return;
   }
   for (; blk < nblocks; blk++) {
     bcount[(size_t)blk * W + w] = nb;
     nb = 0;
   }
+  ntot[w] = n;
 }
 
-// apply the n flips of this word's current NoiseBlock
-__device__ __forceinline__ void jit_apply_flips(uint32_t* F, const uint32_t* __restrict__ flips, uint32_t W,
-                                                uint32_t w, uint32_t& cur, uint32_t n) {
-  uint32_t t = 0;
-  for (; t + 4 <= n; t += 4) {
-    const uint32_t e0 = __ldg(flips + (size_t)(cur + t) * W + w), e1 = __ldg(flips + (size_t)(cur + t + 1) * W + w);
-    const uint32_t e2 = __ldg(flips + (size_t)(cur + t + 2) * W + w), e3 = __ldg(flips + (size_t)(cur + t + 3) * W + w);
-    F[(e0 >> 5) * 32] ^= 1u << (e0 & 31);
-    F[(e1 >> 5) * 32] ^= 1u << (e1 & 31);
-    F[(e2 >> 5) * 32] ^= 1u << (e2 & 31);
-    F[(e3 >> 5) * 32] ^= 1u << (e3 & 31);
-  }
-  for (; t < n; t++) {
-    const uint32_t e = __ldg(flips + (size_t)(cur + t) * W + w);
-    F[(e >> 5) * 32] ^= 1u << (e & 31);
+// apply n staged fault entries (stage[t * 32 + lane]) to the frame
+__device__ __forceinline__ void jit_apply_faults(uint32_t* F, const uint32_t* stage, const uint16_t* __restrict__ pslot,
+                                                 int lane, uint32_t& cur, uint32_t n) {
+  for (uint32_t t = 0; t < n; t++) {
+    const uint32_t e = stage[(cur + t) * 32 + lane];
+    const uint32_t bit = 1u << (e & 31);
+    const int off = (int)(e >> 10), cnt = (int)((e >> 5) & 31);
+    for (int j = 0; j < cnt; j++) F[(uint32_t)__ldg(pslot + off + j) * 32] ^= bit;
   }
   cur += n;
 }

@@ -86,8 +86,9 @@ struct fs_prog {
   void* flist = nullptr;  // per-word fault lists for the specialised kernel
   size_t flist_bytes = 0;
   uint32_t flist_cap = 0;
-  int* d_site_block = nullptr;
+  int* d_site_block = nullptr;  // flip geometry: block_hi | row_off | block_cap
   int jit_nblocks = 0;
+  int flip_rows = 0, flip_capmax = 0;
   // segmented general engine: ping-pong survivor state stores
   void* seg_pool[2] = {nullptr, nullptr};
   size_t seg_bytes[2] = {0, 0};
@@ -276,7 +277,8 @@ extern "C" int fs_debug_jit_source(const fs_prog_desc* d, char* buf, size_t len)
   std::vector<int32_t> bs(d->bit_slot, d->bit_slot + R + D), pl(d->plans, d->plans + 2 * d->num_plans);
   std::vector<int32_t> cpo(d->case_pauli_off, d->case_pauli_off + d->num_cases + 1);
   std::vector<int32_t> sco(d->site_case_off, d->site_case_off + E + 1);
-  fsjit::FrameKernelSource K = fsjit::gen_frame_kernel(*d, ins, g, pa, rl, ro, bs, pl, cpo, sco);
+  std::vector<double> sp(d->site_prob, d->site_prob + E);
+  fsjit::FrameKernelSource K = fsjit::gen_frame_kernel(*d, ins, g, pa, rl, ro, bs, pl, cpo, sco, sp);
   if (buf && len) {
     size_t m = std::min(len - 1, K.src.size());
     std::memcpy(buf, K.src.data(), m);
@@ -311,17 +313,13 @@ int occupancy_blocks(K kernel, int threads, size_t smem) {
 
 // ------------------------------------------------------------------ program-specialised kernel
 int ensure_jit(fs_prog* p) {
-  {
-    cudaError_t pre = cudaGetLastError();
-    if (pre != cudaSuccess) return set_error(FS_ERR_CUDA, std::string("before ensure_jit: ") + cudaGetErrorString(pre));
-  }
   if (p->jit_state == 1) return FS_OK;
   if (p->jit_state == -1) return set_error(FS_ERR_ARG, p->jit_error);
   p->jit_state = -1;
   fsjit::FrameKernelSource K = fsjit::gen_frame_kernel(p->desc, p->h_instrs, p->h_gates, p->h_paulis, p->h_reclists,
                                                        p->h_record_out, p->h_bit_slot, p->h_plans,
-                                                       p->h_case_pauli_off, p->h_site_case_off);
-  const size_t smem = (size_t)4 * K.nslots * 32 * sizeof(uint32_t);
+                                                       p->h_case_pauli_off, p->h_site_case_off, p->h_site_prob);
+  const size_t smem = (size_t)4 * (K.nslots + fsjit::kJitStage) * 32 * sizeof(uint32_t);
   if (smem > kSmemBudget) { p->jit_error = "frame too large for the specialised kernel"; return FS_ERR_ARG; }
   std::string err = fsjit::compile(K.src, fsjit::self_dir() + "/../csrc", p->jit);
   if (!err.empty()) { p->jit_error = err; return set_error(FS_ERR_ARG, err); }
@@ -333,25 +331,10 @@ int ensure_jit(fs_prog* p) {
   FS_CUDA_TRY(cudaMalloc(&p->d_pslot, sizeof(uint16_t) * K.pslot.size()));
   FS_CUDA_TRY(cudaMemcpy(p->d_pslot, K.pslot.data(), sizeof(uint16_t) * K.pslot.size(), cudaMemcpyHostToDevice));
   p->jit_nslots = K.nslots;
-  // flip capacity per 32-shot word: mean + 8 sigma + 64 (overflow falls back in-kernel)
-  double mu = 0.0;
-  for (int s = 0; s < p->desc.num_sites; s++) {
-    const int c0 = p->h_site_case_off[s], c1 = p->h_site_case_off[s + 1];
-    double wsum = 0.0;
-    for (int c = c0; c < c1; c++) wsum += p->h_case_pauli_off[c + 1] - p->h_case_pauli_off[c];
-    const double avgw = c1 > c0 ? wsum / (c1 - c0) : 0.0;
-    mu += 32.0 * std::min(1.0, p->h_site_prob[s]) * std::max(1.0, avgw);
-  }
-  p->flist_cap = (uint32_t)std::min(1.0e6, mu + 8.0 * std::sqrt(mu) + 64.0);
-  if (const char* fc = getenv("FS_JIT_FLIPCAP")) p->flist_cap = (uint32_t)atoi(fc);  // testing
   p->jit_nblocks = K.nblocks;
   FS_CUDA_TRY(cudaMalloc(&p->d_site_block, sizeof(int) * K.site_block.size()));
   FS_CUDA_TRY(cudaMemcpy(p->d_site_block, K.site_block.data(), sizeof(int) * K.site_block.size(), cudaMemcpyHostToDevice));
   p->jit_state = 1;
-  {
-    cudaError_t pre = cudaGetLastError();
-    if (pre != cudaSuccess) return set_error(FS_ERR_CUDA, std::string("end of ensure_jit: ") + cudaGetErrorString(pre));
-  }
   return FS_OK;
 }
 
@@ -781,15 +764,15 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     int rc = ensure_jit(p);
     if (rc == FS_OK) {
       fsjit::Api& J = fsjit::api();
-      const size_t smem = (size_t)4 * p->jit_nslots * 32 * sizeof(uint32_t);
+      const size_t smem = (size_t)4 * (p->jit_nslots + fsjit::kJitStage) * 32 * sizeof(uint32_t);
       int occ = 1;
       J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->jit.fn, 128, smem);
       const size_t groups = (W + 127) / 128;
       const size_t grid = std::min<size_t>(groups, (size_t)p->num_sms * std::max(occ, 1));
-      // 1) per-word noise flips (high-occupancy generator kernel)
-      const uint32_t cap = p->flist_cap;
+      // 1) per-word fault lists (high-occupancy generator kernel)
       const int nb = std::max(1, p->jit_nblocks);
-      const size_t need = align_up((size_t)cap * W * 4, 256) + (size_t)nb * W * 4 + 256;
+      const uint32_t cap = fsjit::kJitStage;
+      const size_t need = align_up((size_t)cap * W * 4, 256) + align_up((size_t)nb * W * 4, 256) + W * 4 + 256;
       if (need > p->flist_bytes) {
         cudaFree(p->flist);
         p->flist = nullptr;
@@ -797,25 +780,20 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
         FS_CUDA_TRY(cudaMalloc(&p->flist, need));
         p->flist_bytes = need;
       }
-      uint32_t* flips = static_cast<uint32_t*>(p->flist);
-      uint32_t* bcount = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(p->flist) + align_up((size_t)cap * W * 4, 256));
-      {
-        cudaError_t pre = cudaGetLastError();
-        if (pre != cudaSuccess) return set_error(FS_ERR_CUDA, std::string("before noise_flip_kernel: ") + cudaGetErrorString(pre));
-      }
-      fs::noise_flip_kernel<<<(unsigned)((W + 255) / 256), 256, 0, stream>>>(dp, a.seed, a.shot0 >> 5, (uint32_t)W,
-                                                                             p->d_pslot, p->d_site_block, nb,
-                                                                             flips, bcount, cap);
-      {
-        cudaError_t e2 = cudaGetLastError();
-        if (e2 != cudaSuccess) return set_error(FS_ERR_CUDA, std::string("noise_flip_kernel launch: ") + cudaGetErrorString(e2));
-      }
+      unsigned char* fb8 = static_cast<unsigned char*>(p->flist);
+      uint32_t* fent = reinterpret_cast<uint32_t*>(fb8);
+      uint32_t* bcount = reinterpret_cast<uint32_t*>(fb8 + align_up((size_t)cap * W * 4, 256));
+      uint32_t* ntot = reinterpret_cast<uint32_t*>(fb8 + align_up((size_t)cap * W * 4, 256) + align_up((size_t)nb * W * 4, 256));
+      fs::fault_list_kernel<<<(unsigned)((W + 255) / 256), 256, 0, stream>>>(
+          dp, a.seed, a.shot0 >> 5, (uint32_t)W, p->d_site_block, p->jit_nblocks, fent, bcount, ntot, cap);
+      FS_CUDA_TRY(cudaGetLastError());
       // 2) the program-specialised frame kernel
       fs::DevProg dpv = dp;
       const uint16_t* ps = p->d_pslot;
-      const uint32_t* fl = flips;
+      const uint32_t* fl = fent;
       const uint32_t* fc = bcount;
-      void* args[] = {&dpv, &a, &ps, &fl, &fc};
+      const uint32_t* ft = ntot;
+      void* args[] = {&dpv, &a, &ps, &fl, &fc, &ft};
       int r = J.cuLaunchKernel(p->jit.fn, (unsigned)grid, 1, 1, 128, 1, 1, (unsigned)smem, stream, args, nullptr);
       if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_jit_frame) failed: " + std::to_string(r));
       return FS_OK;
