@@ -186,7 +186,8 @@ def algorithmic_bytes_per_shot(P: Program) -> float:
     return P.output_bits() / 8.0
 
 
-def time_gpu_config(cfg: int, steps: int, warmup: int, rank: int, shots: int | None = None) -> dict:
+def time_gpu_config(cfg: int, steps: int, warmup: int, rank: int, shots: int | None = None,
+                    warm_shots: int | None = None) -> dict:
     import torch
 
     from paper_2604_27058_b200.engine import DeviceProgram
@@ -199,7 +200,7 @@ def time_gpu_config(cfg: int, steps: int, warmup: int, rank: int, shots: int | N
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
     for w in range(warmup):
-        dp.sample_device(shots, out, seed=1000 + w, shot0=shot0)
+        dp.sample_device(warm_shots or shots, out, seed=1000 + w, shot0=shot0)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for k in range(steps):
@@ -212,6 +213,77 @@ def time_gpu_config(cfg: int, steps: int, warmup: int, rank: int, shots: int | N
     st = int(out["status"].item())
     return {"P": P, "dp": dp, "shots": shots, "shot0": shot0, "ms": ms, "status": st,
             "engine": dp.engine(0), "out": out}
+
+
+def fp64_peak() -> float:
+    """Measured FP64 FMA throughput (TFLOP/s) of this device: the on-chip roofline denominator."""
+    import ctypes as C
+
+    from paper_2604_27058_b200 import _lib
+
+    v = C.c_double(0.0)
+    L = _lib.lib()
+    L.fs_debug_fp64_peak.argtypes = [C.POINTER(C.c_double)]
+    L.fs_debug_fp64_peak(C.byref(v))
+    return float(v.value)
+
+
+def segment_work(P: Program) -> list[tuple[int, int, int]]:
+    """(begin, end, W) of the post-select segments (the whole program if none)."""
+    ops = P.instrs[:, 0] & 0xFF
+    bounds = [0] + [int(i) + 1 for i in np.nonzero(ops == 14)[0] if i + 1 < P.num_instrs] + [P.num_instrs]
+    arr = (1, 2, 4, 7, 8, 9)
+    out = []
+    for b, e in zip(bounds[:-1], bounds[1:]):
+        w = sum(1 << int(P.instrs[i, 6]) for i in range(b, e) if int(ops[i]) in arr)
+        out.append((b, e, w))
+    return out
+
+
+def extra_config(c: int, fp64_tflops: float) -> dict:
+    """Side measurement of another BASELINE config with its own roofline."""
+    import ctypes as C
+
+    steps = 1 if c == 3 else 3
+    rc = time_gpu_config(c, steps, 1, 0, warm_shots=64 if c == 3 else None)
+    P, shots = rc["P"], rc["shots"]
+    ms = float(np.mean(rc["ms"]))
+    rate = shots / (ms / 1e3)
+    d = {"shots_per_s": rate, "ms_per_step": ms, "shots": shots, "k_max": P.k_max, "engine": rc["engine"],
+         "status": rc["status"]}
+    if c == 3:  # HBM bound: 32 B (one complex128 read + write) per element-sweep
+        W = P.work()
+        ach = 32.0 * W * rate / 1e9
+        pk = peaks()["hbm_gbs"]
+        d["roofline"] = {"bound": "hbm", "unit": "GB/s", "achieved": ach, "peak": pk, "frac": ach / pk,
+                         "algorithmic_bytes_per_shot": 32.0 * W,
+                         "note": "W = sum of 2^k over array instructions (reference plan_metrics); "
+                                 "the engine touches only changed elements, so frac can exceed 1"}
+    else:  # on-chip bound: 8 FP64 flop per element-sweep of the executed instructions
+        segs = segment_work(P)
+        if len(segs) > 1:
+            L = rc["dp"]._lib
+            L.fs_debug_seg_counts.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.c_int]
+            buf = (C.c_uint32 * 4096)()
+            n = L.fs_debug_seg_counts(rc["dp"]._h, buf, 4096)
+            counts = list(buf[:n])
+            # counts: per chunk, [n_in(seg0), n_out(seg0)=n_in(seg1), ...]
+            wexec, i = 0.0, 0
+            while i < len(counts):
+                chunk = counts[i:i + len(segs)]
+                for (b, e, w), nin in zip(segs, chunk):
+                    wexec += w * nin
+                i += len(segs)
+            w_exec = wexec / shots
+        else:
+            w_exec = float(segs[0][2])
+        ach = 8.0 * w_exec * rate / 1e12
+        d["roofline"] = {"bound": "fp64", "unit": "TFLOP/s", "achieved": ach, "peak": fp64_tflops,
+                         "frac": ach / fp64_tflops if fp64_tflops else None,
+                         "w_exec_per_shot": w_exec, "flop_per_shot": 8.0 * w_exec,
+                         "peak_source": "measured FP64 FMA microbenchmark (fs_debug_fp64_peak)"}
+    del rc
+    return d
 
 
 def time_e2e(dp, P, shots: int, shot0: int, steps: int) -> dict:
@@ -328,18 +400,15 @@ def main():
 
     extra = {}
     if not args.no_extra and rank == 0:
-        for c in (0, 2, 4):
+        fp64 = fp64_peak()
+        for c in (0, 2, 3, 4):
             if c == args.config:
                 continue
             try:
-                rc = time_gpu_config(c, 3, 1, 0)
-                ms = float(np.mean(rc["ms"]))
-                extra[f"config{c}"] = {"shots_per_s": rc["shots"] / (ms / 1e3), "ms_per_step": ms,
-                                       "shots": rc["shots"], "k_max": rc["P"].k_max,
-                                       "engine": rc["engine"], "status": rc["status"]}
-                del rc
+                extra[f"config{c}"] = extra_config(c, fp64)
             except Exception as exc:  # report, don't mask
                 extra[f"config{c}"] = {"error": repr(exc)}
+        extra["fp64_peak_tflops_measured"] = fp64
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         cpu = cpu_reference_rate(args.config, target_s=8.0)

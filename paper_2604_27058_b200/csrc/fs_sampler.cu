@@ -91,6 +91,7 @@ struct fs_prog {
   int flip_rows = 0, flip_capmax = 0;
   // segmented general engine: ping-pong survivor state stores
   void* seg_pool[2] = {nullptr, nullptr};
+  std::vector<uint32_t> seg_counts;  // diagnostics: shots entering each segment (per chunk)
   size_t seg_bytes[2] = {0, 0};
   // large-k engine state
   void* hbm = nullptr;
@@ -265,6 +266,44 @@ static bool wants_general(const fs_prog* p, uint32_t flags, const fs_trace_out* 
   return false;
 }
 
+// Diagnostics (not part of include/fs_sampler.h): measured FP64 FMA throughput of this device,
+// the denominator of the on-chip roofline of the small-k configurations (bench.py).
+__global__ void fp64_peak_kernel(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+  double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+  const double b = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; i++) {
+    a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+    a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+  }
+  if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 12345.0) out[0] = a0;
+}
+
+extern "C" int fs_debug_fp64_peak(double* tflops) {
+  if (!tflops) return FS_ERR_ARG;
+  int dev = 0, sms = 0;
+  FS_CUDA_TRY(cudaGetDevice(&dev));
+  FS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* d = nullptr;
+  FS_CUDA_TRY(cudaMalloc(&d, 8));
+  const int iters = 1 << 14, threads = 256, blocks = sms * 8;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fp64_peak_kernel<<<blocks, threads>>>(d, iters);  // warm-up
+  cudaEventRecord(e0);
+  for (int r = 0; r < 5; r++) fp64_peak_kernel<<<blocks, threads>>>(d, iters);
+  cudaEventRecord(e1);
+  FS_CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  *tflops = 5.0 * blocks * threads * (double)iters * 8 * 2 / (ms * 1e-3) / 1e12;
+  return FS_OK;
+}
+
 // Diagnostics (not part of include/fs_sampler.h): source of the program-specialised frame kernel
 // and the state of its compilation.  Used by tests/test_host.py to compile the generated
 // kernel with NVRTC on a CPU-only host.
@@ -285,6 +324,14 @@ extern "C" int fs_debug_jit_source(const fs_prog_desc* d, char* buf, size_t len)
     buf[m] = 0;
   }
   return (int)K.src.size();
+}
+
+// segmented engine: shots entering each segment of the last call (chunks concatenated)
+extern "C" int fs_debug_seg_counts(fs_prog* p, uint32_t* out, int cap) {
+  if (!p) return -1;
+  const int n = (int)p->seg_counts.size();
+  for (int i = 0; i < n && i < cap; i++) out[i] = p->seg_counts[i];
+  return n;
 }
 
 extern "C" const char* fs_debug_jit_status(fs_prog* p) {
@@ -458,8 +505,10 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   const uint64_t chunk = (uint64_t)1 << 22;
   if (!p->d_counts) FS_CUDA_TRY(cudaMalloc(&p->d_counts, 64));
   uint32_t* d_nout = reinterpret_cast<uint32_t*>(p->d_counts);
+  p->seg_counts.clear();
   for (uint64_t c0 = 0; c0 < a.nshots; c0 += chunk) {
     uint32_t n_in = (uint32_t)std::min<uint64_t>(chunk, a.nshots - c0);
+    p->seg_counts.push_back(n_in);
     int cur = 0;  // which pool holds the input store
     for (int sgi = 0; sgi < nseg; sgi++) {
       const int b = bounds[sgi], e = bounds[sgi + 1];
@@ -500,6 +549,7 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
       uint32_t n_out = 0;
       FS_CUDA_TRY(cudaMemcpyAsync(&n_out, d_nout, 4, cudaMemcpyDeviceToHost, stream));
       FS_CUDA_TRY(cudaStreamSynchronize(stream));
+      p->seg_counts.push_back(n_out);
       if (n_out == 0) break;
       S.in = S.out;
       cur = 1 - cur;
