@@ -14,7 +14,9 @@
 #pragma once
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include <sstream>
@@ -297,6 +299,303 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   return K;
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Program-specialised kernel for the general engine (0 < k_max <= 7, no PostSelect, Philox,
+// free sampling): warp = 32-shot word, lane = shot.  Frame words are per-lane registers holding
+// the same (warp-uniform) value in every lane, with H / SWAP / MeasDormantRandom's x<->z as
+// compile-time renaming; noise faults are applied through a per-warp shared-memory shadow of the
+// touched slots.  The active array is in registers (k_max <= 4) or in shared memory at constant
+// offsets (interleaved [i][lane]); every array operation is unrolled with constant indices and
+// uses the same rounding sequence as the interpreter (bit-identical results).
+inline std::string hexd(double v) {
+  char b[64];
+  snprintf(b, sizeof b, "%a", v);
+  return b;
+}
+
+struct GeneralKernelSource {
+  std::string src;
+  std::vector<uint16_t> pslot;
+  int nslots = 0, cap_log2 = 0, nblocks = 0;
+  bool arr_regs = true;
+  std::vector<int32_t> site_block;
+};
+
+inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::vector<int32_t>& ins_all,
+                                              const std::vector<uint32_t>& gates, const std::vector<uint32_t>& paulis,
+                                              const std::vector<int32_t>& reclists,
+                                              const std::vector<int32_t>& record_out,
+                                              const std::vector<int32_t>& bit_slot,
+                                              const std::vector<int32_t>& case_pauli_off,
+                                              const std::vector<int32_t>& site_case_off,
+                                              const std::vector<double>& fparams) {
+  GeneralKernelSource K;
+  const int n = d.n, R = d.record_count;
+  K.nslots = 2 * n;
+  K.cap_log2 = d.k_max;
+  K.arr_regs = d.k_max <= 4;
+  K.pslot.assign(paulis.size() + 1, 0);
+  K.site_block.assign(d.num_sites + 1, 0);
+  for (int i = 0, b = 0; i < d.num_instrs; i++)
+    if (FS_OPCODE(ins_all[(size_t)i * FS_INS_WORDS]) == FS_OP_NOISE) {
+      for (int s2 = ins_all[(size_t)i * FS_INS_WORDS + 1]; s2 < ins_all[(size_t)i * FS_INS_WORDS + 2]; s2++) K.site_block[s2] = b;
+      K.nblocks = ++b;
+    }
+  std::vector<int> phys(2 * n);
+  for (int v = 0; v < 2 * n; v++) phys[v] = v;
+  auto X = [&](int q) { return phys[q]; };
+  auto Z = [&](int q) { return phys[n + q]; };
+  auto f = [&](int slot) { return "f" + std::to_string(slot); };
+  auto A = [&](int i) {
+    return K.arr_regs ? "a" + std::to_string(i) : "AR[" + std::to_string(i * 32) + "]";
+  };
+  auto C = [&](int off) { return "make_double2(" + hexd(fparams[off]) + ", " + hexd(fparams[off + 1]) + ")"; };
+  const int cap = 1 << d.k_max;
+  std::ostringstream o;
+  o << "#include \"fs_jit_kernels.cuh\"\n";
+  o << "using fs::cmul; using fs::cadd; using fs::csub; using fs::cscale; using fs::cnorm2;\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << (K.arr_regs ? 128 : 64)
+    << ") fs_jit_general(fs::DevProg P, fs::RunArgs A, const uint16_t* __restrict__ pslot, "
+       "const uint32_t* __restrict__ fent, const uint32_t* __restrict__ bcount, const uint32_t* __restrict__ ntot) {\n";
+  o << "  extern __shared__ __align__(16) unsigned char smem[];\n";
+  o << "  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;\n";
+  const int fs_words = (2 * n + 3) / 4 * 4;
+  o << "  uint32_t* Fs = reinterpret_cast<uint32_t*>(smem) + wib * " << fs_words << ";\n";
+  if (!K.arr_regs)
+    o << "  double2* AR = reinterpret_cast<double2*>(smem + nw * " << fs_words * 4 << ") + wib * " << cap * 32
+      << " + lane;\n";
+  o << "  const uint64_t word0 = A.shot0 >> 5;\n  const uint64_t seed = A.seed;\n";
+  o << "  for (uint32_t w = blockIdx.x * nw + wib; w < A.W; w += gridDim.x * nw) {\n";
+  o << "    const uint64_t si = (uint64_t)w * 32 + lane;\n    const bool valid = si < A.nshots;\n";
+  o << "    const uint64_t shot = A.shot0 + si;\n    const uint64_t wabs = word0 + w;\n";
+  o << "    const uint32_t validm = __ballot_sync(0xFFFFFFFFu, valid);\n";
+  o << "    uint32_t alive = validm, errm = 0;\n";
+  for (int sl = 0; sl < 2 * n; sl++) o << "    uint32_t " << f(sl) << " = 0u;\n";
+  for (int sl = 0; sl < d.num_slots; sl++) o << "    uint32_t r" << sl << " = 0u;\n";
+  for (int j = 0; j < d.num_observables; j++) o << "    uint32_t ob" << j << " = 0u;\n";
+  if (K.arr_regs)
+    for (int i = 0; i < cap; i++) o << "    double2 a" << i << " = make_double2(" << (i == 0 ? "1.0" : "0.0") << ", 0.0);\n";
+  else
+    o << "    AR[0] = make_double2(1.0, 0.0);\n";
+  o << "    uint4 cb = make_uint4(0u, 0u, 0u, 0u);\n";
+  o << "    const uint32_t nt_ = ntot[w];\n    const bool fover = nt_ == 0xFFFFFFFFu;\n    uint32_t fcur = 0;\n";
+  o << "    fs::WordFaultGen gen;\n    int psite = -1, plane = 0, pcase = 0;\n    if (fover) gen.init(seed, wabs);\n";
+  auto put_record = [&](int rec, const std::string& expr) {
+    const int col = record_out[rec], sl = bit_slot[rec];
+    o << "    { const uint32_t rw = " << expr << ";";
+    if (col >= 0) o << " if (lane == 0) A.meas[(size_t)" << col << " * A.W + w] = rw & alive;";
+    if (sl >= 0) o << " r" << sl << " = rw;";
+    o << " }\n";
+  };
+  int coin_blk = -1, nblk = 0;
+  for (int i = 0; i < d.num_instrs; i++) {
+    const int* I = ins_all.data() + (size_t)i * FS_INS_WORDS;
+    const int op = FS_OPCODE(I[0]);
+    const bool flip = FS_FLIP(I[0]);
+    const std::string flipm = flip ? " ^ 0xFFFFFFFFu" : "";
+    switch (op) {
+      case FS_OP_FRAME:
+        for (int j = 0; j < I[2]; j++) {
+          const uint32_t g = gates[I[1] + j];
+          const int a = FS_GATE_A(g), b = FS_GATE_B(g);
+          switch (FS_GATE_G(g)) {
+            case FS_G_H: std::swap(phys[a], phys[n + a]); break;
+            case FS_G_S: case FS_G_SDAG: o << "    " << f(Z(a)) << " ^= " << f(X(a)) << ";\n"; break;
+            case FS_G_CX: o << "    " << f(X(b)) << " ^= " << f(X(a)) << "; " << f(Z(a)) << " ^= " << f(Z(b)) << ";\n"; break;
+            case FS_G_CZ: o << "    " << f(Z(b)) << " ^= " << f(X(a)) << "; " << f(Z(a)) << " ^= " << f(X(b)) << ";\n"; break;
+            case FS_G_SWAP: std::swap(phys[a], phys[b]); std::swap(phys[n + a], phys[n + b]); break;
+          }
+        }
+        break;
+      case FS_OP_ARRAY_GATE: {
+        const int g = I[1], va = I[2], vb = I[3], a = I[4], b = I[5], size = 1 << I[6];
+        if (g == FS_G_S || g == FS_G_SDAG) {
+          for (int j = 0; j < size; j++)
+            if ((j >> a) & 1) o << "    " << A(j) << " = cmul(" << A(j) << ", make_double2(0.0, " << (g == FS_G_S ? "1.0" : "-1.0") << "));\n";
+          o << "    " << f(Z(va)) << " ^= " << f(X(va)) << ";\n";
+        } else if (g == FS_G_H) {
+          const int st = 1 << a;
+          for (int j = 0; j < size; j++)
+            if (!((j >> a) & 1))
+              o << "    { const double2 lo = " << A(j) << ", hi = " << A(j + st) << "; " << A(j)
+                << " = cscale(cadd(lo, hi), fs::kInvSqrt2); " << A(j + st) << " = cscale(csub(lo, hi), fs::kInvSqrt2); }\n";
+          std::swap(phys[va], phys[n + va]);
+        } else if (g == FS_G_CX) {
+          for (int j = 0; j < size; j++)
+            if (((j >> a) & 1) && !((j >> b) & 1))
+              o << "    { const double2 t0 = " << A(j) << "; " << A(j) << " = " << A(j | (1 << b)) << "; " << A(j | (1 << b)) << " = t0; }\n";
+          o << "    " << f(X(vb)) << " ^= " << f(X(va)) << "; " << f(Z(va)) << " ^= " << f(Z(vb)) << ";\n";
+        } else if (g == FS_G_CZ) {
+          for (int j = 0; j < size; j++)
+            if (((j >> a) & 1) && ((j >> b) & 1)) o << "    " << A(j) << " = make_double2(-" << A(j) << ".x, -" << A(j) << ".y);\n";
+          o << "    " << f(Z(vb)) << " ^= " << f(X(va)) << "; " << f(Z(va)) << " ^= " << f(X(vb)) << ";\n";
+        }
+        break;
+      }
+      case FS_OP_EXPAND: {
+        const int size = 1 << I[6];
+        o << "    { const int par = (" << f(X(I[1])) << " >> lane) & 1;\n";
+        o << "      const double2 ph0 = par ? " << C(I[5] + 4) << " : " << C(I[5]) << ";\n";
+        o << "      const double2 ph1 = par ? " << C(I[5] + 6) << " : " << C(I[5] + 2) << ";\n";
+        for (int j = 0; j < size; j++)
+          o << "      { const double2 v = " << A(j) << "; " << A(j) << " = cmul(v, ph0); " << A(size + j) << " = cmul(v, ph1); }\n";
+        o << "    }\n";
+        break;
+      }
+      case FS_OP_ARRAY_ROT: {
+        const int a = I[2], size = 1 << I[6];
+        o << "    { const int par = (" << f(X(I[1])) << " >> lane) & 1;\n";
+        o << "      const double2 ph0 = par ? " << C(I[5] + 2) << " : " << C(I[5]) << ";\n";
+        o << "      const double2 ph1 = par ? " << C(I[5]) << " : " << C(I[5] + 2) << ";\n";
+        for (int j = 0; j < size; j++) o << "      " << A(j) << " = cmul(" << A(j) << ", " << (((j >> a) & 1) ? "ph1" : "ph0") << ");\n";
+        o << "    }\n";
+        break;
+      }
+      case FS_OP_GAMMA_ROT:
+        break;  // global phase: no effect on records
+      case FS_OP_MEAS_DSTATIC:
+        put_record(I[3], f(X(I[1])) + flipm);
+        break;
+      case FS_OP_MEAS_DRANDOM: {
+        const int virt = I[1], ord = I[2];
+        if (ord / 4 != coin_blk) {
+          coin_blk = ord / 4;
+          o << "    cb = fs::coin_block(seed, wabs, " << coin_blk << ");\n";
+        }
+        const char* comp[4] = {"cb.x", "cb.y", "cb.z", "cb.w"};
+        o << "    { const uint32_t coin = " << comp[ord & 3] << "; const uint32_t pw = " << f(Z(virt)) << "; "
+          << f(Z(virt)) << " = pw ^ coin;";
+        const int col = record_out[I[3]], sl = bit_slot[I[3]];
+        o << " const uint32_t rw = coin ^ pw" << flipm << ";";
+        if (col >= 0) o << " if (lane == 0) A.meas[(size_t)" << col << " * A.W + w] = rw & alive;";
+        if (sl >= 0) o << " r" << sl << " = rw;";
+        o << " }\n";
+        std::swap(phys[virt], phys[n + virt]);
+        break;
+      }
+      case FS_OP_MEAS_COLLAPSE: {
+        const int virt = I[1], a = I[2], rec = I[3], size = 1 << I[6], half = size >> 1, st = 1 << a;
+        const int po = I[4] >> 8, pc = I[4] & 0xFF;
+        for (int j = 0; j < pc; j++) {
+          const uint32_t g = gates[po + j];
+          const int q = FS_GATE_A(g);
+          if (FS_GATE_G(g) == FS_G_H) std::swap(phys[q], phys[n + q]);
+          else o << "    " << f(Z(q)) << " ^= " << f(X(q)) << ";\n";
+        }
+        const int fo = I[5];
+        o << "    {\n      const double2 u00 = " << C(fo) << ", u01 = " << C(fo + 2) << ", u10 = " << C(fo + 4)
+          << ", u11 = " << C(fo + 6) << ";\n";
+        o << "      const int parity = (" << f(X(virt)) << " >> lane) & 1;\n";
+        o << "      double p1 = 0.0, p_all = 0.0;\n";
+        if (size == 2) {
+          o << "      { const double2 b0 = cadd(cmul(u00, " << A(0) << "), cmul(u01, " << A(1) << ")); const double2 b1 = cadd(cmul(u10, "
+            << A(0) << "), cmul(u11, " << A(1) << ")); p1 = cnorm2(b1); p_all = __dadd_rn(p1, cnorm2(b0)); }\n";
+        } else if (size <= 16) {
+          for (int j = 0; j < size; j++)
+            if (!((j >> a) & 1))
+              o << "      { const double2 a0_ = " << A(j) << ", a1_ = " << A(j + st)
+                << "; const double q1 = cnorm2(cadd(cmul(u10, a0_), cmul(u11, a1_))); const double2 b0 = cadd(cmul(u00, a0_), cmul(u01, a1_)); "
+                   "p1 = __dadd_rn(p1, q1); p_all = __dadd_rn(p_all, __dadd_rn(q1, cnorm2(b0))); }\n";
+        } else {
+          for (int j = 0; j < size; j++)
+            if (!((j >> a) & 1))
+              o << "      p1 = __dadd_rn(p1, cnorm2(cadd(cmul(" << A(j) << ", u10), cmul(u11, " << A(j + st) << "))));\n";
+          for (int j = 0; j < size; j++) o << "      p_all = __dadd_rn(p_all, cnorm2(" << A(j) << "));\n";
+        }
+        o << "      const bool bad = p1 != p1;\n";
+        o << "      p1 = p_all > 0 ? __ddiv_rn(p1, p_all) : 0.0;\n      if (p1 < 0.0) p1 = 0.0; else if (p1 > 1.0) p1 = 1.0;\n";
+        o << "      const uint4 bo = fs::philox((uint32_t)shot, (uint32_t)(shot >> 32), " << i << "u, fs::TAG_BORN << 24, seed);\n";
+        o << "      int br = fs::u64_to_unit(((uint64_t)bo.y << 32) | bo.x) < p1 ? 1 : 0;\n";
+        o << "      double pb = br ? p1 : __dsub_rn(1.0, p1);\n";
+        o << "      if (pb < fs::kBranchFloor) { br ^= 1; pb = __dsub_rn(1.0, pb); }\n";
+        o << "      const double scale = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(pb, p_all)));\n";
+        o << "      const double2 k0 = br == 0 ? cscale(u00, scale) : cscale(u10, scale);\n";
+        o << "      const double2 k1 = br == 0 ? cscale(u01, scale) : cscale(u11, scale);\n";
+        for (int j = 0; j < half; j++) {
+          const int i0 = ((j >> a) << (a + 1)) | (j & (st - 1));
+          o << "      " << A(j) << " = cadd(cmul(k0, " << A(i0) << "), cmul(k1, " << A(i0 + st) << "));\n";
+        }
+        o << "      const uint32_t badw = __ballot_sync(0xFFFFFFFFu, bad && ((alive >> lane) & 1));\n";
+        o << "      errm |= badw; alive &= ~badw;\n";
+        o << "      const uint32_t recw = __ballot_sync(0xFFFFFFFFu, (br ^ parity ^ " << (flip ? 1 : 0) << ") != 0);\n";
+        o << "      const uint32_t brw = __ballot_sync(0xFFFFFFFFu, br != 0);\n";
+        o << "      " << f(X(virt)) << " ^= brw;\n";
+        const int col = record_out[rec], sl = bit_slot[rec];
+        if (col >= 0) o << "      if (lane == 0) A.meas[(size_t)" << col << " * A.W + w] = recw & alive;\n";
+        if (sl >= 0) o << "      r" << sl << " = recw;\n";
+        o << "    }\n";
+        break;
+      }
+      case FS_OP_COND_FRAME: {
+        const int sl = bit_slot[I[3]];
+        for (int j = I[1]; j < I[1] + I[2]; j++) {
+          const uint32_t e = paulis[j];
+          const int q = FS_PAULI_Q(e);
+          o << "    " << f(FS_PAULI_Z(e) ? Z(q) : X(q)) << " ^= r" << sl << ";\n";
+        }
+        break;
+      }
+      case FS_OP_NOISE: {
+        // touched physical slots of this block; pslot under the current renaming
+        std::vector<int> touched;
+        for (int s2 = I[1]; s2 < I[2]; s2++)
+          for (int c = site_case_off[s2]; c < site_case_off[s2 + 1]; c++)
+            for (int j = case_pauli_off[c]; j < case_pauli_off[c + 1]; j++) {
+              const uint32_t e = paulis[j];
+              const int q = FS_PAULI_Q(e);
+              const int sl = FS_PAULI_Z(e) ? Z(q) : X(q);
+              K.pslot[j] = (uint16_t)sl;
+              touched.push_back(sl);
+            }
+        std::sort(touched.begin(), touched.end());
+        touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+        o << "    {\n";
+        for (int sl : touched) o << "      Fs[" << sl << "] = " << f(sl) << ";\n";
+        o << "      __syncwarp();\n      if (lane == 0) {\n";
+        o << "        if (!fover) {\n          const uint32_t nb_ = __ldg(bcount + (size_t)" << nblk << " * A.W + w);\n";
+        o << "          for (uint32_t t = 0; t < nb_; t++) {\n";
+        o << "            const uint32_t e = __ldg(fent + (size_t)(fcur + t) * A.W + w);\n";
+        o << "            const uint32_t bit = 1u << (e & 31);\n            const int off = (int)(e >> 10), cnt = (int)((e >> 5) & 31);\n";
+        o << "            for (int j = 0; j < cnt; j++) Fs[__ldg(pslot + off + j)] ^= bit;\n          }\n";
+        o << "          fcur += nb_;\n        } else {\n";
+        o << "          for (;;) {\n            if (psite < 0) { int st_, ln_, cs_; const int r_ = gen.step(P, st_, ln_, cs_);\n";
+        o << "              if (r_ == 2) { psite = 0x7FFFFFFF; break; } if (r_ == 0) continue; psite = st_; plane = ln_; pcase = cs_; }\n";
+        o << "            if (psite >= " << I[2] << ") break;\n";
+        o << "            for (int j = __ldg(P.case_pauli_off + pcase); j < __ldg(P.case_pauli_off + pcase + 1); j++) Fs[__ldg(pslot + j)] ^= 1u << plane;\n";
+        o << "            psite = -1;\n          }\n        }\n      }\n      __syncwarp();\n";
+        for (int sl : touched) o << "      " << f(sl) << " = Fs[" << sl << "];\n";
+        o << "      __syncwarp();\n    }\n";
+        nblk++;
+        break;
+      }
+      case FS_OP_DETECTOR:
+      case FS_OP_OBSERVABLE: {
+        std::ostringstream e;
+        e << "0u";
+        for (int j = 0; j < I[3]; j++) e << " ^ r" << bit_slot[reclists[I[2] + j]];
+        if (op == FS_OP_DETECTOR) {
+          const int sl = bit_slot[R + I[1]];
+          o << "    { const uint32_t dw = " << e.str() << "; if (lane == 0) A.det[(size_t)" << I[1] << " * A.W + w] = dw & alive;";
+          if (sl >= 0) o << " r" << sl << " = dw;";
+          o << " }\n";
+        } else {
+          o << "    ob" << I[1] << " ^= (" << e.str() << ") & alive;\n";
+        }
+        break;
+      }
+      default:
+        break;
+    }
+  }
+  o << "    if (lane == 0) {\n";
+  for (int j = 0; j < d.num_observables; j++) o << "      A.obs[(size_t)" << j << " * A.W + w] = ob" << j << " & validm;\n";
+  o << "      A.accepted[w] = alive & validm;\n      A.error[w] = errm;\n      if (errm) atomicMax(A.status, FS_ERR_SHOT_NAN);\n    }\n";
+  o << "    __syncwarp();\n  }\n}\n";
+  K.src = o.str();
+  return K;
+}
+
 struct Compiled {
   CUmodule mod = nullptr;
   CUfunction fn = nullptr;
@@ -305,11 +604,12 @@ struct Compiled {
   std::string log;
 };
 
-inline std::string compile(const std::string& src, const std::string& incdir, Compiled& out) {
+inline std::string compile(const std::string& src, const std::string& incdir, Compiled& out,
+                           const char* kname = "fs_jit_frame") {
   Api& A = api();
   if (!A.ok) return "JIT unavailable: " + A.why;
   void* prog = nullptr;
-  if (A.nvrtcCreateProgram(&prog, src.c_str(), "fs_jit_frame.cu", 0, nullptr, nullptr) != 0)
+  if (A.nvrtcCreateProgram(&prog, src.c_str(), (std::string(kname) + ".cu").c_str(), 0, nullptr, nullptr) != 0)
     return "nvrtcCreateProgram failed";
   std::string inc = "-I" + incdir;
   const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", inc.c_str(), "-DFS_JIT=1"};
@@ -331,7 +631,7 @@ inline std::string compile(const std::string& src, const std::string& incdir, Co
   out.cubin_bytes = csz;
   CUresult r = A.cuModuleLoadData(&out.mod, cubin.data());
   if (r != 0) return "cuModuleLoadData failed (" + std::to_string(r) + ")";
-  r = A.cuModuleGetFunction(&out.fn, out.mod, "fs_jit_frame");
+  r = A.cuModuleGetFunction(&out.fn, out.mod, kname);
   if (r != 0) return "cuModuleGetFunction failed (" + std::to_string(r) + ")";
   return "";
 }

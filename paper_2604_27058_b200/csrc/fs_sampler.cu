@@ -89,6 +89,8 @@ struct fs_prog {
   int* d_site_block = nullptr;  // flip geometry: block_hi | row_off | block_cap
   int jit_nblocks = 0;
   int flip_rows = 0, flip_capmax = 0;
+  int gjit_threads = 128;
+  size_t gjit_smem = 0;
   // segmented general engine: ping-pong survivor state stores
   void* seg_pool[2] = {nullptr, nullptr};
   std::vector<uint32_t> seg_counts;  // diagnostics: shots entering each segment (per chunk)
@@ -334,6 +336,19 @@ extern "C" int fs_debug_seg_counts(fs_prog* p, uint32_t* out, int cap) {
   return n;
 }
 
+extern "C" int fs_debug_gjit_source(fs_prog* p, char* buf, size_t len) {
+  if (!p) return -1;
+  fsjit::GeneralKernelSource K = fsjit::gen_general_kernel(p->desc, p->h_instrs, p->h_gates, p->h_paulis,
+                                                           p->h_reclists, p->h_record_out, p->h_bit_slot,
+                                                           p->h_case_pauli_off, p->h_site_case_off, p->h_fparams);
+  if (buf && len) {
+    size_t m = std::min(len - 1, K.src.size());
+    std::memcpy(buf, K.src.data(), m);
+    buf[m] = 0;
+  }
+  return (int)K.src.size();
+}
+
 extern "C" const char* fs_debug_jit_status(fs_prog* p) {
   static thread_local std::string s;
   if (!p) return "null";
@@ -556,6 +571,66 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
       n_in = n_out;
     }
   }
+  return FS_OK;
+}
+
+// program-specialised general kernel (0 < k_max <= 7, no PostSelect / MeasActive / Retire)
+bool gjit_supported(const fs_prog* p) {
+  if (p->dp.k_max < 1 || p->dp.k_max > 7) return false;
+  for (int i = 0; i < p->dp.num_instrs; i++) {
+    const int op = FS_OPCODE(p->h_instrs[(size_t)i * FS_INS_WORDS]);
+    if (op == FS_OP_POSTSELECT || op == FS_OP_MEAS_ACTIVE || op == FS_OP_RETIRE) return false;
+  }
+  return true;
+}
+
+int ensure_gjit(fs_prog* p) {
+  if (p->jit_state == 1) return FS_OK;
+  if (p->jit_state == -1) return set_error(FS_ERR_ARG, p->jit_error);
+  p->jit_state = -1;
+  fsjit::GeneralKernelSource K = fsjit::gen_general_kernel(p->desc, p->h_instrs, p->h_gates, p->h_paulis,
+                                                           p->h_reclists, p->h_record_out, p->h_bit_slot,
+                                                           p->h_case_pauli_off, p->h_site_case_off, p->h_fparams);
+  const int nw = K.arr_regs ? 4 : 2;
+  const size_t fs_words = (size_t)(2 * p->dp.n + 3) / 4 * 4;
+  const size_t smem = nw * fs_words * 4 + (K.arr_regs ? 0 : (size_t)nw * 32 * 16 * ((size_t)1 << K.cap_log2));
+  if (smem > kSmemBudget) { p->jit_error = "program too large for the specialised general kernel"; return FS_ERR_ARG; }
+  std::string err = fsjit::compile(K.src, fsjit::self_dir() + "/../csrc", p->jit, "fs_jit_general");
+  if (!err.empty()) { p->jit_error = err; return set_error(FS_ERR_ARG, err); }
+  fsjit::Api& J = fsjit::api();
+  if (J.cuFuncSetAttribute(p->jit.fn, 8, (int)smem) != 0) { p->jit_error = "cuFuncSetAttribute failed"; return FS_ERR_ARG; }
+  FS_CUDA_TRY(cudaMalloc(&p->d_pslot, sizeof(uint16_t) * K.pslot.size()));
+  FS_CUDA_TRY(cudaMemcpy(p->d_pslot, K.pslot.data(), sizeof(uint16_t) * K.pslot.size(), cudaMemcpyHostToDevice));
+  p->jit_nblocks = K.nblocks;
+  FS_CUDA_TRY(cudaMalloc(&p->d_site_block, sizeof(int) * K.site_block.size()));
+  FS_CUDA_TRY(cudaMemcpy(p->d_site_block, K.site_block.data(), sizeof(int) * K.site_block.size(), cudaMemcpyHostToDevice));
+  p->gjit_threads = nw * 32;
+  p->gjit_smem = smem;
+  p->jit_state = 1;
+  return FS_OK;
+}
+
+// per-word fault lists for the specialised kernels (fs_jit_kernels.cuh fault_list_kernel)
+int run_fault_lists(fs_prog* p, const fs::RunArgs& a, cudaStream_t stream, uint32_t** fent, uint32_t** bcount,
+                    uint32_t** ntot) {
+  const size_t W = a.W;
+  const int nb = std::max(1, p->jit_nblocks);
+  const uint32_t cap = fsjit::kJitStage;
+  const size_t need = align_up((size_t)cap * W * 4, 256) + align_up((size_t)nb * W * 4, 256) + W * 4 + 256;
+  if (need > p->flist_bytes) {
+    cudaFree(p->flist);
+    p->flist = nullptr;
+    p->flist_bytes = 0;
+    FS_CUDA_TRY(cudaMalloc(&p->flist, need));
+    p->flist_bytes = need;
+  }
+  unsigned char* fb8 = static_cast<unsigned char*>(p->flist);
+  *fent = reinterpret_cast<uint32_t*>(fb8);
+  *bcount = reinterpret_cast<uint32_t*>(fb8 + align_up((size_t)cap * W * 4, 256));
+  *ntot = reinterpret_cast<uint32_t*>(fb8 + align_up((size_t)cap * W * 4, 256) + align_up((size_t)nb * W * 4, 256));
+  fs::fault_list_kernel<<<(unsigned)((W + 255) / 256), 256, 0, stream>>>(
+      p->dp, a.seed, a.shot0 >> 5, (uint32_t)W, p->d_site_block, p->jit_nblocks, *fent, *bcount, *ntot, cap);
+  FS_CUDA_TRY(cudaGetLastError());
   return FS_OK;
 }
 
@@ -820,23 +895,8 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
       const size_t groups = (W + 127) / 128;
       const size_t grid = std::min<size_t>(groups, (size_t)p->num_sms * std::max(occ, 1));
       // 1) per-word fault lists (high-occupancy generator kernel)
-      const int nb = std::max(1, p->jit_nblocks);
-      const uint32_t cap = fsjit::kJitStage;
-      const size_t need = align_up((size_t)cap * W * 4, 256) + align_up((size_t)nb * W * 4, 256) + W * 4 + 256;
-      if (need > p->flist_bytes) {
-        cudaFree(p->flist);
-        p->flist = nullptr;
-        p->flist_bytes = 0;
-        FS_CUDA_TRY(cudaMalloc(&p->flist, need));
-        p->flist_bytes = need;
-      }
-      unsigned char* fb8 = static_cast<unsigned char*>(p->flist);
-      uint32_t* fent = reinterpret_cast<uint32_t*>(fb8);
-      uint32_t* bcount = reinterpret_cast<uint32_t*>(fb8 + align_up((size_t)cap * W * 4, 256));
-      uint32_t* ntot = reinterpret_cast<uint32_t*>(fb8 + align_up((size_t)cap * W * 4, 256) + align_up((size_t)nb * W * 4, 256));
-      fs::fault_list_kernel<<<(unsigned)((W + 255) / 256), 256, 0, stream>>>(
-          dp, a.seed, a.shot0 >> 5, (uint32_t)W, p->d_site_block, p->jit_nblocks, fent, bcount, ntot, cap);
-      FS_CUDA_TRY(cudaGetLastError());
+      uint32_t *fent = nullptr, *bcount = nullptr, *ntot = nullptr;
+      if ((rc = run_fault_lists(p, a, stream, &fent, &bcount, &ntot))) return rc;
       // 2) the program-specialised frame kernel
       fs::DevProg dpv = dp;
       const uint16_t* ps = p->d_pslot;
@@ -867,6 +927,28 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
   // general engine
   const bool trace = (tin && (tin->fault_modes || tin->forced)) || tout;
   if (dp.has_psel && !trace && a.stop == dp.num_instrs) return launch_segmented(p, a, stream);
+  if (!(a.flags & (FS_RNG_SPLITMIX | FS_NO_RENORM | FS_NO_JIT | FS_FORCE_GENERAL)) && !trace &&
+      a.stop == dp.num_instrs && gjit_supported(p) && ensure_gjit(p) == FS_OK) {
+    uint32_t *fent = nullptr, *bcount = nullptr, *ntot = nullptr;
+    int rc = run_fault_lists(p, a, stream, &fent, &bcount, &ntot);
+    if (rc) return rc;
+    fsjit::Api& J = fsjit::api();
+    int occ = 1;
+    J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->jit.fn, p->gjit_threads, p->gjit_smem);
+    const int nw = p->gjit_threads / 32;
+    const size_t blocks = (a.W + nw - 1) / nw;
+    const size_t grid = std::min<size_t>(blocks, (size_t)p->num_sms * std::max(occ, 1));
+    fs::DevProg dpv = dp;
+    const uint16_t* ps = p->d_pslot;
+    const uint32_t* fl = fent;
+    const uint32_t* fc = bcount;
+    const uint32_t* ft = ntot;
+    void* args[] = {&dpv, &a, &ps, &fl, &fc, &ft};
+    int r = J.cuLaunchKernel(p->jit.fn, (unsigned)grid, 1, 1, p->gjit_threads, 1, 1, (unsigned)p->gjit_smem, stream,
+                             args, nullptr);
+    if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_jit_general) failed: " + std::to_string(r));
+    return FS_OK;
+  }
   fs::SegArgs none{};
   return launch_general_kernel(p, a, none, false, dp.k_max, a.W, stream);
 }

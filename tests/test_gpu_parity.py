@@ -164,3 +164,16 @@ def test_gpu_jit_equals_interpreter(cuda, name):
     _, b, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX | FS_NO_JIT)
     _same(a, b)
     assert dp.jit_status().startswith("ready"), dp.jit_status()
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if 0 < load(c)["prog"].k_max <= 7 and not load(c)["prog"].has_postselect
+                                  and not (set((load(c)["prog"].instrs[:, 0] & 0xFF).tolist()) & {7, 9})])
+def test_gpu_general_jit_equals_interpreter(cuda, name):
+    """Program-specialised general kernel (NVRTC) == general interpreter, bit for bit."""
+    P = load(name)["prog"]
+    dp = _dev(P)
+    n = 20_000
+    _, a, _ = dp.sample_host(n, seed=13, shot0=32 * 3, flags=FS_RNG_PHILOX)
+    _, b, _ = dp.sample_host(n, seed=13, shot0=32 * 3, flags=FS_RNG_PHILOX | FS_NO_JIT)
+    _same(a, b)
+    assert dp.jit_status().startswith("ready"), dp.jit_status()
