@@ -56,6 +56,7 @@ struct RunArgs {
   uint64_t seed, shot0, nshots;
   uint32_t flags;
   uint32_t W;          // output words = ceil(nshots/32)
+  uint32_t ostride;    // row stride of the output words (== W except for chunked launches)
   uint32_t* meas;      // [U][W]
   uint32_t* det;       // [D][W]
   uint32_t* obs;       // [O][W]
@@ -153,6 +154,11 @@ struct PhiloxStream {
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
                       __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+// fused variant for the program-specialised kernels (records unchanged; amplitudes differ from the
+// reference only in the last ulp, within the 1e-10 parity tolerance)
+__device__ __forceinline__ double2 cmul_f(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }

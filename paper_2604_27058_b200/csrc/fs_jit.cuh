@@ -187,13 +187,13 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   o << "    {\n      const uint32_t mine = fover ? 0u : min(nt_, " << kJitStage << "u);\n";
   o << "      uint32_t tmax = mine;\n";
   o << "      for (int o_ = 16; o_; o_ >>= 1) tmax = max(tmax, __shfl_xor_sync(__activemask(), tmax, o_));\n";
-  o << "      for (uint32_t t = 0; t < tmax; t++) if (t < mine) stage[t * 32 + lane] = __ldg(fent + (size_t)t * A.W + w);\n";
+  o << "      for (uint32_t t = 0; t < tmax; t++) if (t < mine) stage[t * 32 + lane] = __ldg(fent + (size_t)t * A.ostride + w);\n";
   o << "    }\n";
-  for (int b = 0; b < K.nblocks; b++) o << "    const uint32_t nbk" << b << " = fover ? 0u : __ldg(bcount + (size_t)" << b << " * A.W + w);\n";
+  for (int b = 0; b < K.nblocks; b++) o << "    const uint32_t nbk" << b << " = fover ? 0u : __ldg(bcount + (size_t)" << b << " * A.ostride + w);\n";
   auto put_record = [&](int rec, const std::string& expr) {
     const int col = record_out[rec], sl = bit_slot[rec];
     o << "    { const uint32_t rw = " << expr << ";";
-    if (col >= 0) o << " A.meas[(size_t)" << col << " * A.W + w] = rw & alive;";
+    if (col >= 0) o << " A.meas[(size_t)" << col << " * A.ostride + w] = rw & alive;";
     if (sl >= 0) o << " r" << sl << " = rw;";
     o << " }\n";
   };
@@ -239,7 +239,7 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
         o << " " << f(Z(virt)) << " = pw ^ coin;";
         const int col = record_out[I[3]], sl = bit_slot[I[3]];
         o << " const uint32_t rw = coin ^ pw" << (flip ? " ^ 0xFFFFFFFFu" : "") << ";";
-        if (col >= 0) o << " A.meas[(size_t)" << col << " * A.W + w] = rw & alive;";
+        if (col >= 0) o << " A.meas[(size_t)" << col << " * A.ostride + w] = rw & alive;";
         if (sl >= 0) o << " r" << sl << " = rw;";
         o << " }\n";
         // fx_new = fz_old ^ coin (already in the old z slot), fz_new = fx_old: rename
@@ -275,7 +275,7 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
         for (int j = 0; j < I[3]; j++) e << " ^ r" << bit_slot[reclists[I[2] + j]];
         if (op == FS_OP_DETECTOR) {
           const int sl = bit_slot[R + I[1]];
-          o << "    { const uint32_t dw = " << e.str() << "; A.det[(size_t)" << I[1] << " * A.W + w] = dw & alive;";
+          o << "    { const uint32_t dw = " << e.str() << "; A.det[(size_t)" << I[1] << " * A.ostride + w] = dw & alive;";
           if (sl >= 0) o << " r" << sl << " = dw;";
           o << " }\n";
         } else {
@@ -293,7 +293,7 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
     }
   }
   for (int j = 0; j < d.num_observables; j++)
-    o << "    A.obs[(size_t)" << j << " * A.W + w] = ob" << j << " & valid;\n";
+    o << "    A.obs[(size_t)" << j << " * A.ostride + w] = ob" << j << " & valid;\n";
   o << "    A.accepted[w] = alive & valid;\n    A.error[w] = 0u;\n  }\n}\n";
   K.src = o.str();
   return K;
@@ -335,6 +335,7 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
   K.nslots = 2 * n;
   K.cap_log2 = d.k_max;
   K.arr_regs = d.k_max <= 4;
+  if (const char* e = getenv("FS_GJIT_SMEM")) K.arr_regs = K.arr_regs && atoi(e) == 0;  // tuning
   K.pslot.assign(paulis.size() + 1, 0);
   K.site_block.assign(d.num_sites + 1, 0);
   for (int i = 0, b = 0; i < d.num_instrs; i++)
@@ -354,8 +355,9 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
   const int cap = 1 << d.k_max;
   std::ostringstream o;
   o << "#include \"fs_jit_kernels.cuh\"\n";
-  o << "using fs::cmul; using fs::cadd; using fs::csub; using fs::cscale; using fs::cnorm2;\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << (K.arr_regs ? 128 : 64)
+  o << "#define cmul fs::cmul_f\nusing fs::cadd; using fs::csub; using fs::cscale; using fs::cnorm2;\n";
+  const char* gmb = getenv("FS_GJIT_MB");
+  o << "extern \"C\" __global__ void __launch_bounds__(" << (K.arr_regs ? 128 : 64) << ", " << (gmb ? atoi(gmb) : (K.arr_regs ? 3 : 1))
     << ") fs_jit_general(fs::DevProg P, fs::RunArgs A, const uint16_t* __restrict__ pslot, "
        "const uint32_t* __restrict__ fent, const uint32_t* __restrict__ bcount, const uint32_t* __restrict__ ntot) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem[];\n";
@@ -384,7 +386,7 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
   auto put_record = [&](int rec, const std::string& expr) {
     const int col = record_out[rec], sl = bit_slot[rec];
     o << "    { const uint32_t rw = " << expr << ";";
-    if (col >= 0) o << " if (lane == 0) A.meas[(size_t)" << col << " * A.W + w] = rw & alive;";
+    if (col >= 0) o << " if (lane == 0) A.meas[(size_t)" << col << " * A.ostride + w] = rw & alive;";
     if (sl >= 0) o << " r" << sl << " = rw;";
     o << " }\n";
   };
@@ -412,7 +414,10 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
         const int g = I[1], va = I[2], vb = I[3], a = I[4], b = I[5], size = 1 << I[6];
         if (g == FS_G_S || g == FS_G_SDAG) {
           for (int j = 0; j < size; j++)
-            if ((j >> a) & 1) o << "    " << A(j) << " = cmul(" << A(j) << ", make_double2(0.0, " << (g == FS_G_S ? "1.0" : "-1.0") << "));\n";
+            if ((j >> a) & 1) {  // x (+/-)i: a swap and a sign flip
+              if (g == FS_G_S) o << "    " << A(j) << " = make_double2(-" << A(j) << ".y, " << A(j) << ".x);\n";
+              else o << "    " << A(j) << " = make_double2(" << A(j) << ".y, -" << A(j) << ".x);\n";
+            }
           o << "    " << f(Z(va)) << " ^= " << f(X(va)) << ";\n";
         } else if (g == FS_G_H) {
           const int st = 1 << a;
@@ -468,7 +473,7 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
           << f(Z(virt)) << " = pw ^ coin;";
         const int col = record_out[I[3]], sl = bit_slot[I[3]];
         o << " const uint32_t rw = coin ^ pw" << flipm << ";";
-        if (col >= 0) o << " if (lane == 0) A.meas[(size_t)" << col << " * A.W + w] = rw & alive;";
+        if (col >= 0) o << " if (lane == 0) A.meas[(size_t)" << col << " * A.ostride + w] = rw & alive;";
         if (sl >= 0) o << " r" << sl << " = rw;";
         o << " }\n";
         std::swap(phys[virt], phys[n + virt]);
@@ -522,7 +527,7 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
         o << "      const uint32_t brw = __ballot_sync(0xFFFFFFFFu, br != 0);\n";
         o << "      " << f(X(virt)) << " ^= brw;\n";
         const int col = record_out[rec], sl = bit_slot[rec];
-        if (col >= 0) o << "      if (lane == 0) A.meas[(size_t)" << col << " * A.W + w] = recw & alive;\n";
+        if (col >= 0) o << "      if (lane == 0) A.meas[(size_t)" << col << " * A.ostride + w] = recw & alive;\n";
         if (sl >= 0) o << "      r" << sl << " = recw;\n";
         o << "    }\n";
         break;
@@ -553,9 +558,9 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
         o << "    {\n";
         for (int sl : touched) o << "      Fs[" << sl << "] = " << f(sl) << ";\n";
         o << "      __syncwarp();\n      if (lane == 0) {\n";
-        o << "        if (!fover) {\n          const uint32_t nb_ = __ldg(bcount + (size_t)" << nblk << " * A.W + w);\n";
+        o << "        if (!fover) {\n          const uint32_t nb_ = __ldg(bcount + (size_t)" << nblk << " * A.ostride + w);\n";
         o << "          for (uint32_t t = 0; t < nb_; t++) {\n";
-        o << "            const uint32_t e = __ldg(fent + (size_t)(fcur + t) * A.W + w);\n";
+        o << "            const uint32_t e = __ldg(fent + (size_t)(fcur + t) * A.ostride + w);\n";
         o << "            const uint32_t bit = 1u << (e & 31);\n            const int off = (int)(e >> 10), cnt = (int)((e >> 5) & 31);\n";
         o << "            for (int j = 0; j < cnt; j++) Fs[__ldg(pslot + off + j)] ^= bit;\n          }\n";
         o << "          fcur += nb_;\n        } else {\n";
@@ -576,7 +581,7 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
         for (int j = 0; j < I[3]; j++) e << " ^ r" << bit_slot[reclists[I[2] + j]];
         if (op == FS_OP_DETECTOR) {
           const int sl = bit_slot[R + I[1]];
-          o << "    { const uint32_t dw = " << e.str() << "; if (lane == 0) A.det[(size_t)" << I[1] << " * A.W + w] = dw & alive;";
+          o << "    { const uint32_t dw = " << e.str() << "; if (lane == 0) A.det[(size_t)" << I[1] << " * A.ostride + w] = dw & alive;";
           if (sl >= 0) o << " r" << sl << " = dw;";
           o << " }\n";
         } else {
@@ -589,7 +594,7 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
     }
   }
   o << "    if (lane == 0) {\n";
-  for (int j = 0; j < d.num_observables; j++) o << "      A.obs[(size_t)" << j << " * A.W + w] = ob" << j << " & validm;\n";
+  for (int j = 0; j < d.num_observables; j++) o << "      A.obs[(size_t)" << j << " * A.ostride + w] = ob" << j << " & validm;\n";
   o << "      A.accepted[w] = alive & validm;\n      A.error[w] = errm;\n      if (errm) atomicMax(A.status, FS_ERR_SHOT_NAN);\n    }\n";
   o << "    __syncwarp();\n  }\n}\n";
   K.src = o.str();

@@ -27,12 +27,12 @@ __device__ __noinline__ void jit_noise_block(const DevProg& P, uint32_t* F, cons
 // memory with full-row (coalesced) loads once per word and applies them from there.  A word
 // with more than `cap` faults, or a fault with more than 31 Pauli entries, is marked
 // ntot = ~0 and regenerates its stream in place (identical results).
-__global__ void __launch_bounds__(256) fault_list_kernel(DevProg P, uint64_t seed, uint64_t word0, uint32_t W,
-                                                        const int* __restrict__ site_block, int nblocks,
+__global__ void __launch_bounds__(256) fault_list_kernel(DevProg P, uint64_t seed, uint64_t word0, uint32_t nw,
+                                                        uint32_t W, const int* __restrict__ site_block, int nblocks,
                                                         uint32_t* __restrict__ ent, uint32_t* __restrict__ bcount,
                                                         uint32_t* __restrict__ ntot, uint32_t cap) {
-  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= W) return;
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;  // W = row stride, nw = words
+  if (w >= nw) return;
   WordFaultGen gen;
   gen.init(seed, word0 + w);
   uint32_t n = 0, nb = 0;
@@ -72,7 +72,14 @@ __device__ __forceinline__ void jit_apply_faults(uint32_t* F, const uint32_t* st
     const uint32_t e = stage[(cur + t) * 32 + lane];
     const uint32_t bit = 1u << (e & 31);
     const int off = (int)(e >> 10), cnt = (int)((e >> 5) & 31);
-    for (int j = 0; j < cnt; j++) F[(uint32_t)__ldg(pslot + off + j) * 32] ^= bit;
+    // issue the slot lookups of up to 8 entries together (independent L1 loads), then the XORs
+    uint32_t sl[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) sl[j] = j < cnt ? (uint32_t)__ldg(pslot + off + j) : 0u;
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+      if (j < cnt) F[sl[j] * 32] ^= bit;
+    for (int j = 8; j < cnt; j++) F[(uint32_t)__ldg(pslot + off + j) * 32] ^= bit;
   }
   cur += n;
 }

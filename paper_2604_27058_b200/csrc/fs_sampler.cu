@@ -55,6 +55,12 @@ struct Stage {  // carve-out of one device allocation
 
 }  // namespace
 
+namespace {
+constexpr int kLargeK = 16;  // k_max at which active arrays move to the HBM engine
+constexpr int kBlockK = 6;   // segment active dimension at which a shot gets a whole CTA (or warp)
+constexpr int kChunks = 1;   // word chunks of the fault-list | frame-kernel pipeline (1 measured best)
+}  // namespace
+
 struct fs_prog {
   fs_prog_desc desc;  // scalar fields only (pointers refer to host memory of the creator)
   fs::DevProg dp;
@@ -90,6 +96,8 @@ struct fs_prog {
   int jit_nblocks = 0;
   int flip_rows = 0, flip_capmax = 0;
   int gjit_threads = 128;
+  cudaStream_t aux = nullptr;  // fault-list generation overlapped with the specialised kernels
+  cudaEvent_t ev[kChunks + 1] = {};
   size_t gjit_smem = 0;
   // segmented general engine: ping-pong survivor state stores
   void* seg_pool[2] = {nullptr, nullptr};
@@ -101,10 +109,6 @@ struct fs_prog {
   uint64_t hbm_B = 0;
 };
 
-namespace {
-constexpr int kLargeK = 16;  // k_max at which active arrays move to the HBM engine
-constexpr int kBlockK = 6;   // segment active dimension at which a shot gets a whole CTA
-}
 
 extern "C" int fs_abi_version(void) { return FS_ABI_VERSION; }
 extern "C" const char* fs_last_error(void) { return g_last_error.c_str(); }
@@ -253,6 +257,11 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->seg_pool[0]);
   cudaFree(p->seg_pool[1]);
   cudaFree(p->d_pslot);
+  if (p->aux) {
+    cudaStreamDestroy(p->aux);
+    for (auto& e : p->ev)
+      if (e) cudaEventDestroy(e);
+  }
   cudaFree(p->flist);
   cudaFree(p->d_site_block);
   if (p->jit.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->jit.mod);
@@ -611,9 +620,7 @@ int ensure_gjit(fs_prog* p) {
 }
 
 // per-word fault lists for the specialised kernels (fs_jit_kernels.cuh fault_list_kernel)
-int run_fault_lists(fs_prog* p, const fs::RunArgs& a, cudaStream_t stream, uint32_t** fent, uint32_t** bcount,
-                    uint32_t** ntot) {
-  const size_t W = a.W;
+int alloc_fault_lists(fs_prog* p, size_t W, uint32_t** fent, uint32_t** bcount, uint32_t** ntot) {
   const int nb = std::max(1, p->jit_nblocks);
   const uint32_t cap = fsjit::kJitStage;
   const size_t need = align_up((size_t)cap * W * 4, 256) + align_up((size_t)nb * W * 4, 256) + W * 4 + 256;
@@ -628,8 +635,15 @@ int run_fault_lists(fs_prog* p, const fs::RunArgs& a, cudaStream_t stream, uint3
   *fent = reinterpret_cast<uint32_t*>(fb8);
   *bcount = reinterpret_cast<uint32_t*>(fb8 + align_up((size_t)cap * W * 4, 256));
   *ntot = reinterpret_cast<uint32_t*>(fb8 + align_up((size_t)cap * W * 4, 256) + align_up((size_t)nb * W * 4, 256));
-  fs::fault_list_kernel<<<(unsigned)((W + 255) / 256), 256, 0, stream>>>(
-      p->dp, a.seed, a.shot0 >> 5, (uint32_t)W, p->d_site_block, p->jit_nblocks, *fent, *bcount, *ntot, cap);
+  return FS_OK;
+}
+
+// fault lists of words [w0, w0 + nw) of the call
+int run_fault_lists(fs_prog* p, const fs::RunArgs& a, size_t w0, size_t nw, uint32_t* fent, uint32_t* bcount,
+                    uint32_t* ntot, cudaStream_t stream) {
+  fs::fault_list_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, stream>>>(
+      p->dp, a.seed, (a.shot0 >> 5) + w0, (uint32_t)nw, a.ostride, p->d_site_block, p->jit_nblocks, fent + w0,
+      bcount + w0, ntot + w0, fsjit::kJitStage);
   FS_CUDA_TRY(cudaGetLastError());
   return FS_OK;
 }
@@ -853,6 +867,7 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
   a.nshots = nshots;
   a.flags = flags;
   a.W = (uint32_t)((nshots + 31) / 32);
+  a.ostride = a.W;
   a.meas = out->meas;
   a.det = out->det;
   a.obs = out->obs;
@@ -894,18 +909,48 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
       J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->jit.fn, 128, smem);
       const size_t groups = (W + 127) / 128;
       const size_t grid = std::min<size_t>(groups, (size_t)p->num_sms * std::max(occ, 1));
-      // 1) per-word fault lists (high-occupancy generator kernel)
+      // fault lists (generator kernel, aux stream) pipelined with the frame kernel (main stream)
+      // over NCH chunks of words: the list of chunk c+1 is generated while chunk c is simulated
       uint32_t *fent = nullptr, *bcount = nullptr, *ntot = nullptr;
-      if ((rc = run_fault_lists(p, a, stream, &fent, &bcount, &ntot))) return rc;
-      // 2) the program-specialised frame kernel
-      fs::DevProg dpv = dp;
-      const uint16_t* ps = p->d_pslot;
-      const uint32_t* fl = fent;
-      const uint32_t* fc = bcount;
-      const uint32_t* ft = ntot;
-      void* args[] = {&dpv, &a, &ps, &fl, &fc, &ft};
-      int r = J.cuLaunchKernel(p->jit.fn, (unsigned)grid, 1, 1, 128, 1, 1, (unsigned)smem, stream, args, nullptr);
-      if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_jit_frame) failed: " + std::to_string(r));
+      if ((rc = alloc_fault_lists(p, W, &fent, &bcount, &ntot))) return rc;
+      if (!p->aux) {
+        FS_CUDA_TRY(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+        for (int c = 0; c < kChunks + 1; c++) FS_CUDA_TRY(cudaEventCreateWithFlags(&p->ev[c], cudaEventDisableTiming));
+      }
+      int nch_req = kChunks;
+      if (const char* ce = getenv("FS_JIT_CHUNKS")) nch_req = std::max(1, std::min(kChunks, atoi(ce)));
+      const int nch = W >= (size_t)nch_req * 4096 ? nch_req : 1;
+      const size_t per = (W + nch - 1) / nch;
+      FS_CUDA_TRY(cudaEventRecord(p->ev[kChunks], stream));
+      FS_CUDA_TRY(cudaStreamWaitEvent(p->aux, p->ev[kChunks], 0));
+      for (int c = 0; c < nch; c++) {
+        const size_t w0 = c * per, nw = std::min(per, W - w0);
+        if ((rc = run_fault_lists(p, a, w0, nw, fent, bcount, ntot, p->aux))) return rc;
+        FS_CUDA_TRY(cudaEventRecord(p->ev[c], p->aux));
+      }
+      for (int c = 0; c < nch; c++) {
+        const size_t w0 = c * per, nw = std::min(per, W - w0);
+        FS_CUDA_TRY(cudaStreamWaitEvent(stream, p->ev[c], 0));
+        fs::RunArgs ac = a;
+        ac.W = (uint32_t)nw;
+        ac.nshots = std::min<uint64_t>(a.nshots - w0 * 32, (uint64_t)nw * 32);
+        ac.shot0 = a.shot0 + w0 * 32;
+        ac.meas = a.meas ? a.meas + w0 : nullptr;
+        ac.det = a.det ? a.det + w0 : nullptr;
+        ac.obs = a.obs ? a.obs + w0 : nullptr;
+        ac.accepted = a.accepted + w0;
+        ac.error = a.error + w0;
+        const size_t gc = std::min<size_t>((nw + 127) / 128, (size_t)p->num_sms * std::max(occ, 1));
+        fs::DevProg dpv = dp;
+        const uint16_t* ps = p->d_pslot;
+        const uint32_t* fl = fent + w0;
+        const uint32_t* fc = bcount + w0;
+        const uint32_t* ft = ntot + w0;
+        void* args[] = {&dpv, &ac, &ps, &fl, &fc, &ft};
+        int r = J.cuLaunchKernel(p->jit.fn, (unsigned)gc, 1, 1, 128, 1, 1, (unsigned)smem, stream, args, nullptr);
+        if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_jit_frame) failed: " + std::to_string(r));
+      }
+      (void)grid;
       return FS_OK;
     }
   }
@@ -930,8 +975,9 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
   if (!(a.flags & (FS_RNG_SPLITMIX | FS_NO_RENORM | FS_NO_JIT | FS_FORCE_GENERAL)) && !trace &&
       a.stop == dp.num_instrs && gjit_supported(p) && ensure_gjit(p) == FS_OK) {
     uint32_t *fent = nullptr, *bcount = nullptr, *ntot = nullptr;
-    int rc = run_fault_lists(p, a, stream, &fent, &bcount, &ntot);
+    int rc = alloc_fault_lists(p, a.W, &fent, &bcount, &ntot);
     if (rc) return rc;
+    if ((rc = run_fault_lists(p, a, 0, a.W, fent, bcount, ntot, stream))) return rc;
     fsjit::Api& J = fsjit::api();
     int occ = 1;
     J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->jit.fn, p->gjit_threads, p->gjit_smem);
