@@ -17,6 +17,7 @@
 #include "fs_frame.cuh"
 #include "fs_general.cuh"
 #include "fs_hbm.cuh"
+#include "fs_hbm_fused.cuh"
 #include "fs_block.cuh"
 #include "fs_jit.cuh"
 #include "fs_jit_kernels.cuh"
@@ -54,6 +55,25 @@ struct Stage {  // carve-out of one device allocation
 };
 
 }  // namespace
+
+struct HbmStep {
+  enum Kind { SCALAR, ARR, PASS, MEAS } kind;
+  int i0, i1;
+  fs::ArrOp op;
+  uint64_t count;
+  int pass;
+  int collapse;
+  double2 u10, u11;
+};
+
+struct HbmPlan {
+  bool built = false, fused = false;
+  int stop = -1;
+  std::vector<HbmStep> steps;
+  std::vector<fs::PassDesc> passes;
+  std::vector<fs::TileOp> tileops;
+  std::vector<int> final_live;
+};
 
 namespace {
 constexpr int kLargeK = 16;  // k_max at which active arrays move to the HBM engine
@@ -104,6 +124,9 @@ struct fs_prog {
   std::vector<uint32_t> seg_counts;  // diagnostics: shots entering each segment (per chunk)
   size_t seg_bytes[2] = {0, 0};
   // large-k engine state
+  HbmPlan hplan;
+  fs::PassDesc* d_passes = nullptr;
+  fs::TileOp* d_tileops = nullptr;
   void* hbm = nullptr;
   size_t hbm_bytes = 0;
   uint64_t hbm_B = 0;
@@ -254,6 +277,8 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->stage);
   cudaFree(p->d_counts);
   cudaFree(p->hbm);
+  cudaFree(p->d_passes);
+  cudaFree(p->d_tileops);
   cudaFree(p->seg_pool[0]);
   cudaFree(p->seg_pool[1]);
   cudaFree(p->d_pslot);
@@ -356,6 +381,35 @@ extern "C" int fs_debug_gjit_source(fs_prog* p, char* buf, size_t len) {
     buf[m] = 0;
   }
   return (int)K.src.size();
+}
+
+namespace {
+int plan_hbm(fs_prog* p, int stop, bool fused);
+}
+// large-k plan statistics: [steps, passes, fused ops, unfused array kernels, measurements]
+extern "C" int fs_debug_hbm_plan(fs_prog* p, int64_t* out) {
+  if (!p || plan_hbm(p, p->dp.num_instrs, true)) return -1;
+  const HbmPlan& PL = p->hplan;
+  int64_t arr = 0, meas = 0;
+  for (auto& st : PL.steps) { arr += st.kind == HbmStep::ARR; meas += st.kind == HbmStep::MEAS; }
+  out[0] = (int64_t)PL.steps.size(); out[1] = (int64_t)PL.passes.size(); out[2] = (int64_t)PL.tileops.size();
+  out[3] = arr; out[4] = meas;
+  return 0;
+}
+
+// per fused op: (pass, kind, la, lb, diag_run); returns the op count
+extern "C" int64_t fs_debug_hbm_tileops(fs_prog* p, int32_t* out, int64_t max) {
+  if (!p || plan_hbm(p, p->dp.num_instrs, true)) return -1;
+  const HbmPlan& PL = p->hplan;
+  int64_t n = 0;
+  for (size_t ps = 0; ps < PL.passes.size(); ps++)
+    for (int k = 0; k < PL.passes[ps].nops; k++, n++) {
+      if (n >= max) continue;
+      const fs::TileOp& o = PL.tileops[PL.passes[ps].op_off + k];
+      int32_t* r = out + 5 * n;
+      r[0] = (int32_t)ps; r[1] = o.kind; r[2] = o.la; r[3] = o.lb; r[4] = o.diag_run;
+    }
+  return n;
 }
 
 extern "C" const char* fs_debug_jit_status(fs_prog* p) {
@@ -648,6 +702,273 @@ int run_fault_lists(fs_prog* p, const fs::RunArgs& a, size_t w0, size_t nw, uint
   return FS_OK;
 }
 
+
+// ------------------------------------------------------------------ large-k plan
+// Host walk of the program (shot-independent): logical->physical axis map, the scalar
+// segments, per-instruction array kernels, measurements, and -- when the live dimension is at
+// least fs::kTileBits -- fused tile passes (fs_hbm_fused.cuh).
+int plan_hbm(fs_prog* p, int stop, bool fused) {
+  HbmPlan& PL = p->hplan;
+  if (PL.built && PL.stop == stop && PL.fused == fused) return FS_OK;
+  PL = HbmPlan{};
+  PL.stop = stop;
+  PL.fused = fused;
+  const fs::DevProg& dp = p->dp;
+  const int* ins_all = p->h_instrs.data();
+  const double* fpar = p->h_fparams.data();
+  std::vector<int> live;
+  auto is_live = [&](int q) { return std::find(live.begin(), live.end(), q) != live.end(); };
+  auto dead_list = [&](std::initializer_list<int> extra) {
+    fs::DeadBits d{};
+    int top = -1;
+    for (int x : live) top = std::max(top, x);
+    for (int x : extra) top = std::max(top, x);
+    std::vector<int> pos;
+    for (int q = 0; q <= top; q++) {
+      const bool ise = std::find(extra.begin(), extra.end(), q) != extra.end();
+      if (!is_live(q) || ise) pos.push_back(q);
+    }
+    std::sort(pos.begin(), pos.end());
+    pos.erase(std::unique(pos.begin(), pos.end()), pos.end());
+    d.n = (int)pos.size();
+    for (int t = 0; t < d.n; t++) d.pos[t] = (int8_t)pos[t];
+    return d;
+  };
+  auto lowest_dead = [&]() {
+    for (int q = 0; q < dp.k_max; q++)
+      if (!is_live(q)) return q;
+    return -1;
+  };
+  auto cpx = [&](int off) { return make_double2(fpar[off], fpar[off + 1]); };
+  // pending fused pass
+  std::vector<fs::TileOp> pops;
+  std::vector<int> need;
+  auto flush = [&]() {
+    if (pops.empty()) return;
+    fs::PassDesc D{};
+    std::vector<int> T = need;
+    for (int q = 0; q < 3; q++)
+      if (is_live(q) && std::find(T.begin(), T.end(), q) == T.end()) T.push_back(q);
+    for (int q = 0; (int)T.size() < fs::kTileBits && q < 64; q++)
+      if (is_live(q) && std::find(T.begin(), T.end(), q) == T.end()) T.push_back(q);
+    // register bits (tile bits 8..11): the most-mixed axes of the pass other than the low
+    // physical axes 0..2, which stay thread bits 0..2 for 128-byte coalesced accesses
+    std::vector<std::pair<int, int>> use;  // (-count, axis)
+    for (int q : T) {
+      if (q < 3 && is_live(q)) continue;
+      int cnt = 0;
+      for (auto& o : pops) {
+        const int mix = o.kind == fs::TO_CX ? o.pb : (o.kind == fs::TO_H || o.kind == fs::TO_EXPAND) ? o.pa : -1;
+        cnt += mix == q;
+      }
+      use.push_back({-cnt, q});
+    }
+    std::sort(use.begin(), use.end());
+    std::vector<int> regs, thr;
+    for (auto& u : use) (regs.size() < 4 ? regs : thr).push_back(u.second);
+    std::vector<int> lowq;
+    for (int q : T)
+      if (q < 3 && is_live(q)) lowq.push_back(q);
+    std::sort(lowq.begin(), lowq.end());
+    std::sort(thr.begin(), thr.end());
+    std::sort(regs.begin(), regs.end());
+    T.clear();
+    T.insert(T.end(), lowq.begin(), lowq.end());
+    T.insert(T.end(), thr.begin(), thr.end());
+    T.insert(T.end(), regs.begin(), regs.end());
+    if ((int)T.size() != fs::kTileBits) { pops.clear(); need.clear(); return; }  // cannot happen (k >= kTileBits)
+    for (int i = 0; i < fs::kTileBits; i++) D.T[i] = (int8_t)T[i];
+    std::vector<int> base;
+    for (int q : live)
+      if (std::find(T.begin(), T.end(), q) == T.end()) base.push_back(q);
+    std::sort(base.begin(), base.end());
+    D.nbase = (int)base.size();
+    for (int i = 0; i < D.nbase; i++) D.base[i] = (int8_t)base[i];
+    for (int j = 0; j < fs::kTileElems; j++) {
+      uint32_t g = 0;
+      for (int b = 0; b < fs::kTileBits - 8; b++) g |= (uint32_t)((j >> b) & 1) << T[8 + b];
+      D.dep_hi[j] = g;
+    }
+    auto local = [&](int q) {
+      for (int i = 0; i < fs::kTileBits; i++)
+        if (T[i] == q) return i;
+      return -1;
+    };
+    // la / lb: position in the extended local index (tile bits 0..11, then the base axes)
+    auto ext = [&](int q) -> int8_t {
+      if (q < 0) return (int8_t)-1;
+      const int l = local(q);
+      if (l >= 0) return (int8_t)l;
+      for (int i = 0; i < D.nbase; i++)
+        if (base[i] == q) return (int8_t)(fs::kTileBits + i);
+      return (int8_t)-1;
+    };
+    for (auto& o : pops) {
+      o.la = ext(o.pa);
+      o.lb = ext(o.pb);
+    }
+    auto diag = [](int k) { return k == fs::TO_S || k == fs::TO_SDAG || k == fs::TO_CZ || k == fs::TO_ROT; };
+    for (size_t i = 0; i < pops.size();) {
+      if (!diag(pops[i].kind)) { pops[i].diag_run = 0; i++; continue; }
+      size_t e = i;
+      while (e < pops.size() && diag(pops[e].kind)) e++;
+      for (size_t r = i; r < e; r++) pops[r].diag_run = 0;
+      pops[i].diag_run = (int8_t)std::min<size_t>(e - i, 127);
+      i = i + std::min<size_t>(e - i, 127);
+    }
+    D.nops = (int)pops.size();
+    D.op_off = (int)PL.tileops.size();
+    PL.tileops.insert(PL.tileops.end(), pops.begin(), pops.end());
+    HbmStep st{};
+    st.kind = HbmStep::PASS;
+    st.pass = (int)PL.passes.size();
+    PL.passes.push_back(D);
+    PL.steps.push_back(st);
+    pops.clear();
+    need.clear();
+  };
+  auto arr = [&](const fs::ArrOp& o, uint64_t count) {
+    HbmStep st{};
+    st.kind = HbmStep::ARR;
+    st.op = o;
+    st.count = count;
+    PL.steps.push_back(st);
+  };
+  int i = 0;
+  while (i < stop) {
+    int j = i;
+    while (j < stop) {
+      const int op = FS_OPCODE(ins_all[(size_t)j * FS_INS_WORDS]);
+      if (op == FS_OP_MEAS_ACTIVE || op == FS_OP_MEAS_COLLAPSE) break;
+      j++;
+    }
+    if (j > i) {
+      HbmStep st{};
+      st.kind = HbmStep::SCALAR;
+      st.i0 = i;
+      st.i1 = j;
+      PL.steps.push_back(st);
+    }
+    for (int t = i; t < j; t++) {
+      const int* I = ins_all + (size_t)t * FS_INS_WORDS;
+      const int op = FS_OPCODE(I[0]);
+      if (op != FS_OP_ARRAY_GATE && op != FS_OP_EXPAND && op != FS_OP_ARRAY_ROT && op != FS_OP_RETIRE) continue;
+      const int k_after = p->h_sched[t];
+      // candidate for a fused pass?
+      if (fused && op != FS_OP_RETIRE && k_after >= fs::kTileBits && k_after <= 31 &&
+          (int)live.size() + (op == FS_OP_EXPAND) >= fs::kTileBits) {
+        fs::TileOp to{};
+        to.instr = t;
+        to.pa = to.pb = -1;
+        int mix = -1;
+        if (op == FS_OP_ARRAY_GATE) {
+          const int g = I[1];
+          to.pa = (int8_t)live[I[4]];
+          if (g == FS_G_CX || g == FS_G_CZ) to.pb = (int8_t)live[I[5]];
+          to.kind = g == FS_G_H ? fs::TO_H : g == FS_G_S ? fs::TO_S : g == FS_G_SDAG ? fs::TO_SDAG
+                  : g == FS_G_CX ? fs::TO_CX : fs::TO_CZ;
+          if (g == FS_G_H) mix = to.pa;
+          if (g == FS_G_CX) mix = to.pb;
+        } else if (op == FS_OP_ARRAY_ROT) {
+          to.kind = fs::TO_ROT;
+          to.pa = (int8_t)live[I[2]];
+          to.c0 = cpx(I[5]);
+          to.c1 = cpx(I[5] + 2);
+        } else {  // EXPAND onto the lowest dead physical axis
+          to.kind = fs::TO_EXPAND;
+          to.pa = (int8_t)lowest_dead();
+          mix = to.pa;
+          to.c0 = cpx(I[5]); to.c1 = cpx(I[5] + 2); to.c2 = cpx(I[5] + 4); to.c3 = cpx(I[5] + 6);
+        }
+        if ((int)pops.size() >= fs::kPassMaxOps) flush();
+        if (mix >= 0 && std::find(need.begin(), need.end(), mix) == need.end()) {
+          int low = 0;
+          for (int q = 0; q < 3; q++)
+            if ((is_live(q) || q == mix) && std::find(need.begin(), need.end(), q) == need.end() && q != mix) low++;
+          if ((int)need.size() + 1 + low > fs::kTileBits) flush();
+          need.push_back(mix);
+        }
+        pops.push_back(to);
+        if (op == FS_OP_EXPAND) live.push_back(to.pa);
+        continue;
+      }
+      flush();
+      fs::ArrOp o{};
+      o.instr = t;
+      if (op == FS_OP_ARRAY_GATE) {
+        const int g = I[1], k = I[6];
+        o.pa = live[I[4]];
+        if (g == FS_G_CX || g == FS_G_CZ) {
+          o.pb = live[I[5]];
+          o.kind = g == FS_G_CX ? fs::HA_CX : fs::HA_CZ;
+          o.dead = dead_list({o.pa, o.pb});
+          arr(o, 1ull << (k - 2));
+        } else {
+          o.kind = g == FS_G_H ? fs::HA_H : (g == FS_G_S ? fs::HA_S : fs::HA_SDAG);
+          o.dead = dead_list({o.pa});
+          arr(o, 1ull << (k - 1));
+        }
+      } else if (op == FS_OP_EXPAND) {
+        const int kb = I[6];
+        o.kind = fs::HA_EXPAND;
+        o.pa = lowest_dead();
+        o.dead = dead_list({o.pa});
+        o.c0 = cpx(I[5]); o.c1 = cpx(I[5] + 2); o.c2 = cpx(I[5] + 4); o.c3 = cpx(I[5] + 6);
+        arr(o, 1ull << kb);
+        live.push_back(o.pa);
+      } else if (op == FS_OP_ARRAY_ROT) {
+        const int k = I[6];
+        o.kind = fs::HA_ROT;
+        o.pa = live[I[2]];
+        o.dead = dead_list({o.pa});
+        o.c0 = cpx(I[5]); o.c1 = cpx(I[5] + 2);
+        arr(o, 1ull << (k - 1));
+      } else {  // RETIRE
+        const int k = I[6];
+        o.kind = fs::HA_RETIRE;
+        o.pa = live[I[2]];
+        o.dead = dead_list({o.pa});
+        arr(o, 1ull << (k - 1));
+        live.erase(live.begin() + I[2]);
+      }
+    }
+    flush();
+    if (j >= stop) { i = j; break; }
+    const int* I = ins_all + (size_t)j * FS_INS_WORDS;
+    const int op = FS_OPCODE(I[0]);
+    const int k = I[6];
+    HbmStep st{};
+    st.kind = HbmStep::MEAS;
+    st.i0 = j;
+    st.op.instr = j;
+    st.op.pa = live[I[2]];
+    st.op.dead = dead_list({st.op.pa});
+    st.count = 1ull << (k - 1);
+    st.collapse = op == FS_OP_MEAS_COLLAPSE ? 1 : 0;
+    st.u10 = make_double2(0, 0);
+    st.u11 = make_double2(1, 0);
+    if (st.collapse) { st.u10 = cpx(I[5] + 4); st.u11 = cpx(I[5] + 6); }
+    PL.steps.push_back(st);
+    if (st.collapse) live.erase(live.begin() + I[2]);
+    i = j + 1;
+  }
+  const int kst = stop > 0 ? p->h_sched[stop - 1] : 0;
+  if ((int)live.size() != kst) return set_error(FS_ERR_ARG, "internal: axis map out of sync with schedule");
+  PL.final_live = live;
+  cudaFree(p->d_passes);
+  cudaFree(p->d_tileops);
+  p->d_passes = nullptr;
+  p->d_tileops = nullptr;
+  if (!PL.passes.empty()) {
+    FS_CUDA_TRY(cudaMalloc(&p->d_passes, sizeof(fs::PassDesc) * PL.passes.size()));
+    FS_CUDA_TRY(cudaMemcpy(p->d_passes, PL.passes.data(), sizeof(fs::PassDesc) * PL.passes.size(), cudaMemcpyHostToDevice));
+    FS_CUDA_TRY(cudaMalloc(&p->d_tileops, sizeof(fs::TileOp) * PL.tileops.size()));
+    FS_CUDA_TRY(cudaMemcpy(p->d_tileops, PL.tileops.data(), sizeof(fs::TileOp) * PL.tileops.size(), cudaMemcpyHostToDevice));
+  }
+  PL.built = true;
+  return FS_OK;
+}
+
 // ------------------------------------------------------------------ large-k engine driver
 int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   const fs::DevProg& dp = p->dp;
@@ -715,38 +1036,20 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
     FS_CUDA_TRY(cudaGetLastError());
     return FS_OK;
   };
-  const int* ins_all = p->h_instrs.data();
-  const double* fpar = p->h_fparams.data();
+  const bool fused = !(a.flags & FS_FORCE_HBM) || getenv("FS_HBM_FUSED");
+  int rc0 = plan_hbm(p, a.stop, fused && !getenv("FS_HBM_UNFUSED"));
+  if (rc0) return rc0;
+  const HbmPlan& PL = p->hplan;
+  const size_t pass_smem = ((size_t)16 << fs::kTileBits) + sizeof(fs::StagedOp) * fs::kPassMaxOps;
+  if (!PL.passes.empty())
+    FS_CUDA_TRY(cudaFuncSetAttribute(fs::hbm_fused_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem));
   for (uint64_t batch0 = 0; batch0 < a.nshots; batch0 += B) {
     const uint64_t nb = std::min<uint64_t>(B, a.nshots - batch0);
     const uint32_t W = (uint32_t)((nb + 31) / 32);
     int rc = scalar(0, 0, 1, batch0, W);
     if (rc) return rc;
     fs::hbm_init_amps_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, stream>>>(H, (uint32_t)nb);
-    std::vector<int> live;  // logical axis -> physical position
-    auto dead_list = [&](std::initializer_list<int> extra) {
-      fs::DeadBits d{};
-      int top = -1;
-      for (int x : live) top = std::max(top, x);
-      for (int x : extra) top = std::max(top, x);
-      std::vector<int> pos;
-      for (int q = 0; q <= top; q++) {
-        bool isl = std::find(live.begin(), live.end(), q) != live.end();
-        bool ise = std::find(extra.begin(), extra.end(), q) != extra.end();
-        if (!isl || ise) pos.push_back(q);
-      }
-      std::sort(pos.begin(), pos.end());
-      pos.erase(std::unique(pos.begin(), pos.end()), pos.end());
-      d.n = (int)pos.size();
-      for (int t = 0; t < d.n; t++) d.pos[t] = (int8_t)pos[t];
-      return d;
-    };
-    auto lowest_dead = [&]() {
-      for (int q = 0; q < dp.k_max; q++)
-        if (std::find(live.begin(), live.end(), q) == live.end()) return q;
-      return -1;
-    };
-    auto run_op = [&](fs::ArrOp& o, uint64_t count) -> int {
+    auto run_op = [&](const fs::ArrOp& o, uint64_t count) -> int {
       if (count == 0) return FS_OK;
       const uint64_t want_x = (count + 255) / 256;
       const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(want_x, std::max<uint64_t>(1, 16384 / nb)));
@@ -754,95 +1057,46 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
       FS_CUDA_TRY(cudaGetLastError());
       return FS_OK;
     };
-    auto cpx = [&](int off) { return make_double2(fpar[off], fpar[off + 1]); };
-    int i = 0;
-    const int stop = a.stop;
-    while (i < stop) {
-      int j = i;
-      while (j < stop) {
-        const int op = FS_OPCODE(ins_all[(size_t)j * FS_INS_WORDS]);
-        if (op == FS_OP_MEAS_ACTIVE || op == FS_OP_MEAS_COLLAPSE) break;
-        j++;
-      }
-      if (j > i && (rc = scalar(i, j, 0, batch0, W))) return rc;
-      for (int t = i; t < j; t++) {
-        const int* I = ins_all + (size_t)t * FS_INS_WORDS;
-        const int op = FS_OPCODE(I[0]);
-        fs::ArrOp o{};
-        o.instr = t;
-        if (op == FS_OP_ARRAY_GATE) {
-          const int g = I[1], k = I[6];
-          o.pa = live[I[4]];
-          if (g == FS_G_CX || g == FS_G_CZ) {
-            o.pb = live[I[5]];
-            o.kind = g == FS_G_CX ? fs::HA_CX : fs::HA_CZ;
-            o.dead = dead_list({o.pa, o.pb});
-            if ((rc = run_op(o, 1ull << (k - 2)))) return rc;
+    for (const HbmStep& st : PL.steps) {
+      switch (st.kind) {
+        case HbmStep::SCALAR:
+          if ((rc = scalar(st.i0, st.i1, 0, batch0, W))) return rc;
+          break;
+        case HbmStep::ARR:
+          if ((rc = run_op(st.op, st.count))) return rc;
+          break;
+        case HbmStep::PASS: {
+          const uint64_t ntiles = 1ull << PL.passes[st.pass].nbase;
+          const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(ntiles, std::max<uint64_t>(1, 4096 / nb)));
+          fs::hbm_fused_pass_kernel<<<dim3((unsigned)gx, (unsigned)nb), fs::kTileThreads, pass_smem, stream>>>(
+              H, PL.passes[st.pass], p->d_tileops, W);
+          FS_CUDA_TRY(cudaGetLastError());
+          break;
+        }
+        case HbmStep::MEAS: {
+          const int nbu = (int)std::max<uint64_t>(1, std::min<uint64_t>(nblk, (st.count + 2047) / 2048));
+          fs::hbm_reduce_kernel<<<dim3(nbu, (unsigned)nb), 256, 0, stream>>>(st.op, H, st.count, st.collapse, st.u10, st.u11);
+          fs::hbm_reduce_final_kernel<<<(unsigned)((nb + 127) / 128), 128, 0, stream>>>(H, (uint32_t)nb, nbu);
+          FS_CUDA_TRY(cudaGetLastError());
+          if ((rc = scalar(st.i0, st.i0 + 1, 0, batch0, W))) return rc;
+          fs::ArrOp o = st.op;
+          if (st.collapse) {
+            o.kind = fs::HA_COLLAPSE;
           } else {
-            o.kind = g == FS_G_H ? fs::HA_H : (g == FS_G_S ? fs::HA_S : fs::HA_SDAG);
-            o.dead = dead_list({o.pa});
-            if ((rc = run_op(o, 1ull << (k - 1)))) return rc;
+            o.kind = fs::HA_ACTIVE_ZERO;
+            o.c0 = make_double2((a.flags & FS_NO_RENORM) ? 0.0 : 1.0, 0.0);
           }
-        } else if (op == FS_OP_EXPAND) {
-          const int kb = I[6];
-          o.kind = fs::HA_EXPAND;
-          o.pa = lowest_dead();
-          o.dead = dead_list({o.pa});
-          o.c0 = cpx(I[5]); o.c1 = cpx(I[5] + 2); o.c2 = cpx(I[5] + 4); o.c3 = cpx(I[5] + 6);
-          if ((rc = run_op(o, 1ull << kb))) return rc;
-          live.push_back(o.pa);
-        } else if (op == FS_OP_ARRAY_ROT) {
-          const int k = I[6];
-          o.kind = fs::HA_ROT;
-          o.pa = live[I[2]];
-          o.dead = dead_list({o.pa});
-          o.c0 = cpx(I[5]); o.c1 = cpx(I[5] + 2);
-          if ((rc = run_op(o, 1ull << (k - 1)))) return rc;
-        } else if (op == FS_OP_RETIRE) {
-          const int k = I[6];
-          o.kind = fs::HA_RETIRE;
-          o.pa = live[I[2]];
-          o.dead = dead_list({o.pa});
-          if ((rc = run_op(o, 1ull << (k - 1)))) return rc;
-          live.erase(live.begin() + I[2]);
+          if ((rc = run_op(o, st.count))) return rc;
+          break;
         }
       }
-      if (j >= stop) { i = j; break; }
-      // measurement j: reduction -> decision -> collapse
-      const int* I = ins_all + (size_t)j * FS_INS_WORDS;
-      const int op = FS_OPCODE(I[0]);
-      const int k = I[6];
-      fs::ArrOp o{};
-      o.instr = j;
-      o.pa = live[I[2]];
-      o.dead = dead_list({o.pa});
-      const uint64_t pairs = 1ull << (k - 1);
-      const bool collapse = op == FS_OP_MEAS_COLLAPSE;
-      double2 u10 = make_double2(0, 0), u11 = make_double2(1, 0);
-      if (collapse) { u10 = cpx(I[5] + 4); u11 = cpx(I[5] + 6); }
-      const int nbu = (int)std::max<uint64_t>(1, std::min<uint64_t>(nblk, (pairs + 2047) / 2048));
-      fs::hbm_reduce_kernel<<<dim3(nbu, (unsigned)nb), 256, 0, stream>>>(o, H, pairs, collapse ? 1 : 0, u10, u11);
-      fs::hbm_reduce_final_kernel<<<(unsigned)((nb + 127) / 128), 128, 0, stream>>>(H, (uint32_t)nb, nbu);
-      FS_CUDA_TRY(cudaGetLastError());
-      if ((rc = scalar(j, j + 1, 0, batch0, W))) return rc;
-      if (collapse) {
-        o.kind = fs::HA_COLLAPSE;
-        if ((rc = run_op(o, pairs))) return rc;
-        live.erase(live.begin() + I[2]);
-      } else {
-        o.kind = fs::HA_ACTIVE_ZERO;
-        o.c0 = make_double2((a.flags & FS_NO_RENORM) ? 0.0 : 1.0, 0.0);
-        if ((rc = run_op(o, pairs))) return rc;
-      }
-      i = j + 1;
     }
     fs::hbm_finish_kernel<<<(W + 127) / 128, 128, 0, stream>>>(dp, a, H, batch0, W);
     FS_CUDA_TRY(cudaGetLastError());
     if (a.t_amps) {
-      const int kst = stop > 0 ? p->h_sched[stop - 1] : 0;
-      if ((int)live.size() != kst) return set_error(FS_ERR_ARG, "internal: axis map out of sync with schedule");
+      const int kst = (int)PL.final_live.size();
       fs::DevAxisMap m{};
-      for (int b = 0; b < kst; b++) m.phys[b] = (int8_t)live[b];
+      for (int b = 0; b < kst; b++) m.phys[b] = (int8_t)PL.final_live[b];
       const uint64_t sz = 1ull << kst;
       const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>((sz + 255) / 256, 1024));
       fs::hbm_gather_kernel<<<dim3((unsigned)gx, (unsigned)nb), 256, 0, stream>>>(dp, a, H, batch0, (uint32_t)nb, kst, m);

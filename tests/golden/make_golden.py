@@ -215,6 +215,27 @@ def main(which=("configs", "random", "toys")):
             circ = ftest.random_mirror_circuit(rng, int(rng.integers(2, 7)), int(rng.integers(1, 8)))
             text = str(circ)
             write_case(f"mirror{i:02d}", compile_circuit(text), text, free_shots=512, trace_shots=4, rng=rng)
+    if "fused" in which:  # 12 <= k_max <= 15: the large-k engine's fused tile passes at small sizes
+        from paper_2604_27058_b200.configs import random_near_clifford
+        rng = np.random.default_rng(7)
+        made = 0
+        while made < 4:
+            n = int(rng.integers(13, 18))
+            text = random_near_clifford(n, int(rng.integers(4, 9)), t_cells=int(rng.integers(10, 25)),
+                                        seed=int(rng.integers(0, 2 ** 31)))
+            prog = compile_circuit(text)
+            if not 12 <= prog.k_max <= 15:
+                continue
+            lines = text.strip().split("\n")
+            if made % 2:
+                lines[-1] = "M " + " ".join(str(q) for q in range(0, n, 2))
+            if made >= 2:
+                lines = [x for ln in lines for x in (ln, f"DEPOLARIZE1(0.02) {rng.integers(0, n)}")]
+            text = "\n".join(lines) + "\n"
+            prog = compile_circuit(text)
+            cps = tuple(sorted(set(int(x) for x in rng.integers(0, len(prog.instrs), size=3))))
+            write_case(f"fusedk{made:02d}", prog, text, free_shots=64, trace_shots=4, checkpoints=cps, rng=rng)
+            made += 1
     if "configs" in which:
         for i in range(5):
             text, ps = config_text(i)
@@ -237,4 +258,4 @@ def main(which=("configs", "random", "toys")):
 
 
 if __name__ == "__main__":
-    main(tuple(sys.argv[1:]) or ("toys", "random", "configs"))
+    main(tuple(sys.argv[1:]) or ("toys", "random", "fused", "configs"))

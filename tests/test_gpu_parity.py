@@ -177,3 +177,58 @@ def test_gpu_general_jit_equals_interpreter(cuda, name):
     _, b, _ = dp.sample_host(n, seed=13, shot0=32 * 3, flags=FS_RNG_PHILOX | FS_NO_JIT)
     _same(a, b)
     assert dp.jit_status().startswith("ready"), dp.jit_status()
+
+
+FUSED = [c for c in ALL if load(c)["prog"].k_max >= 12]
+
+
+def _hbm_plan(dp):
+    """(steps, fused passes, fused ops, unfused array kernels, measurements) of the large-k plan."""
+    import ctypes as C
+
+    out = (C.c_int64 * 5)()
+    dp._lib.fs_debug_hbm_plan.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+    assert dp._lib.fs_debug_hbm_plan(dp._h, out) == 0
+    return list(out)
+
+
+@pytest.mark.parametrize("name", [c for c in FUSED if "t_modes" in load(c)])
+def test_gpu_fused_passes_trace_match_reference(cuda, name, monkeypatch):
+    """Large-k engine with fused tile passes (FS_HBM_FUSED) on every k_max >= 12 golden: trace
+    records, frames, gamma, final amplitudes and checkpoints against the REFERENCE."""
+    monkeypatch.setenv("FS_HBM_FUSED", "1")
+    g = load(name)
+    P = g["prog"]
+    dp = _dev(P)
+    assert _hbm_plan(dp)[1] > 0, "no fused pass planned"
+    n = g["t_modes"].shape[0]
+    flags = FS_RNG_SPLITMIX | FS_FORCE_HBM
+    st, out, tb = dp.sample_host(n, seed=int(g["t_seed"][0]), flags=flags, fault_modes=g["t_modes"],
+                                 forced=g["t_forced"], want_state=True)
+    assert st == 0
+    np.testing.assert_array_equal(out.measurements(), g["t_meas"])
+    np.testing.assert_array_equal(out.detectors(), g["t_det"])
+    np.testing.assert_array_equal(out.accepted_bits(), g["t_acc"])
+    np.testing.assert_array_equal(tb.frame_x[:, :P.n], g["t_fx"])
+    assert rel_err(tb.gamma_c(), g["t_gamma"]) < AMP_TOL
+    if "t_amps" in g and g["t_acc"].all():
+        assert rel_err(tb.amps_c(), g["t_amps"]) < AMP_TOL
+    for c in (g["cp_index"].tolist() if "cp_index" in g else []):
+        st, out, tb = dp.sample_host(n, seed=int(g["t_seed"][0]), flags=flags, fault_modes=g["t_modes"],
+                                     forced=g["t_forced"], stop=c + 1, want_state=True)
+        ok = ~np.isnan(g[f"cp{c}_gamma"])
+        assert rel_err(tb.gamma_c()[ok], g[f"cp{c}_gamma"][ok]) < AMP_TOL
+        assert rel_err(tb.amps_c()[ok], g[f"cp{c}_amps"][ok]) < AMP_TOL
+
+
+@pytest.mark.parametrize("name", [c for c in FUSED if "f_meas" in load(c)])
+def test_gpu_fused_passes_free_match_reference(cuda, name, monkeypatch):
+    monkeypatch.setenv("FS_HBM_FUSED", "1")
+    g = load(name)
+    dp = _dev(g["prog"])
+    n = g["f_meas"].shape[0]
+    st, out, _ = dp.sample_host(n, seed=int(g["f_seed"][0]), flags=FS_RNG_SPLITMIX | FS_FORCE_HBM)
+    assert st == 0
+    np.testing.assert_array_equal(out.measurements(), g["f_meas"])
+    np.testing.assert_array_equal(out.detectors(), g["f_det"])
+    np.testing.assert_array_equal(out.accepted_bits(), g["f_acc"])
