@@ -34,9 +34,13 @@ struct TileOp {
 struct PassDesc {
   int nops, op_off;
   int nbase;
+  int ncode, code_off;    // microcode words (see below)
+  int nconst, const_off;  // PassConst entries
   int8_t T[kTileBits];   // physical axis of each tile bit
   int8_t base[32];       // live physical axes outside the tile (tile index bits)
   uint32_t dep_hi[kTileElems];  // physical offset of element j = tid + 256 * j, high part
+  int8_t Tf[kTileBits];          // layout at the end of the pass (after register swaps)
+  uint32_t dep_hi_f[kTileElems];
 };
 
 __device__ __forceinline__ uint64_t deposit_bits(uint64_t v, const int8_t* pos, int n) {
@@ -88,23 +92,36 @@ __device__ __forceinline__ void reg_expand(double2 (&v)[kTileElems], double2 ph0
     }
 }
 
-// pass op staged in shared memory: kind | xa << 4 | xb << 9 | diag_run << 16, where xa / xb are
-// positions in the extended local index X = tid | j << 8 | tile << 12 (tile bits 0..11, then the
-// tile index bits = the pass's base axes); ca / cb = the op's constants with the shot's parity
-// already applied (ROT: factor for bit 0 / 1; EXPAND: phase of the bit-0 / bit-1 half)
-struct StagedOp {
-  uint32_t w, pad;
-  double2 ca, cb;
+// ---- pass microcode (host-compiled by plan_hbm, shot-independent)
+// Positions are bits of the extended local index X = tid | j << 8 | tile << 12: tile bits 0..7 are
+// thread bits, 8..11 register bits (element j of the thread), then the pass's base axes.
+//   MC_H   | m << 4                      Hadamard along tile bit m
+//   MC_CX  | m << 4 | c << 9             X on tile bit m controlled by position c
+//   MC_EXP | m << 4 | k << 16            Expand onto tile bit m, constants k
+// Register bits (m >= 8) are updated in registers; a thread bit (m < 8) exchanges the tile with
+// the partner thread tid ^ (1 << m) through shared memory.
+//   MC_DIAG| nterm << 4 | nrot << 12, then lin0, lin1, M0..M3, sR | QQ << 16,
+//            nterm x (a, N_a), nrot x (a | k << 8)
+// A diagonal run (CZ / S / S_DAG / ROT, which commute) multiplies element X by
+// i^P(X) * prod_rot c(X) with the Z4 quadratic form
+//   P(X) = sum_a s_a x_a + 2 sum_{CZ(a,b)} x_a x_b.
+// Over the constant bits (thread + tile index) of a thread it evaluates to
+//   e0 = popc(X & lin0) + 2 popc(X & lin1) + 2 sum_a x_a popc(X & N_a),
+//   e_R = s_R + 2 popc(X & M_R)          (coefficient of register bit R),
+// plus 2 * QQ (the register-register CZ pattern over j), so a run costs a few popcounts per
+// thread instead of one update of every element per instruction.
+enum : uint32_t { MC_H = 0, MC_CX = 1, MC_EXP = 2, MC_DIAG = 3 };
+
+struct PassConst {  // ROT: c0 / c1 = factor of bit 0 / 1; EXPAND: c0..c3 (parity 0: c0, c1; 1: c2, c3)
+  double2 c0, c1, c2, c3;
+  int instr, kind, pad0, pad1;
 };
-constexpr int kPassMaxOps = kTileThreads;
+constexpr int kPassMaxOps = kTileThreads;  // tile ops per pass (bounds constants and microcode)
+constexpr int kPassMaxCode = 2048;
+constexpr int kPassSmem = (16 << kTileBits) + 4 * kPassMaxCode + 32 * kPassMaxOps;
 
 __device__ __forceinline__ uint32_t reg_mask(int R) {  // j in [0,16) with bit R set
   return (uint32_t)((0xFF00F0F0CCCCAAAAull >> (16 * R)) & 0xFFFFu);
-}
-
-// 16-bit mask over j of the elements whose bit at extended position x is set
-__device__ __forceinline__ uint32_t pos_mask(int x, uint32_t X0) {
-  return (unsigned)(x - 8) < 4u ? reg_mask(x - 8) : (((X0 >> x) & 1u) ? 0xFFFFu : 0u);
 }
 
 __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
@@ -112,49 +129,31 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
 }
 
-// a run of diagonal ops (CZ, S, S_DAG, ROT) on the thread's 16 elements.  Diagonal ops commute,
-// so the run is accumulated as  v[j] *= i^P(j) * g * prod_{R : bit R of j} d_R  with the power P
-// held as two 16-bit planes over j (bit 0 in Lm, bit 1 in Hm) and applied once at the end.
-__device__ __forceinline__ void diag_run_apply(double2 (&v)[kTileElems], const StagedOp* __restrict__ so, int run,
-                                               uint32_t X0) {
-  uint32_t Lm = 0, Hm = 0, rreg = 0;
-  bool grot = false;
-  double2 g = make_double2(1, 0);
-  double2 d[4];
-#pragma unroll
-  for (int q = 0; q < 4; q++) d[q] = make_double2(1, 0);
-  for (int r = 0; r < run; r++) {
-    const uint32_t w = so[r].w;
-    const int kind = w & 15, xa = (w >> 4) & 31, xb = (w >> 9) & 31;
-    const uint32_t ma = pos_mask(xa, X0);
-    if (kind == TO_CZ) {
-      Hm ^= ma & pos_mask(xb, X0);
-    } else if (kind == TO_S) {  // P += 1 where bit set
-      const uint32_t c = Lm & ma;
-      Lm ^= ma;
-      Hm ^= c;
-    } else if (kind == TO_SDAG) {  // P -= 1 where bit set
-      const uint32_t b = ~Lm & ma;
-      Lm ^= ma;
-      Hm ^= b;
-    } else {  // ROT
-      const double2 ca = so[r].ca, cb = so[r].cb;
-      if ((unsigned)(xa - 8) < 4u) {
-        const int R = xa - 8;
-        g = cmul(g, ca);
-        const double2 rat = cdiv(cb, ca);
-#pragma unroll
-        for (int q = 0; q < 4; q++)
-          if (q == R) d[q] = cmul(d[q], rat);
-        rreg |= 1u << R;
-      } else {
-        g = cmul(g, ma ? cb : ca);
-        grot = true;
-      }
-    }
+__device__ __forceinline__ void diag_run_apply(double2 (&v)[kTileElems], const uint32_t* __restrict__ c,
+                                               const double2* __restrict__ cs, uint32_t X0) {
+  const uint32_t w = c[0];
+  const int nterm = (w >> 4) & 0xFF, nrot = (w >> 12) & 0xFF;
+  uint32_t e0 = __popc(X0 & c[1]) + 2u * __popc(X0 & c[2]);
+  uint32_t q = 0;
+  for (int t = 0; t < nterm; t++) {
+    const uint32_t a = c[8 + 2 * t], na = c[9 + 2 * t];
+    q += ((X0 >> a) & 1u) * __popc(X0 & na);
   }
-  Lm &= 0xFFFFu;
-  Hm &= 0xFFFFu;
+  e0 += 2u * q;
+  uint32_t Lm = (e0 & 1u) ? 0xFFFFu : 0u, Hm = (e0 & 2u) ? 0xFFFFu : 0u;
+  const uint32_t sr = c[7];
+#pragma unroll
+  for (int R = 0; R < 4; R++) {
+    const uint32_t eR = ((sr >> (2 * R)) & 3u) + 2u * __popc(X0 & c[3 + R]);
+    const uint32_t m = reg_mask(R);
+    if (eR & 1u) {
+      const uint32_t cy = Lm & m;
+      Lm ^= m;
+      Hm ^= cy;
+    }
+    if (eR & 2u) Hm ^= m;
+  }
+  Hm ^= sr >> 16;
   if (Lm | Hm) {
 #pragma unroll
     for (int j = 0; j < kTileElems; j++) {
@@ -166,55 +165,81 @@ __device__ __forceinline__ void diag_run_apply(double2 (&v)[kTileElems], const S
       v[j] = make_double2(x, y);
     }
   }
+  if (nrot == 0) return;
+  const uint32_t* rt = c + 8 + 2 * nterm;
+  uint32_t rreg = 0;
+  double2 g = make_double2(1, 0);
+  double2 d[4];
+#pragma unroll
+  for (int q4 = 0; q4 < 4; q4++) d[q4] = make_double2(1, 0);
+  for (int r = 0; r < nrot; r++) {
+    const uint32_t rw = rt[r];
+    const int xa = rw & 31, k = rw >> 8;
+    const double2 ca = cs[2 * k], cb = cs[2 * k + 1];
+    if ((unsigned)(xa - 8) < 4u) {
+      const int R = xa - 8;
+      g = cmul(g, ca);
+      const double2 rat = cdiv(cb, ca);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; q4++)
+        if (q4 == R) d[q4] = cmul(d[q4], rat);
+      rreg |= 1u << R;
+    } else {
+      g = cmul(g, ((X0 >> xa) & 1u) ? cb : ca);
+    }
+  }
   if (rreg) {
-    double2 t01[4], t23[4];
+    double2 t01[4];
     t01[0] = g;
     t01[1] = cmul(g, d[0]);
     t01[2] = cmul(g, d[1]);
     t01[3] = cmul(t01[1], d[1]);
-    t23[1] = d[2];
-    t23[2] = d[3];
-    t23[3] = cmul(d[2], d[3]);
+    const double2 d23 = cmul(d[2], d[3]);
 #pragma unroll
     for (int j = 0; j < kTileElems; j++) {
-      const double2 f = (j >> 2) ? cmul(t01[j & 3], t23[j >> 2]) : t01[j & 3];
+      const int hi = j >> 2;
+      const double2 f = hi == 0 ? t01[j & 3] : cmul(t01[j & 3], hi == 1 ? d[2] : hi == 2 ? d[3] : d23);
       v[j] = cmul(v[j], f);
     }
-  } else if (grot) {
+  } else {
 #pragma unroll
     for (int j = 0; j < kTileElems; j++) v[j] = cmul(v[j], g);
   }
 }
 
 __global__ void __launch_bounds__(kTileThreads, 2) hbm_fused_pass_kernel(HbmState H, const PassDesc D,
-                                                                        const TileOp* __restrict__ ops, uint32_t W) {
+                                                                        const uint32_t* __restrict__ code,
+                                                                        const PassConst* __restrict__ consts,
+                                                                        uint32_t W) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* T = reinterpret_cast<double2*>(smem_raw);
-  StagedOp* so = reinterpret_cast<StagedOp*>(smem_raw + sizeof(double2) * (1 << kTileBits));
+  uint32_t* mc = reinterpret_cast<uint32_t*>(smem_raw + (16 << kTileBits));
+  double2* cs = reinterpret_cast<double2*>(smem_raw + (16 << kTileBits) + 4 * kPassMaxCode);
   const uint32_t shot = blockIdx.y;
   const uint32_t w = shot >> 5, bit = 1u << (shot & 31);
   if (!(H.alive[w] & bit)) return;
   const uint32_t tid = threadIdx.x;
-  const int nops = D.nops;
-  if ((int)tid < nops) {  // stage this pass's ops, resolving the shot's parities
-    const TileOp& o = ops[D.op_off + tid];
-    StagedOp s;
-    s.w = (uint32_t)o.kind | (uint32_t)(o.la & 31) << 4 | (uint32_t)(o.lb & 31) << 9 | (uint32_t)o.diag_run << 16;
-    s.pad = 0;
-    s.ca = o.c0;
-    s.cb = o.c1;
-    if (o.kind == TO_ROT || o.kind == TO_EXPAND) {
-      const bool par = (H.par[(size_t)o.instr * W + w] & bit) != 0;
-      if (o.kind == TO_ROT && par) { s.ca = o.c1; s.cb = o.c0; }
-      if (o.kind == TO_EXPAND && par) { s.ca = o.c2; s.cb = o.c3; }
+  for (int i = tid; i < D.ncode; i += kTileThreads) mc[i] = code[D.code_off + i];
+  for (int i = tid; i < D.nconst; i += kTileThreads) {  // resolve the shot's parities
+    const PassConst& k = consts[D.const_off + i];
+    const bool par = (H.par[(size_t)k.instr * W + w] & bit) != 0;
+    double2 a = k.c0, b = k.c1;
+    if (par) {
+      if (k.kind == TO_ROT) { a = k.c1; b = k.c0; }
+      else { a = k.c2; b = k.c3; }
     }
-    so[tid] = s;
+    cs[2 * i] = a;
+    cs[2 * i + 1] = b;
   }
-  uint32_t dep_lo = 0;
+  uint32_t dep_lo = 0, dep_lo_f = 0;
 #pragma unroll
-  for (int i = 0; i < 8; i++) dep_lo |= ((tid >> i) & 1u) << D.T[i];
+  for (int i = 0; i < 8; i++) {
+    dep_lo |= ((tid >> i) & 1u) << D.T[i];
+    dep_lo_f |= ((tid >> i) & 1u) << D.Tf[i];
+  }
   const uint64_t ntiles = 1ull << D.nbase;
   double2* __restrict__ A = H.amps + (size_t)shot * H.cap;
+  const int ncode = D.ncode;
   __syncthreads();
   double2 v[kTileElems];
   for (uint64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
@@ -222,30 +247,31 @@ __global__ void __launch_bounds__(kTileThreads, 2) hbm_fused_pass_kernel(HbmStat
     const uint32_t X0 = tid | (uint32_t)(ti << kTileBits);
 #pragma unroll
     for (int j = 0; j < kTileElems; j++) v[j] = A[base | dep_lo | D.dep_hi[j]];
-    for (int k = 0; k < nops; k++) {
-      const uint32_t ow = so[k].w;
-      const int kind = ow & 15;
-      const int run = (ow >> 16) & 255;
-      if (run > 0) {
-        diag_run_apply(v, so + k, run, X0);
-        k += run - 1;
+    for (int pc = 0; pc < ncode;) {
+      const uint32_t ow = mc[pc];
+      const uint32_t kind = ow & 15u;
+      if (kind == MC_DIAG) {
+        diag_run_apply(v, mc + pc, cs, X0);
+        pc += 8 + 2 * ((ow >> 4) & 0xFF) + ((ow >> 12) & 0xFF);
         continue;
       }
-      const int xa = (ow >> 4) & 31, xb = (ow >> 9) & 31;
-      const int m = kind == TO_CX ? xb : xa;  // mixing bit (always inside the tile)
+      pc++;
+      const int m = (ow >> 4) & 15;
       if (m >= 8) {  // register bit: no data exchange
         const int R = m - 8;
-        if (kind == TO_H) {
+        if (kind == MC_H) {
           if (R == 0) reg_h<0>(v); else if (R == 1) reg_h<1>(v); else if (R == 2) reg_h<2>(v); else reg_h<3>(v);
-        } else if (kind == TO_CX) {
+        } else if (kind == MC_CX) {
+          const int xa = (ow >> 9) & 31;
           const bool creg = (unsigned)(xa - 8) < 4u;
           const int c = creg ? xa - 8 : (int)((X0 >> xa) & 1u);
-          const int ck = creg ? 0 : 3;
           if (!creg && !c) continue;
+          const int ck = creg ? 0 : 3;
           if (R == 0) reg_cx<0>(v, ck, c, tid, 0); else if (R == 1) reg_cx<1>(v, ck, c, tid, 0);
           else if (R == 2) reg_cx<2>(v, ck, c, tid, 0); else reg_cx<3>(v, ck, c, tid, 0);
-        } else {
-          const double2 ph0 = so[k].ca, ph1 = so[k].cb;
+        } else {  // MC_EXP
+          const int k = ow >> 16;
+          const double2 ph0 = cs[2 * k], ph1 = cs[2 * k + 1];
           if (R == 0) reg_expand<0>(v, ph0, ph1); else if (R == 1) reg_expand<1>(v, ph0, ph1);
           else if (R == 2) reg_expand<2>(v, ph0, ph1); else reg_expand<3>(v, ph0, ph1);
         }
@@ -256,30 +282,34 @@ __global__ void __launch_bounds__(kTileThreads, 2) hbm_fused_pass_kernel(HbmStat
       for (int j = 0; j < kTileElems; j++) T[tid + kTileThreads * j] = v[j];
       __syncthreads();
       const uint32_t ptid = tid ^ (1u << m);
-      const int mine_bit = (tid >> m) & 1;
-      if (kind == TO_H) {
+      const bool mine_bit = (tid >> m) & 1u;
+      if (kind == MC_H) {  // bit 0: (v + p) / sqrt2, bit 1: (p - v) / sqrt2
+        const double sg = mine_bit ? -1.0 : 1.0;
 #pragma unroll
         for (int j = 0; j < kTileElems; j++) {
           const double2 pv = T[ptid + kTileThreads * j];
-          v[j] = mine_bit ? cscale(csub(pv, v[j]), kInvSqrt2) : cscale(cadd(v[j], pv), kInvSqrt2);
+          v[j] = make_double2(__dmul_rn(__fma_rn(sg, v[j].x, pv.x), kInvSqrt2),
+                              __dmul_rn(__fma_rn(sg, v[j].y, pv.y), kInvSqrt2));
         }
-      } else if (kind == TO_CX) {
-        const uint32_t cm = pos_mask(xa, X0);
+      } else if (kind == MC_CX) {
+        const int xa = (ow >> 9) & 31;
+        const uint32_t cm = (unsigned)(xa - 8) < 4u ? reg_mask(xa - 8) : (((X0 >> xa) & 1u) ? 0xFFFFu : 0u);
 #pragma unroll
         for (int j = 0; j < kTileElems; j++)
           if ((cm >> j) & 1u) v[j] = T[ptid + kTileThreads * j];
       } else {  // expand: bit-1 half gets the bit-0 partner times ph1
-        const double2 ph0 = so[k].ca, ph1 = so[k].cb;
+        const int k = ow >> 16;
+        const double2 ph = mine_bit ? cs[2 * k + 1] : cs[2 * k];
 #pragma unroll
         for (int j = 0; j < kTileElems; j++) {
           const double2 pv = T[ptid + kTileThreads * j];
-          v[j] = mine_bit ? cmul(pv, ph1) : cmul(v[j], ph0);
+          v[j] = cmul(mine_bit ? pv : v[j], ph);
         }
       }
       __syncthreads();
     }
 #pragma unroll
-    for (int j = 0; j < kTileElems; j++) A[base | dep_lo | D.dep_hi[j]] = v[j];
+    for (int j = 0; j < kTileElems; j++) A[base | dep_lo_f | D.dep_hi_f[j]] = v[j];
   }
 }
 

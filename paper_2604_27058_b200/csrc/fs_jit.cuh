@@ -107,6 +107,7 @@ struct FrameKernelSource {
   std::string src;
   std::vector<uint16_t> pslot;  // per Pauli entry: physical slot under the renaming at its block
   int nslots = 0;               // physical frame slots (2n)
+  int stage = kJitStage;        // staged fault entries per word (smem rows per warp)
   std::vector<int32_t> site_block;  // NoiseBlock ordinal of every site
   int nblocks = 0;
   std::vector<int32_t> block_hi, block_cap, row_off;  // flip rows per NoiseBlock
@@ -124,6 +125,13 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   FrameKernelSource K;
   const int n = d.n;
   K.nslots = 2 * n;
+  // fault staging depth: shrink it (not below 40) when that fits a third 4-warp block per SM
+  // (3 x (smem + 1 KiB reserve) <= 228 KiB); words with more faults generate in place
+  {
+    const int fit = 76800 / (4 * 32 * 4) - K.nslots;
+    if (fit >= 40 && fit < kJitStage) K.stage = fit;
+    if (const char* e = getenv("FS_JIT_STAGE")) K.stage = std::max(8, std::min(kJitStage, atoi(e)));
+  }
   K.site_block.assign(d.num_sites + 1, 0);
   for (int i = 0, b = 0; i < d.num_instrs; i++)
     if (FS_OPCODE(ins_all[(size_t)i * FS_INS_WORDS]) == FS_OP_NOISE) {
@@ -164,8 +172,8 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
        "const uint32_t* __restrict__ ntot) {\n";
   o << "  extern __shared__ uint32_t smem[];\n";
   o << "  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;\n";
-  o << "  uint32_t* F = smem + wib * " << (K.nslots + kJitStage) * 32 << " + lane;\n";
-  o << "  uint32_t* stage = smem + wib * " << (K.nslots + kJitStage) * 32 << " + " << K.nslots * 32 << ";\n";
+  o << "  uint32_t* F = smem + wib * " << (K.nslots + K.stage) * 32 << " + lane;\n";
+  o << "  uint32_t* stage = smem + wib * " << (K.nslots + K.stage) * 32 << " + " << K.nslots * 32 << ";\n";
   o << "  const uint64_t word0 = A.shot0 >> 5;\n";
   o << "  const uint64_t seed = A.seed;\n";
   o << "  for (uint32_t w = (blockIdx.x * 4 + wib) * 32 + lane; w < A.W; w += gridDim.x * 4 * 32) {\n";
@@ -184,7 +192,7 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
   o << "    const uint32_t nt_ = ntot[w];\n    const bool fover = nt_ == 0xFFFFFFFFu;\n";
   o << "    fs::FaultBuffer<fs::kFaultCap> fbuf;\n    if (fover) fbuf.init(P, seed, wabs);\n";
   o << "    uint32_t fcur = 0;\n";
-  o << "    {\n      const uint32_t mine = fover ? 0u : min(nt_, " << kJitStage << "u);\n";
+  o << "    {\n      const uint32_t mine = fover ? 0u : min(nt_, " << K.stage << "u);\n";
   o << "      uint32_t tmax = mine;\n";
   o << "      for (int o_ = 16; o_; o_ >>= 1) tmax = max(tmax, __shfl_xor_sync(__activemask(), tmax, o_));\n";
   o << "      for (uint32_t t = 0; t < tmax; t++) if (t < mine) stage[t * 32 + lane] = __ldg(fent + (size_t)t * A.ostride + w);\n";

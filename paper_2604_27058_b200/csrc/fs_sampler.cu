@@ -72,6 +72,8 @@ struct HbmPlan {
   std::vector<HbmStep> steps;
   std::vector<fs::PassDesc> passes;
   std::vector<fs::TileOp> tileops;
+  std::vector<uint32_t> code;          // pass microcode (fs_hbm_fused.cuh)
+  std::vector<fs::PassConst> consts;
   std::vector<int> final_live;
 };
 
@@ -114,6 +116,7 @@ struct fs_prog {
   uint32_t flist_cap = 0;
   int* d_site_block = nullptr;  // flip geometry: block_hi | row_off | block_cap
   int jit_nblocks = 0;
+  int jit_stage = fsjit::kJitStage;  // fault-list capacity per word (frame kernel: its smem stage)
   int flip_rows = 0, flip_capmax = 0;
   int gjit_threads = 128;
   cudaStream_t aux = nullptr;  // fault-list generation overlapped with the specialised kernels
@@ -127,6 +130,8 @@ struct fs_prog {
   HbmPlan hplan;
   fs::PassDesc* d_passes = nullptr;
   fs::TileOp* d_tileops = nullptr;
+  uint32_t* d_code = nullptr;
+  fs::PassConst* d_consts = nullptr;
   void* hbm = nullptr;
   size_t hbm_bytes = 0;
   uint64_t hbm_B = 0;
@@ -279,6 +284,8 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->hbm);
   cudaFree(p->d_passes);
   cudaFree(p->d_tileops);
+  cudaFree(p->d_code);
+  cudaFree(p->d_consts);
   cudaFree(p->seg_pool[0]);
   cudaFree(p->seg_pool[1]);
   cudaFree(p->d_pslot);
@@ -394,6 +401,19 @@ extern "C" int fs_debug_hbm_plan(fs_prog* p, int64_t* out) {
   for (auto& st : PL.steps) { arr += st.kind == HbmStep::ARR; meas += st.kind == HbmStep::MEAS; }
   out[0] = (int64_t)PL.steps.size(); out[1] = (int64_t)PL.passes.size(); out[2] = (int64_t)PL.tileops.size();
   out[3] = arr; out[4] = meas;
+  // microcode census: smem exchanges, register mixing ops, diagonal runs, code words
+  int64_t sw = 0, mix = 0, dr = 0;
+  for (auto& D : PL.passes)
+    for (int pc = D.code_off; pc < D.code_off + D.ncode;) {
+      const uint32_t w = PL.code[pc];
+      const uint32_t k = w & 15u;
+      if (k == fs::MC_DIAG) { dr++; pc += 8 + 2 * ((w >> 4) & 0xFF) + ((w >> 12) & 0xFF); continue; }
+      const int m = (w >> 4) & 15;
+      sw += m < 8;  // exchanges through shared memory
+      mix += m >= 8;
+      pc++;
+    }
+  out[5] = sw; out[6] = mix; out[7] = dr; out[8] = (int64_t)PL.code.size();
   return 0;
 }
 
@@ -444,7 +464,7 @@ int ensure_jit(fs_prog* p) {
   fsjit::FrameKernelSource K = fsjit::gen_frame_kernel(p->desc, p->h_instrs, p->h_gates, p->h_paulis, p->h_reclists,
                                                        p->h_record_out, p->h_bit_slot, p->h_plans,
                                                        p->h_case_pauli_off, p->h_site_case_off, p->h_site_prob);
-  const size_t smem = (size_t)4 * (K.nslots + fsjit::kJitStage) * 32 * sizeof(uint32_t);
+  const size_t smem = (size_t)4 * (K.nslots + K.stage) * 32 * sizeof(uint32_t);
   if (smem > kSmemBudget) { p->jit_error = "frame too large for the specialised kernel"; return FS_ERR_ARG; }
   std::string err = fsjit::compile(K.src, fsjit::self_dir() + "/../csrc", p->jit);
   if (!err.empty()) { p->jit_error = err; return set_error(FS_ERR_ARG, err); }
@@ -457,6 +477,7 @@ int ensure_jit(fs_prog* p) {
   FS_CUDA_TRY(cudaMemcpy(p->d_pslot, K.pslot.data(), sizeof(uint16_t) * K.pslot.size(), cudaMemcpyHostToDevice));
   p->jit_nslots = K.nslots;
   p->jit_nblocks = K.nblocks;
+  p->jit_stage = K.stage;
   FS_CUDA_TRY(cudaMalloc(&p->d_site_block, sizeof(int) * K.site_block.size()));
   FS_CUDA_TRY(cudaMemcpy(p->d_site_block, K.site_block.data(), sizeof(int) * K.site_block.size(), cudaMemcpyHostToDevice));
   p->jit_state = 1;
@@ -676,7 +697,7 @@ int ensure_gjit(fs_prog* p) {
 // per-word fault lists for the specialised kernels (fs_jit_kernels.cuh fault_list_kernel)
 int alloc_fault_lists(fs_prog* p, size_t W, uint32_t** fent, uint32_t** bcount, uint32_t** ntot) {
   const int nb = std::max(1, p->jit_nblocks);
-  const uint32_t cap = fsjit::kJitStage;
+  const uint32_t cap = (uint32_t)p->jit_stage;
   const size_t need = align_up((size_t)cap * W * 4, 256) + align_up((size_t)nb * W * 4, 256) + W * 4 + 256;
   if (need > p->flist_bytes) {
     cudaFree(p->flist);
@@ -697,13 +718,101 @@ int run_fault_lists(fs_prog* p, const fs::RunArgs& a, size_t w0, size_t nw, uint
                     uint32_t* ntot, cudaStream_t stream) {
   fs::fault_list_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, stream>>>(
       p->dp, a.seed, (a.shot0 >> 5) + w0, (uint32_t)nw, a.ostride, p->d_site_block, p->jit_nblocks, fent + w0,
-      bcount + w0, ntot + w0, fsjit::kJitStage);
+      bcount + w0, ntot + w0, (uint32_t)p->jit_stage);
   FS_CUDA_TRY(cudaGetLastError());
   return FS_OK;
 }
 
 
 // ------------------------------------------------------------------ large-k plan
+// Microcode of one fused pass (format in fs_hbm_fused.cuh).  `T` = the pass's 12 tile axes in
+// tile-bit order (bits 8..11 = register bits), `base` = the live axes outside the tile.  The
+// layout is static over the pass (D.Tf == D.T); a mixing instruction on a thread bit exchanges
+// the tile through shared memory.  (Moving axes into register bits with half-tile swaps and
+// farthest-next-use eviction was measured: config 3 has almost no reuse of thread-bit axes, and
+// the swaps' per-thread register selects cost more than the exchanges they replace.)
+void compile_pass_code(std::vector<fs::TileOp>& pops, const std::vector<int>& T, const std::vector<int>& base,
+                       const std::vector<int>& lowq, fs::PassDesc& D, HbmPlan& PL) {
+  D.code_off = (int)PL.code.size();
+  D.const_off = (int)PL.consts.size();
+  std::vector<uint32_t>& C = PL.code;
+  int at[fs::kTileBits];
+  std::vector<int> pos(64, -1);
+  for (int i = 0; i < fs::kTileBits; i++) { at[i] = T[i]; pos[T[i]] = i; }
+  for (size_t i = 0; i < base.size(); i++) pos[base[i]] = fs::kTileBits + (int)i;
+  auto isreg = [](int x) { return x >= 8 && x < 12; };
+  auto rmask = [](int R) { return (uint32_t)((0xFF00F0F0CCCCAAAAull >> (16 * R)) & 0xFFFFu); };
+  auto mix_axis = [](const fs::TileOp& o) {
+    return o.kind == fs::TO_CX ? o.pb : (o.kind == fs::TO_H || o.kind == fs::TO_EXPAND) ? o.pa : -1;
+  };
+  auto add_const = [&](const fs::TileOp& o) {
+    fs::PassConst k{};
+    k.c0 = o.c0; k.c1 = o.c1; k.c2 = o.c2; k.c3 = o.c3;
+    k.instr = o.instr;
+    k.kind = o.kind;
+    PL.consts.push_back(k);
+    return (uint32_t)(PL.consts.size() - 1 - D.const_off);
+  };
+  for (size_t i = 0; i < pops.size();) {
+    fs::TileOp& o = pops[i];
+    if (o.diag_run > 0) {
+      uint32_t sv[32] = {0}, N[32] = {0}, M[4] = {0}, QQ = 0;
+      std::vector<uint32_t> rots;
+      for (int r = 0; r < o.diag_run; r++) {
+        fs::TileOp& d = pops[i + r];
+        d.la = (int8_t)pos[d.pa];
+        d.lb = d.pb >= 0 ? (int8_t)pos[d.pb] : (int8_t)-1;
+        if (d.kind == fs::TO_S) sv[d.la] += 1;
+        else if (d.kind == fs::TO_SDAG) sv[d.la] += 3;
+        else if (d.kind == fs::TO_CZ) {
+          const int a = d.la, b = d.lb;
+          if (!isreg(a) && !isreg(b)) N[std::min(a, b)] ^= 1u << std::max(a, b);
+          else if (isreg(a) && !isreg(b)) M[a - 8] ^= 1u << b;
+          else if (!isreg(a) && isreg(b)) M[b - 8] ^= 1u << a;
+          else QQ ^= rmask(a - 8) & rmask(b - 8);
+        } else {  // ROT
+          rots.push_back((uint32_t)d.la | add_const(d) << 8);
+        }
+      }
+      uint32_t lin0 = 0, lin1 = 0, sr = 0;
+      for (int x = 0; x < 32; x++) {
+        if (isreg(x)) { sr |= (sv[x] & 3u) << (2 * (x - 8)); continue; }
+        lin0 |= (sv[x] & 1u) << x;
+        lin1 |= ((sv[x] >> 1) & 1u) << x;
+      }
+      std::vector<uint32_t> terms;
+      for (int a2 = 0; a2 < 32; a2++)
+        if (N[a2]) { terms.push_back((uint32_t)a2); terms.push_back(N[a2]); }
+      const uint32_t nterm = (uint32_t)terms.size() / 2;
+      C.push_back(fs::MC_DIAG | nterm << 4 | (uint32_t)rots.size() << 12);
+      C.push_back(lin0);
+      C.push_back(lin1);
+      for (int R = 0; R < 4; R++) C.push_back(M[R]);
+      C.push_back(sr | QQ << 16);
+      C.insert(C.end(), terms.begin(), terms.end());
+      C.insert(C.end(), rots.begin(), rots.end());
+      i += o.diag_run;
+      continue;
+    }
+    const int q = mix_axis(o);
+    const uint32_t m = (uint32_t)pos[q];
+    o.la = (int8_t)pos[o.pa];
+    o.lb = o.pb >= 0 ? (int8_t)pos[o.pb] : (int8_t)-1;
+    if (o.kind == fs::TO_H) C.push_back(fs::MC_H | m << 4);
+    else if (o.kind == fs::TO_CX) C.push_back(fs::MC_CX | m << 4 | (uint32_t)pos[o.pa] << 9);
+    else C.push_back(fs::MC_EXP | m << 4 | add_const(o) << 16);  // EXPAND
+    i++;
+  }
+  for (int i = 0; i < fs::kTileBits; i++) D.Tf[i] = (int8_t)at[i];
+  for (int j = 0; j < fs::kTileElems; j++) {
+    uint32_t g = 0;
+    for (int b = 0; b < fs::kTileBits - 8; b++) g |= (uint32_t)((j >> b) & 1) << at[8 + b];
+    D.dep_hi_f[j] = g;
+  }
+  D.ncode = (int)PL.code.size() - D.code_off;
+  D.nconst = (int)PL.consts.size() - D.const_off;
+}
+
 // Host walk of the program (shot-independent): logical->physical axis map, the scalar
 // segments, per-instruction array kernels, measurements, and -- when the live dimension is at
 // least fs::kTileBits -- fused tile passes (fs_hbm_fused.cuh).
@@ -743,6 +852,7 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
   // pending fused pass
   std::vector<fs::TileOp> pops;
   std::vector<int> need;
+  bool code_overflow = false;
   auto flush = [&]() {
     if (pops.empty()) return;
     fs::PassDesc D{};
@@ -751,11 +861,15 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
       if (is_live(q) && std::find(T.begin(), T.end(), q) == T.end()) T.push_back(q);
     for (int q = 0; (int)T.size() < fs::kTileBits && q < 64; q++)
       if (is_live(q) && std::find(T.begin(), T.end(), q) == T.end()) T.push_back(q);
-    // register bits (tile bits 8..11): the most-mixed axes of the pass other than the low
-    // physical axes 0..2, which stay thread bits 0..2 for 128-byte coalesced accesses
-    std::vector<std::pair<int, int>> use;  // (-count, axis)
+    // layout: live low physical axes 0..2 on thread bits 0..2 (128-byte coalesced accesses),
+    // the four most-mixed other axes on the register bits 8..11, the rest on thread bits
+    std::vector<int> lowq;
+    for (int q : T)
+      if (q < 3 && is_live(q)) lowq.push_back(q);
+    std::sort(lowq.begin(), lowq.end());
+    std::vector<std::pair<int, int>> use;  // (-mixing uses, axis)
     for (int q : T) {
-      if (q < 3 && is_live(q)) continue;
+      if (std::find(lowq.begin(), lowq.end(), q) != lowq.end()) continue;
       int cnt = 0;
       for (auto& o : pops) {
         const int mix = o.kind == fs::TO_CX ? o.pb : (o.kind == fs::TO_H || o.kind == fs::TO_EXPAND) ? o.pa : -1;
@@ -766,12 +880,7 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
     std::sort(use.begin(), use.end());
     std::vector<int> regs, thr;
     for (auto& u : use) (regs.size() < 4 ? regs : thr).push_back(u.second);
-    std::vector<int> lowq;
-    for (int q : T)
-      if (q < 3 && is_live(q)) lowq.push_back(q);
-    std::sort(lowq.begin(), lowq.end());
     std::sort(thr.begin(), thr.end());
-    std::sort(regs.begin(), regs.end());
     T.clear();
     T.insert(T.end(), lowq.begin(), lowq.end());
     T.insert(T.end(), thr.begin(), thr.end());
@@ -789,24 +898,6 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
       for (int b = 0; b < fs::kTileBits - 8; b++) g |= (uint32_t)((j >> b) & 1) << T[8 + b];
       D.dep_hi[j] = g;
     }
-    auto local = [&](int q) {
-      for (int i = 0; i < fs::kTileBits; i++)
-        if (T[i] == q) return i;
-      return -1;
-    };
-    // la / lb: position in the extended local index (tile bits 0..11, then the base axes)
-    auto ext = [&](int q) -> int8_t {
-      if (q < 0) return (int8_t)-1;
-      const int l = local(q);
-      if (l >= 0) return (int8_t)l;
-      for (int i = 0; i < D.nbase; i++)
-        if (base[i] == q) return (int8_t)(fs::kTileBits + i);
-      return (int8_t)-1;
-    };
-    for (auto& o : pops) {
-      o.la = ext(o.pa);
-      o.lb = ext(o.pb);
-    }
     auto diag = [](int k) { return k == fs::TO_S || k == fs::TO_SDAG || k == fs::TO_CZ || k == fs::TO_ROT; };
     for (size_t i = 0; i < pops.size();) {
       if (!diag(pops[i].kind)) { pops[i].diag_run = 0; i++; continue; }
@@ -816,6 +907,8 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
       pops[i].diag_run = (int8_t)std::min<size_t>(e - i, 127);
       i = i + std::min<size_t>(e - i, 127);
     }
+    compile_pass_code(pops, T, base, lowq, D, PL);
+    if (D.ncode > fs::kPassMaxCode || D.nconst > fs::kPassMaxOps) code_overflow = true;
     D.nops = (int)pops.size();
     D.op_off = (int)PL.tileops.size();
     PL.tileops.insert(PL.tileops.end(), pops.begin(), pops.end());
@@ -955,10 +1048,23 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
   const int kst = stop > 0 ? p->h_sched[stop - 1] : 0;
   if ((int)live.size() != kst) return set_error(FS_ERR_ARG, "internal: axis map out of sync with schedule");
   PL.final_live = live;
+  if (code_overflow) return set_error(FS_ERR_ARG, "internal: fused pass microcode exceeds its shared-memory area");
   cudaFree(p->d_passes);
   cudaFree(p->d_tileops);
+  cudaFree(p->d_code);
+  cudaFree(p->d_consts);
   p->d_passes = nullptr;
   p->d_tileops = nullptr;
+  p->d_code = nullptr;
+  p->d_consts = nullptr;
+  if (!PL.code.empty()) {
+    FS_CUDA_TRY(cudaMalloc(&p->d_code, sizeof(uint32_t) * PL.code.size()));
+    FS_CUDA_TRY(cudaMemcpy(p->d_code, PL.code.data(), sizeof(uint32_t) * PL.code.size(), cudaMemcpyHostToDevice));
+  }
+  if (!PL.consts.empty()) {
+    FS_CUDA_TRY(cudaMalloc(&p->d_consts, sizeof(fs::PassConst) * PL.consts.size()));
+    FS_CUDA_TRY(cudaMemcpy(p->d_consts, PL.consts.data(), sizeof(fs::PassConst) * PL.consts.size(), cudaMemcpyHostToDevice));
+  }
   if (!PL.passes.empty()) {
     FS_CUDA_TRY(cudaMalloc(&p->d_passes, sizeof(fs::PassDesc) * PL.passes.size()));
     FS_CUDA_TRY(cudaMemcpy(p->d_passes, PL.passes.data(), sizeof(fs::PassDesc) * PL.passes.size(), cudaMemcpyHostToDevice));
@@ -1040,7 +1146,7 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   int rc0 = plan_hbm(p, a.stop, fused && !getenv("FS_HBM_UNFUSED"));
   if (rc0) return rc0;
   const HbmPlan& PL = p->hplan;
-  const size_t pass_smem = ((size_t)16 << fs::kTileBits) + sizeof(fs::StagedOp) * fs::kPassMaxOps;
+  const size_t pass_smem = fs::kPassSmem;
   if (!PL.passes.empty())
     FS_CUDA_TRY(cudaFuncSetAttribute(fs::hbm_fused_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem));
   for (uint64_t batch0 = 0; batch0 < a.nshots; batch0 += B) {
@@ -1069,7 +1175,7 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
           const uint64_t ntiles = 1ull << PL.passes[st.pass].nbase;
           const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(ntiles, std::max<uint64_t>(1, 4096 / nb)));
           fs::hbm_fused_pass_kernel<<<dim3((unsigned)gx, (unsigned)nb), fs::kTileThreads, pass_smem, stream>>>(
-              H, PL.passes[st.pass], p->d_tileops, W);
+              H, PL.passes[st.pass], p->d_code, p->d_consts, W);
           FS_CUDA_TRY(cudaGetLastError());
           break;
         }
@@ -1158,7 +1264,7 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     int rc = ensure_jit(p);
     if (rc == FS_OK) {
       fsjit::Api& J = fsjit::api();
-      const size_t smem = (size_t)4 * (p->jit_nslots + fsjit::kJitStage) * 32 * sizeof(uint32_t);
+      const size_t smem = (size_t)4 * (p->jit_nslots + p->jit_stage) * 32 * sizeof(uint32_t);
       int occ = 1;
       J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->jit.fn, 128, smem);
       const size_t groups = (W + 127) / 128;

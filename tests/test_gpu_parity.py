@@ -186,7 +186,7 @@ def _hbm_plan(dp):
     """(steps, fused passes, fused ops, unfused array kernels, measurements) of the large-k plan."""
     import ctypes as C
 
-    out = (C.c_int64 * 5)()
+    out = (C.c_int64 * 9)()
     dp._lib.fs_debug_hbm_plan.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     assert dp._lib.fs_debug_hbm_plan(dp._h, out) == 0
     return list(out)

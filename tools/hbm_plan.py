@@ -4,9 +4,9 @@ from paper_2604_27058_b200.program import Program
 from paper_2604_27058_b200.engine import DeviceProgram
 P = Program.load('paper_2604_27058_b200/programs/c3.npz')
 dp = DeviceProgram(P)
-out = (C.c_int64 * 5)()
+out = (C.c_int64 * 9)()
 dp._lib.fs_debug_hbm_plan.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
-print(dp._lib.fs_debug_hbm_plan(dp._h, out), list(out), "(steps, passes, fused ops, unfused array kernels, measurements)")
+print(dp._lib.fs_debug_hbm_plan(dp._h, out), list(out), "(steps, passes, fused ops, unfused array kernels, measurements, smem exchanges, reg mixing ops, diag runs, code words)")
 import numpy as np, collections
 buf = np.zeros((5000, 5), np.int32)
 dp._lib.fs_debug_hbm_tileops.restype = C.c_int64
