@@ -181,6 +181,10 @@ def workload_config(cfg: int) -> dict:
             "parallelism": "replicas (shot ranges), no collective"}
 
 
+KERNEL_NAME = {"frame": "fs_jit_frame (program-specialised frame kernel)",
+               "general": "general / block kernel", "hbm": "hbm_fused_pass_kernel"}
+
+
 def algorithmic_bytes_per_shot(P: Program) -> float:
     """Output-bound unit: user records + detectors + observables, bit-packed."""
     return P.output_bits() / 8.0
@@ -188,6 +192,8 @@ def algorithmic_bytes_per_shot(P: Program) -> float:
 
 def time_gpu_config(cfg: int, steps: int, warmup: int, rank: int, shots: int | None = None,
                     warm_shots: int | None = None) -> dict:
+    import ctypes as C
+
     import torch
 
     from paper_2604_27058_b200.engine import DeviceProgram
@@ -202,6 +208,13 @@ def time_gpu_config(cfg: int, steps: int, warmup: int, rank: int, shots: int | N
     for w in range(warmup):
         dp.sample_device(warm_shots or shots, out, seed=1000 + w, shot0=shot0)
     torch.cuda.synchronize()
+    L = dp._lib
+    L.fs_debug_launches.restype = C.c_uint64
+    L.fs_debug_launches.argtypes = [C.c_void_p]
+    L.fs_debug_kernel_timer.argtypes = [C.c_void_p, C.c_int]
+    L.fs_debug_kernel_time.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    L.fs_debug_kernel_timer(dp._h, 1)  # events around the dominant kernel's launches
+    n0 = L.fs_debug_launches(dp._h)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for k in range(steps):
         flush.fill_(k & 0xFF)
@@ -209,10 +222,15 @@ def time_gpu_config(cfg: int, steps: int, warmup: int, rank: int, shots: int | N
         dp.sample_device(shots, out, seed=k, shot0=shot0)
         ev[k][1].record(stream)
     torch.cuda.synchronize()
+    launches = int(L.fs_debug_launches(dp._h) - n0)
+    kms, kn = C.c_double(0.0), C.c_int64(0)
+    L.fs_debug_kernel_time(dp._h, C.byref(kms), C.byref(kn))
+    L.fs_debug_kernel_timer(dp._h, 0)
     ms = [a.elapsed_time(b) for a, b in ev]
     st = int(out["status"].item())
     return {"P": P, "dp": dp, "shots": shots, "shot0": shot0, "ms": ms, "status": st,
-            "engine": dp.engine(0), "out": out}
+            "engine": dp.engine(0), "out": out, "launches": launches,
+            "kernel_ms": float(kms.value), "kernel_launches": int(kn.value)}
 
 
 def fp64_peak() -> float:
@@ -251,14 +269,24 @@ def extra_config(c: int, fp64_tflops: float) -> dict:
     rate = shots / (ms / 1e3)
     d = {"shots_per_s": rate, "ms_per_step": ms, "shots": shots, "k_max": P.k_max, "engine": rc["engine"],
          "status": rc["status"]}
-    if c == 3:  # HBM bound: 32 B (one complex128 read + write) per element-sweep
-        W = P.work()
-        ach = 32.0 * W * rate / 1e9
+    d["gpu_launches_per_step"] = rc["launches"] / steps
+    d["dominant_kernel_share"] = rc["kernel_ms"] / (ms * steps)
+    if c == 3:  # fused tile passes: each reads + writes the live array of every shot once
+        bits = (C.c_int32 * 4096)()
+        L = rc["dp"]._lib
+        L.fs_debug_hbm_pass_bits.restype = C.c_int64
+        L.fs_debug_hbm_pass_bits.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.c_int64]
+        npass = L.fs_debug_hbm_pass_bits(rc["dp"]._h, bits, 4096)
+        pass_bytes = sum(32.0 * (1 << bits[i]) for i in range(npass)) * shots * steps
+        ach = pass_bytes / (rc["kernel_ms"] / 1e3) / 1e9
         pk = peaks()["hbm_gbs"]
+        W = P.work()
         d["roofline"] = {"bound": "hbm", "unit": "GB/s", "achieved": ach, "peak": pk, "frac": ach / pk,
-                         "algorithmic_bytes_per_shot": 32.0 * W,
-                         "note": "W = sum of 2^k over array instructions (reference plan_metrics); "
-                                 "the engine touches only changed elements, so frac can exceed 1"}
+                         "kernel": "hbm_fused_pass_kernel", "passes": npass,
+                         "bytes_per_shot": pass_bytes / (shots * steps),
+                         "unfused_algorithmic_bytes_per_shot": 32.0 * W,
+                         "note": "bytes = one complex128 read + write of the live array per fused pass; "
+                                 "the reference's per-instruction sweeps would move 32*W bytes per shot"}
     else:  # on-chip bound: 8 FP64 flop per element-sweep of the executed instructions
         segs = segment_work(P)
         if len(segs) > 1:
@@ -277,7 +305,7 @@ def extra_config(c: int, fp64_tflops: float) -> dict:
             w_exec = wexec / shots
         else:
             w_exec = float(segs[0][2])
-        ach = 8.0 * w_exec * rate / 1e12
+        ach = 8.0 * w_exec * shots * steps / (rc["kernel_ms"] / 1e3) / 1e12
         d["roofline"] = {"bound": "fp64", "unit": "TFLOP/s", "achieved": ach, "peak": fp64_tflops,
                          "frac": ach / fp64_tflops if fp64_tflops else None,
                          "w_exec_per_shot": w_exec, "flop_per_shot": 8.0 * w_exec,
@@ -379,8 +407,10 @@ def main():
     value = total_shots / dev_s
     avg_ms = dev_s / args.steps * 1e3
     pk = peaks()
-    bytes_per_launch = algorithmic_bytes_per_shot(P) * shots
-    achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
+    # dominant kernel: its own launches, timed with CUDA events on the launching stream
+    kern_ms = r["kernel_ms"] / max(r["kernel_launches"], 1)
+    bytes_per_launch = algorithmic_bytes_per_shot(P) * shots * args.steps / max(r["kernel_launches"], 1)
+    achieved = bytes_per_launch / (kern_ms / 1e3) / 1e9
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
@@ -422,11 +452,14 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
+                         "kernel": KERNEL_NAME.get(r["engine"], r["engine"]),
+                         "kernel_ms_per_launch": kern_ms,
+                         "kernel_share_of_step": r["kernel_ms"] / (avg_ms * args.steps),
                          "peak_source": pk["source"]},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "shots/s", "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
                     "d2h_bytes_per_step": e2e["d2h_bytes_per_step"]},
-            "gpu_launches": args.steps,
+            "gpu_launches": r["launches"],
             "clocks": clocks,
             "extra_configs": extra,
         }

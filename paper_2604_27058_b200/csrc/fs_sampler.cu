@@ -116,7 +116,12 @@ struct fs_prog {
   uint32_t flist_cap = 0;
   int* d_site_block = nullptr;  // flip geometry: block_hi | row_off | block_cap
   int jit_nblocks = 0;
-  int jit_stage = fsjit::kJitStage;  // fault-list capacity per word (frame kernel: its smem stage)
+  int jit_stage = fsjit::kJitStage;
+  // instrumentation: kernel launch count, optional events around the dominant kernel's launches
+  uint64_t launches = 0;
+  bool ktimer = false;
+  std::vector<cudaEvent_t> kev;
+  size_t kev_n = 0;  // fault-list capacity per word (frame kernel: its smem stage)
   int flip_rows = 0, flip_capmax = 0;
   int gjit_threads = 128;
   cudaStream_t aux = nullptr;  // fault-list generation overlapped with the specialised kernels
@@ -289,6 +294,7 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->seg_pool[0]);
   cudaFree(p->seg_pool[1]);
   cudaFree(p->d_pslot);
+  for (auto e : p->kev) cudaEventDestroy(e);
   if (p->aux) {
     cudaStreamDestroy(p->aux);
     for (auto& e : p->ev)
@@ -417,6 +423,19 @@ extern "C" int fs_debug_hbm_plan(fs_prog* p, int64_t* out) {
   return 0;
 }
 
+// live dimension (tile bits + base axes) of every fused pass, in execution order
+extern "C" int64_t fs_debug_hbm_pass_bits(fs_prog* p, int32_t* out, int64_t max) {
+  if (!p || plan_hbm(p, p->dp.num_instrs, true)) return -1;
+  const HbmPlan& PL = p->hplan;
+  int64_t n = 0;
+  for (const HbmStep& st : PL.steps)
+    if (st.kind == HbmStep::PASS) {
+      if (n < max) out[n] = fs::kTileBits + PL.passes[st.pass].nbase;
+      n++;
+    }
+  return n;
+}
+
 // per fused op: (pass, kind, la, lb, diag_run); returns the op count
 extern "C" int64_t fs_debug_hbm_tileops(fs_prog* p, int32_t* out, int64_t max) {
   if (!p || plan_hbm(p, p->dp.num_instrs, true)) return -1;
@@ -430,6 +449,34 @@ extern "C" int64_t fs_debug_hbm_tileops(fs_prog* p, int32_t* out, int64_t max) {
       r[0] = (int32_t)ps; r[1] = o.kind; r[2] = o.la; r[3] = o.lb; r[4] = o.diag_run;
     }
   return n;
+}
+
+// kernel launches issued by this program so far (all engines, all kernels of this library)
+extern "C" uint64_t fs_debug_launches(const fs_prog* p) { return p ? p->launches : 0; }
+
+// enable (1) / disable (0) CUDA events around the dominant kernel's launches; resets the record
+extern "C" int fs_debug_kernel_timer(fs_prog* p, int enable) {
+  if (!p) return -1;
+  std::lock_guard<std::mutex> g(p->mu);
+  p->ktimer = enable != 0;
+  p->kev_n = 0;
+  return 0;
+}
+
+// total device time (ms) and count of the recorded dominant-kernel launches (synchronizes)
+extern "C" int fs_debug_kernel_time(fs_prog* p, double* total_ms, int64_t* count) {
+  if (!p) return -1;
+  std::lock_guard<std::mutex> g(p->mu);
+  double t = 0.0;
+  for (size_t i = 0; i + 1 < p->kev_n; i += 2) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(p->kev[i + 1]) != cudaSuccess) return -1;
+    if (cudaEventElapsedTime(&ms, p->kev[i], p->kev[i + 1]) != cudaSuccess) return -1;
+    t += ms;
+  }
+  *total_ms = t;
+  *count = (int64_t)(p->kev_n / 2);
+  return 0;
 }
 
 extern "C" const char* fs_debug_jit_status(fs_prog* p) {
@@ -447,6 +494,22 @@ extern "C" int fs_program_engine(const fs_prog* p, uint32_t flags) {
 }
 
 namespace {
+
+// events around the dominant kernel of an engine (bench.py: roofline of that kernel)
+void kt_begin(fs_prog* p, cudaStream_t s) {
+  if (!p->ktimer) return;
+  while (p->kev.size() < p->kev_n + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) { p->ktimer = false; return; }
+    p->kev.push_back(e);
+  }
+  cudaEventRecord(p->kev[p->kev_n], s);
+}
+void kt_end(fs_prog* p, cudaStream_t s) {
+  if (!p->ktimer || p->kev.size() < p->kev_n + 2) return;
+  cudaEventRecord(p->kev[p->kev_n + 1], s);
+  p->kev_n += 2;
+}
 
 template <class K>
 int occupancy_blocks(K kernel, int threads, size_t smem) {
@@ -527,7 +590,10 @@ int launch_general_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, bool seg, 
     }
     a.scratch = p->scratch;
   }
+  kt_begin(p, stream);
   kern<<<(unsigned)grid, threads, smem, stream>>>(p->dp, a, words_per_warp, S);
+  kt_end(p, stream);
+  p->launches++;
   FS_CUDA_TRY(cudaGetLastError());
   return FS_OK;
 }
@@ -549,7 +615,10 @@ int launch_block_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cu
   const int occ = occupancy_blocks(kern, nt, smem);
   const size_t blocks_needed = (S.n_in + ngroups - 1) / ngroups;
   const size_t grid = std::max<size_t>(1, std::min<size_t>(blocks_needed, (size_t)p->num_sms * occ));
+  kt_begin(p, stream);
   kern<<<(unsigned)grid, nt, smem, stream>>>(dp, a, S, karr, (int)group_bytes);
+  kt_end(p, stream);
+  p->launches++;
   FS_CUDA_TRY(cudaGetLastError());
   return FS_OK;
 }
@@ -719,6 +788,7 @@ int run_fault_lists(fs_prog* p, const fs::RunArgs& a, size_t w0, size_t nw, uint
   fs::fault_list_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, stream>>>(
       p->dp, a.seed, (a.shot0 >> 5) + w0, (uint32_t)nw, a.ostride, p->d_site_block, p->jit_nblocks, fent + w0,
       bcount + w0, ntot + w0, (uint32_t)p->jit_stage);
+  p->launches++;
   FS_CUDA_TRY(cudaGetLastError());
   return FS_OK;
 }
@@ -1139,6 +1209,7 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
     dim3 g((W + 127) / 128);
     if (splitmix) fs::hbm_scalar_kernel<true><<<g, 128, 0, stream>>>(dp, a, H, i0, i1, init, batch0, W);
     else fs::hbm_scalar_kernel<false><<<g, 128, 0, stream>>>(dp, a, H, i0, i1, init, batch0, W);
+    p->launches++;
     FS_CUDA_TRY(cudaGetLastError());
     return FS_OK;
   };
@@ -1155,11 +1226,13 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
     int rc = scalar(0, 0, 1, batch0, W);
     if (rc) return rc;
     fs::hbm_init_amps_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, stream>>>(H, (uint32_t)nb);
+    p->launches++;
     auto run_op = [&](const fs::ArrOp& o, uint64_t count) -> int {
       if (count == 0) return FS_OK;
       const uint64_t want_x = (count + 255) / 256;
       const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(want_x, std::max<uint64_t>(1, 16384 / nb)));
       fs::hbm_array_kernel<<<dim3((unsigned)gx, (unsigned)nb), 256, 0, stream>>>(o, H, count, W);
+      p->launches++;
       FS_CUDA_TRY(cudaGetLastError());
       return FS_OK;
     };
@@ -1174,8 +1247,11 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
         case HbmStep::PASS: {
           const uint64_t ntiles = 1ull << PL.passes[st.pass].nbase;
           const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(ntiles, std::max<uint64_t>(1, 4096 / nb)));
+          kt_begin(p, stream);
           fs::hbm_fused_pass_kernel<<<dim3((unsigned)gx, (unsigned)nb), fs::kTileThreads, pass_smem, stream>>>(
               H, PL.passes[st.pass], p->d_code, p->d_consts, W);
+          kt_end(p, stream);
+          p->launches++;
           FS_CUDA_TRY(cudaGetLastError());
           break;
         }
@@ -1183,6 +1259,7 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
           const int nbu = (int)std::max<uint64_t>(1, std::min<uint64_t>(nblk, (st.count + 2047) / 2048));
           fs::hbm_reduce_kernel<<<dim3(nbu, (unsigned)nb), 256, 0, stream>>>(st.op, H, st.count, st.collapse, st.u10, st.u11);
           fs::hbm_reduce_final_kernel<<<(unsigned)((nb + 127) / 128), 128, 0, stream>>>(H, (uint32_t)nb, nbu);
+          p->launches += 2;
           FS_CUDA_TRY(cudaGetLastError());
           if ((rc = scalar(st.i0, st.i0 + 1, 0, batch0, W))) return rc;
           fs::ArrOp o = st.op;
@@ -1198,6 +1275,7 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
       }
     }
     fs::hbm_finish_kernel<<<(W + 127) / 128, 128, 0, stream>>>(dp, a, H, batch0, W);
+    p->launches++;
     FS_CUDA_TRY(cudaGetLastError());
     if (a.t_amps) {
       const int kst = (int)PL.final_live.size();
@@ -1206,6 +1284,7 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
       const uint64_t sz = 1ull << kst;
       const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>((sz + 255) / 256, 1024));
       fs::hbm_gather_kernel<<<dim3((unsigned)gx, (unsigned)nb), 256, 0, stream>>>(dp, a, H, batch0, (uint32_t)nb, kst, m);
+      p->launches++;
       FS_CUDA_TRY(cudaGetLastError());
     }
   }
@@ -1307,7 +1386,10 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
         const uint32_t* fc = bcount + w0;
         const uint32_t* ft = ntot + w0;
         void* args[] = {&dpv, &ac, &ps, &fl, &fc, &ft};
+        kt_begin(p, stream);
         int r = J.cuLaunchKernel(p->jit.fn, (unsigned)gc, 1, 1, 128, 1, 1, (unsigned)smem, stream, args, nullptr);
+        kt_end(p, stream);
+        p->launches++;
         if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_jit_frame) failed: " + std::to_string(r));
       }
       (void)grid;
@@ -1325,7 +1407,10 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     const size_t groups = (W + threads - 1) / threads;
     const int occ = occupancy_blocks(kern, threads, smem);
     const size_t grid = std::min<size_t>(groups, (size_t)p->num_sms * occ);
+    kt_begin(p, stream);
     kern<<<(unsigned)grid, threads, smem, stream>>>(dp, a, words_per_warp);
+    kt_end(p, stream);
+    p->launches++;
     FS_CUDA_TRY(cudaGetLastError());
     return FS_OK;
   }
@@ -1350,8 +1435,11 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     const uint32_t* fc = bcount;
     const uint32_t* ft = ntot;
     void* args[] = {&dpv, &a, &ps, &fl, &fc, &ft};
+    kt_begin(p, stream);
     int r = J.cuLaunchKernel(p->jit.fn, (unsigned)grid, 1, 1, p->gjit_threads, 1, 1, (unsigned)p->gjit_smem, stream,
                              args, nullptr);
+    kt_end(p, stream);
+    p->launches++;
     if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_jit_general) failed: " + std::to_string(r));
     return FS_OK;
   }
@@ -1525,6 +1613,7 @@ extern "C" int fs_accumulate(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t
     if (rc != FS_OK) return rc;
     dim3 grid(std::min<uint32_t>((W + 255) / 256, 64), nrows + 1);
     accumulate_kernel<<<grid, 256, 0, stream>>>(rows, nrows, o.accepted, W, counts);
+    p->launches++;
     FS_CUDA_TRY(cudaGetLastError());
   }
   return FS_OK;
