@@ -11,8 +11,10 @@
 namespace fs {
 
 // G threads per shot: G = 32 (warp per shot, several shots per CTA) or G = 256 (CTA per shot)
+constexpr int kBlockMaxGroups = 16;  // warp-per-shot groups per CTA (bounded by shared memory)
+
 template <bool SPLITMIX, int G>
-__global__ void __launch_bounds__(256, 4) block_kernel(DevProg P, RunArgs A, SegArgs S, int karr, int group_bytes) {
+__global__ void __launch_bounds__(G == 32 ? 32 * kBlockMaxGroups : 256, G == 32 ? 2 : 4) block_kernel(DevProg P, RunArgs A, SegArgs S, int karr, int group_bytes) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t cap = 1u << karr;
   const int group = threadIdx.x / G, ngroups = blockDim.x / G;
@@ -21,17 +23,18 @@ __global__ void __launch_bounds__(256, 4) block_kernel(DevProg P, RunArgs A, Seg
   uint32_t* fz = fx + P.n;
   uint32_t* slots = fz + P.n;
   uint32_t* obsb = slots + P.num_slots;
-  __shared__ double red1s[256], red2s[256];
-  __shared__ double2 sh_k0s[8], sh_k1s[8];
-  __shared__ int sh_alives[8], sh_branchs[8], sh_errs[8];
-  __shared__ uint32_t sh_slots[8];
+  // reduction scratch only for the CTA-per-shot form (warp groups reduce with shuffles)
+  __shared__ double red1s[G == 256 ? 256 : 1], red2s[G == 256 ? 256 : 1];
+  __shared__ double2 sh_k0s[kBlockMaxGroups], sh_k1s[kBlockMaxGroups];
+  __shared__ int sh_alives[kBlockMaxGroups], sh_branchs[kBlockMaxGroups], sh_errs[kBlockMaxGroups];
+  __shared__ uint32_t sh_slots[kBlockMaxGroups];
   double2& sh_k0 = sh_k0s[group];
   double2& sh_k1 = sh_k1s[group];
   int& sh_alive = sh_alives[group];
   int& sh_branch = sh_branchs[group];
   int& sh_err = sh_errs[group];
-  double* red1 = red1s + group * G;
-  double* red2 = red2s + group * G;
+  double* red1 = red1s;
+  double* red2 = red2s;
   const int tid = threadIdx.x % G, nt = G;
   const bool renorm = !(A.flags & FS_NO_RENORM);
 #define FS_BAR() do { if (G == 32) __syncwarp(); else __syncthreads(); } while (0)
@@ -180,6 +183,34 @@ __global__ void __launch_bounds__(256, 4) block_kernel(DevProg P, RunArgs A, Seg
       const int op = FS_OPCODE(I0.x);
       const int flip = FS_FLIP(I0.x);
       switch (op) {
+        case FS_OP_FRAME: {  // GF(2) matrix (next_array stops here only when it exists)
+          const int mo = __ldg(P.frame_mat_off + i);
+          if (tid < 32) {
+            const int n2 = 2 * P.n;
+            uint32_t v[4], o[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const int bb = tid + 32 * k;
+              v[k] = __ballot_sync(0xFFFFFFFFu, bb < n2 && (fx[bb] & 1u));
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const int r = tid + 32 * k;
+              o[k] = 0u;
+              if (r < n2) {
+                const uint4 row = __ldg(reinterpret_cast<const uint4*>(P.frame_mat + mo) + r);
+                o[k] = (uint32_t)(__popc(row.x & v[0]) + __popc(row.y & v[1]) + __popc(row.z & v[2]) +
+                                  __popc(row.w & v[3])) & 1u;
+              }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+              if (tid + 32 * k < n2) fx[tid + 32 * k] = o[k];
+          }
+          FS_BAR();
+          break;
+        }
         case FS_OP_ARRAY_GATE: {
           const int g = ins[1], va = ins[2], vb = ins[3], a = ins[4], b = ins[5];
           const uint32_t size = 1u << ins[6];
@@ -273,22 +304,36 @@ __global__ void __launch_bounds__(256, 4) block_kernel(DevProg P, RunArgs A, Seg
             }
             sa = __dadd_rn(sa, __dadd_rn(cnorm2(a0), cnorm2(a1)));
           }
-          red1[tid] = s1;
-          red2[tid] = sa;
-          FS_BAR();
-          for (int w = nt >> 1; w; w >>= 1) {
-            if (tid < w) {
-              red1[tid] = __dadd_rn(red1[tid], red1[tid + w]);
-              red2[tid] = __dadd_rn(red2[tid], red2[tid + w]);
+          // fixed-order tree: element t += element t + w for w = nt/2 .. 1 (same pairs either way)
+          if (G == 32) {
+#pragma unroll
+            for (int w = 16; w; w >>= 1) {
+              const double o1 = __shfl_down_sync(0xFFFFFFFFu, s1, w), o2 = __shfl_down_sync(0xFFFFFFFFu, sa, w);
+              if (tid < w) {
+                s1 = __dadd_rn(s1, o1);
+                sa = __dadd_rn(sa, o2);
+              }
             }
+          } else {
+            red1[tid] = s1;
+            red2[tid] = sa;
             FS_BAR();
+            for (int w = nt >> 1; w; w >>= 1) {
+              if (tid < w) {
+                red1[tid] = __dadd_rn(red1[tid], red1[tid + w]);
+                red2[tid] = __dadd_rn(red2[tid], red2[tid + w]);
+              }
+              FS_BAR();
+            }
+            s1 = red1[0];
+            sa = red2[0];
           }
           if (tid == 0) {
             if (collapse) {
               const int po = ins[4] >> 8, pc = ins[4] & 0xFF;
               for (int j = 0; j < pc; j++) word_gate(fx, fz, __ldg(P.gates + po + j));
             }
-            double p1 = red1[0], p_all = red2[0];
+            double p1 = s1, p_all = sa;
             const int parity = fx[virt] & 1;
             int bad = 0;
             if (p1 != p1) bad = FS_ERR_SHOT_NAN;

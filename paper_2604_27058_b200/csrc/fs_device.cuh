@@ -49,7 +49,12 @@ struct DevProg {
   const int* __restrict__ run_len;
   const double* __restrict__ run_lp;
   const double* __restrict__ site_acc;  // p_site / q of its run (thinning), 1.0 when equal
-  const int* __restrict__ next_array;   // [N] first array instruction >= i (N if none)
+  const int* __restrict__ next_array;   // [N] first array instruction >= i (N if none); with frame
+                                        // matrices also the first FrameGates instruction
+  // FrameGates as GF(2) matrices (block engine, 2n <= 128): instruction i maps the frame vector
+  // v = (x_0..x_{n-1}, z_0..z_{n-1}) to v' with v'_r = parity(row_r & v); rows are 4 words
+  const uint32_t* __restrict__ frame_mat;
+  const int* __restrict__ frame_mat_off;  // [N] word offset of instruction i's rows, -1 if none
 };
 
 struct RunArgs {

@@ -215,11 +215,55 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   size_t o_rl2 = add(run_len.data(), sizeof(int32_t) * nruns);
   size_t o_rlp = add(run_lp.data(), sizeof(double) * nruns);
   size_t o_sacc = add(site_acc.data(), sizeof(double) * site_acc.size());
+  // FrameGates as GF(2) matrices for the block engine (a warp applies one with ballots + popcounts
+  // instead of thread 0 walking the gate list): column j = the gate list applied to basis bit j
+  const int n2 = 2 * d->n;
+  const bool mats = n2 <= 128 && d->k_max > 0;
+  std::vector<uint32_t> frame_mat;
+  std::vector<int32_t> frame_mat_off(d->num_instrs + 1, -1);
+  if (mats) {
+    std::vector<uint32_t> v(n2);
+    for (int i = 0; i < d->num_instrs; i++) {
+      const int* I = d->instrs + (size_t)i * FS_INS_WORDS;
+      if (FS_OPCODE(I[0]) != FS_OP_FRAME) continue;
+      frame_mat_off[i] = (int32_t)frame_mat.size();
+      frame_mat.resize(frame_mat.size() + (size_t)n2 * 4, 0u);
+      uint32_t* M = frame_mat.data() + frame_mat_off[i];
+      for (int j = 0; j < n2; j++) {
+        std::fill(v.begin(), v.end(), 0u);
+        v[j] = 1u;
+        uint32_t* fx = v.data();
+        uint32_t* fz = v.data() + d->n;
+        for (int t = 0; t < I[2]; t++) {
+          const uint32_t g = d->gates[I[1] + t];
+          const int a = FS_GATE_A(g), b = FS_GATE_B(g);
+          uint32_t tt;
+          switch (FS_GATE_G(g)) {
+            case FS_G_H: tt = fx[a]; fx[a] = fz[a]; fz[a] = tt; break;
+            case FS_G_S: case FS_G_SDAG: fz[a] ^= fx[a]; break;
+            case FS_G_CX: fx[b] ^= fx[a]; fz[a] ^= fz[b]; break;
+            case FS_G_CZ: fz[b] ^= fx[a]; fz[a] ^= fx[b]; break;
+            case FS_G_SWAP:
+              tt = fx[a]; fx[a] = fx[b]; fx[b] = tt;
+              tt = fz[a]; fz[a] = fz[b]; fz[b] = tt;
+              break;
+            default: break;
+          }
+        }
+        for (int r = 0; r < n2; r++)
+          if (v[r] & 1u) M[(size_t)r * 4 + (j >> 5)] |= 1u << (j & 31);
+      }
+    }
+  }
+  if (frame_mat.empty()) frame_mat.push_back(0u);
+  size_t o_fm = add(frame_mat.data(), sizeof(uint32_t) * frame_mat.size());
+  size_t o_fmo = add(frame_mat_off.data(), sizeof(int32_t) * frame_mat_off.size());
   std::vector<int32_t> next_array(d->num_instrs + 1, d->num_instrs);
   for (int i = d->num_instrs - 1; i >= 0; i--) {
     const int op = FS_OPCODE(d->instrs[(size_t)i * FS_INS_WORDS]);
     const bool arr = op == FS_OP_ARRAY_GATE || op == FS_OP_EXPAND || op == FS_OP_ARRAY_ROT ||
-                     op == FS_OP_MEAS_ACTIVE || op == FS_OP_MEAS_COLLAPSE || op == FS_OP_RETIRE;
+                     op == FS_OP_MEAS_ACTIVE || op == FS_OP_MEAS_COLLAPSE || op == FS_OP_RETIRE ||
+                     (op == FS_OP_FRAME && frame_mat_off[i] >= 0);
     next_array[i] = arr ? i : next_array[i + 1];
   }
   size_t o_na = add(next_array.data(), sizeof(int32_t) * next_array.size());
@@ -261,6 +305,8 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   dp.run_lp = reinterpret_cast<const double*>(b + o_rlp);
   dp.site_acc = reinterpret_cast<const double*>(b + o_sacc);
   dp.next_array = reinterpret_cast<const int*>(b + o_na);
+  dp.frame_mat = reinterpret_cast<const uint32_t*>(b + o_fm);
+  dp.frame_mat_off = reinterpret_cast<const int*>(b + o_fmo);
   p->h_instrs.assign(d->instrs, d->instrs + (size_t)FS_INS_WORDS * d->num_instrs);
   p->h_sched.assign(d->schedule, d->schedule + d->num_instrs);
   if (d->num_fparams) p->h_fparams.assign(d->fparams, d->fparams + d->num_fparams);
@@ -479,6 +525,20 @@ extern "C" int fs_debug_kernel_time(fs_prog* p, double* total_ms, int64_t* count
   return 0;
 }
 
+// per-launch device times (ms) of the recorded dominant-kernel launches; returns the count
+extern "C" int64_t fs_debug_kernel_times(fs_prog* p, double* out, int64_t max) {
+  if (!p) return -1;
+  std::lock_guard<std::mutex> g(p->mu);
+  int64_t n = 0;
+  for (size_t i = 0; i + 1 < p->kev_n; i += 2, n++) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(p->kev[i + 1]) != cudaSuccess) return -1;
+    cudaEventElapsedTime(&ms, p->kev[i], p->kev[i + 1]);
+    if (n < max) out[n] = ms;
+  }
+  return n;
+}
+
 extern "C" const char* fs_debug_jit_status(fs_prog* p) {
   static thread_local std::string s;
   if (!p) return "null";
@@ -604,7 +664,9 @@ int launch_block_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cu
   const size_t group_bytes = align_up(((size_t)16 << karr) + (size_t)4 * (2 * dp.n + dp.num_slots + dp.O + 4), 16);
   if (group_bytes > kSmemBudget) return set_error(FS_ERR_ARG, "active array too large for the block engine");
   const bool warp_mode = karr <= 10;
-  const int ngroups = warp_mode ? (int)std::max<size_t>(1, std::min<size_t>(8, kSmemBudget / group_bytes)) : 1;
+  // as many warp groups as fit next to the static shared arrays (a k = 10 shot is ~17 KB)
+  const size_t dyn_budget = 220 * 1024;
+  const int ngroups = warp_mode ? (int)std::max<size_t>(1, std::min<size_t>(fs::kBlockMaxGroups, dyn_budget / group_bytes)) : 1;
   const int nt = warp_mode ? 32 * ngroups : 256;
   const size_t smem = group_bytes * ngroups;
   void (*kern)(fs::DevProg, fs::RunArgs, fs::SegArgs, int, int);
