@@ -572,11 +572,8 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
         o << "            const uint32_t bit = 1u << (e & 31);\n            const int off = (int)(e >> 10), cnt = (int)((e >> 5) & 31);\n";
         o << "            for (int j = 0; j < cnt; j++) Fs[__ldg(pslot + off + j)] ^= bit;\n          }\n";
         o << "          fcur += nb_;\n        } else {\n";
-        o << "          for (;;) {\n            if (psite < 0) { int st_, ln_, cs_; const int r_ = gen.step(P, st_, ln_, cs_);\n";
-        o << "              if (r_ == 2) { psite = 0x7FFFFFFF; break; } if (r_ == 0) continue; psite = st_; plane = ln_; pcase = cs_; }\n";
-        o << "            if (psite >= " << I[2] << ") break;\n";
-        o << "            for (int j = __ldg(P.case_pauli_off + pcase); j < __ldg(P.case_pauli_off + pcase + 1); j++) Fs[__ldg(pslot + j)] ^= 1u << plane;\n";
-        o << "            psite = -1;\n          }\n        }\n      }\n      __syncwarp();\n";
+        o << "          fs::gjit_noise_fallback(P, Fs, pslot, gen, psite, plane, pcase, " << I[2] << ");\n";
+        o << "        }\n      }\n      __syncwarp();\n";
         for (int sl : touched) o << "      " << f(sl) << " = Fs[" << sl << "];\n";
         o << "      __syncwarp();\n    }\n";
         nblk++;

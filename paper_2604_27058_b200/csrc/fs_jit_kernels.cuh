@@ -20,6 +20,25 @@ __device__ __noinline__ void jit_noise_block(const DevProg& P, uint32_t* F, cons
   });
 }
 
+// general kernel: regenerate the word's faults with sites < hi in place (overflowed fault list;
+// rare) -- one out-of-line copy instead of one inlined generator per NoiseBlock
+__device__ __noinline__ void gjit_noise_fallback(const DevProg& P, uint32_t* Fs, const uint16_t* __restrict__ pslot,
+                                                 WordFaultGen& gen, int& psite, int& plane, int& pcase, int hi) {
+  for (;;) {
+    if (psite < 0) {
+      int st_, ln_, cs_;
+      const int r_ = gen.step(P, st_, ln_, cs_);
+      if (r_ == 2) { psite = 0x7FFFFFFF; break; }
+      if (r_ == 0) continue;
+      psite = st_; plane = ln_; pcase = cs_;
+    }
+    if (psite >= hi) break;
+    for (int j = __ldg(P.case_pauli_off + pcase); j < __ldg(P.case_pauli_off + pcase + 1); j++)
+      Fs[__ldg(pslot + j)] ^= 1u << plane;
+    psite = -1;
+  }
+}
+
 // Noise for the specialised frame kernel.  fault_list_kernel generates each 32-shot word's
 // faults (WordFaultGen: the engine stream; lane = word) and writes one entry per fault,
 // ent[i][W] = pauli_off << 10 | pauli_cnt << 5 | shot_bit, plus per-NoiseBlock counts
