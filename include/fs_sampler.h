@@ -167,6 +167,23 @@ int fs_sample_host(fs_prog* prog, uint64_t seed, uint64_t shot0, uint64_t nshots
  * (runtime.py:857-865) */
 int fs_accumulate(fs_prog* prog, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t flags,
                   int64_t* counts, void* stream);
+
+/* The reference CLI's sample formats (cli.py:66-69, :94-109), produced on the device from the
+ * shot-bit words of an fs_sample call over `nshots` shots (row stride ceil(nshots/32)).  Record
+ * bits = user measurements ++ detectors ++ observables; a shot is written when accepted or
+ * keep_rejected.  FS_FMT_01: '0'/'1' chars + " rejected" (keep_rejected, not accepted) + '\n';
+ * FS_FMT_BIN: np.packbits(bits, bitorder="little"); FS_FMT_CSV: "<index>,<weight_text>,<bits>\n"
+ * with index = index0 + position among the written records (the header line is the caller's).
+ * dst: device buffer of `cap` bytes (>= fs_format_bound).  *nbytes / *nkept (host) = bytes and
+ * records written. */
+#define FS_FMT_01 0
+#define FS_FMT_BIN 1
+#define FS_FMT_CSV 2
+int fs_format(fs_prog* prog, const fs_sample_out* words, uint64_t nshots, int format, int keep_rejected,
+              uint64_t index0, const char* weight_text, uint8_t* dst, uint64_t cap, uint64_t* nbytes,
+              uint64_t* nkept, void* stream);
+uint64_t fs_format_bound(const fs_prog* prog, uint64_t nshots, int format, uint64_t index0,
+                         const char* weight_text);
 #endif
 
 #ifdef __cplusplus

@@ -83,3 +83,30 @@ def accumulate(prog, nshots: int, seed: int = 0, shot0: int = 0, flags: int = 0)
     return st, {"shots": nshots, "accepted": int(counts[-1]),
                 "measurements": counts[:U], "detectors": counts[U:U + D],
                 "observables": counts[U + D:-1]}
+
+
+def format_records(meas, det, obs, accepted, fmt: str, keep_rejected: bool, weight: float = 1.0,
+                   index0: int = 0) -> bytes:
+    """CPU restatement of the reference CLI writer (cli.py:66-69, :94-109) over uint8 record arrays
+    [shots, ...] -- the checker for the device formatter (fs_format).  The csv header line is not
+    included."""
+    import numpy as np
+
+    out = []
+    idx = index0
+    for i in range(len(accepted)):
+        if not (accepted[i] or keep_rejected):
+            continue
+        bits = np.concatenate([meas[i], det[i], obs[i]]).astype(np.uint8)
+        if fmt == "bin":
+            out.append(np.packbits(bits, bitorder="little").tobytes())
+        else:
+            text = "".join("1" if b else "0" for b in bits)
+            if fmt == "csv":
+                out.append(f"{idx},{weight:.17g},{text}\n".encode())
+            else:
+                if keep_rejected and not accepted[i]:
+                    text += " rejected"
+                out.append((text + "\n").encode())
+        idx += 1
+    return b"".join(out)

@@ -206,3 +206,8 @@ class TraceBuffers:
 
     def amps_c(self):
         return self.amps[..., 0] + 1j * self.amps[..., 1]
+
+# output formats (include/fs_sampler.h fs_format; cli.py:94-109)
+FS_FMT_01 = 0
+FS_FMT_BIN = 1
+FS_FMT_CSV = 2

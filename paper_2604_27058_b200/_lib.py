@@ -89,6 +89,12 @@ def lib():
             L.fs_accumulate.restype = C.c_int
             L.fs_accumulate.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
                                         C.c_void_p, C.c_void_p]
+            L.fs_format.restype = C.c_int
+            L.fs_format.argtypes = [C.c_void_p, C.POINTER(FsSampleOut), C.c_uint64, C.c_int, C.c_int,
+                                    C.c_uint64, C.c_char_p, C.c_void_p, C.c_uint64,
+                                    C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_void_p]
+            L.fs_format_bound.restype = C.c_uint64
+            L.fs_format_bound.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_uint64, C.c_char_p]
             if L.fs_abi_version() != 1:
                 raise EngineUnavailable("ABI version mismatch")
             _lib = L

@@ -5,6 +5,7 @@
 //
 // No CPU fallback exists: if CUDA is unavailable every entry point fails with FS_ERR_CUDA.
 #include <cuda_runtime.h>
+#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -21,6 +22,7 @@
 #include "fs_block.cuh"
 #include "fs_jit.cuh"
 #include "fs_jit_kernels.cuh"
+#include "fs_format.cuh"
 
 namespace {
 
@@ -117,6 +119,9 @@ struct fs_prog {
   int* d_site_block = nullptr;  // flip geometry: block_hi | row_off | block_cap
   int jit_nblocks = 0;
   int jit_stage = fsjit::kJitStage;
+  // fs_format scratch (kept flags, ranks, lengths, offsets, scan temp, weight text)
+  void* fmt = nullptr;
+  size_t fmt_bytes = 0;
   // instrumentation: kernel launch count, optional events around the dominant kernel's launches
   uint64_t launches = 0;
   bool ktimer = false;
@@ -341,6 +346,7 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->seg_pool[1]);
   cudaFree(p->d_pslot);
   for (auto e : p->kev) cudaEventDestroy(e);
+  cudaFree(p->fmt);
   if (p->aux) {
     cudaStreamDestroy(p->aux);
     for (auto& e : p->ev)
@@ -1678,5 +1684,102 @@ extern "C" int fs_accumulate(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t
     p->launches++;
     FS_CUDA_TRY(cudaGetLastError());
   }
+  return FS_OK;
+}
+
+// ------------------------------------------------------------------ output formats (cli.py)
+namespace {
+int fmt_nbits(const fs_prog* p) { return p->dp.U + p->dp.D + p->dp.O; }
+uint64_t dec_digits_h(uint64_t v) {
+  uint64_t d = 1;
+  while (v >= 10) { v /= 10; d++; }
+  return d;
+}
+}  // namespace
+
+extern "C" uint64_t fs_format_bound(const fs_prog* p, uint64_t nshots, int format, uint64_t index0,
+                                    const char* weight_text) {
+  if (!p) return 0;
+  const uint64_t nb = (uint64_t)fmt_nbits(p);
+  if (format == FS_FMT_BIN) return nshots * ((nb + 7) / 8);
+  if (format == FS_FMT_CSV) {
+    const uint64_t wl = weight_text ? std::strlen(weight_text) : 1;
+    return nshots * (dec_digits_h(index0 + nshots) + 2 + wl + nb + 1);
+  }
+  return nshots * (nb + 1 + 9);
+}
+
+extern "C" int fs_format(fs_prog* p, const fs_sample_out* words, uint64_t nshots, int format, int keep_rejected,
+                         uint64_t index0, const char* weight_text, uint8_t* dst, uint64_t cap, uint64_t* nbytes,
+                         uint64_t* nkept, void* stream_) {
+  if (!p || !words || !dst || !nbytes) return set_error(FS_ERR_ARG, "null argument");
+  if (format < FS_FMT_01 || format > FS_FMT_CSV) return set_error(FS_ERR_ARG, "unknown format");
+  *nbytes = 0;
+  if (nkept) *nkept = 0;
+  if (nshots == 0) return FS_OK;
+  std::lock_guard<std::mutex> lk(p->mu);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const fs::DevProg& dp = p->dp;
+  const char* wt = weight_text ? weight_text : "1";
+  const int wlen = (int)std::strlen(wt);
+  if (wlen > 64) return set_error(FS_ERR_ARG, "weight text longer than 64 characters");
+  // scratch: kept u32, rank u32, len u64, off u64, weight text, scan temp
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t1, (uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)nshots, stream);
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)nshots, stream);
+  const size_t temp = std::max(t1, t2);
+  const size_t need = align_up(4 * nshots, 256) * 2 + align_up(8 * nshots, 256) * 2 + 256 + align_up(temp, 256);
+  if (need > p->fmt_bytes) {
+    cudaFree(p->fmt);
+    p->fmt = nullptr;
+    p->fmt_bytes = 0;
+    FS_CUDA_TRY(cudaMalloc(&p->fmt, need));
+    p->fmt_bytes = need;
+  }
+  Stage st;
+  st.base = static_cast<unsigned char*>(p->fmt);
+  uint32_t* kept = st.take<uint32_t>(nshots);
+  uint32_t* rank = st.take<uint32_t>(nshots);
+  uint64_t* len = st.take<uint64_t>(nshots);
+  uint64_t* off = st.take<uint64_t>(nshots);
+  char* dw = st.take<char>(256);
+  void* tmp = st.take<unsigned char>(temp);
+  FS_CUDA_TRY(cudaMemcpyAsync(dw, wt, wlen + 1, cudaMemcpyHostToDevice, stream));
+  fs::FmtArgs F{};
+  F.meas = words->meas;
+  F.det = words->det;
+  F.obs = words->obs;
+  F.accepted = words->accepted;
+  F.n = nshots;
+  F.W = (uint32_t)((nshots + 31) / 32);
+  F.U = dp.U;
+  F.D = dp.D;
+  F.O = dp.O;
+  F.format = format;
+  F.keep_rejected = keep_rejected ? 1 : 0;
+  F.index0 = index0;
+  F.weight = dw;
+  F.wlen = wlen;
+  const unsigned g = (unsigned)((nshots + 255) / 256);
+  fs::fmt_kept_kernel<<<g, 256, 0, stream>>>(F, kept);
+  size_t tb = temp;
+  FS_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, kept, rank, (int64_t)nshots, stream));
+  fs::fmt_len_kernel<<<g, 256, 0, stream>>>(F, kept, rank, len);
+  tb = temp;
+  FS_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, len, off, (int64_t)nshots, stream));
+  uint64_t last[2] = {0, 0};
+  uint32_t lk2[2] = {0, 0};
+  FS_CUDA_TRY(cudaMemcpyAsync(&last[0], off + nshots - 1, 8, cudaMemcpyDeviceToHost, stream));
+  FS_CUDA_TRY(cudaMemcpyAsync(&last[1], len + nshots - 1, 8, cudaMemcpyDeviceToHost, stream));
+  FS_CUDA_TRY(cudaMemcpyAsync(&lk2[0], rank + nshots - 1, 4, cudaMemcpyDeviceToHost, stream));
+  FS_CUDA_TRY(cudaMemcpyAsync(&lk2[1], kept + nshots - 1, 4, cudaMemcpyDeviceToHost, stream));
+  FS_CUDA_TRY(cudaStreamSynchronize(stream));
+  const uint64_t total = last[0] + last[1];
+  if (total > cap) return set_error(FS_ERR_ARG, "format destination too small (see fs_format_bound)");
+  fs::fmt_write_kernel<<<g, 256, 0, stream>>>(F, kept, rank, off, dst);
+  p->launches += 4;
+  FS_CUDA_TRY(cudaGetLastError());
+  *nbytes = total;
+  if (nkept) *nkept = (uint64_t)lk2[0] + lk2[1];
   return FS_OK;
 }

@@ -121,6 +121,29 @@ class DeviceProgram:
         if rc != 0:
             raise_for_status(rc)
 
+    def format_device(self, nshots: int, out: dict, fmt: int, keep_rejected: bool, index0: int,
+                      weight_text: str, dst, stream=None) -> tuple[int, int]:
+        """fs_format: reference CLI bytes of the shots in `out` into the uint8 device tensor `dst`.
+        Returns (bytes, records) written; synchronizes `stream`."""
+        import torch
+
+        o = FsSampleOut()
+        o.meas = vptr(out["meas"].data_ptr(), C.c_uint32)
+        o.det = vptr(out["det"].data_ptr(), C.c_uint32)
+        o.obs = vptr(out["obs"].data_ptr(), C.c_uint32)
+        o.accepted = vptr(out["accepted"].data_ptr(), C.c_uint32)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        nb, nk = C.c_uint64(0), C.c_uint64(0)
+        rc = self._lib.fs_format(self._h, C.byref(o), nshots, fmt, 1 if keep_rejected else 0, index0,
+                                 weight_text.encode(), C.c_void_p(dst.data_ptr()), dst.numel(), C.byref(nb),
+                                 C.byref(nk), C.c_void_p(s.cuda_stream))
+        if rc != 0:
+            raise_for_status(rc)
+        return int(nb.value), int(nk.value)
+
+    def format_bound(self, nshots: int, fmt: int, index0: int, weight_text: str) -> int:
+        return int(self._lib.fs_format_bound(self._h, nshots, fmt, index0, weight_text.encode()))
+
     def accumulate_device(self, nshots: int, counts, seed: int = 0, shot0: int = 0, flags: int = 0,
                           stream=None) -> None:
         import torch

@@ -36,8 +36,9 @@ from .program import OP_NAMES, Program, as_program
 BRANCH_FLOOR = 1e-12  # runtime.py:47
 _CHUNK = 1 << 20      # shots per device call in the record iterator
 
-__all__ = ["BRANCH_FLOOR", "ShotError", "ShotRecord", "ShotState", "run_shot", "sample",
-           "sample_accumulate", "sample_batch", "Sampler", "compile_circuit"]
+__all__ = ["BRANCH_FLOOR", "FORMATS", "ShotError", "ShotRecord", "ShotState", "run_shot", "sample",
+           "sample_accumulate", "sample_batch", "sample_formatted", "write_samples", "Sampler",
+           "compile_circuit"]
 
 
 @dataclass(slots=True)
@@ -144,6 +145,116 @@ def _iter_records(s: Sampler, shots: int, seed: int, keep_rejected: bool):
         for i in range(n):
             if a[i] or keep_rejected:
                 yield ShotRecord(m[i], d[i], o[i], bool(a[i]), 1.0)
+
+
+FORMATS = {"01": _abi.FS_FMT_01, "bin": _abi.FS_FMT_BIN, "csv": _abi.FS_FMT_CSV}
+_PROFILE = bool(__import__("os").environ.get("FS_FORMAT_PROFILE"))
+
+
+def write_samples(prog, shots: int, out, seed: int = 0, format: str = "01", keep_rejected: bool = True,
+                  stratum=None, rng: str = "reference", renormalize: bool = True, chunk: int = 1 << 20) -> int:
+    """Write what ``framesim sample --format {01,bin,csv}`` writes (cli.py:94-109) to the binary
+    stream ``out`` (anything with ``.write(bytes)``); returns the number of records written.
+
+    The records are formatted on the GPU (``fs_format``), so only the final bytes cross PCIe;
+    chunk i's device->host copy overlaps chunk i+1's sampling and formatting."""
+    import torch
+
+    if shots < 1:
+        raise ValueError("shots must be >= 1")
+    if format not in FORMATS:
+        raise ValueError(f"unknown format {format!r} (expected one of {sorted(FORMATS)})")
+    if chunk % 32:
+        raise ValueError("chunk must be a multiple of 32")
+    fmt = FORMATS[format]
+    s = Sampler(prog, rng=rng, renormalize=renormalize)
+    dp = s.dp
+    weight = 1.0
+    if stratum is not None:
+        raise NotImplementedError("stratified sampling: see sample(..., stratum=)")
+    wtext = f"{weight:.17g}"
+    if format == "csv":
+        out.write(b"shot,weight,bits\n")
+    chunk = min(chunk, (shots + 31) // 32 * 32)
+    cap = dp.format_bound(chunk, fmt, shots, wtext)
+    comp, copy, slots = _format_buffers(dp, cap)
+    written = 0
+    pending = None  # (slot, nbytes, event)
+
+    def flush(p):
+        slot, nb, ev = p
+        ev.synchronize()
+        out.write(memoryview(slot["host"][:nb].numpy()))  # straight from pinned memory
+
+    for i, c0 in enumerate(range(0, shots, chunk)):
+        n = min(chunk, shots - c0)
+        slot = slots[i % 2]
+        if slot["copied"] is not None:
+            comp.wait_event(slot["copied"])
+        words = slot["words"].get(n)
+        if words is None:
+            with torch.cuda.stream(comp):
+                words = dp.alloc_device_outputs(n)
+            if len(slot["words"]) >= 4:
+                slot["words"].clear()
+            slot["words"][n] = words
+        if _PROFILE:
+            import time as _t
+            _t0 = _t.perf_counter()
+        dp.sample_device(n, words, seed=seed, shot0=c0, flags=s.flags, stream=comp)
+        nb, nk = dp.format_device(n, words, fmt, keep_rejected, written, wtext, slot["dev"], stream=comp)
+        if _PROFILE:
+            _t1 = _t.perf_counter()
+        st = int(words["status"].item())
+        if st:
+            from .engine import raise_for_status
+            raise_for_status(st)
+        ev_fmt = torch.cuda.Event()
+        ev_fmt.record(comp)
+        copy.wait_event(ev_fmt)
+        with torch.cuda.stream(copy):
+            slot["host"][:nb].copy_(slot["dev"][:nb], non_blocking=True)
+        ev_cp = torch.cuda.Event()
+        ev_cp.record(copy)
+        slot["copied"] = ev_cp
+        if pending is not None:
+            flush(pending)
+        if _PROFILE:
+            print(f"chunk {i}: compute+format {1e3 * (_t1 - _t0):.2f} ms, to flush {1e3 * (_t.perf_counter() - _t1):.2f} ms")
+        pending = (slot, nb, ev_cp)
+        written += nk
+    if pending is not None:
+        flush(pending)
+    return written
+
+
+def _format_buffers(dp: DeviceProgram, cap: int):
+    """Streams and two (device bytes, pinned host bytes, words) slots cached on the program:
+    pinned allocations cost far more than the transfers they serve."""
+    import torch
+
+    st = dp.__dict__.setdefault("_fmt_state", {})
+    if "streams" not in st:
+        st["streams"] = (torch.cuda.Stream(), torch.cuda.Stream())
+        st["slots"] = [{"words": {}, "dev": None, "host": None, "copied": None} for _ in range(2)]
+    for slot in st["slots"]:
+        if slot["dev"] is None or slot["dev"].numel() < cap:
+            if slot["copied"] is not None:
+                slot["copied"].synchronize()
+            slot["dev"] = torch.empty(cap, dtype=torch.uint8, device="cuda")
+            slot["host"] = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+    return st["streams"][0], st["streams"][1], st["slots"]
+
+
+def sample_formatted(prog, shots: int, seed: int = 0, format: str = "01", keep_rejected: bool = True,
+                     stratum=None, rng: str = "reference", renormalize: bool = True, chunk: int = 1 << 20) -> bytes:
+    """The bytes ``framesim sample --format FORMAT`` writes for these arguments (cli.py:94-109)."""
+    import io
+
+    buf = io.BytesIO()
+    write_samples(prog, shots, buf, seed=seed, format=format, keep_rejected=keep_rejected, stratum=stratum,
+                  rng=rng, renormalize=renormalize, chunk=chunk)
+    return buf.getvalue()
 
 
 def sample_accumulate(prog, shots: int, seed: int = 0, stratum=None, rng: str = "reference") -> dict:

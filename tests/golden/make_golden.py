@@ -236,6 +236,42 @@ def main(which=("configs", "random", "toys")):
             cps = tuple(sorted(set(int(x) for x in rng.integers(0, len(prog.instrs), size=3))))
             write_case(f"fusedk{made:02d}", prog, text, free_shots=64, trace_shots=4, checkpoints=cps, rng=rng)
             made += 1
+    if "formats" in which:  # reference CLI bytes (cli.py:72-113) for the device output formats
+        from framesim import cli as fcli
+        import tempfile
+        fdir = OUT / "formats"
+        fdir.mkdir(exist_ok=True)
+        toys_txt = {
+            "toy_repetition": (str(ftest.repetition_code_circuit(3, 5, 0.05)), ""),
+            "toy_repetition_ps": (str(ftest.repetition_code_circuit(3, 4, 0.08)), "0,2,3"),
+            "toy_postselect": ("H 0\nM 0\nPOSTSELECT rec[-1]\nH 1\nT 1\nH 1\nM 1\nDEPOLARIZE1(0.5) 1\nM 1\n", ""),
+            "toy_feedforward": ("H 0\nT 0\nH 0\nM 0\nCX rec[-1] 1\nX_ERROR(0.3) 1\nM 1\nDETECTOR rec[-1] rec[-2]\n"
+                                "OBSERVABLE_INCLUDE(0) rec[-1]\nOBSERVABLE_INCLUDE(0) rec[-2]\n", ""),
+            "toy_worked": ("H 0\nT 0\nT 0\nT 0\nCX 0 1\nDEPOLARIZE1(0.001) 0 1\nCX 0 1\nT_DAG 0\nH 0\nM 0 1\n", ""),
+            "surface_d3": (config_text(2)[0], ""),
+        }
+        for name, (text, ps) in toys_txt.items():
+            t0 = time.time()
+            pstuple = tuple(int(x) for x in ps.split(",")) if ps else ()
+            prog = compile_circuit(text, postselect_detectors=pstuple)
+            payload = {"program": np.frombuffer(serialize(prog, name=name).to_npz_bytes(), dtype=np.uint8),
+                       "circuit": np.array(text), "postselect": np.array(ps), "shots": np.array([300]),
+                       "seed": np.array([7])}
+            with tempfile.TemporaryDirectory() as td:
+                cpath = f"{td}/c.txt"
+                open(cpath, "w").write(text)
+                for fmt in ("01", "bin", "csv"):
+                    for keep in (False, True):
+                        opath = f"{td}/o_{fmt}_{int(keep)}"
+                        argv = ["sample", cpath, "--shots", "300", "--seed", "7", "--format", fmt, "--out", opath]
+                        if ps:
+                            argv += ["--postselect-detectors", ps]
+                        if keep:
+                            argv.append("--keep-rejected")
+                        assert fcli.main(argv) == 0
+                        payload[f"{fmt}_{int(keep)}"] = np.frombuffer(open(opath, "rb").read(), dtype=np.uint8)
+            np.savez_compressed(fdir / f"{name}.npz", **payload)
+            print(f"formats/{name:20s} ({time.time() - t0:.1f}s)", flush=True)
     if "configs" in which:
         for i in range(5):
             text, ps = config_text(i)
