@@ -184,6 +184,20 @@ int fs_format(fs_prog* prog, const fs_sample_out* words, uint64_t nshots, int fo
               uint64_t* nkept, void* stream);
 uint64_t fs_format_bound(const fs_prog* prog, uint64_t nshots, int format, uint64_t index0,
                          const char* weight_text);
+
+/* Stratified importance sampling (runtime.py:886-945): every shot conditioned on exactly w
+ * realised faults.  fs_stratum_weight = StratumSpec(prog, w).weight = Pr[W = w] (FS_ERR_ARG with
+ * "stratum fault count w exceeds E sites" when w > E).  The forced sites of a shot are drawn by
+ * StratumSpec.draw_forced's sequential conditioning: FS_RNG_SPLITMIX consumes the shot's reference
+ * stream exactly like the reference (records identical to framesim.sample(..., stratum=)); the
+ * Philox stream uses its own draws.  Outputs / accumulate as fs_sample / fs_accumulate. */
+int fs_stratum_weight(fs_prog* prog, uint32_t w, double* weight);
+int fs_sample_stratum(fs_prog* prog, uint32_t w, uint64_t seed, uint64_t shot0, uint64_t nshots,
+                      uint32_t flags, const fs_sample_out* out, void* stream);
+int fs_sample_stratum_host(fs_prog* prog, uint32_t w, uint64_t seed, uint64_t shot0, uint64_t nshots,
+                           uint32_t flags, const fs_sample_out* out);
+int fs_accumulate_stratum(fs_prog* prog, uint32_t w, uint64_t seed, uint64_t shot0, uint64_t nshots,
+                          uint32_t flags, int64_t* counts, void* stream);
 #endif
 
 #ifdef __cplusplus

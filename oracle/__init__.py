@@ -42,6 +42,11 @@ def lib():
             L.fso_sample.argtypes = [C.POINTER(FsProgDesc), C.c_uint64, C.c_uint64, C.c_uint64,
                                      C.c_uint32, C.POINTER(FsTraceIn), C.POINTER(FsSampleOut),
                                      C.POINTER(FsTraceOut)]
+            L.fso_sample_stratum.restype = C.c_int
+            L.fso_sample_stratum.argtypes = [C.POINTER(FsProgDesc), C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                             C.c_uint32, C.POINTER(FsSampleOut)]
+            L.fso_stratum_weight.restype = C.c_int
+            L.fso_stratum_weight.argtypes = [C.POINTER(FsProgDesc), C.c_int, C.POINTER(C.c_double)]
             L.fso_accumulate.restype = C.c_int
             L.fso_accumulate.argtypes = [C.POINTER(FsProgDesc), C.c_uint64, C.c_uint64, C.c_uint64,
                                          C.c_uint32, C.POINTER(C.c_int64)]
@@ -68,6 +73,27 @@ def sample(prog, nshots: int, seed: int = 0, shot0: int = 0, flags: int = 0,
         tout = C.byref(tb.tout) if tb.tout is not None else None
     st = L.fso_sample(C.byref(h.desc), seed, shot0, nshots, flags, tin, C.byref(out.struct), tout)
     return st, out, tb
+
+
+def sample_stratum(prog, w: int, nshots: int, seed: int = 0, shot0: int = 0, flags: int = 0):
+    """sample(prog, nshots, seed, stratum=StratumSpec(prog, w)) on the CPU oracle: (status, HostOutputs)."""
+    from paper_2604_27058_b200._abi import DescHolder, HostOutputs
+
+    L = lib()
+    h = DescHolder(prog)
+    out = HostOutputs(prog, nshots)
+    st = L.fso_sample_stratum(C.byref(h.desc), int(w), seed, shot0, nshots, flags, C.byref(out.struct))
+    return st, out
+
+
+def stratum_weight(prog, w: int) -> float:
+    from paper_2604_27058_b200._abi import DescHolder
+
+    h = DescHolder(prog)
+    v = C.c_double(0.0)
+    if lib().fso_stratum_weight(C.byref(h.desc), int(w), C.byref(v)) != 0:
+        raise ValueError(f"stratum fault count {w} exceeds {prog.num_sites} sites")
+    return float(v.value)
 
 
 def accumulate(prog, nshots: int, seed: int = 0, shot0: int = 0, flags: int = 0):

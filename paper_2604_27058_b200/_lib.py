@@ -95,6 +95,17 @@ def lib():
                                     C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_void_p]
             L.fs_format_bound.restype = C.c_uint64
             L.fs_format_bound.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_uint64, C.c_char_p]
+            L.fs_stratum_weight.restype = C.c_int
+            L.fs_stratum_weight.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_double)]
+            L.fs_sample_stratum.restype = C.c_int
+            L.fs_sample_stratum.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64,
+                                            C.c_uint32, C.POINTER(FsSampleOut), C.c_void_p]
+            L.fs_sample_stratum_host.restype = C.c_int
+            L.fs_sample_stratum_host.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64,
+                                                 C.c_uint32, C.POINTER(FsSampleOut)]
+            L.fs_accumulate_stratum.restype = C.c_int
+            L.fs_accumulate_stratum.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64,
+                                                C.c_uint32, C.c_void_p, C.c_void_p]
             if L.fs_abi_version() != 1:
                 raise EngineUnavailable("ABI version mismatch")
             _lib = L

@@ -78,13 +78,15 @@ struct RunArgs {
   double* t_gamma;
   double* t_amps;
   uint32_t* t_draws;
+  const uint32_t* draw0;  // [nshots] reference-stream draws consumed before the program
+                          // (stratified sampling: StratumSpec.draw_forced), NULL = 0
   // general engine: per-resident-warp array storage when it does not fit in shared memory
   double2* scratch;
   int arr_log2;  // log2 capacity (k_max)
 };
 
 // ------------------------------------------------------------------ random streams
-enum : uint32_t { TAG_COIN = 1, TAG_BORN = 2, TAG_NOISE = 3, TAG_FORCED = 4 };
+enum : uint32_t { TAG_COIN = 1, TAG_BORN = 2, TAG_NOISE = 3, TAG_FORCED = 4, TAG_STRATUM = 5 };
 
 __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint64_t seed) {
   uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);

@@ -305,6 +305,7 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp, SegArgs S) {
     rng.seed = A.seed;
     rng.shot = shot;
     if (SPLITMIX) rng.sm.reset(A.seed, shot);
+    if (SPLITMIX && A.draw0 && valid) rng.sm.count = A.draw0[si];
     const int16_t* fmodes = A.fault_modes ? A.fault_modes + (valid ? si : 0) * (size_t)P.E : nullptr;
     const int8_t* forced = A.forced ? A.forced + (valid ? si : 0) * (size_t)P.R : nullptr;
     int branch = 0;

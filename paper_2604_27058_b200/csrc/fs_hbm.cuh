@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(128) hbm_scalar_kernel(DevProg P, RunArgs A, H
       const uint64_t bs = (uint64_t)w * 32 + j;  // shot within the batch
       if (!((validmask >> j) & 1)) continue;
       H.gamma[bs] = make_double2(1.0, 0.0);
-      H.smcount[bs] = 0;
+      H.smcount[bs] = A.draw0 ? A.draw0[si0 + j] : 0u;
     }
   }
   uint32_t alive = H.alive[w];

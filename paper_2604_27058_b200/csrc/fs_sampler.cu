@@ -23,6 +23,7 @@
 #include "fs_jit.cuh"
 #include "fs_jit_kernels.cuh"
 #include "fs_format.cuh"
+#include "fs_stratum.cuh"
 
 namespace {
 
@@ -119,6 +120,12 @@ struct fs_prog {
   int* d_site_block = nullptr;  // flip geometry: block_hi | row_off | block_cap
   int jit_nblocks = 0;
   int jit_stage = fsjit::kJitStage;
+  // stratified sampling: suffix Poisson-binomial table of stratum w, per-chunk modes + outputs
+  int strat_w = -1;
+  double strat_weight = 0.0;
+  double* d_strat = nullptr;
+  void* strat_buf = nullptr;
+  size_t strat_bytes = 0;
   // fs_format scratch (kept flags, ranks, lengths, offsets, scan temp, weight text)
   void* fmt = nullptr;
   size_t fmt_bytes = 0;
@@ -347,6 +354,8 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->d_pslot);
   for (auto e : p->kev) cudaEventDestroy(e);
   cudaFree(p->fmt);
+  cudaFree(p->d_strat);
+  cudaFree(p->strat_buf);
   if (p->aux) {
     cudaStreamDestroy(p->aux);
     for (auto& e : p->ev)
@@ -1360,7 +1369,8 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
 }
 
 int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t flags, const fs_trace_in* tin,
-           const fs_sample_out* out, const fs_trace_out* tout, cudaStream_t stream) {
+           const fs_sample_out* out, const fs_trace_out* tout, cudaStream_t stream,
+           const uint32_t* draw0 = nullptr) {
   if (shot0 % 32) return set_error(FS_ERR_ARG, "shot0 must be a multiple of 32");
   if (nshots == 0) return FS_OK;
   if (nshots > (uint64_t)0xFFFFFFFFull * 32) return set_error(FS_ERR_ARG, "too many shots for one call");
@@ -1396,6 +1406,7 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     if ((a.t_fx == nullptr) != (a.t_fz == nullptr)) return set_error(FS_ERR_ARG, "frame_x/frame_z must both be set");
   }
   a.arr_log2 = dp.k_max;
+  a.draw0 = draw0;
   if (!out->status) FS_CUDA_TRY(cudaMemsetAsync(p->d_status, 0, sizeof(int), stream));
   if (wants_hbm(p, flags)) return launch_hbm(p, a, stream);
   const size_t W = a.W;
@@ -1781,5 +1792,214 @@ extern "C" int fs_format(fs_prog* p, const fs_sample_out* words, uint64_t nshots
   FS_CUDA_TRY(cudaGetLastError());
   *nbytes = total;
   if (nkept) *nkept = (uint64_t)lk2[0] + lk2[1];
+  return FS_OK;
+}
+
+// ------------------------------------------------------------------ stratified sampling
+namespace {
+// suffix[i][m] = Pr[m faults among sites i..E-1] for m <= w, built exactly like StratumSpec
+// (runtime.py:898-908): nxt[m] = prev[m] * (1 - p) + prev[m - 1] * p in that order
+int stratum_prepare(fs_prog* p, uint32_t w) {
+  const int E = p->dp.E;
+  if ((int64_t)w > E)
+    return set_error(FS_ERR_ARG, "stratum fault count " + std::to_string(w) + " exceeds " + std::to_string(E) + " sites");
+  if (p->strat_w == (int)w && p->d_strat) return FS_OK;
+  const size_t w1 = (size_t)w + 1;
+  std::vector<double> T((size_t)(E + 1) * w1, 0.0);
+  T[(size_t)E * w1] = 1.0;
+  for (int i = E - 1; i >= 0; i--) {
+    const double pr = p->h_site_prob[i];
+    const double omp = 1.0 - pr;
+    const double* prev = T.data() + (size_t)(i + 1) * w1;
+    double* nxt = T.data() + (size_t)i * w1;
+    for (size_t m = 0; m < w1; m++) {
+      volatile double a = prev[m] * omp;  // volatile: no contraction into an FMA
+      double v = a;
+      if (m) {
+        volatile double b = prev[m - 1] * pr;
+        v = a + b;
+      }
+      nxt[m] = v;
+    }
+  }
+  cudaFree(p->d_strat);
+  p->d_strat = nullptr;
+  FS_CUDA_TRY(cudaMalloc(&p->d_strat, sizeof(double) * T.size()));
+  FS_CUDA_TRY(cudaMemcpy(p->d_strat, T.data(), sizeof(double) * T.size(), cudaMemcpyHostToDevice));
+  p->strat_w = (int)w;
+  p->strat_weight = T[w];
+  return FS_OK;
+}
+
+// stratified shots [shot0, shot0 + nshots) into device outputs (row stride ceil(nshots / 32));
+// caller holds p->mu
+int sample_stratum_impl(fs_prog* p, uint32_t w, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t flags,
+                        const fs_sample_out* out, cudaStream_t stream) {
+  if (shot0 % 32) return set_error(FS_ERR_ARG, "shot0 must be a multiple of 32");
+  if (int rc = stratum_prepare(p, w)) return rc;
+  const fs::DevProg& dp = p->dp;
+  const size_t E = (size_t)std::max(dp.E, 1);
+  const size_t W = (nshots + 31) / 32;
+  const int rows = dp.U + dp.D + dp.O + 2;
+  uint64_t chunk = std::max<uint64_t>(32, ((uint64_t)1 << 30) / (2 * E) / 32 * 32);
+  if (const char* e = getenv("FS_STRATUM_CHUNK")) chunk = std::max<uint64_t>(32, (uint64_t)atoll(e) / 32 * 32);  // tests
+  chunk = std::min<uint64_t>(chunk, (nshots + 31) / 32 * 32);
+  const size_t Wc = chunk / 32;
+  const size_t need = align_up(2 * E * chunk, 256) + align_up(4 * chunk, 256) + align_up(4 * Wc * rows, 256) + 256;
+  if (need > p->strat_bytes) {
+    cudaFree(p->strat_buf);
+    p->strat_buf = nullptr;
+    p->strat_bytes = 0;
+    FS_CUDA_TRY(cudaMalloc(&p->strat_buf, need));
+    p->strat_bytes = need;
+  }
+  Stage st;
+  st.base = static_cast<unsigned char*>(p->strat_buf);
+  int16_t* modes = st.take<int16_t>(E * chunk);
+  uint32_t* draw0 = st.take<uint32_t>(chunk);
+  uint32_t* crow = st.take<uint32_t>(Wc * rows);
+  const bool splitmix = flags & FS_RNG_SPLITMIX;
+  for (uint64_t c0 = 0; c0 < nshots; c0 += chunk) {
+    const uint64_t nc = std::min<uint64_t>(chunk, nshots - c0);
+    const size_t wc = (nc + 31) / 32;
+    const uint64_t cells = nc * (uint64_t)dp.E;
+    if (cells) {
+      fs::fill_modes_kernel<<<(unsigned)((cells / 8 + 1 + 255) / 256), 256, 0, stream>>>(modes, cells);
+      p->launches++;
+    }
+    const unsigned g = (unsigned)((nc + 127) / 128);
+    if (splitmix) fs::stratum_kernel<true><<<g, 128, 0, stream>>>(dp, p->d_strat, (int)w, seed, shot0 + c0, nc, modes, draw0);
+    else fs::stratum_kernel<false><<<g, 128, 0, stream>>>(dp, p->d_strat, (int)w, seed, shot0 + c0, nc, modes, draw0);
+    p->launches++;
+    FS_CUDA_TRY(cudaGetLastError());
+    fs_trace_in tin{};
+    tin.fault_modes = dp.E ? modes : nullptr;
+    tin.forced = nullptr;
+    tin.stop = -1;
+    const bool whole = nc == nshots;
+    fs_sample_out o{};
+    if (whole) {
+      o = *out;
+    } else {
+      o.meas = crow;
+      o.det = crow + wc * dp.U;
+      o.obs = crow + wc * (dp.U + dp.D);
+      o.accepted = crow + wc * (dp.U + dp.D + dp.O);
+      o.error = o.accepted + wc;
+      o.status = out->status;
+    }
+    int rc = launch(p, seed, shot0 + c0, nc, flags, &tin, &o, nullptr, stream, splitmix ? draw0 : nullptr);
+    if (rc != FS_OK) return rc;
+    if (!whole) {  // place the chunk's words at word offset c0 / 32 of every output row
+      const size_t w0 = c0 / 32;
+      auto put = [&](uint32_t* dst, const uint32_t* src, int nrow) -> int {
+        if (!nrow || !dst) return FS_OK;
+        FS_CUDA_TRY(cudaMemcpy2DAsync(dst + w0, 4 * W, src, 4 * wc, 4 * wc, nrow, cudaMemcpyDeviceToDevice, stream));
+        return FS_OK;
+      };
+      if ((rc = put(out->meas, o.meas, dp.U)) || (rc = put(out->det, o.det, dp.D)) || (rc = put(out->obs, o.obs, dp.O)) ||
+          (rc = put(out->accepted, o.accepted, 1)) || (rc = put(out->error, o.error, 1)))
+        return rc;
+    }
+  }
+  return FS_OK;
+}
+}  // namespace
+
+extern "C" int fs_stratum_weight(fs_prog* p, uint32_t w, double* weight) {
+  if (!p || !weight) return set_error(FS_ERR_ARG, "null argument");
+  std::lock_guard<std::mutex> lk(p->mu);
+  if (int rc = stratum_prepare(p, w)) return rc;
+  *weight = p->strat_weight;
+  return FS_OK;
+}
+
+extern "C" int fs_sample_stratum(fs_prog* p, uint32_t w, uint64_t seed, uint64_t shot0, uint64_t nshots,
+                                 uint32_t flags, const fs_sample_out* out, void* stream) {
+  if (!p || !out) return set_error(FS_ERR_ARG, "null argument");
+  if (nshots == 0) return FS_OK;
+  std::lock_guard<std::mutex> lk(p->mu);
+  return sample_stratum_impl(p, w, seed, shot0, nshots, flags, out, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int fs_sample_stratum_host(fs_prog* p, uint32_t w, uint64_t seed, uint64_t shot0, uint64_t nshots,
+                                      uint32_t flags, const fs_sample_out* out) {
+  if (!p || !out) return set_error(FS_ERR_ARG, "null argument");
+  if (nshots == 0) return FS_OK;
+  std::lock_guard<std::mutex> lk(p->mu);
+  const fs::DevProg& dp = p->dp;
+  const size_t W = (nshots + 31) / 32;
+  const size_t rows = (size_t)dp.U + dp.D + dp.O + 2;
+  const size_t need = align_up(4 * W * rows + 64, 256);
+  if (need > p->stage_bytes) {
+    cudaFree(p->stage);
+    p->stage = nullptr;
+    p->stage_bytes = 0;
+    FS_CUDA_TRY(cudaMalloc(&p->stage, need));
+    p->stage_bytes = need;
+  }
+  uint32_t* r = static_cast<uint32_t*>(p->stage);
+  fs_sample_out d{};
+  d.meas = r;
+  d.det = r + W * dp.U;
+  d.obs = r + W * (dp.U + dp.D);
+  d.accepted = r + W * (dp.U + dp.D + dp.O);
+  d.error = d.accepted + W;
+  d.status = reinterpret_cast<int32_t*>(d.error + W);
+  cudaStream_t s = 0;
+  FS_CUDA_TRY(cudaMemsetAsync(d.status, 0, 4, s));
+  int rc = sample_stratum_impl(p, w, seed, shot0, nshots, flags, &d, s);
+  if (rc != FS_OK) return rc;
+  if (dp.U) FS_CUDA_TRY(cudaMemcpyAsync(out->meas, d.meas, 4 * W * dp.U, cudaMemcpyDeviceToHost, s));
+  if (dp.D) FS_CUDA_TRY(cudaMemcpyAsync(out->det, d.det, 4 * W * dp.D, cudaMemcpyDeviceToHost, s));
+  if (dp.O) FS_CUDA_TRY(cudaMemcpyAsync(out->obs, d.obs, 4 * W * dp.O, cudaMemcpyDeviceToHost, s));
+  FS_CUDA_TRY(cudaMemcpyAsync(out->accepted, d.accepted, 4 * W, cudaMemcpyDeviceToHost, s));
+  FS_CUDA_TRY(cudaMemcpyAsync(out->error, d.error, 4 * W, cudaMemcpyDeviceToHost, s));
+  int status = 0;
+  FS_CUDA_TRY(cudaMemcpyAsync(&status, d.status, 4, cudaMemcpyDeviceToHost, s));
+  FS_CUDA_TRY(cudaStreamSynchronize(s));
+  if (out->status) *out->status = status;
+  if (status) {
+    g_last_error = status == FS_ERR_SHOT_NAN ? "NaN amplitude encountered at an active measurement"
+                                             : "forced outcome has probability below BRANCH_FLOOR";
+  }
+  return status;
+}
+
+extern "C" int fs_accumulate_stratum(fs_prog* p, uint32_t w, uint64_t seed, uint64_t shot0, uint64_t nshots,
+                                     uint32_t flags, int64_t* counts, void* stream_) {
+  if (!p || !counts) return set_error(FS_ERR_ARG, "null argument");
+  std::lock_guard<std::mutex> lk(p->mu);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const fs::DevProg& dp = p->dp;
+  const int nrows = dp.U + dp.D + dp.O;
+  FS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (nrows + 1), stream));
+  const uint64_t chunk = (uint64_t)1 << 22;
+  const size_t Wc = chunk / 32;
+  const size_t need = align_up(4 * Wc * (nrows + 2) + 256, 256);
+  if (need > p->stage_bytes) {
+    cudaFree(p->stage);
+    p->stage = nullptr;
+    p->stage_bytes = 0;
+    FS_CUDA_TRY(cudaMalloc(&p->stage, need));
+    p->stage_bytes = need;
+  }
+  for (uint64_t s0 = 0; s0 < nshots; s0 += chunk) {
+    const uint64_t ns = std::min<uint64_t>(chunk, nshots - s0);
+    const uint32_t W = (uint32_t)((ns + 31) / 32);
+    uint32_t* rows = static_cast<uint32_t*>(p->stage);
+    fs_sample_out o{};
+    o.meas = rows;
+    o.det = rows + (size_t)W * dp.U;
+    o.obs = rows + (size_t)W * (dp.U + dp.D);
+    o.accepted = rows + (size_t)W * nrows;
+    o.error = rows + (size_t)W * (nrows + 1);
+    int rc = sample_stratum_impl(p, w, seed, shot0 + s0, ns, flags, &o, stream);
+    if (rc != FS_OK) return rc;
+    dim3 grid(std::min<uint32_t>((W + 255) / 256, 64), nrows + 1);
+    accumulate_kernel<<<grid, 256, 0, stream>>>(rows, nrows, o.accepted, W, counts);
+    p->launches++;
+    FS_CUDA_TRY(cudaGetLastError());
+  }
   return FS_OK;
 }

@@ -165,3 +165,64 @@ class DeviceProgram:
         U, D = p.num_user_records, p.num_detectors
         return {"shots": nshots, "accepted": int(c[-1]),
                 "measurements": c[:U], "detectors": c[U:U + D], "observables": c[U + D:-1]}
+
+    # -- stratified importance sampling (runtime.py:886-945) ------------------------------
+    def stratum_weight(self, w: int) -> float:
+        """StratumSpec(prog, w).weight = Pr[W = w] (ValueError when w exceeds the site count)."""
+        v = C.c_double(0.0)
+        rc = self._lib.fs_stratum_weight(self._h, int(w), C.byref(v))
+        if rc != 0:
+            raise ValueError(self._lib.fs_last_error().decode())
+        return float(v.value)
+
+    def sample_stratum_host(self, w: int, nshots: int, seed: int = 0, shot0: int = 0, flags: int = 0,
+                            check: bool = True):
+        """Shots conditioned on exactly w faults: (status, HostOutputs)."""
+        if nshots < 1:
+            raise ValueError("shots must be >= 1")
+        out = HostOutputs(self.prog, nshots)
+        status = np.zeros(1, dtype=np.int32)
+        out.struct.status = status.ctypes.data_as(C.POINTER(C.c_int32))
+        rc = self._lib.fs_sample_stratum_host(self._h, int(w), seed, shot0, nshots, flags, C.byref(out.struct))
+        if rc < 0:
+            raise ValueError(self._lib.fs_last_error().decode())
+        if check and rc != 0:
+            raise_for_status(rc)
+        return rc, out
+
+    def sample_stratum_device(self, w: int, nshots: int, out: dict, seed: int = 0, shot0: int = 0,
+                              flags: int = 0, stream=None) -> None:
+        import torch
+
+        o = FsSampleOut()
+        o.meas = vptr(out["meas"].data_ptr(), C.c_uint32)
+        o.det = vptr(out["det"].data_ptr(), C.c_uint32)
+        o.obs = vptr(out["obs"].data_ptr(), C.c_uint32)
+        o.accepted = vptr(out["accepted"].data_ptr(), C.c_uint32)
+        o.error = vptr(out["error"].data_ptr(), C.c_uint32)
+        o.status = vptr(out["status"].data_ptr(), C.c_int32)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = self._lib.fs_sample_stratum(self._h, int(w), seed, shot0, nshots, flags, C.byref(o),
+                                         C.c_void_p(s.cuda_stream))
+        if rc < 0:
+            raise ValueError(self._lib.fs_last_error().decode())
+        if rc != 0:
+            raise_for_status(rc)
+
+    def accumulate_stratum(self, w: int, nshots: int, seed: int = 0, shot0: int = 0, flags: int = 0) -> dict:
+        import torch
+
+        p = self.prog
+        nrows = p.num_user_records + p.num_detectors + p.num_observables
+        counts = torch.zeros(nrows + 1, dtype=torch.int64, device="cuda")
+        s = torch.cuda.current_stream()
+        rc = self._lib.fs_accumulate_stratum(self._h, int(w), seed, shot0, nshots, flags,
+                                             C.c_void_p(counts.data_ptr()), C.c_void_p(s.cuda_stream))
+        if rc < 0:
+            raise ValueError(self._lib.fs_last_error().decode())
+        if rc != 0:
+            raise_for_status(rc)
+        c = counts.cpu().numpy()
+        U, D = p.num_user_records, p.num_detectors
+        return {"shots": nshots, "accepted": int(c[-1]),
+                "measurements": c[:U], "detectors": c[U:U + D], "observables": c[U + D:-1]}

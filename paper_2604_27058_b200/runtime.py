@@ -8,6 +8,9 @@ Same names, arguments and error behaviour as the reference:
 * ``run_shot(prog, state=None, shot=0, seed=0, forced_faults=None,
   forced_outcomes=None, weight=1.0, trace=None)`` -> ShotRecord (runtime.py:731-751)
 * ``ShotState``, ``ShotRecord``, ``ShotError``, ``BRANCH_FLOOR``
+* ``StratumSpec(prog, w)``, ``importance_sample(prog, stratum, shots, seed=0, workers=1,
+  keep_rejected=True)`` -- stratified importance sampling (runtime.py:886-945); the per-shot
+  conditional draw runs on the GPU (``fs_sample_stratum``)
 
 ``prog`` is either the reference compiler's ``BytecodeProgram`` (serialized on
 first use and cached on the object) or a :class:`~.program.Program`.
@@ -36,9 +39,9 @@ from .program import OP_NAMES, Program, as_program
 BRANCH_FLOOR = 1e-12  # runtime.py:47
 _CHUNK = 1 << 20      # shots per device call in the record iterator
 
-__all__ = ["BRANCH_FLOOR", "FORMATS", "ShotError", "ShotRecord", "ShotState", "run_shot", "sample",
-           "sample_accumulate", "sample_batch", "sample_formatted", "write_samples", "Sampler",
-           "compile_circuit"]
+__all__ = ["BRANCH_FLOOR", "FORMATS", "ShotError", "ShotRecord", "ShotState", "StratumSpec", "importance_sample",
+           "run_shot", "sample", "sample_accumulate", "sample_batch", "sample_formatted", "write_samples",
+           "Sampler", "compile_circuit"]
 
 
 @dataclass(slots=True)
@@ -106,6 +109,16 @@ class Sampler:
         return {"measurements": out.measurements(), "detectors": out.detectors(),
                 "observables": out.observables(), "accepted": out.accepted_bits().astype(bool)}
 
+    def sample_stratum_batch(self, w: int, shots: int, seed: int = 0, shot0: int = 0) -> dict:
+        """sample_batch conditioned on exactly w faults (StratumSpec.draw_forced per shot, on the GPU)."""
+        if shots < 1:
+            raise ValueError("shots must be >= 1")
+        if shot0 % 32:
+            raise ValueError("shot0 must be a multiple of 32")
+        _, out = self.dp.sample_stratum_host(w, shots, seed=seed, shot0=shot0, flags=self.flags)
+        return {"measurements": out.measurements(), "detectors": out.detectors(),
+                "observables": out.observables(), "accepted": out.accepted_bits().astype(bool)}
+
     def sample_packed(self, shots: int, seed: int = 0, shot0: int = 0):
         """Raw shot-bit words (include/fs_sampler.h layout): HostOutputs."""
         _, out, _ = self.dp.sample_host(shots, seed=seed, shot0=shot0, flags=self.flags)
@@ -130,21 +143,76 @@ def sample(prog, shots: int, seed: int = 0, workers: int = 1, renormalize: bool 
     """
     if shots < 1:
         raise ValueError("shots must be >= 1")
-    if stratum is not None:
-        raise NotImplementedError("stratified importance sampling (runtime.py:873-945) is not on "
-                                  "the GPU path yet; use framesim.runtime.importance_sample")
     s = Sampler(prog, rng=rng, renormalize=renormalize)
-    return _iter_records(s, shots, seed, keep_rejected)
+    spec = _as_stratum(prog, stratum)
+    return _iter_records(s, shots, seed, keep_rejected, spec)
 
 
-def _iter_records(s: Sampler, shots: int, seed: int, keep_rejected: bool):
+def _iter_records(s: Sampler, shots: int, seed: int, keep_rejected: bool, spec=None):
+    weight = 1.0 if spec is None else spec.weight
     for c0 in range(0, shots, _CHUNK):
         n = min(_CHUNK, shots - c0)
-        b = s.sample_batch(n, seed=seed, shot0=c0)
+        if spec is None:
+            b = s.sample_batch(n, seed=seed, shot0=c0)
+        else:
+            b = s.sample_stratum_batch(spec.w, n, seed=seed, shot0=c0)
         m, d, o, a = b["measurements"], b["detectors"], b["observables"], b["accepted"]
         for i in range(n):
             if a[i] or keep_rejected:
-                yield ShotRecord(m[i], d[i], o[i], bool(a[i]), 1.0)
+                yield ShotRecord(m[i], d[i], o[i], bool(a[i]), weight)
+
+
+class StratumSpec:
+    """Shot batch conditioned on exactly ``w`` realised faults (runtime.py:886-932).
+
+    ``weight`` is Pr[W = w] under the Poisson-binomial law of the site probabilities (computed by
+    the library exactly as the reference builds its suffix table); the per-shot conditional draw
+    (``draw_forced``) runs on the GPU inside ``sample`` / ``sample_accumulate``."""
+
+    def __init__(self, prog, w: int):
+        P = as_program(prog)
+        e = P.num_sites
+        w = int(w)
+        if w > e:
+            raise ValueError(f"stratum fault count {w} exceeds {e} sites")
+        if w < 0:
+            raise ValueError("stratum fault count must be >= 0")
+        self.w = w
+        self.probs = [float(x) for x in P.site_prob]
+        self.weight = _device_program(prog).stratum_weight(w)
+
+
+def _as_stratum(prog, stratum):
+    """None, a fault count, our StratumSpec or the reference's (anything with ``.w``)."""
+    if stratum is None:
+        return None
+    if isinstance(stratum, StratumSpec):
+        return stratum
+    w = getattr(stratum, "w", stratum)
+    return StratumSpec(prog, int(w))
+
+
+def importance_sample(prog, stratum, shots: int, seed: int = 0, workers: int = 1, keep_rejected: bool = True,
+                      rng: str = "reference"):
+    """Weighted records conditioned on a fault-count stratum (runtime.py:935-945): ``stratum`` is
+    a StratumSpec or a fault count w; every record carries weight Pr[W = w]."""
+    return sample(prog, shots, seed=seed, workers=workers, stratum=_as_stratum(prog, stratum),
+                  keep_rejected=keep_rejected, rng=rng)
+
+
+def _weight_sum(weight: float, count: int) -> float:
+    """The reference's running ``weight_sum += state.weight`` over accepted shots (sequential
+    float additions, runtime.py:859), reproduced exactly in chunks."""
+    acc = 0.0
+    left = int(count)
+    while left:
+        m = min(left, 1 << 20)
+        seq = np.empty(m + 1)
+        seq[0] = acc
+        seq[1:] = weight
+        acc = float(np.cumsum(seq)[-1])
+        left -= m
+    return acc
 
 
 FORMATS = {"01": _abi.FS_FMT_01, "bin": _abi.FS_FMT_BIN, "csv": _abi.FS_FMT_CSV}
@@ -169,9 +237,8 @@ def write_samples(prog, shots: int, out, seed: int = 0, format: str = "01", keep
     fmt = FORMATS[format]
     s = Sampler(prog, rng=rng, renormalize=renormalize)
     dp = s.dp
-    weight = 1.0
-    if stratum is not None:
-        raise NotImplementedError("stratified sampling: see sample(..., stratum=)")
+    spec = _as_stratum(prog, stratum)
+    weight = 1.0 if spec is None else spec.weight
     wtext = f"{weight:.17g}"
     if format == "csv":
         out.write(b"shot,weight,bits\n")
@@ -201,7 +268,10 @@ def write_samples(prog, shots: int, out, seed: int = 0, format: str = "01", keep
         if _PROFILE:
             import time as _t
             _t0 = _t.perf_counter()
-        dp.sample_device(n, words, seed=seed, shot0=c0, flags=s.flags, stream=comp)
+        if spec is None:
+            dp.sample_device(n, words, seed=seed, shot0=c0, flags=s.flags, stream=comp)
+        else:
+            dp.sample_stratum_device(spec.w, n, words, seed=seed, shot0=c0, flags=s.flags, stream=comp)
         nb, nk = dp.format_device(n, words, fmt, keep_rejected, written, wtext, slot["dev"], stream=comp)
         if _PROFILE:
             _t1 = _t.perf_counter()
@@ -259,14 +329,18 @@ def sample_formatted(prog, shots: int, seed: int = 0, format: str = "01", keep_r
 
 def sample_accumulate(prog, shots: int, seed: int = 0, stratum=None, rng: str = "reference") -> dict:
     """Bit sums over accepted shots (runtime.py:836-867), reduced on the device."""
-    if stratum is not None:
-        raise NotImplementedError("stratified importance sampling is not on the GPU path yet")
     if shots < 1:
         return {"shots": shots, "accepted": 0, "weight_sum": 0.0,
                 "measurements": np.zeros(as_program(prog).num_user_records, np.int64),
                 "detectors": np.zeros(as_program(prog).num_detectors, np.int64),
                 "observables": np.zeros(as_program(prog).num_observables, np.int64)}
-    return Sampler(prog, rng=rng).accumulate(shots, seed=seed)
+    spec = _as_stratum(prog, stratum)
+    s = Sampler(prog, rng=rng)
+    if spec is None:
+        return s.accumulate(shots, seed=seed)
+    acc = s.dp.accumulate_stratum(spec.w, shots, seed=seed, flags=s.flags)
+    acc["weight_sum"] = _weight_sum(spec.weight, acc["accepted"])
+    return acc
 
 
 class ShotState:

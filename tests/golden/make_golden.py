@@ -272,6 +272,57 @@ def main(which=("configs", "random", "toys")):
                         payload[f"{fmt}_{int(keep)}"] = np.frombuffer(open(opath, "rb").read(), dtype=np.uint8)
             np.savez_compressed(fdir / f"{name}.npz", **payload)
             print(f"formats/{name:20s} ({time.time() - t0:.1f}s)", flush=True)
+    if "stratum" in which:  # stratified importance sampling (runtime.py:886-945)
+        from framesim.runtime import StratumSpec
+        from framesim import cli as fcli
+        import tempfile
+        sdir = OUT / "stratum"
+        sdir.mkdir(exist_ok=True)
+        from paper_2604_27058_b200.configs import random_near_clifford
+        nc_text = random_near_clifford(6, 5, t_cells=6, seed=11)
+        nc_lines = nc_text.strip().split("\n")
+        nc_lines = [x for ln in nc_lines for x in (ln, "DEPOLARIZE1(0.02) 1 3")]
+        cases = {
+            "repetition": (str(ftest.repetition_code_circuit(3, 5, 0.05)), True, ()),
+            "postselect": ("H 0\nM 0\nPOSTSELECT rec[-1]\nH 1\nT 1\nH 1\nM 1\nDEPOLARIZE1(0.5) 1\nM 1\n", True, ()),
+            "noise_twice": ("H 0\nT 0\nH 0\nM 0\nDEPOLARIZE1(0.3) 0\nM 0\n", True, ()),
+            "certain": ("X_ERROR(1.0) 0\nX_ERROR(0.5) 1\nX_ERROR(0.0) 2\nDEPOLARIZE1(1.0) 3\nM 0 1 2 3\n", False, ()),
+            "surface_d3": (config_text(2)[0], True, ()),
+            "near_clifford": ("\n".join(nc_lines) + "\n", True, ()),
+            "repetition_ps": (str(ftest.repetition_code_circuit(3, 4, 0.08)), True, (0, 2, 3)),
+        }
+        for name, (text, opt, ps) in cases.items():
+            t0 = time.time()
+            prog = compile_circuit(text, optimize=opt, postselect_detectors=ps)
+            E = len(prog.sites)
+            payload = {"program": np.frombuffer(serialize(prog, name=name).to_npz_bytes(), dtype=np.uint8),
+                       "circuit": np.array(text)}
+            ws = [w for w in (0, 1, 2, 3, 5) if w <= E]
+            payload["ws"] = np.array(ws)
+            for w in ws:
+                spec = StratumSpec(prog, w)
+                recs = list(sample(prog, 96, seed=5, stratum=spec))
+                payload[f"w{w}_meas"] = np.array([r.measurements for r in recs], np.uint8).reshape(len(recs), -1)
+                payload[f"w{w}_det"] = np.array([r.detectors for r in recs], np.uint8).reshape(len(recs), -1)
+                payload[f"w{w}_obs"] = np.array([r.observables for r in recs], np.uint8).reshape(len(recs), -1)
+                payload[f"w{w}_acc"] = np.array([r.accepted for r in recs], np.uint8)
+                payload[f"w{w}_weight"] = np.array([spec.weight])
+                assert all(r.weight == spec.weight for r in recs)
+            try:
+                StratumSpec(prog, E + 1)
+            except ValueError as exc:
+                payload["too_many_error"] = np.array(str(exc))
+            if opt and not ps:  # the CLI path (compile with defaults) pins the csv weight text
+                with tempfile.TemporaryDirectory() as td:
+                    cpath, opath = f"{td}/c.txt", f"{td}/o.csv"
+                    open(cpath, "w").write(text)
+                    w = ws[min(1, len(ws) - 1)]
+                    assert fcli.main(["sample", cpath, "--shots", "96", "--seed", "5", "--format", "csv",
+                                      "--stratum-w", str(w), "--out", opath, "--keep-rejected"]) == 0
+                    payload["cli_w"] = np.array([w])
+                    payload["cli_csv"] = np.frombuffer(open(opath, "rb").read(), dtype=np.uint8)
+            np.savez_compressed(sdir / f"{name}.npz", **payload)
+            print(f"stratum/{name:16s} E={E:4d} ws={ws} ({time.time() - t0:.1f}s)", flush=True)
     if "configs" in which:
         for i in range(5):
             text, ps = config_text(i)
