@@ -51,6 +51,8 @@ __global__ void __launch_bounds__(G == 32 ? 32 * kBlockMaxGroups : 256, G == 32 
     WordFaultGen gen;
     int pend_site = -1, pend_lane = 0, pend_case = 0;
     int branch = 0;
+    int coin_blk = -1;  // thread 0: Philox coin block of ordinals 4b..4b+3, reused across coins
+    uint4 coin_b = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
       sh_alive = 1;
       sh_err = 0;
@@ -109,7 +111,18 @@ __global__ void __launch_bounds__(G == 32 ? 32 * kBlockMaxGroups : 256, G == 32 
             bit = fx[virt] ^ (uint32_t)flip;
           } else {
             const uint32_t pz = fz[virt];
-            uint32_t coin = SPLITMIX ? (uint32_t)sm.bit() : ((coin_word(A.seed, wabs, ins[2]) >> mylane) & 1u);
+            uint32_t coin;
+            if (SPLITMIX) {
+              coin = (uint32_t)sm.bit();
+            } else {
+              if ((ins[2] >> 2) != coin_blk) {
+                coin_blk = ins[2] >> 2;
+                coin_b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), (uint32_t)coin_blk, TAG_COIN << 24, A.seed);
+              }
+              const int cj = ins[2] & 3;
+              const uint32_t cw = cj == 0 ? coin_b.x : (cj == 1 ? coin_b.y : (cj == 2 ? coin_b.z : coin_b.w));
+              coin = (cw >> mylane) & 1u;
+            }
             bit = coin ^ pz ^ (uint32_t)flip;
             const uint32_t t = fx[virt];
             fx[virt] = fz[virt] ^ coin;

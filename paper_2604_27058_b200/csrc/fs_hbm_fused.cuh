@@ -98,8 +98,8 @@ __device__ __forceinline__ void reg_expand(double2 (&v)[kTileElems], double2 ph0
 //   MC_H   | m << 4                      Hadamard along tile bit m
 //   MC_CX  | m << 4 | c << 9             X on tile bit m controlled by position c
 //   MC_EXP | m << 4 | k << 16            Expand onto tile bit m, constants k
-// Register bits (m >= 8) are updated in registers; a thread bit (m < 8) exchanges the tile with
-// the partner thread tid ^ (1 << m) through shared memory.
+// Register bits (m >= 8) are updated in registers; a lane bit (m < 5) exchanges with the partner
+// lane by register shuffles; a warp bit (5 <= m < 8) exchanges the tile through shared memory.
 //   MC_DIAG| nterm << 4 | nrot << 12, then lin0, lin1, M0..M3, sR | QQ << 16,
 //            nterm x (a, N_a), nrot x (a | k << 8)
 // A diagonal run (CZ / S / S_DAG / ROT, which commute) multiplies element X by
@@ -277,12 +277,41 @@ __global__ void __launch_bounds__(kTileThreads, 2) hbm_fused_pass_kernel(HbmStat
         }
         continue;
       }
-      // thread bit: exchange with partner thread tid ^ (1 << m) through shared memory
+      const bool mine_bit = (tid >> m) & 1u;
+      if (m < 5) {  // lane bit: the partner is in this warp -- register shuffles, no barrier
+        const int lm = 1 << m;
+        if (kind == MC_H) {
+          const double sg = mine_bit ? -1.0 : 1.0;
+#pragma unroll
+          for (int j = 0; j < kTileElems; j++) {
+            const double px = __shfl_xor_sync(0xFFFFFFFFu, v[j].x, lm), py = __shfl_xor_sync(0xFFFFFFFFu, v[j].y, lm);
+            v[j] = make_double2(__dmul_rn(__fma_rn(sg, v[j].x, px), kInvSqrt2),
+                                __dmul_rn(__fma_rn(sg, v[j].y, py), kInvSqrt2));
+          }
+        } else if (kind == MC_CX) {
+          const int xa = (ow >> 9) & 31;
+          const uint32_t cm = (unsigned)(xa - 8) < 4u ? reg_mask(xa - 8) : (((X0 >> xa) & 1u) ? 0xFFFFu : 0u);
+#pragma unroll
+          for (int j = 0; j < kTileElems; j++) {
+            const double px = __shfl_xor_sync(0xFFFFFFFFu, v[j].x, lm), py = __shfl_xor_sync(0xFFFFFFFFu, v[j].y, lm);
+            if ((cm >> j) & 1u) v[j] = make_double2(px, py);
+          }
+        } else {  // expand
+          const int k = ow >> 16;
+          const double2 ph = mine_bit ? cs[2 * k + 1] : cs[2 * k];
+#pragma unroll
+          for (int j = 0; j < kTileElems; j++) {
+            const double px = __shfl_xor_sync(0xFFFFFFFFu, v[j].x, lm), py = __shfl_xor_sync(0xFFFFFFFFu, v[j].y, lm);
+            v[j] = cmul(mine_bit ? make_double2(px, py) : v[j], ph);
+          }
+        }
+        continue;
+      }
+      // warp bit: exchange with partner thread tid ^ (1 << m) through shared memory
 #pragma unroll
       for (int j = 0; j < kTileElems; j++) T[tid + kTileThreads * j] = v[j];
       __syncthreads();
       const uint32_t ptid = tid ^ (1u << m);
-      const bool mine_bit = (tid >> m) & 1u;
       if (kind == MC_H) {  // bit 0: (v + p) / sqrt2, bit 1: (p - v) / sqrt2
         const double sg = mine_bit ? -1.0 : 1.0;
 #pragma unroll

@@ -83,7 +83,7 @@ struct HbmPlan {
 namespace {
 constexpr int kLargeK = 16;  // k_max at which active arrays move to the HBM engine
 constexpr int kBlockK = 6;   // segment active dimension at which a shot gets a whole CTA (or warp)
-constexpr int kChunks = 1;   // word chunks of the fault-list | frame-kernel pipeline (1 measured best)
+constexpr int kChunks = 4;   // max word chunks of the fault-list | frame-kernel pipeline; default 1 (2-4 measured 10-27 % slower), FS_JIT_CHUNKS overrides
 }  // namespace
 
 struct fs_prog {
@@ -1435,7 +1435,7 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
         FS_CUDA_TRY(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
         for (int c = 0; c < kChunks + 1; c++) FS_CUDA_TRY(cudaEventCreateWithFlags(&p->ev[c], cudaEventDisableTiming));
       }
-      int nch_req = kChunks;
+      int nch_req = 1;
       if (const char* ce = getenv("FS_JIT_CHUNKS")) nch_req = std::max(1, std::min(kChunks, atoi(ce)));
       const int nch = W >= (size_t)nch_req * 4096 ? nch_req : 1;
       const size_t per = (W + nch - 1) / nch;

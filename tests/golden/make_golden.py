@@ -323,6 +323,26 @@ def main(which=("configs", "random", "toys")):
                     payload["cli_csv"] = np.frombuffer(open(opath, "rb").read(), dtype=np.uint8)
             np.savez_compressed(sdir / f"{name}.npz", **payload)
             print(f"stratum/{name:16s} E={E:4d} ws={ws} ({time.time() - t0:.1f}s)", flush=True)
+    if "laws" in which:  # known-answer laws of the reference tests (test_runtime.py, test_acceptance.py)
+        ldir = OUT / "laws"
+        ldir.mkdir(exist_ok=True)
+        laws = {
+            "htm": "H 0\nT 0\nH 0\nM 0\n",                     # P[1] = sin^2(pi/8)  test_runtime.py:53-59
+            "coin": "H 0\nM 0\n",                                # fair coin           test_runtime.py:44-50
+            "hazard_pair": "X_ERROR(0.1) 0\nX_ERROR(0.3) 1\nM 0 1\n",  # joint chi^2  test_runtime.py:110-121
+            "pbinom": "X_ERROR(0.05) 0\nX_ERROR(0.2) 1\nX_ERROR(0.35) 2\nX_ERROR(0.5) 3\nM 0 1 2 3\n",
+            "certain": "X_ERROR(1.0) 0\nX_ERROR(0.0) 1\nM 0 1\n",  # p=1 / p=0 sites test_runtime.py:78-107
+            "depol1": "DEPOLARIZE1(0.3) 0\nM 0\n",
+            "depol2": "DEPOLARIZE2(0.15) 0 1\nM 0 1\n",
+            "postselect_half": "H 0\nM 0\nPOSTSELECT rec[-1]\nH 1\nT 1\nH 1\nM 1\n",
+        }
+        for name, text in laws.items():
+            opt = name != "certain"
+            prog = compile_circuit(text, optimize=opt)
+            np.savez_compressed(ldir / f"{name}.npz",
+                                program=np.frombuffer(serialize(prog, name=name).to_npz_bytes(), dtype=np.uint8),
+                                circuit=np.array(text))
+            print(f"laws/{name}", flush=True)
     if "configs" in which:
         for i in range(5):
             text, ps = config_text(i)
