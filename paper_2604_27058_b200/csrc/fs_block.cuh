@@ -388,15 +388,19 @@ __global__ void __launch_bounds__(G == 32 ? 32 * kBlockMaxGroups : 256, G == 32 
           branch = sh_branch;
           if (collapse) {  // compaction: gather sources first (in-place, different threads)
             const double2 k0 = sh_k0, k1 = sh_k1;
-            double2 v[16];
-            int nv = 0;
-            for (uint32_t j = tid; j < half && nv < 16; j += nt, nv++) {
-              const uint32_t i0 = ins0(j, a);
-              v[nv] = cadd(cmul(k0, amp[i0]), cmul(k1, amp[i0 + st]));
+            // in place, one strip of nt outputs at a time: strip b reads indices >= its own
+            // outputs, all above what earlier strips wrote
+            for (uint32_t b0 = 0; b0 < half; b0 += nt) {
+              const uint32_t j = b0 + tid;
+              double2 val = make_double2(0.0, 0.0);
+              if (j < half) {
+                const uint32_t i0 = ins0(j, a);
+                val = cadd(cmul(k0, amp[i0]), cmul(k1, amp[i0 + st]));
+              }
+              FS_BAR();
+              if (j < half) amp[j] = val;
+              FS_BAR();
             }
-            FS_BAR();
-            nv = 0;
-            for (uint32_t j = tid; j < half && nv < 16; j += nt, nv++) amp[j] = v[nv];
           } else {
             const double s = sh_k0.x;
             const uint32_t dead = 1u - (uint32_t)branch;
@@ -412,12 +416,14 @@ __global__ void __launch_bounds__(G == 32 ? 32 * kBlockMaxGroups : 256, G == 32 
           const int virt = ins[1], a = ins[2];
           const uint32_t half = (1u << ins[6]) >> 1;
           const int br = sh_branch;
-          double2 v[16];
-          int nv = 0;
-          for (uint32_t j = tid; j < half && nv < 16; j += nt, nv++) v[nv] = amp[ins0(j, a) + ((uint32_t)br << a)];
-          FS_BAR();
-          nv = 0;
-          for (uint32_t j = tid; j < half && nv < 16; j += nt, nv++) amp[j] = v[nv];
+          for (uint32_t b0 = 0; b0 < half; b0 += nt) {  // in place, strip by strip (as collapse)
+            const uint32_t j = b0 + tid;
+            double2 val = make_double2(0.0, 0.0);
+            if (j < half) val = amp[ins0(j, a) + ((uint32_t)br << a)];
+            FS_BAR();
+            if (j < half) amp[j] = val;
+            FS_BAR();
+          }
           if (tid == 0) fx[virt] ^= (uint32_t)br;
           FS_BAR();
           break;

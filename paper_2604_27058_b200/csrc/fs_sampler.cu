@@ -82,7 +82,7 @@ struct HbmPlan {
 
 namespace {
 constexpr int kLargeK = 16;  // k_max at which active arrays move to the HBM engine
-constexpr int kBlockK = 6;   // segment active dimension at which a shot gets a whole CTA (or warp)
+constexpr int kBlockK = 9;   // segment active dimension at which a shot gets a whole CTA (or warp); measured on config 4: lane-per-shot 2.4x faster at k = 7, 2.6x slower at k = 10
 constexpr int kChunks = 4;   // max word chunks of the fault-list | frame-kernel pipeline; default 1 (2-4 measured 10-27 % slower), FS_JIT_CHUNKS overrides
 }  // namespace
 
@@ -751,6 +751,8 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   if (!p->d_counts) FS_CUDA_TRY(cudaMalloc(&p->d_counts, 64));
   uint32_t* d_nout = reinterpret_cast<uint32_t*>(p->d_counts);
   p->seg_counts.clear();
+  int block_k = kBlockK;
+  if (const char* e = getenv("FS_BLOCK_K")) block_k = std::max(1, atoi(e));  // experiments
   for (uint64_t c0 = 0; c0 < a.nshots; c0 += chunk) {
     uint32_t n_in = (uint32_t)std::min<uint64_t>(chunk, a.nshots - c0);
     p->seg_counts.push_back(n_in);
@@ -783,11 +785,11 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
           p->seg_bytes[1 - cur] = need;
         }
         S.out = carve_store(p->seg_pool[1 - cur], S, n_in, S.k_out);
-        S.out.shot_major = karr_next >= kBlockK ? 1 : 0;
+        S.out.shot_major = karr_next >= block_k ? 1 : 0;
         FS_CUDA_TRY(cudaMemsetAsync(d_nout, 0, 4, stream));
       }
       S.n_out = d_nout;
-      int rc = karr >= kBlockK ? launch_block_kernel(p, a, S, karr, stream)
+      int rc = karr >= block_k ? launch_block_kernel(p, a, S, karr, stream)
                                : launch_general_kernel(p, a, S, true, karr, (n_in + 31) / 32, stream);
       if (rc) return rc;
       if (S.last) break;
