@@ -343,6 +343,30 @@ def main(which=("configs", "random", "toys")):
                                 program=np.frombuffer(serialize(prog, name=name).to_npz_bytes(), dtype=np.uint8),
                                 circuit=np.array(text))
             print(f"laws/{name}", flush=True)
+    if "edges" in which:  # degenerate programs the reference accepts (empty, no records, ...)
+        edir = OUT / "edges"
+        edir.mkdir(exist_ok=True)
+        edges = {
+            "empty": "",
+            "no_measure": "H 0\nT 0\n",
+            "measure_only": "M 0\n",
+            "noise_only": "DEPOLARIZE1(0.1) 0\n",
+            "empty_detector": "X_ERROR(0.2) 0\nDETECTOR\n",
+            "empty_observable": "OBSERVABLE_INCLUDE(0)\n",
+            "active_unmeasured": "H 0\nT 0\nH 1\nT 1\nCX 0 1\n",
+            "wide_sparse": "H 0\nT 0\nH 0\nM 0\nX_ERROR(0.3) 299\nM 299\nDETECTOR rec[-1]\n",
+        }
+        for name, text in edges.items():
+            prog = compile_circuit(text)
+            recs = list(sample(prog, 100, seed=9))
+            m = np.array([r.measurements for r in recs], np.uint8).reshape(100, -1)
+            d = np.array([r.detectors for r in recs], np.uint8).reshape(100, -1)
+            o = np.array([r.observables for r in recs], np.uint8).reshape(100, -1)
+            a = np.array([r.accepted for r in recs], np.uint8)
+            np.savez_compressed(edir / f"{name}.npz",
+                                program=np.frombuffer(serialize(prog, name=name).to_npz_bytes(), dtype=np.uint8),
+                                circuit=np.array(text), f_meas=m, f_det=d, f_obs=o, f_acc=a, f_seed=np.array([9]))
+            print(f"edges/{name}", flush=True)
     if "configs" in which:
         for i in range(5):
             text, ps = config_text(i)
