@@ -198,6 +198,12 @@ int fs_sample_stratum_host(fs_prog* prog, uint32_t w, uint64_t seed, uint64_t sh
                            uint32_t flags, const fs_sample_out* out);
 int fs_accumulate_stratum(fs_prog* prog, uint32_t w, uint64_t seed, uint64_t shot0, uint64_t nshots,
                           uint32_t flags, int64_t* counts, void* stream);
+
+/* expectation_probe traversal (runtime.py:951-989): for the device active array amps[2^k][2],
+ * out[0] = Re sum_idx conj(a[idx ^ xm]) i^ycount (-1)^popcount(idx & zm) a[idx],
+ * out[1] = sum |a|^2 (host doubles).  The Pauli mapping through the final tableau, the frame
+ * parity and the sign stay with the caller (host compiler objects). */
+int fs_probe(const double* amps, int32_t k, uint64_t xm, uint64_t zm, int32_t ycount, double* out, void* stream);
 #endif
 
 #ifdef __cplusplus

@@ -106,6 +106,9 @@ def lib():
             L.fs_accumulate_stratum.restype = C.c_int
             L.fs_accumulate_stratum.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64,
                                                 C.c_uint32, C.c_void_p, C.c_void_p]
+            L.fs_probe.restype = C.c_int
+            L.fs_probe.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, C.c_uint64, C.c_int32,
+                                   C.POINTER(C.c_double), C.c_void_p]
             if L.fs_abi_version() != 1:
                 raise EngineUnavailable("ABI version mismatch")
             _lib = L

@@ -2005,3 +2005,59 @@ extern "C" int fs_accumulate_stratum(fs_prog* p, uint32_t w, uint64_t seed, uint
   }
   return FS_OK;
 }
+
+// ------------------------------------------------------------------ expectation probe
+namespace {
+constexpr int kProbeBlocks = 296;
+// <a| i^y (-1)^{popc(idx & zm)} |a[idx ^ xm]> terms and |a|^2, per block (fixed order within a
+// block), finished on the host in block order (runtime.py:951-989, one traversal)
+__global__ void probe_kernel(const double2* __restrict__ a, uint64_t size, uint64_t xm, uint64_t zm, int y,
+                             double* __restrict__ part) {
+  double re = 0.0, nn = 0.0;
+  const double2 iy = (y & 3) == 0 ? make_double2(1, 0) : (y & 3) == 1 ? make_double2(0, 1)
+                   : (y & 3) == 2 ? make_double2(-1, 0) : make_double2(0, -1);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 ai = a[i], aj = a[i ^ xm];
+    double2 t = fs::cmul(iy, ai);
+    if (__popcll(i & zm) & 1) t = make_double2(-t.x, -t.y);
+    re = __dadd_rn(re, __dadd_rn(__dmul_rn(aj.x, t.x), __dmul_rn(aj.y, t.y)));  // Re(conj(aj) * t)
+    nn = __dadd_rn(nn, fs::cnorm2(ai));
+  }
+  __shared__ double s1[256], s2[256];
+  s1[threadIdx.x] = re;
+  s2[threadIdx.x] = nn;
+  __syncthreads();
+  for (int w = 128; w; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      s1[threadIdx.x] = __dadd_rn(s1[threadIdx.x], s1[threadIdx.x + w]);
+      s2[threadIdx.x] = __dadd_rn(s2[threadIdx.x], s2[threadIdx.x + w]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s1[0];
+    part[2 * blockIdx.x + 1] = s2[0];
+  }
+}
+}  // namespace
+
+extern "C" int fs_probe(const double* amps, int32_t k, uint64_t xm, uint64_t zm, int32_t ycount, double* out,
+                        void* stream_) {
+  if (!amps || !out || k < 0 || k > 40) return set_error(FS_ERR_ARG, "bad probe arguments");
+  const uint64_t size = 1ull << k;
+  if ((xm | zm) >> k) return set_error(FS_ERR_ARG, "probe masks outside the active array");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  static thread_local double* part = nullptr;
+  if (!part) FS_CUDA_TRY(cudaMalloc(&part, sizeof(double) * 2 * kProbeBlocks));
+  const unsigned g = (unsigned)std::min<uint64_t>(kProbeBlocks, (size + 255) / 256);
+  probe_kernel<<<g, 256, 0, stream>>>(reinterpret_cast<const double2*>(amps), size, xm, zm, ycount, part);
+  FS_CUDA_TRY(cudaGetLastError());
+  std::vector<double> h(2 * g);
+  FS_CUDA_TRY(cudaMemcpyAsync(h.data(), part, sizeof(double) * 2 * g, cudaMemcpyDeviceToHost, stream));
+  FS_CUDA_TRY(cudaStreamSynchronize(stream));
+  double re = 0.0, nn = 0.0;
+  for (unsigned b = 0; b < g; b++) { re += h[2 * b]; nn += h[2 * b + 1]; }
+  out[0] = re;
+  out[1] = nn;
+  return FS_OK;
+}

@@ -8,6 +8,8 @@ Same names, arguments and error behaviour as the reference:
 * ``run_shot(prog, state=None, shot=0, seed=0, forced_faults=None,
   forced_outcomes=None, weight=1.0, trace=None)`` -> ShotRecord (runtime.py:731-751)
 * ``ShotState``, ``ShotRecord``, ``ShotError``, ``BRANCH_FLOOR``
+* ``expectation_probe(prog, state, observable)`` (runtime.py:951-989): the active-array traversal
+  runs on the GPU (``fs_probe``); the Pauli mapping uses the reference program's final tableau
 * ``StratumSpec(prog, w)``, ``importance_sample(prog, stratum, shots, seed=0, workers=1,
   keep_rejected=True)`` -- stratified importance sampling (runtime.py:886-945); the per-shot
   conditional draw runs on the GPU (``fs_sample_stratum``)
@@ -39,7 +41,8 @@ from .program import OP_NAMES, Program, as_program
 BRANCH_FLOOR = 1e-12  # runtime.py:47
 _CHUNK = 1 << 20      # shots per device call in the record iterator
 
-__all__ = ["BRANCH_FLOOR", "FORMATS", "ShotError", "ShotRecord", "ShotState", "StratumSpec", "importance_sample",
+__all__ = ["BRANCH_FLOOR", "FORMATS", "ShotError", "ShotRecord", "ShotState", "StratumSpec", "expectation_probe",
+           "importance_sample",
            "run_shot", "sample", "sample_accumulate", "sample_batch", "sample_formatted", "write_samples",
            "Sampler", "compile_circuit"]
 
@@ -474,3 +477,59 @@ def _copy_state(state: ShotState, P: Program, out, tb, lane: int, stop: int) -> 
         state.detectors[:] = out.detectors()[lane]
     if P.num_observables:
         state.observables[:] = out.observables()[lane]
+
+
+# -- expectation probe (runtime.py:951-989) --------------------------------------------------
+def expectation_probe(prog, state: ShotState, observable) -> float:
+    """<psi|P|psi> of the current factored state, non-collapsing (runtime.py:951-989).
+
+    ``prog`` must be the reference compiler's BytecodeProgram: the observable is mapped through
+    its ``final_tableau`` (host Pauli algebra) onto ``final_active``; the traversal of the active
+    array runs on the GPU."""
+    if not hasattr(prog, "final_tableau") or not hasattr(prog, "final_active"):
+        raise TypeError("expectation_probe needs the reference BytecodeProgram (final_tableau, final_active)")
+    if not observable.is_hermitian():
+        raise ValueError("probe observable must be Hermitian")
+    mapped = prog.final_tableau.heisenberg_map(observable)
+    word = mapped.hermitian_word()
+    return probe_mapped(state, np.asarray(word.x, np.uint8), np.asarray(word.z, np.uint8),
+                        int(mapped.hermitian_sign()), list(prog.final_active))
+
+
+def probe_mapped(state: ShotState, word_x, word_z, sign: int, final_active) -> float:
+    """expectation_probe after the tableau mapping: Hermitian word (x, z bits over the n virtual
+    qubits) with sign, on the state's frames and active array (positions = final_active)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+
+    word_x = np.asarray(word_x, np.uint8)
+    word_z = np.asarray(word_z, np.uint8)
+    par = (int(np.count_nonzero(word_x & state.frame_z)) + int(np.count_nonzero(word_z & state.frame_x))) & 1
+    active_pos = {int(v): p for p, v in enumerate(final_active)}
+    xm = zm = 0
+    ycount = 0
+    for j in np.flatnonzero(word_x | word_z):
+        j = int(j)
+        if j not in active_pos:
+            if word_x[j]:
+                return 0.0
+            continue
+        p = active_pos[j]
+        if word_x[j]:
+            xm |= 1 << p
+        if word_z[j]:
+            zm |= 1 << p
+        if word_x[j] and word_z[j]:
+            ycount += 1
+    amps = np.ascontiguousarray(state.active_view())
+    dev = torch.from_numpy(amps.view(np.float64)).to("cuda")
+    out = (C.c_double * 2)()
+    s = torch.cuda.current_stream()
+    rc = _lib.lib().fs_probe(C.c_void_p(dev.data_ptr()), int(state.k), xm, zm, ycount, out, C.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise ValueError(_lib.last_error())
+    val = out[0] / out[1]
+    return sign * (-1.0 if par else 1.0) * val

@@ -367,6 +367,47 @@ def main(which=("configs", "random", "toys")):
                                 program=np.frombuffer(serialize(prog, name=name).to_npz_bytes(), dtype=np.uint8),
                                 circuit=np.array(text), f_meas=m, f_det=d, f_obs=o, f_acc=a, f_seed=np.array([9]))
             print(f"edges/{name}", flush=True)
+    if "probe" in which:  # expectation_probe (runtime.py:951-989) values of the reference
+        from framesim.runtime import expectation_probe
+        from framesim.pauli import PauliString
+        pdir = OUT / "probe"
+        pdir.mkdir(exist_ok=True)
+        from paper_2604_27058_b200.configs import random_near_clifford
+        rng = np.random.default_rng(31)
+        circuits = {
+            "trivial": "TICK\nZ 0\n",
+            "t_state": "H 0\nT 0\n",
+            "active_pair": "H 0\nT 0\nH 1\nT 1\nCX 0 1\n",
+            "near_clifford": random_near_clifford(7, 4, t_cells=6, seed=5).rsplit("M ", 1)[0],
+            "mid_measure": "H 0\nT 0\nH 1\nT 1\nCX 0 1\nH 0\nM 0\nH 2\nT 2\nCX 1 2\n",
+        }
+        for name, text in circuits.items():
+            prog = compile_circuit(text)
+            n = prog.n
+            labels = [(q, k) for q in range(n) for k in "XYZ"]
+            multi = []
+            for _ in range(6):
+                lab = "".join(rng.choice(list("IXYZ")) for _ in range(n))
+                multi.append(lab)
+            payload = {"program": np.frombuffer(serialize(prog, name=name).to_npz_bytes(), dtype=np.uint8),
+                       "circuit": np.array(text), "final_active": np.array(list(prog.final_active), np.int64)}
+            rows = []
+            for shot in (0, 1, 2):
+                st = ShotState(prog, seed=4)
+                run_shot(prog, st, shot=shot)
+                obs = [PauliString.single(n, q, k) for q, k in labels] + [PauliString.from_label(l) for l in multi]
+                for o in obs:
+                    mapped = prog.final_tableau.heisenberg_map(o)
+                    word = mapped.hermitian_word()
+                    rows.append((shot, np.asarray(word.x, np.uint8), np.asarray(word.z, np.uint8),
+                                 int(mapped.hermitian_sign()), float(expectation_probe(prog, st, o))))
+            payload["shot"] = np.array([r[0] for r in rows])
+            payload["wx"] = np.array([r[1] for r in rows], np.uint8).reshape(len(rows), -1)
+            payload["wz"] = np.array([r[2] for r in rows], np.uint8).reshape(len(rows), -1)
+            payload["sign"] = np.array([r[3] for r in rows])
+            payload["value"] = np.array([r[4] for r in rows])
+            np.savez_compressed(pdir / f"{name}.npz", **payload)
+            print(f"probe/{name} n={n} k={prog.k_max} probes={len(rows)}", flush=True)
     if "configs" in which:
         for i in range(5):
             text, ps = config_text(i)
