@@ -129,6 +129,59 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
 }
 
+// i^P(j) from the run's coefficients: e0 on every element, eR[R] on elements with bit R of j,
+// 2 * QQ (register-register CZ pattern over j); P held as two 16-bit planes (bit 0 / bit 1)
+__device__ __forceinline__ void ipow_planes(uint32_t e0, const uint32_t (&eR)[4], uint32_t QQ, uint32_t& Lm,
+                                            uint32_t& Hm) {
+  Lm = (e0 & 1u) ? 0xFFFFu : 0u;
+  Hm = (e0 & 2u) ? 0xFFFFu : 0u;
+#pragma unroll
+  for (int R = 0; R < 4; R++) {
+    const uint32_t m = reg_mask(R);
+    if (eR[R] & 1u) {
+      const uint32_t cy = Lm & m;
+      Lm ^= m;
+      Hm ^= cy;
+    }
+    if (eR[R] & 2u) Hm ^= m;
+  }
+  Hm ^= QQ;
+}
+
+__device__ __forceinline__ void apply_ipow(double2 (&v)[kTileElems], uint32_t Lm, uint32_t Hm) {
+  if (!(Lm | Hm)) return;
+#pragma unroll
+  for (int j = 0; j < kTileElems; j++) {
+    const uint32_t lb = (Lm >> j) & 1u, hb = (Hm >> j) & 1u;
+    double x = v[j].x, y = v[j].y;
+    if (lb) { const double t = x; x = y; y = t; }
+    if (lb ^ hb) x = -x;
+    if (hb) y = -y;
+    v[j] = make_double2(x, y);
+  }
+}
+
+// v[j] *= g * prod_{R : bit R of j, R in rreg} d[R]
+__device__ __forceinline__ void apply_rot(double2 (&v)[kTileElems], double2 g, const double2 (&d)[4], uint32_t rreg) {
+  if (rreg) {
+    double2 t01[4];
+    t01[0] = g;
+    t01[1] = cmul(g, d[0]);
+    t01[2] = cmul(g, d[1]);
+    t01[3] = cmul(t01[1], d[1]);
+    const double2 d23 = cmul(d[2], d[3]);
+#pragma unroll
+    for (int j = 0; j < kTileElems; j++) {
+      const int hi = j >> 2;
+      const double2 f = hi == 0 ? t01[j & 3] : cmul(t01[j & 3], hi == 1 ? d[2] : hi == 2 ? d[3] : d23);
+      v[j] = cmul(v[j], f);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kTileElems; j++) v[j] = cmul(v[j], g);
+  }
+}
+
 __device__ __forceinline__ void diag_run_apply(double2 (&v)[kTileElems], const uint32_t* __restrict__ c,
                                                const double2* __restrict__ cs, uint32_t X0) {
   const uint32_t w = c[0];
@@ -140,31 +193,13 @@ __device__ __forceinline__ void diag_run_apply(double2 (&v)[kTileElems], const u
     q += ((X0 >> a) & 1u) * __popc(X0 & na);
   }
   e0 += 2u * q;
-  uint32_t Lm = (e0 & 1u) ? 0xFFFFu : 0u, Hm = (e0 & 2u) ? 0xFFFFu : 0u;
   const uint32_t sr = c[7];
+  uint32_t eR[4];
 #pragma unroll
-  for (int R = 0; R < 4; R++) {
-    const uint32_t eR = ((sr >> (2 * R)) & 3u) + 2u * __popc(X0 & c[3 + R]);
-    const uint32_t m = reg_mask(R);
-    if (eR & 1u) {
-      const uint32_t cy = Lm & m;
-      Lm ^= m;
-      Hm ^= cy;
-    }
-    if (eR & 2u) Hm ^= m;
-  }
-  Hm ^= sr >> 16;
-  if (Lm | Hm) {
-#pragma unroll
-    for (int j = 0; j < kTileElems; j++) {
-      const uint32_t lb = (Lm >> j) & 1u, hb = (Hm >> j) & 1u;
-      double x = v[j].x, y = v[j].y;
-      if (lb) { const double t = x; x = y; y = t; }
-      if (lb ^ hb) x = -x;
-      if (hb) y = -y;
-      v[j] = make_double2(x, y);
-    }
-  }
+  for (int R = 0; R < 4; R++) eR[R] = ((sr >> (2 * R)) & 3u) + 2u * __popc(X0 & c[3 + R]);
+  uint32_t Lm, Hm;
+  ipow_planes(e0, eR, sr >> 16, Lm, Hm);
+  apply_ipow(v, Lm, Hm);
   if (nrot == 0) return;
   const uint32_t* rt = c + 8 + 2 * nterm;
   uint32_t rreg = 0;
@@ -188,23 +223,78 @@ __device__ __forceinline__ void diag_run_apply(double2 (&v)[kTileElems], const u
       g = cmul(g, ((X0 >> xa) & 1u) ? cb : ca);
     }
   }
-  if (rreg) {
-    double2 t01[4];
-    t01[0] = g;
-    t01[1] = cmul(g, d[0]);
-    t01[2] = cmul(g, d[1]);
-    t01[3] = cmul(t01[1], d[1]);
-    const double2 d23 = cmul(d[2], d[3]);
+  apply_rot(v, g, d, rreg);
+}
+
+// ---- thread-bit exchanges (shared by the interpreter and the generated pass kernels) --------
+// control mask over j of a CX whose control sits at extended position xa
+__device__ __forceinline__ uint32_t cx_ctl_mask(int xa, uint32_t X0) {
+  return (unsigned)(xa - 8) < 4u ? reg_mask(xa - 8) : (((X0 >> xa) & 1u) ? 0xFFFFu : 0u);
+}
+// lane bit m < 5: partner lane by register shuffles.  H: bit 0 -> (v + p)/sqrt2, bit 1 -> (p - v)/sqrt2
+__device__ __forceinline__ void xlane_h(double2 (&v)[kTileElems], uint32_t tid, int m) {
+  const double sg = ((tid >> m) & 1u) ? -1.0 : 1.0;
 #pragma unroll
-    for (int j = 0; j < kTileElems; j++) {
-      const int hi = j >> 2;
-      const double2 f = hi == 0 ? t01[j & 3] : cmul(t01[j & 3], hi == 1 ? d[2] : hi == 2 ? d[3] : d23);
-      v[j] = cmul(v[j], f);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < kTileElems; j++) v[j] = cmul(v[j], g);
+  for (int j = 0; j < kTileElems; j++) {
+    const double px = __shfl_xor_sync(0xFFFFFFFFu, v[j].x, 1 << m), py = __shfl_xor_sync(0xFFFFFFFFu, v[j].y, 1 << m);
+    v[j] = make_double2(__dmul_rn(__fma_rn(sg, v[j].x, px), kInvSqrt2), __dmul_rn(__fma_rn(sg, v[j].y, py), kInvSqrt2));
   }
+}
+__device__ __forceinline__ void xlane_cx(double2 (&v)[kTileElems], int m, uint32_t cm) {
+#pragma unroll
+  for (int j = 0; j < kTileElems; j++) {
+    const double px = __shfl_xor_sync(0xFFFFFFFFu, v[j].x, 1 << m), py = __shfl_xor_sync(0xFFFFFFFFu, v[j].y, 1 << m);
+    if ((cm >> j) & 1u) v[j] = make_double2(px, py);
+  }
+}
+// expand: the bit-1 half gets the bit-0 partner times ph1, the bit-0 half is scaled by ph0
+__device__ __forceinline__ void xlane_exp(double2 (&v)[kTileElems], uint32_t tid, int m, double2 ph0, double2 ph1) {
+  const bool mb = (tid >> m) & 1u;
+  const double2 ph = mb ? ph1 : ph0;
+#pragma unroll
+  for (int j = 0; j < kTileElems; j++) {
+    const double px = __shfl_xor_sync(0xFFFFFFFFu, v[j].x, 1 << m), py = __shfl_xor_sync(0xFFFFFFFFu, v[j].y, 1 << m);
+    v[j] = cmul(mb ? make_double2(px, py) : v[j], ph);
+  }
+}
+// warp bit 5 <= m < 8: exchange the tile with thread tid ^ (1 << m) through shared memory
+__device__ __forceinline__ void xsmem_h(double2 (&v)[kTileElems], double2* T, uint32_t tid, int m) {
+#pragma unroll
+  for (int j = 0; j < kTileElems; j++) T[tid + kTileThreads * j] = v[j];
+  __syncthreads();
+  const uint32_t pt = tid ^ (1u << m);
+  const double sg = ((tid >> m) & 1u) ? -1.0 : 1.0;
+#pragma unroll
+  for (int j = 0; j < kTileElems; j++) {
+    const double2 pv = T[pt + kTileThreads * j];
+    v[j] = make_double2(__dmul_rn(__fma_rn(sg, v[j].x, pv.x), kInvSqrt2), __dmul_rn(__fma_rn(sg, v[j].y, pv.y), kInvSqrt2));
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void xsmem_cx(double2 (&v)[kTileElems], double2* T, uint32_t tid, int m, uint32_t cm) {
+#pragma unroll
+  for (int j = 0; j < kTileElems; j++) T[tid + kTileThreads * j] = v[j];
+  __syncthreads();
+  const uint32_t pt = tid ^ (1u << m);
+#pragma unroll
+  for (int j = 0; j < kTileElems; j++)
+    if ((cm >> j) & 1u) v[j] = T[pt + kTileThreads * j];
+  __syncthreads();
+}
+__device__ __forceinline__ void xsmem_exp(double2 (&v)[kTileElems], double2* T, uint32_t tid, int m, double2 ph0,
+                                          double2 ph1) {
+#pragma unroll
+  for (int j = 0; j < kTileElems; j++) T[tid + kTileThreads * j] = v[j];
+  __syncthreads();
+  const uint32_t pt = tid ^ (1u << m);
+  const bool mb = (tid >> m) & 1u;
+  const double2 ph = mb ? ph1 : ph0;
+#pragma unroll
+  for (int j = 0; j < kTileElems; j++) {
+    const double2 pv = T[pt + kTileThreads * j];
+    v[j] = cmul(mb ? pv : v[j], ph);
+  }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(kTileThreads, 2) hbm_fused_pass_kernel(HbmState H, const PassDesc D,
@@ -277,65 +367,19 @@ __global__ void __launch_bounds__(kTileThreads, 2) hbm_fused_pass_kernel(HbmStat
         }
         continue;
       }
-      const bool mine_bit = (tid >> m) & 1u;
+      const uint32_t cm = kind == MC_CX ? cx_ctl_mask((ow >> 9) & 31, X0) : 0u;
+      const int k = kind == MC_EXP ? (int)(ow >> 16) : 0;
+      const double2 ph0 = kind == MC_EXP ? cs[2 * k] : make_double2(1, 0);
+      const double2 ph1 = kind == MC_EXP ? cs[2 * k + 1] : make_double2(1, 0);
       if (m < 5) {  // lane bit: the partner is in this warp -- register shuffles, no barrier
-        const int lm = 1 << m;
-        if (kind == MC_H) {
-          const double sg = mine_bit ? -1.0 : 1.0;
-#pragma unroll
-          for (int j = 0; j < kTileElems; j++) {
-            const double px = __shfl_xor_sync(0xFFFFFFFFu, v[j].x, lm), py = __shfl_xor_sync(0xFFFFFFFFu, v[j].y, lm);
-            v[j] = make_double2(__dmul_rn(__fma_rn(sg, v[j].x, px), kInvSqrt2),
-                                __dmul_rn(__fma_rn(sg, v[j].y, py), kInvSqrt2));
-          }
-        } else if (kind == MC_CX) {
-          const int xa = (ow >> 9) & 31;
-          const uint32_t cm = (unsigned)(xa - 8) < 4u ? reg_mask(xa - 8) : (((X0 >> xa) & 1u) ? 0xFFFFu : 0u);
-#pragma unroll
-          for (int j = 0; j < kTileElems; j++) {
-            const double px = __shfl_xor_sync(0xFFFFFFFFu, v[j].x, lm), py = __shfl_xor_sync(0xFFFFFFFFu, v[j].y, lm);
-            if ((cm >> j) & 1u) v[j] = make_double2(px, py);
-          }
-        } else {  // expand
-          const int k = ow >> 16;
-          const double2 ph = mine_bit ? cs[2 * k + 1] : cs[2 * k];
-#pragma unroll
-          for (int j = 0; j < kTileElems; j++) {
-            const double px = __shfl_xor_sync(0xFFFFFFFFu, v[j].x, lm), py = __shfl_xor_sync(0xFFFFFFFFu, v[j].y, lm);
-            v[j] = cmul(mine_bit ? make_double2(px, py) : v[j], ph);
-          }
-        }
-        continue;
+        if (kind == MC_H) xlane_h(v, tid, m);
+        else if (kind == MC_CX) xlane_cx(v, m, cm);
+        else xlane_exp(v, tid, m, ph0, ph1);
+      } else {  // warp bit: through shared memory
+        if (kind == MC_H) xsmem_h(v, T, tid, m);
+        else if (kind == MC_CX) xsmem_cx(v, T, tid, m, cm);
+        else xsmem_exp(v, T, tid, m, ph0, ph1);
       }
-      // warp bit: exchange with partner thread tid ^ (1 << m) through shared memory
-#pragma unroll
-      for (int j = 0; j < kTileElems; j++) T[tid + kTileThreads * j] = v[j];
-      __syncthreads();
-      const uint32_t ptid = tid ^ (1u << m);
-      if (kind == MC_H) {  // bit 0: (v + p) / sqrt2, bit 1: (p - v) / sqrt2
-        const double sg = mine_bit ? -1.0 : 1.0;
-#pragma unroll
-        for (int j = 0; j < kTileElems; j++) {
-          const double2 pv = T[ptid + kTileThreads * j];
-          v[j] = make_double2(__dmul_rn(__fma_rn(sg, v[j].x, pv.x), kInvSqrt2),
-                              __dmul_rn(__fma_rn(sg, v[j].y, pv.y), kInvSqrt2));
-        }
-      } else if (kind == MC_CX) {
-        const int xa = (ow >> 9) & 31;
-        const uint32_t cm = (unsigned)(xa - 8) < 4u ? reg_mask(xa - 8) : (((X0 >> xa) & 1u) ? 0xFFFFu : 0u);
-#pragma unroll
-        for (int j = 0; j < kTileElems; j++)
-          if ((cm >> j) & 1u) v[j] = T[ptid + kTileThreads * j];
-      } else {  // expand: bit-1 half gets the bit-0 partner times ph1
-        const int k = ow >> 16;
-        const double2 ph = mine_bit ? cs[2 * k + 1] : cs[2 * k];
-#pragma unroll
-        for (int j = 0; j < kTileElems; j++) {
-          const double2 pv = T[ptid + kTileThreads * j];
-          v[j] = cmul(mine_bit ? pv : v[j], ph);
-        }
-      }
-      __syncthreads();
     }
 #pragma unroll
     for (int j = 0; j < kTileElems; j++) A[base | dep_lo_f | D.dep_hi_f[j]] = v[j];

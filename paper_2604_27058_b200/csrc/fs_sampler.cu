@@ -11,7 +11,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -149,6 +151,10 @@ struct fs_prog {
   fs::TileOp* d_tileops = nullptr;
   uint32_t* d_code = nullptr;
   fs::PassConst* d_consts = nullptr;
+  // program-specialised pass kernels (NVRTC) of the current plan: 0 = not built, 1 = ready, -1 = failed
+  int pass_jit = 0;
+  std::vector<fsjit::CUfunction> pass_fn;
+  std::string pass_jit_err;
   void* hbm = nullptr;
   size_t hbm_bytes = 0;
   uint64_t hbm_B = 0;
@@ -971,6 +977,8 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
   PL = HbmPlan{};
   PL.stop = stop;
   PL.fused = fused;
+  p->pass_jit = 0;
+  p->pass_fn.clear();
   const fs::DevProg& dp = p->dp;
   const int* ins_all = p->h_instrs.data();
   const double* fpar = p->h_fparams.data();
@@ -1224,6 +1232,155 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
   return FS_OK;
 }
 
+// ------------------------------------------------------------------ specialised pass kernels
+// Each fused pass's microcode compiled to straight-line code (NVRTC): masks, register bits,
+// exchange partners and address deposits become constants; the interpreter
+// (fs_hbm_fused.cuh hbm_fused_pass_kernel) remains the fallback (FS_HBM_NO_JIT).
+std::string gen_pass_source(const HbmPlan& PL) {
+  std::ostringstream o;
+  o << "#include \"fs_hbm_fused.cuh\"\nusing namespace fs;\n";
+  auto hexu = [](uint32_t x) {
+    std::ostringstream t;
+    t << "0x" << std::hex << x << "u";
+    return t.str();
+  };
+  for (size_t pi = 0; pi < PL.passes.size(); pi++) {
+    const fs::PassDesc& D = PL.passes[pi];
+    o << "extern \"C\" __global__ void __launch_bounds__(256, 2) fs_pass_" << pi
+      << "(HbmState H, const PassConst* __restrict__ consts, uint32_t W) {\n"
+      << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
+      << "  double2* T = reinterpret_cast<double2*>(smem_raw);\n"
+      << "  double2* cs = reinterpret_cast<double2*>(smem_raw + " << (16 << fs::kTileBits) << ");\n"
+      << "  const uint32_t shot = blockIdx.y, w = shot >> 5, bit = 1u << (shot & 31);\n"
+      << "  if (!(H.alive[w] & bit)) return;\n"
+      << "  const uint32_t tid = threadIdx.x;\n";
+    if (D.nconst)
+      o << "  for (int i = tid; i < " << D.nconst << "; i += 256) {\n"
+        << "    const PassConst& k = consts[" << D.const_off << " + i];\n"
+        << "    const bool par = (H.par[(size_t)k.instr * W + w] & bit) != 0;\n"
+        << "    double2 a = k.c0, b = k.c1;\n"
+        << "    if (par) { if (k.kind == TO_ROT) { a = k.c1; b = k.c0; } else { a = k.c2; b = k.c3; } }\n"
+        << "    cs[2 * i] = a;\n    cs[2 * i + 1] = b;\n  }\n";
+    o << "  const uint32_t dep_lo = 0u";
+    for (int i = 0; i < 8; i++) o << " | (((tid >> " << i << ") & 1u) << " << (int)D.T[i] << ")";
+    o << ";\n  const uint32_t dep_lo_f = 0u";
+    for (int i = 0; i < 8; i++) o << " | (((tid >> " << i << ") & 1u) << " << (int)D.Tf[i] << ")";
+    o << ";\n  __syncthreads();\n"
+      << "  double2* __restrict__ A = H.amps + (size_t)shot * H.cap;\n"
+      << "  double2 v[16];\n"
+      << "  for (uint32_t ti = blockIdx.x; ti < " << (1u << D.nbase) << "u; ti += gridDim.x) {\n"
+      << "    const uint64_t base = 0ull";
+    for (int i = 0; i < D.nbase; i++) o << " | ((uint64_t)((ti >> " << i << ") & 1u) << " << (int)D.base[i] << ")";
+    o << ";\n    const uint32_t X0 = tid | (ti << " << fs::kTileBits << ");\n";
+    for (int j = 0; j < fs::kTileElems; j++) o << "    v[" << j << "] = A[base | dep_lo | " << hexu(D.dep_hi[j]) << "];\n";
+    const uint32_t* C = PL.code.data() + D.code_off;
+    for (int pc = 0; pc < D.ncode;) {
+      const uint32_t ow = C[pc];
+      const uint32_t kind = ow & 15u;
+      if (kind == fs::MC_DIAG) {
+        const int nterm = (ow >> 4) & 0xFF, nrot = (ow >> 12) & 0xFF;
+        const uint32_t lin0 = C[pc + 1], lin1 = C[pc + 2], sr = C[pc + 7];
+        o << "    {\n      uint32_t e0 = 0u";
+        if (lin0) o << " + __popc(X0 & " << hexu(lin0) << ")";
+        if (lin1) o << " + 2u * __popc(X0 & " << hexu(lin1) << ")";
+        o << ";\n";
+        if (nterm) {
+          o << "      uint32_t q = 0u";
+          for (int t = 0; t < nterm; t++)
+            o << " + ((X0 >> " << C[pc + 8 + 2 * t] << ") & 1u) * __popc(X0 & " << hexu(C[pc + 9 + 2 * t]) << ")";
+          o << ";\n      e0 += 2u * q;\n";
+        }
+        o << "      const uint32_t eR[4] = {";
+        for (int R = 0; R < 4; R++) {
+          o << ((sr >> (2 * R)) & 3u) << "u";
+          if (C[pc + 3 + R]) o << " + 2u * __popc(X0 & " << hexu(C[pc + 3 + R]) << ")";
+          o << (R < 3 ? ", " : "};\n");
+        }
+        o << "      uint32_t Lm, Hm;\n      ipow_planes(e0, eR, " << hexu(sr >> 16) << ", Lm, Hm);\n"
+          << "      apply_ipow(v, Lm, Hm);\n";
+        if (nrot) {
+          uint32_t rreg = 0;
+          o << "      double2 g = make_double2(1, 0);\n"
+            << "      double2 d[4] = {make_double2(1, 0), make_double2(1, 0), make_double2(1, 0), make_double2(1, 0)};\n";
+          for (int r = 0; r < nrot; r++) {
+            const uint32_t rw = C[pc + 8 + 2 * nterm + r];
+            const int xa = rw & 31, k = rw >> 8;
+            if (xa >= 8 && xa < 12) {
+              o << "      g = cmul(g, cs[" << 2 * k << "]);\n      d[" << xa - 8 << "] = cmul(d[" << xa - 8
+                << "], cdiv(cs[" << 2 * k + 1 << "], cs[" << 2 * k << "]));\n";
+              rreg |= 1u << (xa - 8);
+            } else {
+              o << "      g = cmul(g, ((X0 >> " << xa << ") & 1u) ? cs[" << 2 * k + 1 << "] : cs[" << 2 * k << "]);\n";
+            }
+          }
+          o << "      apply_rot(v, g, d, " << rreg << "u);\n";
+        }
+        o << "    }\n";
+        pc += 8 + 2 * nterm + nrot;
+        continue;
+      }
+      pc++;
+      const int m = (ow >> 4) & 15;
+      const int xa = (ow >> 9) & 31, k = (int)(ow >> 16);
+      if (m >= 8) {
+        const int R = m - 8;
+        if (kind == fs::MC_H) {
+          o << "    reg_h<" << R << ">(v);\n";
+        } else if (kind == fs::MC_CX) {
+          if (xa >= 8 && xa < 12) o << "    reg_cx<" << R << ">(v, 0, " << xa - 8 << ", tid, 0);\n";
+          else o << "    if ((X0 >> " << xa << ") & 1u) reg_cx<" << R << ">(v, 3, 1, tid, 0);\n";
+        } else {
+          o << "    reg_expand<" << R << ">(v, cs[" << 2 * k << "], cs[" << 2 * k + 1 << "]);\n";
+        }
+        continue;
+      }
+      const char* pre = m < 5 ? "xlane_" : "xsmem_";
+      const std::string Targ = m < 5 ? "" : "T, ";
+      if (kind == fs::MC_H) o << "    " << pre << "h(v, " << Targ << "tid, " << m << ");\n";
+      else if (kind == fs::MC_CX)
+        o << "    " << pre << "cx(v, " << Targ << (m < 5 ? "" : "tid, ") << m << ", cx_ctl_mask(" << xa << ", X0));\n";
+      else
+        o << "    " << pre << "exp(v, " << Targ << "tid, " << m << ", cs[" << 2 * k << "], cs[" << 2 * k + 1 << "]);\n";
+    }
+    for (int j = 0; j < fs::kTileElems; j++) o << "    A[base | dep_lo_f | " << hexu(D.dep_hi_f[j]) << "] = v[" << j << "];\n";
+    o << "  }\n}\n";
+  }
+  return o.str();
+}
+
+int ensure_pass_jit(fs_prog* p) {
+  if (p->pass_jit == 1) return FS_OK;
+  if (p->pass_jit == -1) return FS_ERR_ARG;
+  p->pass_jit = -1;
+  const HbmPlan& PL = p->hplan;
+  const std::string src = gen_pass_source(PL);
+  // one module per distinct source per process (tests and benches create many programs)
+  static std::mutex mu;
+  static std::map<std::string, fsjit::CUmodule> cache;
+  std::lock_guard<std::mutex> g(mu);
+  fsjit::Api& J = fsjit::api();
+  fsjit::CUmodule mod = nullptr;
+  auto it = cache.find(src);
+  if (it != cache.end()) {
+    mod = it->second;
+  } else {
+    fsjit::Compiled c;
+    std::string err = fsjit::compile(src, fsjit::self_dir() + "/../csrc", c, "fs_pass_0");
+    if (!err.empty()) { p->pass_jit_err = err; return FS_ERR_ARG; }
+    mod = c.mod;
+    cache[src] = mod;
+  }
+  p->pass_fn.assign(PL.passes.size(), nullptr);
+  for (size_t i = 0; i < PL.passes.size(); i++) {
+    const std::string name = "fs_pass_" + std::to_string(i);
+    if (J.cuModuleGetFunction(&p->pass_fn[i], mod, name.c_str()) != 0) { p->pass_jit_err = "missing " + name; return FS_ERR_ARG; }
+    const int smem = (16 << fs::kTileBits) + 32 * std::max(PL.passes[i].nconst, 1);
+    if (J.cuFuncSetAttribute(p->pass_fn[i], 8, smem) != 0) { p->pass_jit_err = "cuFuncSetAttribute"; return FS_ERR_ARG; }
+  }
+  p->pass_jit = 1;
+  return FS_OK;
+}
+
 // ------------------------------------------------------------------ large-k engine driver
 int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   const fs::DevProg& dp = p->dp;
@@ -1297,6 +1454,7 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   if (rc0) return rc0;
   const HbmPlan& PL = p->hplan;
   const size_t pass_smem = fs::kPassSmem;
+  const bool use_pass_jit = !PL.passes.empty() && !getenv("FS_HBM_NO_JIT") && ensure_pass_jit(p) == FS_OK;
   if (!PL.passes.empty())
     FS_CUDA_TRY(cudaFuncSetAttribute(fs::hbm_fused_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem));
   for (uint64_t batch0 = 0; batch0 < a.nshots; batch0 += B) {
@@ -1327,8 +1485,18 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
           const uint64_t ntiles = 1ull << PL.passes[st.pass].nbase;
           const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(ntiles, std::max<uint64_t>(1, 4096 / nb)));
           kt_begin(p, stream);
-          fs::hbm_fused_pass_kernel<<<dim3((unsigned)gx, (unsigned)nb), fs::kTileThreads, pass_smem, stream>>>(
-              H, PL.passes[st.pass], p->d_code, p->d_consts, W);
+          if (use_pass_jit) {
+            const fs::PassConst* cp = p->d_consts;
+            uint32_t Wv = W;
+            void* args[] = {&H, &cp, &Wv};
+            const int smem = (16 << fs::kTileBits) + 32 * std::max(PL.passes[st.pass].nconst, 1);
+            if (fsjit::api().cuLaunchKernel(p->pass_fn[st.pass], (unsigned)gx, (unsigned)nb, 1, fs::kTileThreads, 1, 1,
+                                            (unsigned)smem, stream, args, nullptr) != 0)
+              return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_pass) failed");
+          } else {
+            fs::hbm_fused_pass_kernel<<<dim3((unsigned)gx, (unsigned)nb), fs::kTileThreads, pass_smem, stream>>>(
+                H, PL.passes[st.pass], p->d_code, p->d_consts, W);
+          }
           kt_end(p, stream);
           p->launches++;
           FS_CUDA_TRY(cudaGetLastError());

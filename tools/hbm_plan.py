@@ -21,3 +21,10 @@ for ps, k, la, lb, dr in ops:
 print(n, dict(c))
 runs = [dr for *_, dr in ops if dr > 0]
 print('diag runs', len(runs), 'mean len', np.mean(runs), 'hist', np.bincount(runs)[:20])
+m = collections.Counter()
+for ps, k, la, lb, dr in ops:
+    if k in (0, 3, 6):
+        mm = lb if k == 3 else la
+        if mm < 8:
+            m[int(mm)] += 1
+print('exchanges by thread bit', sorted(m.items()))
