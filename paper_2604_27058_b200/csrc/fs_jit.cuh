@@ -618,6 +618,12 @@ inline std::string compile(const std::string& src, const std::string& incdir, Co
                            const char* kname = "fs_jit_frame") {
   Api& A = api();
   if (!A.ok) return "JIT unavailable: " + A.why;
+  if (const char* dump = getenv("FS_JIT_DUMP")) {  // debugging: keep the generated source
+    if (FILE* f = fopen((std::string(dump) + "/" + kname + ".cu").c_str(), "w")) {
+      fwrite(src.data(), 1, src.size(), f);
+      fclose(f);
+    }
+  }
   void* prog = nullptr;
   if (A.nvrtcCreateProgram(&prog, src.c_str(), (std::string(kname) + ".cu").c_str(), 0, nullptr, nullptr) != 0)
     return "nvrtcCreateProgram failed";
