@@ -297,6 +297,40 @@ __device__ __forceinline__ void xsmem_exp(double2 (&v)[kTileElems], double2* T, 
   __syncthreads();
 }
 
+// ---- half-buffer warp-bit exchanges (the specialised pass kernels keep a 64 KiB staging buffer
+// for the next tile, so the exchange goes through 32 KiB in two rounds of 8 elements)
+template <int OP>  // 0 = H, 1 = CX (mask cm), 2 = Expand (ph0, ph1)
+__device__ __forceinline__ void xsmem_half(double2 (&v)[kTileElems], double2* T, uint32_t tid, int m, uint32_t cm,
+                                           double2 ph0, double2 ph1) {
+  const uint32_t pt = tid ^ (1u << m);
+  const bool mb = (tid >> m) & 1u;
+  const double sg = mb ? -1.0 : 1.0;
+  const double2 ph = mb ? ph1 : ph0;
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+#pragma unroll
+    for (int j = 0; j < kTileElems / 2; j++) T[tid + kTileThreads * j] = v[8 * h + j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kTileElems / 2; j++) {
+      const double2 pv = T[pt + kTileThreads * j];
+      double2& x = v[8 * h + j];
+      if (OP == 0) x = make_double2(__dmul_rn(__fma_rn(sg, x.x, pv.x), kInvSqrt2), __dmul_rn(__fma_rn(sg, x.y, pv.y), kInvSqrt2));
+      else if (OP == 1) { if ((cm >> (8 * h + j)) & 1u) x = pv; }
+      else x = cmul(mb ? pv : x, ph);
+    }
+    __syncthreads();
+  }
+}
+
+// 16-byte asynchronous global -> shared copy (L2 only), and the wait for this thread's copies
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 __global__ void __launch_bounds__(kTileThreads, 2) hbm_fused_pass_kernel(HbmState H, const PassDesc D,
                                                                         const uint32_t* __restrict__ code,
                                                                         const PassConst* __restrict__ consts,

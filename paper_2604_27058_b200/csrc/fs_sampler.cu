@@ -1435,11 +1435,13 @@ std::string gen_pass_source(const HbmPlan& PL) {
   };
   for (size_t pi = 0; pi < PL.passes.size(); pi++) {
     const fs::PassDesc& D = PL.passes[pi];
+    // smem: exchange half-buffer (32 KiB) | next-tile staging (64 KiB) | resolved constants
     o << "extern \"C\" __global__ void __launch_bounds__(256, 2) fs_pass_" << pi
       << "(HbmState H, const PassConst* __restrict__ consts, uint32_t W) {\n"
       << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
       << "  double2* T = reinterpret_cast<double2*>(smem_raw);\n"
-      << "  double2* cs = reinterpret_cast<double2*>(smem_raw + " << (16 << fs::kTileBits) << ");\n"
+      << "  double2* Sg = reinterpret_cast<double2*>(smem_raw + " << (8 << fs::kTileBits) << ");\n"
+      << "  double2* cs = reinterpret_cast<double2*>(smem_raw + " << (24 << fs::kTileBits) << ");\n"
       << "  const uint32_t shot = blockIdx.y, w = shot >> 5, bit = 1u << (shot & 31);\n"
       << "  if (!(H.alive[w] & bit)) return;\n"
       << "  const uint32_t tid = threadIdx.x;\n";
@@ -1454,14 +1456,32 @@ std::string gen_pass_source(const HbmPlan& PL) {
     for (int i = 0; i < 8; i++) o << " | (((tid >> " << i << ") & 1u) << " << (int)D.T[i] << ")";
     o << ";\n  const uint32_t dep_lo_f = 0u";
     for (int i = 0; i < 8; i++) o << " | (((tid >> " << i << ") & 1u) << " << (int)D.Tf[i] << ")";
+    auto deposit = [&](const char* t) {
+      std::ostringstream d;
+      d << "0ull";
+      for (int i = 0; i < D.nbase; i++) d << " | ((uint64_t)((" << t << " >> " << i << ") & 1u) << " << (int)D.base[i] << ")";
+      return d.str();
+    };
+    auto prefetch = [&](const char* basevar) {  // this thread's 16 elements of a tile -> its Sg slots
+      for (int j = 0; j < fs::kTileElems; j++)
+        o << "      cp_async16(Sg + tid + " << 256 * j << ", A + (" << basevar << " | dep_lo | " << hexu(D.dep_hi[j]) << "));\n";
+      o << "      cp_async_commit();\n";
+    };
     o << ";\n  __syncthreads();\n"
       << "  double2* __restrict__ A = H.amps + (size_t)shot * H.cap;\n"
       << "  double2 v[16];\n"
-      << "  for (uint32_t ti = blockIdx.x; ti < " << (1u << D.nbase) << "u; ti += gridDim.x) {\n"
-      << "    const uint64_t base = 0ull";
-    for (int i = 0; i < D.nbase; i++) o << " | ((uint64_t)((ti >> " << i << ") & 1u) << " << (int)D.base[i] << ")";
-    o << ";\n    const uint32_t X0 = tid | (ti << " << fs::kTileBits << ");\n";
-    for (int j = 0; j < fs::kTileElems; j++) o << "    v[" << j << "] = A[base | dep_lo | " << hexu(D.dep_hi[j]) << "];\n";
+      << "  const uint32_t NT = " << (1u << D.nbase) << "u;\n"
+      << "  if (blockIdx.x < NT) {\n    const uint64_t b0 = " << deposit("blockIdx.x") << ";\n";
+    prefetch("b0");
+    o << "  }\n"
+      << "  for (uint32_t ti = blockIdx.x; ti < NT; ti += gridDim.x) {\n"
+      << "    const uint64_t base = " << deposit("ti") << ";\n"
+      << "    const uint32_t X0 = tid | (ti << " << fs::kTileBits << ");\n"
+      << "    cp_async_wait_all();\n";
+    for (int j = 0; j < fs::kTileElems; j++) o << "    v[" << j << "] = Sg[tid + " << 256 * j << "];\n";
+    o << "    if (ti + gridDim.x < NT) {\n      const uint32_t tn = ti + gridDim.x;\n      const uint64_t bn = " << deposit("tn") << ";\n";
+    prefetch("bn");
+    o << "    }\n";
     const uint32_t* C = PL.code.data() + D.code_off;
     for (int pc = 0; pc < D.ncode;) {
       const uint32_t ow = C[pc];
@@ -1523,13 +1543,15 @@ std::string gen_pass_source(const HbmPlan& PL) {
         }
         continue;
       }
-      const char* pre = m < 5 ? "xlane_" : "xsmem_";
-      const std::string Targ = m < 5 ? "" : "T, ";
-      if (kind == fs::MC_H) o << "    " << pre << "h(v, " << Targ << "tid, " << m << ");\n";
-      else if (kind == fs::MC_CX)
-        o << "    " << pre << "cx(v, " << Targ << (m < 5 ? "" : "tid, ") << m << ", cx_ctl_mask(" << xa << ", X0));\n";
-      else
-        o << "    " << pre << "exp(v, " << Targ << "tid, " << m << ", cs[" << 2 * k << "], cs[" << 2 * k + 1 << "]);\n";
+      if (m < 5) {
+        if (kind == fs::MC_H) o << "    xlane_h(v, tid, " << m << ");\n";
+        else if (kind == fs::MC_CX) o << "    xlane_cx(v, " << m << ", cx_ctl_mask(" << xa << ", X0));\n";
+        else o << "    xlane_exp(v, tid, " << m << ", cs[" << 2 * k << "], cs[" << 2 * k + 1 << "]);\n";
+      } else {
+        if (kind == fs::MC_H) o << "    xsmem_half<0>(v, T, tid, " << m << ", 0u, make_double2(1, 0), make_double2(1, 0));\n";
+        else if (kind == fs::MC_CX) o << "    xsmem_half<1>(v, T, tid, " << m << ", cx_ctl_mask(" << xa << ", X0), make_double2(1, 0), make_double2(1, 0));\n";
+        else o << "    xsmem_half<2>(v, T, tid, " << m << ", 0u, cs[" << 2 * k << "], cs[" << 2 * k + 1 << "]);\n";
+      }
     }
     for (int j = 0; j < fs::kTileElems; j++) o << "    A[base | dep_lo_f | " << hexu(D.dep_hi_f[j]) << "] = v[" << j << "];\n";
     o << "  }\n}\n";
@@ -1563,7 +1585,7 @@ int ensure_pass_jit(fs_prog* p) {
   for (size_t i = 0; i < PL.passes.size(); i++) {
     const std::string name = "fs_pass_" + std::to_string(i);
     if (J.cuModuleGetFunction(&p->pass_fn[i], mod, name.c_str()) != 0) { p->pass_jit_err = "missing " + name; return FS_ERR_ARG; }
-    const int smem = (16 << fs::kTileBits) + 32 * std::max(PL.passes[i].nconst, 1);
+    const int smem = (24 << fs::kTileBits) + 32 * std::max(PL.passes[i].nconst, 1);
     if (J.cuFuncSetAttribute(p->pass_fn[i], 8, smem) != 0) { p->pass_jit_err = "cuFuncSetAttribute"; return FS_ERR_ARG; }
   }
   p->pass_jit = 1;
@@ -1678,7 +1700,7 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
             const fs::PassConst* cp = p->d_consts;
             uint32_t Wv = W;
             void* args[] = {&H, &cp, &Wv};
-            const int smem = (16 << fs::kTileBits) + 32 * std::max(PL.passes[st.pass].nconst, 1);
+            const int smem = (24 << fs::kTileBits) + 32 * std::max(PL.passes[st.pass].nconst, 1);
             if (fsjit::api().cuLaunchKernel(p->pass_fn[st.pass], (unsigned)gx, (unsigned)nb, 1, fs::kTileThreads, 1, 1,
                                             (unsigned)smem, stream, args, nullptr) != 0)
               return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_pass) failed");
