@@ -810,10 +810,12 @@ int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector
   std::vector<int> begins;
   for (size_t s = 0; s + 1 < bounds.size(); s++) {
     const int karr = karrs[s];
-    // CTA-per-shot segments only: measured 1.2-1.8x faster specialised; the warp-per-shot ones
-    // ran ~2x slower specialised than interpreted (code size / scheduling) and keep the interpreter
-    if (karr < block_k || karr <= 10) continue;
-    gen_segment(o, p, bounds[s], bounds[s + 1], karr, 256);
+    // CTA-per-shot segments only: measured 1.2-1.8x faster specialised.  The warp-per-shot ones
+    // ran ~2x slower specialised than interpreted (instruction-fetch stalls: every scalar run and
+    // measurement inlines the scalar VM; out-of-line calls cost more than they saved) and keep
+    // the interpreter unless FS_BLOCK_JIT_WARP is set
+    if (karr < block_k || (karr <= 10 && !getenv("FS_BLOCK_JIT_WARP"))) continue;
+    gen_segment(o, p, bounds[s], bounds[s + 1], karr, karr <= 10 ? 32 : 256);
     begins.push_back(bounds[s]);
   }
   if (begins.empty()) { p->seg_jit = 1; return FS_OK; }
