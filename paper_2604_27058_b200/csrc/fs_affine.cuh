@@ -1,0 +1,538 @@
+// fs_affine.cuh -- host side of the affine frame kernel (frame-only programs, Philox stream).
+//
+// A frame-only program (k_max = 0: FrameGates, MeasDormantStatic/Random, CondFrame, NoiseBlock,
+// Detector/Observable/PostSelect; runtime.py:130-151, :296-330, :546-641) is an affine map over
+// GF(2) from (coins, fault indicators) to the output bits: every frame update is an XOR, the
+// x<->z swap of MeasDormantRandom and H/SWAP are permutations, and CondFrame XORs a record (itself
+// affine) into the frame.  So, per output row r,
+//
+//     bit_r = const_r  XOR  (XOR of the coins in C_r)  XOR  (XOR over faults f of [r in rows(f)]),
+//
+// where rows(f) is the set of output rows a single Pauli fault of that case at that site flips
+// (its propagation through the rest of the program).  The generator finds const_r, C_r and
+// rows(site, case) by propagating one symbolic source per constant / coin / (site, qubit, X|Z)
+// element through the program with bitsets, and emits a kernel that never simulates the frame:
+//
+//   * a warp owns a group of kAffGroup = 8 consecutive 32-shot words (one 32-byte sector of
+//     every output row) and a shared-memory row buffer B[row][8] for them;
+//   * faults: for each word of the group the 32 lanes evaluate 32 consecutive steps of that
+//     word's noise stream at once (WordFaultGen's process -- the engine stream, so every engine
+//     draws the same faults: one Philox block per step, geometric gap floor(ln(U) / log1p(-q)),
+//     thinning, case pick), place them with a warp prefix sum of the gaps, and XOR each fault's
+//     lane bit into its rows with shared atomics;
+//   * outputs: lanes 0..7 (one word each) draw their coin words and write every row once as
+//     (const ^ coins ^ B[row]) & alive, in program order, so PostSelect reads the full noisy bit
+//     and masks later rows exactly like the interpreter (fs_frame.cuh).
+#pragma once
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
+
+namespace fsjit {
+
+constexpr int kAffGroup = 8;              // 32-shot words per warp group (one 32 B sector per row)
+constexpr int kAffMaxCoins = 128;         // coin words kept in registers
+constexpr size_t kAffMaxTerms = 1 << 16;  // coin XOR terms over all rows (code size)
+
+struct AffineKernelSource {
+  std::string src;
+  std::vector<uint32_t> tables;  // fault tables (case rows, site -> class/case, classes), 16 B sections
+  bool tables_smem = false;      // copied into shared memory by every block (else read from HBM/L1)
+  int nrows = 0;                 // row-buffer rows per word (+ one zero row)
+  int threads = 0;               // block size
+  size_t smem = 0;
+  std::string why;  // non-empty: not applicable
+};
+
+inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const std::vector<int32_t>& ins_all,
+                                                  const std::vector<uint32_t>& gates,
+                                                  const std::vector<uint32_t>& paulis,
+                                                  const std::vector<int32_t>& reclists,
+                                                  const std::vector<int32_t>& record_out,
+                                                  const std::vector<int32_t>& bit_slot,
+                                                  const std::vector<int32_t>& case_pauli_off,
+                                                  const std::vector<int32_t>& site_case_off,
+                                                  const std::vector<double>& site_prob,
+                                                  const std::vector<double>& case_cum, size_t smem_budget) {
+  AffineKernelSource K;
+  const int n = d.n, R = d.record_count, U = d.num_user_records, D = d.num_detectors, E = d.num_sites;
+  (void)bit_slot;
+  if (d.k_max != 0) { K.why = "not frame-only"; return K; }
+  // ---- rows: user records (col), detectors, one per ObservableIns, hidden bits read by PostSelect
+  int n_obs_ins = 0, n_coins = 0;
+  std::vector<int> psel_bits;
+  for (int i = 0; i < d.num_instrs; i++) {
+    const int* I = ins_all.data() + (size_t)i * FS_INS_WORDS;
+    const int op = FS_OPCODE(I[0]);
+    if (op == FS_OP_OBSERVABLE) n_obs_ins++;
+    if (op == FS_OP_POSTSELECT) psel_bits.push_back(I[1] == 0 ? R + I[2] : I[2]);
+    if (op == FS_OP_MEAS_DRANDOM) n_coins = std::max(n_coins, I[2] + 1);
+    if (op != FS_OP_FRAME && op != FS_OP_MEAS_DSTATIC && op != FS_OP_MEAS_DRANDOM && op != FS_OP_COND_FRAME &&
+        op != FS_OP_NOISE && op != FS_OP_DETECTOR && op != FS_OP_OBSERVABLE && op != FS_OP_POSTSELECT &&
+        op != FS_OP_GAMMA_ROT) {
+      K.why = "array instruction";
+      return K;
+    }
+  }
+  if (n_coins > kAffMaxCoins) { K.why = "too many coins"; return K; }
+  // buffer rows: user records [0, U), detectors [U4, U4 + D), ObservableIns rows from U4 + D4,
+  // then hidden bits read by PostSelect (U4, D4 = U, D rounded up to 4: the copy-out writes 4 rows
+  // of one kind per instruction)
+  const int U4 = (U + 3) & ~3, D4 = (D + 3) & ~3;
+  std::vector<int> bit_row(R + D, -1);  // record / detector id -> buffer row
+  for (int r = 0; r < R; r++)
+    if (record_out[r] >= 0) bit_row[r] = record_out[r];
+  for (int j = 0; j < D; j++) bit_row[R + j] = U4 + j;
+  int nrows = U4 + D4 + n_obs_ins;
+  for (int b : psel_bits)
+    if (bit_row[b] < 0) bit_row[b] = nrows++;
+  if (nrows >= 8192) { K.why = "too many output rows"; return K; }
+  // ---- sources: 0 = constant 1, 1..n_coins = coin ords, then one per (site, qubit, X|Z) element
+  const int el0 = 1 + n_coins;
+  std::vector<int> site_el0(E + 1, 0);
+  std::vector<uint32_t> el_pauli;                   // element -> pauli entry (q << 1 | z)
+  std::vector<int> case_el(paulis.size() + 1, -1);  // per pauli entry: element id
+  for (int s = 0; s < E; s++) {
+    site_el0[s] = (int)el_pauli.size();
+    std::map<uint32_t, int> m;
+    for (int c = site_case_off[s]; c < site_case_off[s + 1]; c++)
+      for (int j = case_pauli_off[c]; j < case_pauli_off[c + 1]; j++) {
+        auto it = m.find(paulis[j]);
+        if (it == m.end()) {
+          it = m.emplace(paulis[j], (int)el_pauli.size()).first;
+          el_pauli.push_back(paulis[j]);
+        }
+        case_el[j] = it->second;
+      }
+  }
+  site_el0[E] = (int)el_pauli.size();
+  const size_t NE = el_pauli.size(), NS = el0 + NE, NW = (NS + 63) / 64;
+  if ((double)(2 * n + R + D + nrows) * NW * 8 > 2e9) { K.why = "fault-effect table too large"; return K; }
+  // ---- symbolic propagation: frame slots and records as bitsets over sources
+  std::vector<uint64_t> fr((size_t)2 * n * NW, 0), rec((size_t)(R + D) * NW, 0), rowb((size_t)nrows * NW, 0);
+  auto S = [&](int slot) { return fr.data() + (size_t)slot * NW; };
+  auto RB = [&](int b) { return rec.data() + (size_t)b * NW; };
+  auto xr = [&](uint64_t* a, const uint64_t* b) { for (size_t t = 0; t < NW; t++) a[t] ^= b[t]; };
+  auto tog = [&](uint64_t* a, size_t src) { a[src >> 6] ^= 1ull << (src & 63); };
+  int obs_row = U4 + D4;
+  for (int i = 0; i < d.num_instrs; i++) {
+    const int* I = ins_all.data() + (size_t)i * FS_INS_WORDS;
+    const bool flip = FS_FLIP(I[0]);
+    switch (FS_OPCODE(I[0])) {
+      case FS_OP_FRAME:
+        for (int j = 0; j < I[2]; j++) {
+          const uint32_t g = gates[I[1] + j];
+          const int a = FS_GATE_A(g), b = FS_GATE_B(g);
+          switch (FS_GATE_G(g)) {
+            case FS_G_H: std::swap_ranges(S(a), S(a) + NW, S(n + a)); break;
+            case FS_G_S: case FS_G_SDAG: xr(S(n + a), S(a)); break;
+            case FS_G_CX: xr(S(b), S(a)); xr(S(n + a), S(n + b)); break;
+            case FS_G_CZ: xr(S(n + b), S(a)); xr(S(n + a), S(b)); break;
+            case FS_G_SWAP:
+              std::swap_ranges(S(a), S(a) + NW, S(b));
+              std::swap_ranges(S(n + a), S(n + a) + NW, S(n + b));
+              break;
+            default: break;
+          }
+        }
+        break;
+      case FS_OP_MEAS_DSTATIC:  // record = x ^ flip
+        std::copy(S(I[1]), S(I[1]) + NW, RB(I[3]));
+        if (flip) tog(RB(I[3]), 0);
+        break;
+      case FS_OP_MEAS_DRANDOM: {  // record = coin ^ z ^ flip; x' = z ^ coin, z' = x
+        const int v = I[1];
+        tog(S(n + v), 1 + I[2]);
+        std::copy(S(n + v), S(n + v) + NW, RB(I[3]));
+        if (flip) tog(RB(I[3]), 0);
+        std::swap_ranges(S(v), S(v) + NW, S(n + v));
+        break;
+      }
+      case FS_OP_COND_FRAME:
+        for (int j = I[1]; j < I[1] + I[2]; j++) {
+          const uint32_t e = paulis[j];
+          xr(S(FS_PAULI_Z(e) ? n + FS_PAULI_Q(e) : FS_PAULI_Q(e)), RB(I[3]));
+        }
+        break;
+      case FS_OP_NOISE:
+        for (int s = I[1]; s < I[2]; s++)
+          for (int el = site_el0[s]; el < site_el0[s + 1]; el++) {
+            const uint32_t e = el_pauli[el];
+            tog(S(FS_PAULI_Z(e) ? n + FS_PAULI_Q(e) : FS_PAULI_Q(e)), el0 + el);
+          }
+        break;
+      case FS_OP_DETECTOR:
+      case FS_OP_OBSERVABLE: {
+        std::vector<uint64_t> v(NW, 0);
+        for (int j = 0; j < I[3]; j++) xr(v.data(), RB(reclists[I[2] + j]));
+        if (FS_OPCODE(I[0]) == FS_OP_DETECTOR) std::copy(v.begin(), v.end(), RB(R + I[1]));
+        else std::copy(v.begin(), v.end(), rowb.data() + (size_t)(obs_row++) * NW);
+        break;
+      }
+      default: break;
+    }
+  }
+  for (int b = 0; b < R + D; b++)
+    if (bit_row[b] >= 0) std::copy(RB(b), RB(b) + NW, rowb.data() + (size_t)bit_row[b] * NW);
+  // ---- sparser rows by differencing: a copied-out row r may be stored as y_r = v_r ^ v_p for a
+  // parent row p in an earlier 4-row chunk of the copy-out (p < (r & ~3)); the copy-out then
+  // rebuilds v_r = B[r] ^ v_p in order.  For memory experiments the record of ancilla a in round t
+  // differs from its round t-1 record by one detector's worth of faults, so record rows shrink
+  // to about the size of detector rows.  Rows read before the copy-out (PostSelect, observables)
+  // are never differenced.
+  std::vector<int> parent(nrows, -1);
+  {
+    std::vector<uint8_t> fixed_row(nrows, 0);
+    for (int r = U4 + D4; r < nrows; r++) fixed_row[r] = 1;
+    for (int b : psel_bits) fixed_row[bit_row[b]] = 1;
+    auto el_count = [&](const uint64_t* v) {
+      size_t c = 0;
+      for (size_t t = 0; t < NW; t++) {
+        uint64_t m = v[t];
+        if (t * 64 < (size_t)el0) m &= (el0 - t * 64 >= 64) ? 0ull : (~0ull << (el0 - t * 64));
+        c += __builtin_popcountll(m);
+      }
+      return c;
+    };
+    std::vector<std::vector<int>> orows(NE);  // element -> rows (original vectors)
+    std::vector<size_t> sz(nrows);
+    for (int r = 0; r < nrows; r++) {
+      const uint64_t* v = rowb.data() + (size_t)r * NW;
+      sz[r] = el_count(v);
+      for (size_t t = 0; t < NW; t++)
+        for (uint64_t m = v[t]; m; m &= m - 1) {
+          const size_t src = t * 64 + __builtin_ctzll(m);
+          if (src >= (size_t)el0) orows[src - el0].push_back(r);
+        }
+    }
+    std::vector<int> ov(nrows, 0);
+    std::vector<int> cand;
+    const bool nodiff = getenv("FS_AFF_NO_DIFF") != nullptr;
+    std::vector<uint64_t> y((size_t)nrows * NW);
+    std::copy(rowb.begin(), rowb.end(), y.begin());
+    for (int r = 0; r < nrows && !nodiff; r++) {
+      if (fixed_row[r] || sz[r] == 0) continue;
+      const uint64_t* v = rowb.data() + (size_t)r * NW;
+      cand.clear();
+      for (size_t t = 0; t < NW; t++)
+        for (uint64_t m = v[t]; m; m &= m - 1) {
+          const size_t src = t * 64 + __builtin_ctzll(m);
+          if (src < (size_t)el0) continue;
+          for (int q : orows[src - el0]) {
+            if (q >= (r & ~3)) break;
+            if (ov[q]++ == 0) cand.push_back(q);
+          }
+        }
+      int best = -1;
+      size_t bsz = sz[r];
+      for (int q : cand) {
+        const size_t dsz = sz[r] + sz[q] - 2 * (size_t)ov[q];
+        if (dsz < bsz) { bsz = dsz; best = q; }
+        ov[q] = 0;
+      }
+      if (best >= 0) {
+        parent[r] = best;
+        uint64_t* yr = y.data() + (size_t)r * NW;
+        xr(yr, rowb.data() + (size_t)best * NW);
+      }
+    }
+    rowb.swap(y);
+  }
+  // ---- transpose: element -> rows; case -> XOR of its elements' rows
+  std::vector<std::vector<uint16_t>> el_rows(NE);
+  for (int r = 0; r < nrows; r++) {
+    const uint64_t* v = rowb.data() + (size_t)r * NW;
+    for (size_t t = 0; t < NW; t++)
+      for (uint64_t m = v[t]; m; m &= m - 1) {
+        const size_t src = t * 64 + __builtin_ctzll(m);
+        if (src >= (size_t)el0) el_rows[src - el0].push_back((uint16_t)r);
+      }
+  }
+  std::vector<uint32_t> crow_off(d.num_cases + 1, 0);
+  std::vector<uint16_t> crows;
+  std::vector<uint8_t> par(nrows, 0);
+  std::vector<uint16_t> touched;
+  for (int c = 0; c < d.num_cases; c++) {
+    crow_off[c] = (uint32_t)crows.size();
+    touched.clear();
+    for (int j = case_pauli_off[c]; j < case_pauli_off[c + 1]; j++) {
+      if (case_el[j] < 0) continue;
+      for (uint16_t r : el_rows[case_el[j]]) {
+        touched.push_back(r);
+        par[r] ^= 1;
+      }
+    }
+    std::sort(touched.begin(), touched.end());
+    touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+    for (uint16_t r : touched) {  // stored as the row's buffer slot for word 0: slot(r, wi) = e ^ wi
+      if (par[r]) crows.push_back((uint16_t)(r * 8 | ((r >> 2) & 7)));
+      par[r] = 0;
+    }
+  }
+  crow_off[d.num_cases] = (uint32_t)crows.size();
+  // ---- site classes: sites with identical (p, case_cum) share one entry of the case-pick table
+  int cw = 1;  // case_cum width per class
+  for (int st = 0; st < E; st++) cw = std::max(cw, site_case_off[st + 1] - site_case_off[st]);
+  std::map<std::vector<uint64_t>, int> cls_of;
+  std::vector<std::vector<double>> cls_cum;
+  std::vector<double> cls_prob;
+  std::vector<int32_t> cls_nc;
+  std::vector<uint16_t> site_cls(E);
+  for (int st = 0; st < E; st++) {
+    std::vector<uint64_t> key;
+    auto bits = [](double v) { uint64_t u; memcpy(&u, &v, 8); return u; };
+    key.push_back(bits(site_prob[st]));
+    for (int c = site_case_off[st]; c < site_case_off[st + 1]; c++) key.push_back(bits(case_cum[c]));
+    auto it = cls_of.find(key);
+    if (it == cls_of.end()) {
+      it = cls_of.emplace(key, (int)cls_prob.size()).first;
+      cls_prob.push_back(site_prob[st]);
+      cls_nc.push_back(site_case_off[st + 1] - site_case_off[st]);
+      std::vector<double> cc(cw, 0.0);
+      for (int c = site_case_off[st]; c < site_case_off[st + 1]; c++) cc[c - site_case_off[st]] = case_cum[c];
+      cls_cum.push_back(cc);
+    }
+    site_cls[st] = (uint16_t)it->second;
+  }
+  if (cls_prob.size() >= 65535) { K.why = "too many site classes"; return K; }
+  // ---- table blob (u32 words, 16 B sections): crows u16 | crow_off u16 or u32 | site_case u32 |
+  // site_cls u16 | cls_nc i32 | cls_prob f64 | cls_cum f64 [ncls][cw]
+  const bool off16 = crows.size() < 65536;
+  const int ncls = (int)cls_prob.size();
+  auto& T = K.tables;
+  auto sec = [&](size_t bytes) {
+    size_t w = T.size();
+    T.resize(w + ((bytes + 15) / 16) * 4 + 4, 0u);  // +16 B keeps empty sections distinct
+    return w;
+  };
+  const size_t o_crows = sec(crows.size() * 2);
+  memcpy(T.data() + o_crows, crows.data(), crows.size() * 2);
+  const size_t o_coff = sec(crow_off.size() * (off16 ? 2 : 4));
+  if (off16) {
+    std::vector<uint16_t> c16(crow_off.begin(), crow_off.end());
+    memcpy(T.data() + o_coff, c16.data(), c16.size() * 2);
+  } else {
+    memcpy(T.data() + o_coff, crow_off.data(), crow_off.size() * 4);
+  }
+  const size_t o_scase = sec((size_t)E * 4);
+  if (E) memcpy(T.data() + o_scase, site_case_off.data(), (size_t)E * 4);
+  const size_t o_scls = sec((size_t)E * 2);
+  if (E) memcpy(T.data() + o_scls, site_cls.data(), (size_t)E * 2);
+  const size_t o_cnc = sec((size_t)ncls * 4);
+  if (ncls) memcpy(T.data() + o_cnc, cls_nc.data(), (size_t)ncls * 4);
+  const size_t o_cp = sec((size_t)ncls * 8);
+  if (ncls) memcpy(T.data() + o_cp, cls_prob.data(), (size_t)ncls * 8);
+  const size_t o_cc = sec((size_t)ncls * cw * 8);
+  for (int c = 0; c < ncls; c++) memcpy(T.data() + o_cc + (size_t)c * cw * 2, cls_cum[c].data(), (size_t)cw * 8);
+  const size_t o_ln = sec(FS_LN_TAB_ENTRIES * 16);
+  {
+    static const double lt[FS_LN_TAB_ENTRIES][2] = FS_LN_TAB_INIT;
+    memcpy(T.data() + o_ln, lt, sizeof lt);
+  }
+  const size_t tbl_bytes = T.size() * 4;
+  // ---- launch shape: 8-word groups, one warp each; row buffer (+ a zero row) and alive masks per warp
+  const int zrow = nrows;
+  K.nrows = nrows + 1;
+  const int nblk = (n_coins + 3) / 4, cstride = n_coins ? (4 * nblk) | 1 : 0;  // coin words per word (odd stride)
+  const size_t per_warp = ((size_t)K.nrows + psel_bits.size() + 1) * kAffGroup * 4 + (size_t)kAffGroup * cstride * 4;
+  {
+    int wps = (int)std::min<size_t>(16, tbl_bytes < smem_budget ? (smem_budget - tbl_bytes) / per_warp : 0);
+    if (const char* e = getenv("FS_AFF_WARPS")) wps = std::min(wps, std::max(1, atoi(e)));
+    K.tables_smem = wps >= 8 && !getenv("FS_AFF_GLOBAL_TABLES");
+    if (!K.tables_smem) {
+      wps = (int)std::min<size_t>(16, smem_budget / per_warp);
+      if (const char* e = getenv("FS_AFF_WARPS")) wps = std::min(wps, std::max(1, atoi(e)));
+    }
+    if (wps < 1) { K.why = "row buffer does not fit shared memory"; return K; }
+    K.threads = wps * 32;
+    K.smem = per_warp * wps + (K.tables_smem ? tbl_bytes : 0);
+  }
+  // noiseless part of a row: constant word and coin list
+  size_t terms = 0;
+  auto row_expr = [&](const uint64_t* v) {
+    std::ostringstream e;
+    e << ((v[0] & 1ull) ? "0xFFFFFFFFu" : "0u");
+    for (int c = 0; c < n_coins; c++)
+      if ((v[(1 + c) >> 6] >> ((1 + c) & 63)) & 1ull) { e << " ^ k" << c; terms++; }
+    return e.str();
+  };
+  if (getenv("FS_AFF_VERBOSE")) {
+    size_t el_total = 0;
+    for (auto& v : el_rows) el_total += v.size();
+    fprintf(stderr,
+            "aff: rows %d coins %d elements %zu element-rows %zu cases %d case-rows %zu classes %d tables %zu B "
+            "(%s) warps %d\n",
+            nrows, n_coins, NE, el_total, d.num_cases, crows.size(), ncls, tbl_bytes,
+            K.tables_smem ? "smem" : "global", K.threads / 32);
+  }
+
+  // ---- kernel source
+  // phase 1 (all lanes): zero the group's row buffer, XOR in the faults of its 8 words
+  // phase 2 (lanes 0..7, lane = word): XOR the noiseless part (constant ^ coins) into the rows
+  //   that have one, evaluate PostSelect / observables in program order, keep the alive mask of
+  //   every post-select segment in AL[seg][word]
+  // phase 3 (all lanes, lane = (row & 3, word)): copy rows out, 4 rows x 8 words (four 32 B
+  //   sectors) per instruction, each masked with the alive mask in effect at its write
+  const int G = kAffGroup, NWARP = K.threads / 32;
+  int npsel = 0;
+  std::vector<int> row_seg(nrows, 0);
+  std::ostringstream p2;
+  {
+    int seg = 0;
+    obs_row = U4 + D4;
+    for (int i = 0; i < d.num_instrs; i++) {
+      const int* I = ins_all.data() + (size_t)i * FS_INS_WORDS;
+      switch (FS_OPCODE(I[0])) {
+        case FS_OP_MEAS_DSTATIC:
+        case FS_OP_MEAS_DRANDOM:
+          if (record_out[I[3]] >= 0) row_seg[record_out[I[3]]] = seg;
+          break;
+        case FS_OP_DETECTOR: row_seg[bit_row[R + I[1]]] = seg; break;
+        case FS_OP_OBSERVABLE: {
+          const int row = obs_row++;
+          p2 << "      ob" << I[1] << " ^= B[" << row * G << " + (lane ^ " << ((row >> 2) & 7) << ")] & alive;\n";
+          break;
+        }
+        case FS_OP_POSTSELECT: {
+          const int bid = I[1] == 0 ? R + I[2] : I[2];
+          const int row = bit_row[bid];
+          p2 << "      alive &= ~((B[" << row * G << " + (lane ^ " << ((row >> 2) & 7) << ")]" << (I[3] ? " ^ 0xFFFFFFFFu" : "")
+             << ") & alive);\n";
+          p2 << "      AL[" << (seg + 1) * G << " + lane] = alive;\n";
+          seg++;
+          break;
+        }
+        default: break;
+      }
+    }
+    npsel = seg;
+  }
+  std::ostringstream o;
+  o << "#include \"fs_jit_kernels.cuh\"\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << K.threads << ", 1) fs_aff_frame(fs::DevProg P, fs::RunArgs A, "
+       "const uint32_t* __restrict__ tbl) {\n";
+  o << "  extern __shared__ __align__(16) uint32_t smem[];\n";
+  o << "  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;\n";
+  size_t bufw = 0;
+  if (K.tables_smem) {
+    bufw = T.size();
+    o << "  for (int i = threadIdx.x; i < " << T.size() / 4 << "; i += " << K.threads
+      << ") reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(tbl) + i);\n";
+    o << "  __syncthreads();\n";
+    o << "  const uint32_t* const tb = smem;\n";
+  } else {
+    o << "  const uint32_t* const tb = tbl;\n";
+  }
+  o << "  fs::AffTabs<" << (off16 ? "true" : "false") << "> tabs;\n";
+  o << "  tabs.crows = reinterpret_cast<const uint16_t*>(tb + " << o_crows << ");\n";
+  o << "  tabs.crow_off = tb + " << o_coff << ";\n";
+  o << "  tabs.site_case = tb + " << o_scase << ";\n";
+  o << "  tabs.site_cls = reinterpret_cast<const uint16_t*>(tb + " << o_scls << ");\n";
+  o << "  tabs.cls_nc = reinterpret_cast<const int*>(tb + " << o_cnc << ");\n";
+  o << "  tabs.cls_prob = reinterpret_cast<const double*>(tb + " << o_cp << ");\n";
+  o << "  tabs.cls_cum = reinterpret_cast<const double*>(tb + " << o_cc << ");\n";
+  o << "  tabs.lntab = reinterpret_cast<const double2*>(tb + " << o_ln << ");\n";
+  o << "  tabs.cw = " << cw << ";\n";
+  o << "  uint32_t* const B = smem + " << bufw << " + wib * " << (size_t)K.nrows * G << ";\n";
+  o << "  uint32_t* const AL = smem + " << bufw + (size_t)NWARP * K.nrows * G << " + wib * " << (npsel + 1) * G << ";\n";
+  o << "  uint32_t* const CW = smem + " << bufw + (size_t)NWARP * (K.nrows + npsel + 1) * G << " + wib * " << G * cstride
+    << ";\n";
+  o << "  const uint64_t word0 = A.shot0 >> 5;\n  const uint64_t seed = A.seed;\n";
+  o << "  const uint32_t ngroups = (A.W + " << G - 1 << ") / " << G << ";\n";
+  o << "  const int j4 = lane >> 3, wi = lane & 7;\n";
+  o << "  for (uint32_t grp = blockIdx.x * " << NWARP << " + wib; grp < ngroups; grp += gridDim.x * " << NWARP << ") {\n";
+  o << "    fs::aff_group_faults<" << K.nrows << ">(P, tabs, B, seed, word0, grp, A.W, lane);\n";
+  if (n_coins > 0) {  // coin blocks of the group's 8 words, all 32 lanes: lane = (block % 4, word)
+    o << "    for (int cb = j4; cb < " << nblk << "; cb += 4) {\n";
+    o << "      const uint4 v = fs::coin_block(seed, word0 + grp * " << G << " + wi, cb);\n";
+    o << "      uint32_t* const d = CW + wi * " << cstride << " + cb * 4;\n";
+    o << "      d[0] = v.x;";
+    o << " if (cb * 4 + 1 < " << n_coins << ") d[1] = v.y;";
+    o << " if (cb * 4 + 2 < " << n_coins << ") d[2] = v.z;";
+    o << " if (cb * 4 + 3 < " << n_coins << ") d[3] = v.w;\n";
+    o << "    }\n    __syncwarp();\n";
+  }
+  o << "    if (lane < " << G << ") {\n";
+  o << "      const uint32_t w = grp * " << G << " + lane;\n";
+  o << "      const uint64_t wabs = word0 + w;\n";
+  o << "      const uint64_t nleft = w < A.W ? A.nshots - (uint64_t)w * 32 : 0;\n";
+  o << "      const uint32_t valid = nleft >= 32 ? 0xFFFFFFFFu : ((1u << nleft) - 1u);\n";
+  o << "      uint32_t alive = valid;\n";
+  o << "      AL[lane] = valid;\n";
+  for (int cc = 0; cc < n_coins; cc++) o << "      const uint32_t k" << cc << " = CW[lane * " << cstride << " + " << cc << "];\n";
+  for (int r = 0; r < nrows; r++) {
+    const uint64_t* v = rowb.data() + (size_t)r * NW;
+    bool any = false;
+    for (int src = 0; src < el0 && !any; src++) any = ((v[src >> 6] >> (src & 63)) & 1ull) != 0;
+    if (any) o << "      B[" << r * G << " + (lane ^ " << ((r >> 2) & 7) << ")] ^= " << row_expr(v) << ";\n";
+  }
+  for (int jj = 0; jj < d.num_observables; jj++) o << "      uint32_t ob" << jj << " = 0u;\n";
+  o << p2.str();
+  o << "      if (w < A.W) {\n";
+  for (int jj = 0; jj < d.num_observables; jj++)
+    o << "        A.obs[(size_t)" << jj << " * A.ostride + w] = ob" << jj << " & valid;\n";
+  o << "        A.accepted[w] = alive & valid;\n        A.error[w] = 0u;\n      }\n";
+  o << "    }\n";
+  o << "    __syncwarp();\n";
+  o << "    {\n";
+  o << "      const uint32_t w = grp * " << G << " + wi;\n";
+  o << "      if (w < A.W) {\n";
+  if (npsel == 0) o << "        const uint32_t m0 = AL[wi];\n";
+  o << "        uint32_t* const mo = A.meas + (size_t)j4 * A.ostride + w;\n";
+  o << "        uint32_t* const dout = A.det + (size_t)j4 * A.ostride + w;\n";
+  o << "        const size_t s4 = (size_t)4 * A.ostride;\n";
+  auto slot_expr = [&](int row, const std::string& wexpr) {
+    return std::to_string(row * G) + " + (" + wexpr + " ^ " + std::to_string((row >> 2) & 7) + ")";
+  };
+  auto emit_copy = [&](int r0, int cnt, const char* base, int rbase) {
+    for (int r = r0; r < r0 + cnt; r += 4) {
+      // rows r..r+3 (r a multiple of 4): lane row r + j4 at slot (r + j4) * 8 + (wi ^ ((r >> 2) & 7));
+      // a differenced row adds its (already rebuilt) parent and is written back for later children
+      std::string m;
+      if (npsel == 0) m = "m0";
+      else {
+        std::ostringstream t;
+        t << "AL[(j4 == 0 ? " << row_seg[r] << " : j4 == 1 ? " << (r + 1 < nrows ? row_seg[r + 1] : 0) << " : j4 == 2 ? "
+          << (r + 2 < nrows ? row_seg[r + 2] : 0) << " : " << (r + 3 < nrows ? row_seg[r + 3] : 0) << ") * " << G << " + wi]";
+        m = t.str();
+      }
+      const int rem = std::min(4, r0 + cnt - r);
+      bool anyp = false;
+      int pr[4];
+      for (int q = 0; q < 4; q++) {
+        pr[q] = (q < rem && parent[r + q] >= 0) ? parent[r + q] : -1;
+        anyp |= pr[q] >= 0;
+      }
+      o << "        {";
+      if (rem < 4) o << " if (j4 < " << rem << ") {";
+      o << " uint32_t v = B[" << r * G << " + j4 * " << G << " + (wi ^ " << ((r >> 2) & 7) << ")];";
+      if (anyp) {
+        std::string ps[4];
+        for (int q = 0; q < 4; q++) ps[q] = std::to_string(pr[q] >= 0 ? pr[q] : zrow);
+        bool same_off = true;
+        for (int q = 1; q < 4; q++) same_off &= (pr[q] >= 0) == (pr[0] >= 0) && (pr[q] < 0 || pr[q] - (r + q) == pr[0] - r);
+        if (same_off && pr[0] >= 0 && ((pr[0] & 3) == 0))
+          o << " v ^= B[" << pr[0] * G << " + j4 * " << G << " + (wi ^ " << ((pr[0] >> 2) & 7) << ")];";
+        else
+          o << " { const int pp = j4 == 0 ? " << ps[0] << " : j4 == 1 ? " << ps[1] << " : j4 == 2 ? " << ps[2] << " : " << ps[3]
+            << "; v ^= B[pp * " << G << " + (wi ^ ((pp >> 2) & 7))]; }";
+        o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << ((r >> 2) & 7) << ")] = v;";
+      }
+      o << " " << base << "[" << (r - rbase) / 4 << " * s4] = v & " << m << ";";
+      if (rem < 4) o << " }";
+      o << " }\n";
+    }
+  };
+  emit_copy(0, U, "mo", 0);
+  emit_copy(U4, D, "dout", U4);
+  o << "      }\n    }\n";
+  o << "    __syncwarp();\n  }\n}\n";
+  if (terms > kAffMaxTerms) { K.why = "noiseless part too large"; return K; }
+  K.src = o.str();
+  return K;
+}
+
+}  // namespace fsjit

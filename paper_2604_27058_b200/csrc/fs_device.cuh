@@ -16,6 +16,7 @@ typedef unsigned long long uintptr_t;
 #endif
 
 #include "../../include/fs_sampler.h"
+#include "fs_lntab.h"
 
 namespace fs {
 
@@ -43,12 +44,13 @@ struct DevProg {
   const int* __restrict__ record_out;
   const int* __restrict__ bit_slot;
   // Philox noise runs (host-computed): maximal runs of consecutive sites with equal 0<p<1
-  // (run_len > 0, run_lp = 1/log1p(-q)) or a single certain site (run_len == 0)
+  // (run_len > 0, run_lp = 1/log1p(-q), run_q = q = the run's largest p) or a single certain
+  // site (run_len == 0)
   int num_runs;
   const int* __restrict__ run_start;
   const int* __restrict__ run_len;
   const double* __restrict__ run_lp;
-  const double* __restrict__ site_acc;  // p_site / q of its run (thinning), 1.0 when equal
+  const double* __restrict__ run_q;
   const int* __restrict__ next_array;   // [N] first array instruction >= i (N if none); with frame
                                         // matrices also the first FrameGates instruction
   // FrameGates as GF(2) matrices (block engine, 2n <= 128): instruction i maps the frame vector
@@ -116,6 +118,33 @@ __device__ __forceinline__ uint32_t coin_word(uint64_t seed, uint64_t wabs, int 
 __device__ __forceinline__ double u64_to_unit(uint64_t x) {
   return __dmul_rn(__ull2double_rn(x), 5.421010862427522e-20);
 }
+
+// ln(U) for the noise stream's gap draws, U = (2 * (bits >> 12) + 1) * 2^-53 in (0, 1) (exact).
+// U = m * 2^e with m in [1, 2) read off the bits; ln m = T_k + ln(1 + r) with the 64-interval
+// table of fs_lntab.h (r = fma(m, inv_k, -1), |r| < 2^-7) and an 8-term series for ln(1 + r).
+// IEEE basic operations and explicit FMAs only, in a fixed order, so the CPU oracle
+// (oracle/fs_oracle.c ln_unit) reproduces it bit for bit; |error| <= 1e-14 absolute.
+__device__ const double2 kLnTab[FS_LN_TAB_ENTRIES] = FS_LN_TAB_INIT;
+
+__device__ __forceinline__ double ln_unit_t(uint64_t bits, const double2* __restrict__ tab) {
+  const uint64_t v = ((bits >> 12) << 1) | 1ull;
+  const int p = 63 - __clzll((long long)v);
+  const uint64_t mant = (v << (52 - p)) & ((1ull << 52) - 1ull);
+  const double m = __longlong_as_double((long long)((1023ull << 52) | mant));
+  const double2 t = tab[mant >> 46];
+  const double r = fma(m, t.x, -1.0);
+  double P = -0.125;
+  P = fma(P, r, 0x1.2492492492492p-3);
+  P = fma(P, r, -0x1.5555555555555p-3);
+  P = fma(P, r, 0x1.999999999999ap-3);
+  P = fma(P, r, -0.25);
+  P = fma(P, r, 0x1.5555555555555p-2);
+  P = fma(P, r, -0.5);
+  P = fma(P, r, 1.0);
+  P = __dmul_rn(P, r);
+  return __dadd_rn(__dadd_rn(__dmul_rn((double)(p - 53), 0x1.62e42fefa39efp-1), t.y), P);
+}
+__device__ __forceinline__ double ln_unit(uint64_t bits) { return ln_unit_t(bits, kLnTab); }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ULL;
@@ -197,6 +226,14 @@ __device__ __forceinline__ int bisect_right(const double* __restrict__ S, double
 __device__ __forceinline__ int pick_case(const DevProg& P, int site, double u) {
   int c0 = __ldg(P.site_case_off + site), nc = __ldg(P.site_case_off + site + 1) - c0;
   double x = u * __ldg(P.site_prob + site);
+  int c = bisect_right(P.case_cum + c0, x, 0, nc);
+  return c0 + (c < nc - 1 ? c : nc - 1);
+}
+
+// case of a fault given x uniform on [0, p_site): bisect_right over the site's cumulative case
+// probabilities, clamped to the last case (the _pick_case law, runtime.py:702-707)
+__device__ __forceinline__ int pick_case_x(const DevProg& P, int site, double x) {
+  int c0 = __ldg(P.site_case_off + site), nc = __ldg(P.site_case_off + site + 1) - c0;
   int c = bisect_right(P.case_cum + c0, x, 0, nc);
   return c0 + (c < nc - 1 ? c : nc - 1);
 }

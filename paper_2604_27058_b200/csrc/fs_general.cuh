@@ -83,17 +83,16 @@ struct WordFaultGen {
       if (num_cases(P, site) > 1) cs = pick_case(P, site, u2);
       return 1;
     }
-    const double u1 = u64_to_unit(((uint64_t)b.y << 32) | b.x);
-    const double g = floor(__dmul_rn(log1p(-u1), __ldg(P.run_lp + run)));
+    const double g = floor(__dmul_rn(ln_unit(((uint64_t)b.y << 32) | b.x), __ldg(P.run_lp + run)));
     c = __dadd_rn(__dadd_rn(c, 1.0), g);
     if (!(c < (double)(32 * len))) { run++; c = -1.0; return 0; }
     const long long ci = (long long)c;
     lane = (int)(ci & 31);
     site = start + (int)(ci >> 5);
-    const double acc = __ldg(P.site_acc + site);
-    if (!(u2 < acc)) return 0;  // thinning: p_site < q
+    const double x = __dmul_rn(u2, __ldg(P.run_q + run));  // uniform on [0, q)
+    if (!(x < __ldg(P.site_prob + site))) return 0;        // thinning: p_site < q
     cs = __ldg(P.site_case_off + site);
-    if (num_cases(P, site) > 1) cs = pick_case(P, site, acc < 1.0 ? __ddiv_rn(u2, acc) : u2);
+    if (num_cases(P, site) > 1) cs = pick_case_x(P, site, x);
     return 1;
   }
 };

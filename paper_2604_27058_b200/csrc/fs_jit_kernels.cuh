@@ -108,3 +108,180 @@ __device__ __forceinline__ uint4 coin_block(uint64_t seed, uint64_t wabs, int bl
 }
 
 }  // namespace fs
+
+namespace fs {
+
+// Affine frame kernel (fs_affine.cuh).  Fault tables (shared memory when they fit): rows flipped
+// by each case (as buffer slots for word 0), site -> (first case, class), class -> (case count, p,
+// cumulative case probabilities), the ln table of the gap draws.
+template <bool OFF16>
+struct AffTabs {
+  const uint16_t* crows;
+  const uint32_t* crow_off;  // u16 entries when OFF16
+  const uint32_t* site_case;
+  const uint16_t* site_cls;
+  const int* cls_nc;
+  const double* cls_prob;
+  const double* cls_cum;
+  const double2* lntab;
+  int cw;
+  __device__ __forceinline__ uint32_t off(int c) const {
+    return OFF16 ? (uint32_t)reinterpret_cast<const uint16_t*>(crow_off)[c] : crow_off[c];
+  }
+};
+
+// One fault: case pick by bisect_right over the class's cumulative case probabilities (clamped),
+// then its shot bit XORed into the case's rows of word wi.  Row r of word wi lives at
+// slot(r, wi) = r * 8 + (wi ^ ((r >> 2) & 7)) = slot(r, 0) ^ wi: the lanes working on one word
+// spread over all 32 banks (shared atomics: two lanes may flip the same row).
+template <bool OFF16>
+__device__ __forceinline__ void aff_apply(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, int site, int cls, int fl,
+                                          double x) {
+  const int nc = T.cls_nc[cls];
+  int lo = 0;
+  if (nc > 1) {
+    const double* cum = T.cls_cum + cls * T.cw;
+    int hi = nc;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (x < cum[mid]) hi = mid; else lo = mid + 1;
+    }
+    lo = lo < nc - 1 ? lo : nc - 1;
+  }
+  const int cs = (int)T.site_case[site] + lo;
+  const uint32_t bit = 1u << fl;
+  uint32_t j = T.off(cs);
+  const uint32_t o1 = T.off(cs + 1);
+  for (; j + 1 < o1; j += 2) {
+    const uint32_t a = T.crows[j], b = T.crows[j + 1];
+    atomicXor(B + (a ^ wi), bit);
+    atomicXor(B + (b ^ wi), bit);
+  }
+  if (j < o1) atomicXor(B + ((uint32_t)T.crows[j] ^ wi), bit);
+}
+
+// Faults of one 32-shot word, warp-cooperatively: lane j evaluates step st + j of the word's
+// noise stream (the WordFaultGen process, step by step the same draws and decisions), the cell
+// positions of a run are an inclusive warp scan of the per-step advances 1 + floor(ln(U) * lp), and
+// the first step past the run's last cell ends it (the following lanes start the next run).
+// Generic over runs (certain sites, several probabilities).
+template <bool OFF16>
+__device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi,
+                                                uint64_t seed, uint64_t wabs, int lane) {
+  const int nruns = P.num_runs;
+  uint32_t st = 0;
+  int run = 0, cl = 0;
+  long long c = -1;
+  while (run < nruns) {
+    const uint4 b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), 0u, (TAG_NOISE << 24) | (st + lane), seed);
+    const double u2 = u64_to_unit(((uint64_t)b.w << 32) | b.z);
+    const double L = ln_unit_t(((uint64_t)b.y << 32) | b.x, T.lntab);
+    int first = 0;
+    while (first < 32 && run < nruns) {
+      const int start = __ldg(P.run_start + run), len = __ldg(P.run_len + run);
+      int site = -1, fl = 0, cls = 0;
+      double x = 0.0;
+      if (len == 0) {  // certain site: the run's steps fire shot bits cl, cl + 1, ..., 31 in order
+        const int take = min(32 - first, 32 - cl);
+        if (lane >= first && lane < first + take) {
+          site = start;
+          fl = cl + lane - first;
+          cls = T.site_cls[site];
+          x = u2 * T.cls_prob[cls];
+        }
+        cl += take;
+        first += take;
+        if (cl == 32) { run++; cl = 0; }
+      } else {
+        long long inc = 0;
+        if (lane >= first) {
+          const double g = floor(__dmul_rn(L, __ldg(P.run_lp + run)));
+          inc = g < 4.0e12 ? (long long)g + 1 : (1LL << 42);
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+          if (lane >= o) inc += t;
+        }
+        const long long pos = c + inc, limit = 32LL * len;
+        const uint32_t endm = __ballot_sync(0xFFFFFFFFu, lane >= first && pos >= limit);
+        if (lane >= first && pos < limit) {
+          const int s = start + (int)(pos >> 5);
+          const double xs = __dmul_rn(u2, __ldg(P.run_q + run));
+          const int k = T.site_cls[s];
+          if (xs < T.cls_prob[k]) {  // thinning: p_site < q
+            site = s;
+            fl = (int)(pos & 31);
+            cls = k;
+            x = xs;
+          }
+        }
+        if (endm) {
+          first = __ffs(endm);  // the lane after the ending step
+          run++;
+          c = -1;
+        } else {
+          c = __shfl_sync(0xFFFFFFFFu, pos, 31);
+          first = 32;
+        }
+      }
+      if (site >= 0) aff_apply<OFF16>(T, B, wi, site, cls, fl, x);
+    }
+    st += 32;
+  }
+}
+
+// The common case of one geometric run over all noisy sites (every site of the program has the
+// same p up to 1e-9, e.g. a uniform circuit-level noise model) with fewer than 2^25 cells: the
+// run parameters stay in registers and the scan is 32-bit.
+template <bool OFF16>
+__device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, uint64_t seed,
+                                                     uint64_t wabs, int lane, int start, uint32_t limit, double lp,
+                                                     double q) {
+  uint32_t st = 0;
+  int c = -1;
+  for (;;) {
+    const uint4 b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), 0u, (TAG_NOISE << 24) | (st + lane), seed);
+    const double u2 = u64_to_unit(((uint64_t)b.w << 32) | b.z);
+    const double g = floor(__dmul_rn(ln_unit_t(((uint64_t)b.y << 32) | b.x, T.lntab), lp));
+    int inc = g < 33554432.0 ? (int)g + 1 : 33554432;  // 2^25 >= limit: a clamped step ends the run
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const int pos = c + inc;
+    const bool in = pos < (int)limit;
+    const uint32_t endm = __ballot_sync(0xFFFFFFFFu, !in);
+    if (in) {
+      const int s = start + (pos >> 5);
+      const double x = __dmul_rn(u2, q);
+      const int k = T.site_cls[s];
+      if (x < T.cls_prob[k]) aff_apply<OFF16>(T, B, wi, s, k, pos & 31, x);  // thinning: p_site < q
+    }
+    if (endm) return;
+    c = __shfl_sync(0xFFFFFFFFu, pos, 31);
+    st += 32;
+  }
+}
+
+// zero a warp group's row buffer (8 words x NROWS rows) and apply the faults of its 8 words
+template <int NROWS, bool OFF16>
+__device__ __forceinline__ void aff_group_faults(const DevProg& P, const AffTabs<OFF16>& T, uint32_t* B, uint64_t seed,
+                                                 uint64_t word0, uint32_t grp, uint32_t W, int lane) {
+  for (int i = lane; i < NROWS * 2; i += 32) reinterpret_cast<uint4*>(B)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncwarp();
+  const bool one = P.num_runs == 1 && __ldg(P.run_len) > 0 && __ldg(P.run_len) < (1 << 20);
+  for (uint32_t wi = 0; wi < 8; wi++) {
+    const uint32_t w = grp * 8 + wi;
+    if (w >= W) break;
+    if (one)
+      aff_word_faults_1run<OFF16>(T, B, wi, seed, word0 + w, lane, __ldg(P.run_start), 32u * __ldg(P.run_len),
+                                  __ldg(P.run_lp), __ldg(P.run_q));
+    else
+      aff_word_faults<OFF16>(P, T, B, wi, seed, word0 + w, lane);
+  }
+  __syncwarp();
+}
+
+}  // namespace fs

@@ -24,6 +24,7 @@
 #include "fs_hbm_fused.cuh"
 #include "fs_block.cuh"
 #include "fs_jit.cuh"
+#include "fs_affine.cuh"
 #include "fs_jit_kernels.cuh"
 #include "fs_format.cuh"
 #include "fs_stratum.cuh"
@@ -45,6 +46,7 @@ int set_error(int code, const std::string& msg) {
   } while (0)
 
 constexpr size_t kSmemBudget = 200 * 1024;  // per block, leaves room for L1
+constexpr size_t kAffSmemBudget = 208 * 1024;  // affine frame kernel: row buffers of one block per SM
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -110,7 +112,7 @@ struct fs_prog {
   std::vector<double> h_fparams;
   std::vector<uint32_t> h_gates, h_paulis;
   std::vector<int32_t> h_reclists, h_record_out, h_bit_slot, h_plans, h_case_pauli_off, h_site_case_off;
-  std::vector<double> h_site_prob;
+  std::vector<double> h_site_prob, h_case_cum;
   // program-specialised frame kernel (fs_jit.cuh); built on first use
   int jit_state = 0;  // 0 not tried, 1 ready, -1 failed (interpreter is used)
   std::string jit_error;
@@ -123,6 +125,13 @@ struct fs_prog {
   int* d_site_block = nullptr;  // flip geometry: block_hi | row_off | block_cap
   int jit_nblocks = 0;
   int jit_stage = fsjit::kJitStage;
+  // affine frame kernel (fs_affine.cuh): 0 not tried, 1 ready, -1 not applicable / failed
+  int aff_state = 0;
+  std::string aff_error;
+  fsjit::Compiled aff;
+  uint32_t* d_aff_tables = nullptr;
+  int aff_threads = 0, aff_rows = 0;
+  size_t aff_smem = 0;
   // stratified sampling: suffix Poisson-binomial table of stratum w, per-chunk modes + outputs
   int strat_w = -1;
   double strat_weight = 0.0;
@@ -211,13 +220,13 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   // (relative) share one geometric process at q = max p, thinned by p/q per candidate; certain
   // sites (p >= 1) are single runs; p = 0 / caseless sites never fire
   std::vector<int32_t> run_start, run_len;
-  std::vector<double> run_lp, site_acc(E > 0 ? E : 1, 1.0);
+  std::vector<double> run_lp, run_q;
   for (int site = 0; site < E;) {
     const double prob = d->site_prob[site];
     const int nc = d->site_case_off[site + 1] - d->site_case_off[site];
     if (!(prob > 0.0) || nc == 0) { site++; continue; }
     if (prob >= 1.0) {
-      run_start.push_back(site); run_len.push_back(0); run_lp.push_back(0.0);
+      run_start.push_back(site); run_len.push_back(0); run_lp.push_back(0.0); run_q.push_back(1.0);
       site++;
       continue;
     }
@@ -230,15 +239,14 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
       if (!(nhi <= nlo * (1.0 + 1e-9))) break;
       lo = nlo; hi = nhi; len++;
     }
-    for (int t = site; t < site + len; t++) site_acc[t] = d->site_prob[t] / hi;
-    run_start.push_back(site); run_len.push_back(len); run_lp.push_back(1.0 / log1p(-hi));
+    run_start.push_back(site); run_len.push_back(len); run_lp.push_back(1.0 / log1p(-hi)); run_q.push_back(hi);
     site += len;
   }
   const int nruns = (int)run_start.size();
   size_t o_rs = add(run_start.data(), sizeof(int32_t) * nruns);
   size_t o_rl2 = add(run_len.data(), sizeof(int32_t) * nruns);
   size_t o_rlp = add(run_lp.data(), sizeof(double) * nruns);
-  size_t o_sacc = add(site_acc.data(), sizeof(double) * site_acc.size());
+  size_t o_rq = add(run_q.data(), sizeof(double) * nruns);
   // FrameGates as GF(2) matrices for the block engine (a warp applies one with ballots + popcounts
   // instead of thread 0 walking the gate list): column j = the gate list applied to basis bit j
   const int n2 = 2 * d->n;
@@ -327,7 +335,7 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   dp.run_start = reinterpret_cast<const int*>(b + o_rs);
   dp.run_len = reinterpret_cast<const int*>(b + o_rl2);
   dp.run_lp = reinterpret_cast<const double*>(b + o_rlp);
-  dp.site_acc = reinterpret_cast<const double*>(b + o_sacc);
+  dp.run_q = reinterpret_cast<const double*>(b + o_rq);
   dp.next_array = reinterpret_cast<const int*>(b + o_na);
   dp.frame_mat = reinterpret_cast<const uint32_t*>(b + o_fm);
   p->h_next_array = next_array;
@@ -345,6 +353,7 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   p->h_case_pauli_off.assign(d->case_pauli_off, d->case_pauli_off + d->num_cases + 1);
   p->h_site_case_off.assign(d->site_case_off, d->site_case_off + E + 1);
   p->h_site_prob.assign(d->site_prob, d->site_prob + E);
+  p->h_case_cum.assign(d->case_cum, d->case_cum + d->num_cases);
   // pointers of the creator's arrays are not retained
   p->desc.instrs = nullptr;
   *out = p;
@@ -377,6 +386,8 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   }
   cudaFree(p->flist);
   cudaFree(p->d_site_block);
+  cudaFree(p->d_aff_tables);
+  if (p->aff.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->aff.mod);
   if (p->jit.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->jit.mod);
   delete p;
 }
@@ -442,6 +453,27 @@ extern "C" int fs_debug_jit_source(const fs_prog_desc* d, char* buf, size_t len)
   std::vector<int32_t> sco(d->site_case_off, d->site_case_off + E + 1);
   std::vector<double> sp(d->site_prob, d->site_prob + E);
   fsjit::FrameKernelSource K = fsjit::gen_frame_kernel(*d, ins, g, pa, rl, ro, bs, pl, cpo, sco, sp);
+  if (buf && len) {
+    size_t m = std::min(len - 1, K.src.size());
+    std::memcpy(buf, K.src.data(), m);
+    buf[m] = 0;
+  }
+  return (int)K.src.size();
+}
+
+// source of the affine frame kernel (fs_affine.cuh); negative if not applicable
+extern "C" int fs_debug_aff_source(const fs_prog_desc* d, char* buf, size_t len) {
+  if (!d) return -1;
+  const int R = d->record_count, D = d->num_detectors, E = d->num_sites;
+  std::vector<int32_t> ins(d->instrs, d->instrs + (size_t)FS_INS_WORDS * d->num_instrs);
+  std::vector<uint32_t> g(d->gates, d->gates + d->num_gates), pa(d->paulis, d->paulis + d->num_paulis);
+  std::vector<int32_t> rl(d->reclists, d->reclists + d->num_reclists), ro(d->record_out, d->record_out + R);
+  std::vector<int32_t> bs(d->bit_slot, d->bit_slot + R + D);
+  std::vector<int32_t> cpo(d->case_pauli_off, d->case_pauli_off + d->num_cases + 1);
+  std::vector<int32_t> sco(d->site_case_off, d->site_case_off + E + 1);
+  std::vector<double> sp(d->site_prob, d->site_prob + E), cc(d->case_cum, d->case_cum + d->num_cases);
+  fsjit::AffineKernelSource K = fsjit::gen_affine_frame_kernel(*d, ins, g, pa, rl, ro, bs, cpo, sco, sp, cc, kAffSmemBudget);
+  if (!K.why.empty()) return -2;
   if (buf && len) {
     size_t m = std::min(len - 1, K.src.size());
     std::memcpy(buf, K.src.data(), m);
@@ -573,6 +605,8 @@ extern "C" const char* fs_debug_jit_status(fs_prog* p) {
   if (!p) return "null";
   s = p->jit_state == 1 ? "ready compile_bytes=" + std::to_string(p->jit.cubin_bytes)
                         : (p->jit_state == 0 ? "not built" : "failed: " + p->jit_error);
+  s += p->aff_state == 1 ? "; affine: ready threads=" + std::to_string(p->aff_threads)
+                         : (p->aff_state == 0 ? "; affine: not built" : "; affine: n/a (" + p->aff_error + ")");
   return s.c_str();
 }
 
@@ -633,6 +667,50 @@ int ensure_jit(fs_prog* p) {
   FS_CUDA_TRY(cudaMalloc(&p->d_site_block, sizeof(int) * K.site_block.size()));
   FS_CUDA_TRY(cudaMemcpy(p->d_site_block, K.site_block.data(), sizeof(int) * K.site_block.size(), cudaMemcpyHostToDevice));
   p->jit_state = 1;
+  return FS_OK;
+}
+
+
+// affine frame kernel (fs_affine.cuh) for frame-only programs, Philox free sampling
+int ensure_aff(fs_prog* p) {
+  if (p->aff_state == 1) return FS_OK;
+  if (p->aff_state == -1) return FS_ERR_ARG;
+  p->aff_state = -1;
+  fsjit::AffineKernelSource K = fsjit::gen_affine_frame_kernel(
+      p->desc, p->h_instrs, p->h_gates, p->h_paulis, p->h_reclists, p->h_record_out, p->h_bit_slot,
+      p->h_case_pauli_off, p->h_site_case_off, p->h_site_prob, p->h_case_cum, kAffSmemBudget);
+  if (!K.why.empty()) { p->aff_error = K.why; return FS_ERR_ARG; }
+  std::string err = fsjit::compile(K.src, fsjit::self_dir() + "/../csrc", p->aff, "fs_aff_frame");
+  if (!err.empty()) { p->aff_error = err; return set_error(FS_ERR_ARG, err); }
+  fsjit::Api& J = fsjit::api();
+  if (J.cuFuncSetAttribute(p->aff.fn, 8 /* MAX_DYNAMIC_SHARED_SIZE_BYTES */, (int)K.smem) != 0) {
+    p->aff_error = "cuFuncSetAttribute failed";
+    return FS_ERR_ARG;
+  }
+  FS_CUDA_TRY(cudaMalloc(&p->d_aff_tables, sizeof(uint32_t) * K.tables.size()));
+  FS_CUDA_TRY(cudaMemcpy(p->d_aff_tables, K.tables.data(), sizeof(uint32_t) * K.tables.size(), cudaMemcpyHostToDevice));
+  p->aff_threads = K.threads;
+  p->aff_rows = K.nrows;
+  p->aff_smem = K.smem;
+  p->aff_state = 1;
+  return FS_OK;
+}
+
+int launch_aff(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
+  fsjit::Api& J = fsjit::api();
+  int occ = 1;
+  J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->aff.fn, p->aff_threads, p->aff_smem);
+  const size_t blocks = (a.W + p->aff_threads - 1) / p->aff_threads;
+  const size_t grid = std::min<size_t>(blocks, (size_t)p->num_sms * std::max(occ, 1));
+  fs::DevProg dpv = p->dp;
+  const uint32_t* tb = p->d_aff_tables;
+  void* args[] = {&dpv, &a, &tb};
+  kt_begin(p, stream);
+  int r = J.cuLaunchKernel(p->aff.fn, (unsigned)grid, 1, 1, (unsigned)p->aff_threads, 1, 1, (unsigned)p->aff_smem,
+                           stream, args, nullptr);
+  kt_end(p, stream);
+  p->launches++;
+  if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_aff_frame) failed: " + std::to_string(r));
   return FS_OK;
 }
 
@@ -1801,6 +1879,9 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
   }
   const bool general = wants_general(p, flags, tout);
   const bool trace_in = tin && (tin->fault_modes || tin->forced);
+  if (!general && !trace_in && !(tout && tout->frame_x) && !(flags & FS_NO_JIT) && a.stop == dp.num_instrs &&
+      !getenv("FS_NO_AFFINE") && ensure_aff(p) == FS_OK)
+    return launch_aff(p, a, stream);
   if (!general && !trace_in && !(tout && tout->frame_x) && !(flags & FS_NO_JIT) && a.stop == dp.num_instrs) {
     int rc = ensure_jit(p);
     if (rc == FS_OK) {

@@ -155,15 +155,20 @@ def test_gpu_large_k_config3_philox_matches_oracle(cuda):
 
 
 @pytest.mark.parametrize("name", [c for c in CASES if load(c)["prog"].k_max == 0])
-def test_gpu_jit_equals_interpreter(cuda, name):
-    """Program-specialised frame kernel (NVRTC) == frame interpreter, bit for bit."""
+def test_gpu_jit_equals_interpreter(cuda, name, monkeypatch):
+    """Affine frame kernel == fault-list frame kernel (NVRTC) == frame interpreter, bit for bit."""
     P = load(name)["prog"]
     dp = _dev(P)
     n = 70_000
     _, a, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX)
-    _, b, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX | FS_NO_JIT)
-    _same(a, b)
+    assert "affine: ready" in dp.jit_status(), dp.jit_status()
+    monkeypatch.setenv("FS_NO_AFFINE", "1")
+    _, b, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX)
     assert dp.jit_status().startswith("ready"), dp.jit_status()
+    monkeypatch.delenv("FS_NO_AFFINE")
+    _, c, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX | FS_NO_JIT)
+    _same(a, c)
+    _same(b, c)
 
 
 @pytest.mark.parametrize("name", [c for c in CASES if 0 < load(c)["prog"].k_max <= 7 and not load(c)["prog"].has_postselect
