@@ -33,7 +33,11 @@
 
 namespace fsjit {
 
-constexpr int kAffGroup = 8;              // 32-shot words per warp group (one 32 B sector per row)
+constexpr int kAffGroup = 4;              // 32-shot words per warp group (16 B of every output row)
+constexpr int kAffChunk = 32 / kAffGroup;  // rows per copy-out instruction
+constexpr int kAffMaxWarps = 24;          // per block (one block per SM; 85 registers per thread)
+// buffer slot of row r for word wi: r * G + (wi ^ sw(r)), sw(r) = (r / kAffChunk) % G (bank spread)
+inline int aff_sw(int r) { return (r / kAffChunk) % kAffGroup; }
 constexpr int kAffMaxCoins = 128;         // coin words kept in registers
 constexpr size_t kAffMaxTerms = 1 << 16;  // coin XOR terms over all rows (code size)
 
@@ -81,7 +85,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   // buffer rows: user records [0, U), detectors [U4, U4 + D), ObservableIns rows from U4 + D4,
   // then hidden bits read by PostSelect (U4, D4 = U, D rounded up to 4: the copy-out writes 4 rows
   // of one kind per instruction)
-  const int U4 = (U + 3) & ~3, D4 = (D + 3) & ~3;
+  const int U4 = (U + kAffChunk - 1) / kAffChunk * kAffChunk, D4 = (D + kAffChunk - 1) / kAffChunk * kAffChunk;
   std::vector<int> bit_row(R + D, -1);  // record / detector id -> buffer row
   for (int r = 0; r < R; r++)
     if (record_out[r] >= 0) bit_row[r] = record_out[r];
@@ -222,7 +226,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
           const size_t src = t * 64 + __builtin_ctzll(m);
           if (src < (size_t)el0) continue;
           for (int q : orows[src - el0]) {
-            if (q >= (r & ~3)) break;
+            if (q >= r - r % kAffChunk) break;
             if (ov[q]++ == 0) cand.push_back(q);
           }
         }
@@ -268,7 +272,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     std::sort(touched.begin(), touched.end());
     touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
     for (uint16_t r : touched) {  // stored as the row's buffer slot for word 0: slot(r, wi) = e ^ wi
-      if (par[r]) crows.push_back((uint16_t)(r * 8 | ((r >> 2) & 7)));
+      if (par[r]) crows.push_back((uint16_t)(r * kAffGroup | aff_sw(r)));
       par[r] = 0;
     }
   }
@@ -327,6 +331,11 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   if (ncls) memcpy(T.data() + o_cp, cls_prob.data(), (size_t)ncls * 8);
   const size_t o_cc = sec((size_t)ncls * cw * 8);
   for (int c = 0; c < ncls; c++) memcpy(T.data() + o_cc + (size_t)c * cw * 2, cls_cum[c].data(), (size_t)cw * 8);
+  const size_t o_cs = sec((size_t)ncls * 8);
+  for (int c = 0; c < ncls; c++) {
+    const double sc = cls_prob[c] > 0.0 ? (double)cls_nc[c] / cls_prob[c] : 0.0;
+    memcpy(T.data() + o_cs + 2 * c, &sc, 8);
+  }
   const size_t o_ln = sec(FS_LN_TAB_ENTRIES * 16);
   {
     static const double lt[FS_LN_TAB_ENTRIES][2] = FS_LN_TAB_INIT;
@@ -339,11 +348,11 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   const int nblk = (n_coins + 3) / 4, cstride = n_coins ? (4 * nblk) | 1 : 0;  // coin words per word (odd stride)
   const size_t per_warp = ((size_t)K.nrows + psel_bits.size() + 1) * kAffGroup * 4 + (size_t)kAffGroup * cstride * 4;
   {
-    int wps = (int)std::min<size_t>(16, tbl_bytes < smem_budget ? (smem_budget - tbl_bytes) / per_warp : 0);
+    int wps = (int)std::min<size_t>(kAffMaxWarps, tbl_bytes < smem_budget ? (smem_budget - tbl_bytes) / per_warp : 0);
     if (const char* e = getenv("FS_AFF_WARPS")) wps = std::min(wps, std::max(1, atoi(e)));
     K.tables_smem = wps >= 8 && !getenv("FS_AFF_GLOBAL_TABLES");
     if (!K.tables_smem) {
-      wps = (int)std::min<size_t>(16, smem_budget / per_warp);
+      wps = (int)std::min<size_t>(kAffMaxWarps, smem_budget / per_warp);
       if (const char* e = getenv("FS_AFF_WARPS")) wps = std::min(wps, std::max(1, atoi(e)));
     }
     if (wps < 1) { K.why = "row buffer does not fit shared memory"; return K; }
@@ -360,6 +369,11 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     return e.str();
   };
   if (getenv("FS_AFF_VERBOSE")) {
+    std::vector<int> hist(34, 0);
+    for (int c = 0; c < d.num_cases; c++) hist[std::min<uint32_t>(33, crow_off[c + 1] - crow_off[c])]++;
+    fprintf(stderr, "aff: case row-count histogram:");
+    for (int h = 0; h < 34; h++) if (hist[h]) fprintf(stderr, " %d:%d", h, hist[h]);
+    fprintf(stderr, "\n");
     size_t el_total = 0;
     for (auto& v : el_rows) el_total += v.size();
     fprintf(stderr,
@@ -393,13 +407,13 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
         case FS_OP_DETECTOR: row_seg[bit_row[R + I[1]]] = seg; break;
         case FS_OP_OBSERVABLE: {
           const int row = obs_row++;
-          p2 << "      ob" << I[1] << " ^= B[" << row * G << " + (lane ^ " << ((row >> 2) & 7) << ")] & alive;\n";
+          p2 << "      ob" << I[1] << " ^= B[" << row * G << " + (lane ^ " << aff_sw(row) << ")] & alive;\n";
           break;
         }
         case FS_OP_POSTSELECT: {
           const int bid = I[1] == 0 ? R + I[2] : I[2];
           const int row = bit_row[bid];
-          p2 << "      alive &= ~((B[" << row * G << " + (lane ^ " << ((row >> 2) & 7) << ")]" << (I[3] ? " ^ 0xFFFFFFFFu" : "")
+          p2 << "      alive &= ~((B[" << row * G << " + (lane ^ " << aff_sw(row) << ")]" << (I[3] ? " ^ 0xFFFFFFFFu" : "")
              << ") & alive);\n";
           p2 << "      AL[" << (seg + 1) * G << " + lane] = alive;\n";
           seg++;
@@ -435,6 +449,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   o << "  tabs.cls_prob = reinterpret_cast<const double*>(tb + " << o_cp << ");\n";
   o << "  tabs.cls_cum = reinterpret_cast<const double*>(tb + " << o_cc << ");\n";
   o << "  tabs.lntab = reinterpret_cast<const double2*>(tb + " << o_ln << ");\n";
+  o << "  tabs.cls_scale = reinterpret_cast<const double*>(tb + " << o_cs << ");\n";
   o << "  tabs.cw = " << cw << ";\n";
   o << "  uint32_t* const B = smem + " << bufw << " + wib * " << (size_t)K.nrows * G << ";\n";
   o << "  uint32_t* const AL = smem + " << bufw + (size_t)NWARP * K.nrows * G << " + wib * " << (npsel + 1) * G << ";\n";
@@ -442,11 +457,14 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     << ";\n";
   o << "  const uint64_t word0 = A.shot0 >> 5;\n  const uint64_t seed = A.seed;\n";
   o << "  const uint32_t ngroups = (A.W + " << G - 1 << ") / " << G << ";\n";
-  o << "  const int j4 = lane >> 3, wi = lane & 7;\n";
+  o << "  const int j4 = lane / " << G << ", wi = lane % " << G << ";\n";
   o << "  for (uint32_t grp = blockIdx.x * " << NWARP << " + wib; grp < ngroups; grp += gridDim.x * " << NWARP << ") {\n";
-  o << "    fs::aff_group_faults<" << K.nrows << ">(P, tabs, B, seed, word0, grp, A.W, lane);\n";
+  uint32_t maxr = 0;
+  for (int c = 0; c < d.num_cases; c++) maxr = std::max(maxr, crow_off[c + 1] - crow_off[c]);
+  o << "    fs::aff_group_faults<" << G << ", " << K.nrows << ", " << (off16 ? "true" : "false") << ", " << std::min<uint32_t>(maxr, 16)
+    << ">(P, tabs, B, seed, word0, grp, A.W, lane);\n";
   if (n_coins > 0) {  // coin blocks of the group's 8 words, all 32 lanes: lane = (block % 4, word)
-    o << "    for (int cb = j4; cb < " << nblk << "; cb += 4) {\n";
+    o << "    for (int cb = j4; cb < " << nblk << "; cb += " << kAffChunk << ") {\n";
     o << "      const uint4 v = fs::coin_block(seed, word0 + grp * " << G << " + wi, cb);\n";
     o << "      uint32_t* const d = CW + wi * " << cstride << " + cb * 4;\n";
     o << "      d[0] = v.x;";
@@ -467,7 +485,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     const uint64_t* v = rowb.data() + (size_t)r * NW;
     bool any = false;
     for (int src = 0; src < el0 && !any; src++) any = ((v[src >> 6] >> (src & 63)) & 1ull) != 0;
-    if (any) o << "      B[" << r * G << " + (lane ^ " << ((r >> 2) & 7) << ")] ^= " << row_expr(v) << ";\n";
+    if (any) o << "      B[" << r * G << " + (lane ^ " << aff_sw(r) << ")] ^= " << row_expr(v) << ";\n";
   }
   for (int jj = 0; jj < d.num_observables; jj++) o << "      uint32_t ob" << jj << " = 0u;\n";
   o << p2.str();
@@ -483,46 +501,44 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   if (npsel == 0) o << "        const uint32_t m0 = AL[wi];\n";
   o << "        uint32_t* const mo = A.meas + (size_t)j4 * A.ostride + w;\n";
   o << "        uint32_t* const dout = A.det + (size_t)j4 * A.ostride + w;\n";
-  o << "        const size_t s4 = (size_t)4 * A.ostride;\n";
-  auto slot_expr = [&](int row, const std::string& wexpr) {
-    return std::to_string(row * G) + " + (" + wexpr + " ^ " + std::to_string((row >> 2) & 7) + ")";
-  };
+  o << "        const size_t sc = (size_t)" << kAffChunk << " * A.ostride;\n";
   auto emit_copy = [&](int r0, int cnt, const char* base, int rbase) {
-    for (int r = r0; r < r0 + cnt; r += 4) {
-      // rows r..r+3 (r a multiple of 4): lane row r + j4 at slot (r + j4) * 8 + (wi ^ ((r >> 2) & 7));
+    const int RC = kAffChunk;
+    auto sel = [&](const std::vector<std::string>& v) {  // value for this lane's row r + j4
+      bool same = true;
+      for (auto& x : v) same &= x == v[0];
+      if (same) return v[0];
+      std::string e = v[RC - 1];
+      for (int q = RC - 2; q >= 0; q--) e = "(j4 == " + std::to_string(q) + " ? " + v[q] + " : " + e + ")";
+      return e;
+    };
+    for (int r = r0; r < r0 + cnt; r += RC) {
+      // rows r..r+RC-1 (r a multiple of RC): lane row r + j4 at slot (r + j4) * G + (wi ^ sw(r));
       // a differenced row adds its (already rebuilt) parent and is written back for later children
-      std::string m;
-      if (npsel == 0) m = "m0";
-      else {
-        std::ostringstream t;
-        t << "AL[(j4 == 0 ? " << row_seg[r] << " : j4 == 1 ? " << (r + 1 < nrows ? row_seg[r + 1] : 0) << " : j4 == 2 ? "
-          << (r + 2 < nrows ? row_seg[r + 2] : 0) << " : " << (r + 3 < nrows ? row_seg[r + 3] : 0) << ") * " << G << " + wi]";
-        m = t.str();
-      }
-      const int rem = std::min(4, r0 + cnt - r);
-      bool anyp = false;
-      int pr[4];
-      for (int q = 0; q < 4; q++) {
-        pr[q] = (q < rem && parent[r + q] >= 0) ? parent[r + q] : -1;
-        anyp |= pr[q] >= 0;
+      const int rem = std::min(RC, r0 + cnt - r);
+      std::vector<std::string> mv(RC), pv(RC);
+      bool anyp = false, same_off = true;
+      for (int q = 0; q < RC; q++) {
+        const int rr = r + q;
+        mv[q] = npsel == 0 ? "m0" : "AL[" + std::to_string((rr < nrows ? row_seg[rr] : 0) * G) + " + wi]";
+        const int pp = (q < rem && parent[rr] >= 0) ? parent[rr] : -1;
+        anyp |= pp >= 0;
+        pv[q] = std::to_string(pp >= 0 ? pp : zrow);
+        const int p0 = (parent[r] >= 0) ? parent[r] : -1;
+        same_off &= q < rem && pp >= 0 && p0 >= 0 && pp - rr == p0 - r && p0 % RC == 0;
       }
       o << "        {";
-      if (rem < 4) o << " if (j4 < " << rem << ") {";
-      o << " uint32_t v = B[" << r * G << " + j4 * " << G << " + (wi ^ " << ((r >> 2) & 7) << ")];";
+      if (rem < RC) o << " if (j4 < " << rem << ") {";
+      o << " uint32_t v = B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")];";
       if (anyp) {
-        std::string ps[4];
-        for (int q = 0; q < 4; q++) ps[q] = std::to_string(pr[q] >= 0 ? pr[q] : zrow);
-        bool same_off = true;
-        for (int q = 1; q < 4; q++) same_off &= (pr[q] >= 0) == (pr[0] >= 0) && (pr[q] < 0 || pr[q] - (r + q) == pr[0] - r);
-        if (same_off && pr[0] >= 0 && ((pr[0] & 3) == 0))
-          o << " v ^= B[" << pr[0] * G << " + j4 * " << G << " + (wi ^ " << ((pr[0] >> 2) & 7) << ")];";
+        if (same_off)
+          o << " v ^= B[" << parent[r] * G << " + j4 * " << G << " + (wi ^ " << aff_sw(parent[r]) << ")];";
         else
-          o << " { const int pp = j4 == 0 ? " << ps[0] << " : j4 == 1 ? " << ps[1] << " : j4 == 2 ? " << ps[2] << " : " << ps[3]
-            << "; v ^= B[pp * " << G << " + (wi ^ ((pp >> 2) & 7))]; }";
-        o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << ((r >> 2) & 7) << ")] = v;";
+          o << " { const int pp = " << sel(pv) << "; v ^= B[pp * " << G << " + (wi ^ ((pp / " << RC << ") % " << G << "))]; }";
+        o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")] = v;";
       }
-      o << " " << base << "[" << (r - rbase) / 4 << " * s4] = v & " << m << ";";
-      if (rem < 4) o << " }";
+      o << " " << base << "[" << (r - rbase) / RC << " * sc] = v & " << sel(mv) << ";";
+      if (rem < RC) o << " }";
       o << " }\n";
     }
   };

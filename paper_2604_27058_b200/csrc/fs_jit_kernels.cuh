@@ -123,6 +123,7 @@ struct AffTabs {
   const int* cls_nc;
   const double* cls_prob;
   const double* cls_cum;
+  const double* cls_scale;  // nc / p: first guess of the case index
   const double2* lntab;
   int cw;
   __device__ __forceinline__ uint32_t off(int c) const {
@@ -132,32 +133,36 @@ struct AffTabs {
 
 // One fault: case pick by bisect_right over the class's cumulative case probabilities (clamped),
 // then its shot bit XORed into the case's rows of word wi.  Row r of word wi lives at
-// slot(r, wi) = r * 8 + (wi ^ ((r >> 2) & 7)) = slot(r, 0) ^ wi: the lanes working on one word
-// spread over all 32 banks (shared atomics: two lanes may flip the same row).
-template <bool OFF16>
+// slot(r, wi) = r * G + (wi ^ sw(r)) = slot(r, 0) ^ wi (fs_affine.cuh aff_sw): the lanes working on
+// one word spread over all 32 banks (shared atomics: two lanes may flip the same row).
+template <bool OFF16, int MAXR>
 __device__ __forceinline__ void aff_apply(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, int site, int cls, int fl,
                                           double x) {
   const int nc = T.cls_nc[cls];
-  int lo = 0;
+  int c = 0;
   if (nc > 1) {
+    // bisect_right(cum, x) clamped to nc - 1 == the first c < nc - 1 with x < cum[c], else nc - 1:
+    // the uniform-case guess x * nc / p corrected by one step each way, exact bisect if still off
     const double* cum = T.cls_cum + cls * T.cw;
-    int hi = nc;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (x < cum[mid]) hi = mid; else lo = mid + 1;
+    c = min((int)(x * T.cls_scale[cls]), nc - 1);
+    c -= (c > 0 && x < cum[c - 1]) ? 1 : 0;
+    c += (c < nc - 1 && !(x < cum[c])) ? 1 : 0;
+    if ((c > 0 && x < cum[c - 1]) || (c < nc - 1 && !(x < cum[c]))) {
+      int lo = 0, hi = nc;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (x < cum[mid]) hi = mid; else lo = mid + 1;
+      }
+      c = lo < nc - 1 ? lo : nc - 1;
     }
-    lo = lo < nc - 1 ? lo : nc - 1;
   }
-  const int cs = (int)T.site_case[site] + lo;
+  const int cs = (int)T.site_case[site] + c;
   const uint32_t bit = 1u << fl;
-  uint32_t j = T.off(cs);
-  const uint32_t o1 = T.off(cs + 1);
-  for (; j + 1 < o1; j += 2) {
-    const uint32_t a = T.crows[j], b = T.crows[j + 1];
-    atomicXor(B + (a ^ wi), bit);
-    atomicXor(B + (b ^ wi), bit);
-  }
-  if (j < o1) atomicXor(B + ((uint32_t)T.crows[j] ^ wi), bit);
+  const uint32_t j0 = T.off(cs), n = T.off(cs + 1) - j0;
+#pragma unroll
+  for (int t = 0; t < MAXR; t++)
+    if ((uint32_t)t < n) atomicXor(B + ((uint32_t)T.crows[j0 + t] ^ wi), bit);
+  for (uint32_t t = MAXR; t < n; t++) atomicXor(B + ((uint32_t)T.crows[j0 + t] ^ wi), bit);
 }
 
 // Faults of one 32-shot word, warp-cooperatively: lane j evaluates step st + j of the word's
@@ -165,7 +170,7 @@ __device__ __forceinline__ void aff_apply(const AffTabs<OFF16>& T, uint32_t* B, 
 // positions of a run are an inclusive warp scan of the per-step advances 1 + floor(ln(U) * lp), and
 // the first step past the run's last cell ends it (the following lanes start the next run).
 // Generic over runs (certain sites, several probabilities).
-template <bool OFF16>
+template <bool OFF16, int MAXR>
 __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi,
                                                 uint64_t seed, uint64_t wabs, int lane) {
   const int nruns = P.num_runs;
@@ -225,7 +230,7 @@ __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<
           first = 32;
         }
       }
-      if (site >= 0) aff_apply<OFF16>(T, B, wi, site, cls, fl, x);
+      if (site >= 0) aff_apply<OFF16, MAXR>(T, B, wi, site, cls, fl, x);
     }
     st += 32;
   }
@@ -234,16 +239,21 @@ __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<
 // The common case of one geometric run over all noisy sites (every site of the program has the
 // same p up to 1e-9, e.g. a uniform circuit-level noise model) with fewer than 2^25 cells: the
 // run parameters stay in registers and the scan is 32-bit.
-template <bool OFF16>
+struct AffRun1 {
+  int start;
+  uint32_t limit;
+  double lp, q;
+};
+
+template <bool OFF16, int MAXR>
 __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, uint64_t seed,
-                                                     uint64_t wabs, int lane, int start, uint32_t limit, double lp,
-                                                     double q) {
+                                                     uint64_t wabs, int lane, const AffRun1& R) {
   uint32_t st = 0;
   int c = -1;
   for (;;) {
     const uint4 b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), 0u, (TAG_NOISE << 24) | (st + lane), seed);
     const double u2 = u64_to_unit(((uint64_t)b.w << 32) | b.z);
-    const double g = floor(__dmul_rn(ln_unit_t(((uint64_t)b.y << 32) | b.x, T.lntab), lp));
+    const double g = floor(__dmul_rn(ln_unit_t(((uint64_t)b.y << 32) | b.x, T.lntab), R.lp));
     int inc = g < 33554432.0 ? (int)g + 1 : 33554432;  // 2^25 >= limit: a clamped step ends the run
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -251,13 +261,13 @@ __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, ui
       if (lane >= o) inc += t;
     }
     const int pos = c + inc;
-    const bool in = pos < (int)limit;
+    const bool in = pos < (int)R.limit;
     const uint32_t endm = __ballot_sync(0xFFFFFFFFu, !in);
     if (in) {
-      const int s = start + (pos >> 5);
-      const double x = __dmul_rn(u2, q);
+      const int s = R.start + (pos >> 5);
+      const double x = __dmul_rn(u2, R.q);
       const int k = T.site_cls[s];
-      if (x < T.cls_prob[k]) aff_apply<OFF16>(T, B, wi, s, k, pos & 31, x);  // thinning: p_site < q
+      if (x < T.cls_prob[k]) aff_apply<OFF16, MAXR>(T, B, wi, s, k, pos & 31, x);  // thinning: p_site < q
     }
     if (endm) return;
     c = __shfl_sync(0xFFFFFFFFu, pos, 31);
@@ -265,21 +275,30 @@ __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, ui
   }
 }
 
-// zero a warp group's row buffer (8 words x NROWS rows) and apply the faults of its 8 words
-template <int NROWS, bool OFF16>
+// zero a warp group's row buffer (G words x NROWS rows) and apply the faults of its G words
+template <int G, int NROWS, bool OFF16, int MAXR>
 __device__ __forceinline__ void aff_group_faults(const DevProg& P, const AffTabs<OFF16>& T, uint32_t* B, uint64_t seed,
                                                  uint64_t word0, uint32_t grp, uint32_t W, int lane) {
-  for (int i = lane; i < NROWS * 2; i += 32) reinterpret_cast<uint4*>(B)[i] = make_uint4(0u, 0u, 0u, 0u);
+  static_assert((NROWS * G) % 4 == 0, "row buffer is zeroed with 16-byte stores");
+  for (int i = lane; i < NROWS * G / 4; i += 32) reinterpret_cast<uint4*>(B)[i] = make_uint4(0u, 0u, 0u, 0u);
   __syncwarp();
-  const bool one = P.num_runs == 1 && __ldg(P.run_len) > 0 && __ldg(P.run_len) < (1 << 20);
-  for (uint32_t wi = 0; wi < 8; wi++) {
-    const uint32_t w = grp * 8 + wi;
-    if (w >= W) break;
-    if (one)
-      aff_word_faults_1run<OFF16>(T, B, wi, seed, word0 + w, lane, __ldg(P.run_start), 32u * __ldg(P.run_len),
-                                  __ldg(P.run_lp), __ldg(P.run_q));
-    else
-      aff_word_faults<OFF16>(P, T, B, wi, seed, word0 + w, lane);
+  if (P.num_runs == 1 && __ldg(P.run_len) > 0 && __ldg(P.run_len) < (1 << 20)) {
+    AffRun1 R;
+    R.start = __ldg(P.run_start);
+    R.limit = 32u * __ldg(P.run_len);
+    R.lp = __ldg(P.run_lp);
+    R.q = __ldg(P.run_q);
+    for (uint32_t wi = 0; wi < G; wi++) {
+      const uint32_t w = grp * G + wi;
+      if (w >= W) break;
+      aff_word_faults_1run<OFF16, MAXR>(T, B, wi, seed, word0 + w, lane, R);
+    }
+  } else {
+    for (uint32_t wi = 0; wi < G; wi++) {
+      const uint32_t w = grp * G + wi;
+      if (w >= W) break;
+      aff_word_faults<OFF16, MAXR>(P, T, B, wi, seed, word0 + w, lane);
+    }
   }
   __syncwarp();
 }
