@@ -33,9 +33,9 @@
 
 namespace fsjit {
 
-constexpr int kAffGroup = 4;              // 32-shot words per warp group (16 B of every output row)
+constexpr int kAffGroup = 8;              // 32-shot words per group (one 32 B sector of every output row)
 constexpr int kAffChunk = 32 / kAffGroup;  // rows per copy-out instruction
-constexpr int kAffMaxWarps = 24;          // per block (one block per SM; 85 registers per thread)
+constexpr int kAffMaxPairs = 12;          // warp pairs per block (one block per SM; 85 registers per thread)
 // buffer slot of row r for word wi: r * G + (wi ^ sw(r)), sw(r) = (r / kAffChunk) % G (bank spread)
 inline int aff_sw(int r) { return (r / kAffChunk) % kAffGroup; }
 constexpr int kAffMaxCoins = 128;         // coin words kept in registers
@@ -227,6 +227,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
           if (src < (size_t)el0) continue;
           for (int q : orows[src - el0]) {
             if (q >= r - r % kAffChunk) break;
+            if ((q / kAffChunk) % 2 != (r / kAffChunk) % 2) continue;  // copied out by the other warp
             if (ov[q]++ == 0) cand.push_back(q);
           }
         }
@@ -336,38 +337,73 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     const double sc = cls_prob[c] > 0.0 ? (double)cls_nc[c] / cls_prob[c] : 0.0;
     memcpy(T.data() + o_cs + 2 * c, &sc, 8);
   }
+  // copy-out side tables: parent slot of every row (the zero row when not differenced), its
+  // post-select segment (alive mask in effect at its write), noiseless terms (row slot, coin word;
+  // coin n_coins = the all-ones word of a constant)
+  const int zrow = nrows;
+  std::vector<int> row_seg(nrows + 1, 0);
+  int npsel = 0;
+  for (int i = 0; i < d.num_instrs; i++) {
+    const int* I = ins_all.data() + (size_t)i * FS_INS_WORDS;
+    switch (FS_OPCODE(I[0])) {
+      case FS_OP_MEAS_DSTATIC:
+      case FS_OP_MEAS_DRANDOM:
+        if (record_out[I[3]] >= 0) row_seg[record_out[I[3]]] = npsel;
+        break;
+      case FS_OP_DETECTOR: row_seg[bit_row[R + I[1]]] = npsel; break;
+      case FS_OP_POSTSELECT: npsel++; break;
+      default: break;
+    }
+  }
+  const size_t o_ps = sec((size_t)(nrows + 1) * 2);
+  {
+    std::vector<uint16_t> ps(nrows + 1);
+    for (int r = 0; r <= nrows; r++) {
+      const int pr = r < nrows && parent[r] >= 0 ? parent[r] : zrow;
+      ps[r] = (uint16_t)(pr * kAffGroup | aff_sw(pr));
+    }
+    memcpy(T.data() + o_ps, ps.data(), ps.size() * 2);
+  }
+  const size_t o_seg = sec((size_t)(nrows + 1) * 2);
+  {
+    std::vector<uint16_t> sg(row_seg.begin(), row_seg.end());
+    memcpy(T.data() + o_seg, sg.data(), sg.size() * 2);
+  }
+  std::vector<uint32_t> terms_tab;  // slot0 | coin << 16
+  for (int r = 0; r < nrows; r++) {
+    const uint64_t* v = rowb.data() + (size_t)r * NW;
+    const uint32_t sl = (uint32_t)(r * kAffGroup | aff_sw(r));
+    if (v[0] & 1ull) terms_tab.push_back(sl | (uint32_t)n_coins << 16);
+    for (int c = 0; c < n_coins; c++)
+      if ((v[(1 + c) >> 6] >> ((1 + c) & 63)) & 1ull) terms_tab.push_back(sl | (uint32_t)c << 16);
+  }
+  if (terms_tab.size() > kAffMaxTerms) { K.why = "noiseless part too large"; return K; }
+  const size_t o_terms = sec(terms_tab.size() * 4);
+  if (!terms_tab.empty()) memcpy(T.data() + o_terms, terms_tab.data(), terms_tab.size() * 4);
   const size_t o_ln = sec(FS_LN_TAB_ENTRIES * 16);
   {
     static const double lt[FS_LN_TAB_ENTRIES][2] = FS_LN_TAB_INIT;
     memcpy(T.data() + o_ln, lt, sizeof lt);
   }
   const size_t tbl_bytes = T.size() * 4;
-  // ---- launch shape: 8-word groups, one warp each; row buffer (+ a zero row) and alive masks per warp
-  const int zrow = nrows;
+  // ---- launch shape: a pair of warps per 8-word group; per pair a row buffer (+ a zero row),
+  // the alive masks of the post-select segments and the group's coin words
   K.nrows = nrows + 1;
-  const int nblk = (n_coins + 3) / 4, cstride = n_coins ? (4 * nblk) | 1 : 0;  // coin words per word (odd stride)
-  const size_t per_warp = ((size_t)K.nrows + psel_bits.size() + 1) * kAffGroup * 4 + (size_t)kAffGroup * cstride * 4;
+  const int nblk = (n_coins + 3) / 4, cstride = (n_coins + 1) | 1;  // coin words + all-ones word (odd stride)
+  const size_t per_pair = ((size_t)K.nrows + psel_bits.size() + 1) * kAffGroup * 4 + (size_t)kAffGroup * cstride * 4;
+  int npairs = 0;
   {
-    int wps = (int)std::min<size_t>(kAffMaxWarps, tbl_bytes < smem_budget ? (smem_budget - tbl_bytes) / per_warp : 0);
-    if (const char* e = getenv("FS_AFF_WARPS")) wps = std::min(wps, std::max(1, atoi(e)));
-    K.tables_smem = wps >= 8 && !getenv("FS_AFF_GLOBAL_TABLES");
+    npairs = (int)std::min<size_t>(kAffMaxPairs, tbl_bytes < smem_budget ? (smem_budget - tbl_bytes) / per_pair : 0);
+    if (const char* e = getenv("FS_AFF_PAIRS")) npairs = std::min(npairs, std::max(1, atoi(e)));
+    K.tables_smem = npairs >= 4 && !getenv("FS_AFF_GLOBAL_TABLES");
     if (!K.tables_smem) {
-      wps = (int)std::min<size_t>(kAffMaxWarps, smem_budget / per_warp);
-      if (const char* e = getenv("FS_AFF_WARPS")) wps = std::min(wps, std::max(1, atoi(e)));
+      npairs = (int)std::min<size_t>(kAffMaxPairs, smem_budget / per_pair);
+      if (const char* e = getenv("FS_AFF_PAIRS")) npairs = std::min(npairs, std::max(1, atoi(e)));
     }
-    if (wps < 1) { K.why = "row buffer does not fit shared memory"; return K; }
-    K.threads = wps * 32;
-    K.smem = per_warp * wps + (K.tables_smem ? tbl_bytes : 0);
+    if (npairs < 1) { K.why = "row buffer does not fit shared memory"; return K; }
+    K.threads = npairs * 64;
+    K.smem = per_pair * npairs + (K.tables_smem ? tbl_bytes : 0);
   }
-  // noiseless part of a row: constant word and coin list
-  size_t terms = 0;
-  auto row_expr = [&](const uint64_t* v) {
-    std::ostringstream e;
-    e << ((v[0] & 1ull) ? "0xFFFFFFFFu" : "0u");
-    for (int c = 0; c < n_coins; c++)
-      if ((v[(1 + c) >> 6] >> ((1 + c) & 63)) & 1ull) { e << " ^ k" << c; terms++; }
-    return e.str();
-  };
   if (getenv("FS_AFF_VERBOSE")) {
     std::vector<int> hist(34, 0);
     for (int c = 0; c < d.num_cases; c++) hist[std::min<uint32_t>(33, crow_off[c + 1] - crow_off[c])]++;
@@ -390,9 +426,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   //   every post-select segment in AL[seg][word]
   // phase 3 (all lanes, lane = (row & 3, word)): copy rows out, 4 rows x 8 words (four 32 B
   //   sectors) per instruction, each masked with the alive mask in effect at its write
-  const int G = kAffGroup, NWARP = K.threads / 32;
-  int npsel = 0;
-  std::vector<int> row_seg(nrows, 0);
+  const int G = kAffGroup;
   std::ostringstream p2;
   {
     int seg = 0;
@@ -400,11 +434,6 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     for (int i = 0; i < d.num_instrs; i++) {
       const int* I = ins_all.data() + (size_t)i * FS_INS_WORDS;
       switch (FS_OPCODE(I[0])) {
-        case FS_OP_MEAS_DSTATIC:
-        case FS_OP_MEAS_DRANDOM:
-          if (record_out[I[3]] >= 0) row_seg[record_out[I[3]]] = seg;
-          break;
-        case FS_OP_DETECTOR: row_seg[bit_row[R + I[1]]] = seg; break;
         case FS_OP_OBSERVABLE: {
           const int row = obs_row++;
           p2 << "      ob" << I[1] << " ^= B[" << row * G << " + (lane ^ " << aff_sw(row) << ")] & alive;\n";
@@ -422,7 +451,6 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
         default: break;
       }
     }
-    npsel = seg;
   }
   std::ostringstream o;
   o << "#include \"fs_jit_kernels.cuh\"\n";
@@ -451,42 +479,51 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   o << "  tabs.lntab = reinterpret_cast<const double2*>(tb + " << o_ln << ");\n";
   o << "  tabs.cls_scale = reinterpret_cast<const double*>(tb + " << o_cs << ");\n";
   o << "  tabs.cw = " << cw << ";\n";
-  o << "  uint32_t* const B = smem + " << bufw << " + wib * " << (size_t)K.nrows * G << ";\n";
-  o << "  uint32_t* const AL = smem + " << bufw + (size_t)NWARP * K.nrows * G << " + wib * " << (npsel + 1) * G << ";\n";
-  o << "  uint32_t* const CW = smem + " << bufw + (size_t)NWARP * (K.nrows + npsel + 1) * G << " + wib * " << G * cstride
+  o << "  const uint16_t* const PS = reinterpret_cast<const uint16_t*>(tb + " << o_ps << ");\n";
+  o << "  const uint16_t* const SEG = reinterpret_cast<const uint16_t*>(tb + " << o_seg << ");\n";
+  o << "  const uint32_t* const TERMS = tb + " << o_terms << ";\n";
+  (void)o_seg;
+  o << "  const int pair = wib >> 1, half = wib & 1, t64 = threadIdx.x & 63;\n";
+  o << "  uint32_t* const B = smem + " << bufw << " + pair * " << (size_t)K.nrows * G << ";\n";
+  o << "  uint32_t* const AL = smem + " << bufw + (size_t)npairs * K.nrows * G << " + pair * " << (npsel + 1) * G << ";\n";
+  o << "  uint32_t* const CW = smem + " << bufw + (size_t)npairs * (K.nrows + npsel + 1) * G << " + pair * " << G * cstride
     << ";\n";
   o << "  const uint64_t word0 = A.shot0 >> 5;\n  const uint64_t seed = A.seed;\n";
   o << "  const uint32_t ngroups = (A.W + " << G - 1 << ") / " << G << ";\n";
   o << "  const int j4 = lane / " << G << ", wi = lane % " << G << ";\n";
-  o << "  for (uint32_t grp = blockIdx.x * " << NWARP << " + wib; grp < ngroups; grp += gridDim.x * " << NWARP << ") {\n";
+  o << "  if (t64 < " << G << ") CW[t64 * " << cstride << " + " << n_coins << "] = 0xFFFFFFFFu;\n";
+  o << "  for (uint32_t grp = blockIdx.x * " << npairs << " + pair; grp < ngroups; grp += gridDim.x * " << npairs << ") {\n";
+  o << "    for (int i = t64; i < " << (size_t)K.nrows * G / 4
+    << "; i += 64) reinterpret_cast<uint4*>(B)[i] = make_uint4(0u, 0u, 0u, 0u);\n";
+  o << "    fs::pair_sync(pair);\n";
   uint32_t maxr = 0;
   for (int c = 0; c < d.num_cases; c++) maxr = std::max(maxr, crow_off[c + 1] - crow_off[c]);
-  o << "    fs::aff_group_faults<" << G << ", " << K.nrows << ", " << (off16 ? "true" : "false") << ", " << std::min<uint32_t>(maxr, 16)
-    << ">(P, tabs, B, seed, word0, grp, A.W, lane);\n";
-  if (n_coins > 0) {  // coin blocks of the group's 8 words, all 32 lanes: lane = (block % 4, word)
-    o << "    for (int cb = j4; cb < " << nblk << "; cb += " << kAffChunk << ") {\n";
-    o << "      const uint4 v = fs::coin_block(seed, word0 + grp * " << G << " + wi, cb);\n";
-    o << "      uint32_t* const d = CW + wi * " << cstride << " + cb * 4;\n";
+  o << "    fs::aff_group_faults<" << G << ", " << (off16 ? "true" : "false") << ", " << std::min<uint32_t>(maxr, 16)
+    << ">(P, tabs, B, seed, word0, grp, A.W, lane, half * " << G / 2 << ", half * " << G / 2 << " + " << G / 2 << ");\n";
+  if (n_coins > 0) {  // coin blocks of the warp's 4 words: lane = (block % 8, word)
+    o << "    for (int cb = lane >> 2; cb < " << nblk << "; cb += 8) {\n";
+    o << "      const int cw_ = half * " << G / 2 << " + (lane & 3);\n";
+    o << "      const uint4 v = fs::coin_block(seed, word0 + grp * " << G << " + cw_, cb);\n";
+    o << "      uint32_t* const d = CW + cw_ * " << cstride << " + cb * 4;\n";
     o << "      d[0] = v.x;";
     o << " if (cb * 4 + 1 < " << n_coins << ") d[1] = v.y;";
     o << " if (cb * 4 + 2 < " << n_coins << ") d[2] = v.z;";
     o << " if (cb * 4 + 3 < " << n_coins << ") d[3] = v.w;\n";
-    o << "    }\n    __syncwarp();\n";
+    o << "    }\n";
   }
-  o << "    if (lane < " << G << ") {\n";
+  o << "    fs::pair_sync(pair);\n";
+  if (!terms_tab.empty()) {
+    o << "    for (int t = j4 + half * " << kAffChunk << "; t < " << terms_tab.size() << "; t += " << 2 * kAffChunk << ") {\n";
+    o << "      const uint32_t e = TERMS[t];\n";
+    o << "      atomicXor(B + ((e & 0xFFFFu) ^ wi), CW[wi * " << cstride << " + (e >> 16)]);\n";
+    o << "    }\n    fs::pair_sync(pair);\n";
+  }
+  o << "    if (half == 0 && lane < " << G << ") {\n";
   o << "      const uint32_t w = grp * " << G << " + lane;\n";
-  o << "      const uint64_t wabs = word0 + w;\n";
   o << "      const uint64_t nleft = w < A.W ? A.nshots - (uint64_t)w * 32 : 0;\n";
   o << "      const uint32_t valid = nleft >= 32 ? 0xFFFFFFFFu : ((1u << nleft) - 1u);\n";
   o << "      uint32_t alive = valid;\n";
   o << "      AL[lane] = valid;\n";
-  for (int cc = 0; cc < n_coins; cc++) o << "      const uint32_t k" << cc << " = CW[lane * " << cstride << " + " << cc << "];\n";
-  for (int r = 0; r < nrows; r++) {
-    const uint64_t* v = rowb.data() + (size_t)r * NW;
-    bool any = false;
-    for (int src = 0; src < el0 && !any; src++) any = ((v[src >> 6] >> (src & 63)) & 1ull) != 0;
-    if (any) o << "      B[" << r * G << " + (lane ^ " << aff_sw(r) << ")] ^= " << row_expr(v) << ";\n";
-  }
   for (int jj = 0; jj < d.num_observables; jj++) o << "      uint32_t ob" << jj << " = 0u;\n";
   o << p2.str();
   o << "      if (w < A.W) {\n";
@@ -494,7 +531,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     o << "        A.obs[(size_t)" << jj << " * A.ostride + w] = ob" << jj << " & valid;\n";
   o << "        A.accepted[w] = alive & valid;\n        A.error[w] = 0u;\n      }\n";
   o << "    }\n";
-  o << "    __syncwarp();\n";
+  o << "    fs::pair_sync(pair);\n";
   o << "    {\n";
   o << "      const uint32_t w = grp * " << G << " + wi;\n";
   o << "      if (w < A.W) {\n";
@@ -502,6 +539,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   o << "        uint32_t* const mo = A.meas + (size_t)j4 * A.ostride + w;\n";
   o << "        uint32_t* const dout = A.det + (size_t)j4 * A.ostride + w;\n";
   o << "        const size_t sc = (size_t)" << kAffChunk << " * A.ostride;\n";
+  int cur_half = 0;
   auto emit_copy = [&](int r0, int cnt, const char* base, int rbase) {
     const int RC = kAffChunk;
     auto sel = [&](const std::vector<std::string>& v) {  // value for this lane's row r + j4
@@ -513,6 +551,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
       return e;
     };
     for (int r = r0; r < r0 + cnt; r += RC) {
+      if (r / RC % 2 != cur_half) continue;  // the other warp of the pair copies this chunk
       // rows r..r+RC-1 (r a multiple of RC): lane row r + j4 at slot (r + j4) * G + (wi ^ sw(r));
       // a differenced row adds its (already rebuilt) parent and is written back for later children
       const int rem = std::min(RC, r0 + cnt - r);
@@ -520,7 +559,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
       bool anyp = false, same_off = true;
       for (int q = 0; q < RC; q++) {
         const int rr = r + q;
-        mv[q] = npsel == 0 ? "m0" : "AL[" + std::to_string((rr < nrows ? row_seg[rr] : 0) * G) + " + wi]";
+        mv[q] = npsel == 0 ? "m0" : "AL[SEG[" + std::to_string(r) + " + j4] * " + std::to_string(G) + " + wi]";
         const int pp = (q < rem && parent[rr] >= 0) ? parent[rr] : -1;
         anyp |= pp >= 0;
         pv[q] = std::to_string(pp >= 0 ? pp : zrow);
@@ -534,7 +573,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
         if (same_off)
           o << " v ^= B[" << parent[r] * G << " + j4 * " << G << " + (wi ^ " << aff_sw(parent[r]) << ")];";
         else
-          o << " { const int pp = " << sel(pv) << "; v ^= B[pp * " << G << " + (wi ^ ((pp / " << RC << ") % " << G << "))]; }";
+          o << " v ^= B[PS[" << r << " + j4] ^ wi];";
         o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")] = v;";
       }
       o << " " << base << "[" << (r - rbase) / RC << " * sc] = v & " << sel(mv) << ";";
@@ -542,11 +581,14 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
       o << " }\n";
     }
   };
-  emit_copy(0, U, "mo", 0);
-  emit_copy(U4, D, "dout", U4);
+  for (cur_half = 0; cur_half < 2; cur_half++) {
+    o << "        " << (cur_half == 0 ? "if (half == 0) {" : "} else {") << "\n";
+    emit_copy(0, U, "mo", 0);
+    emit_copy(U4, D, "dout", U4);
+  }
+  o << "        }\n";
   o << "      }\n    }\n";
-  o << "    __syncwarp();\n  }\n}\n";
-  if (terms > kAffMaxTerms) { K.why = "noiseless part too large"; return K; }
+  o << "    fs::pair_sync(pair);\n  }\n}\n";
   K.src = o.str();
   return K;
 }

@@ -275,32 +275,32 @@ __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, ui
   }
 }
 
-// zero a warp group's row buffer (G words x NROWS rows) and apply the faults of its G words
-template <int G, int NROWS, bool OFF16, int MAXR>
+// faults of words [wi0, wi1) of group grp (row buffer B of the group, zeroed by the caller)
+template <int G, bool OFF16, int MAXR>
 __device__ __forceinline__ void aff_group_faults(const DevProg& P, const AffTabs<OFF16>& T, uint32_t* B, uint64_t seed,
-                                                 uint64_t word0, uint32_t grp, uint32_t W, int lane) {
-  static_assert((NROWS * G) % 4 == 0, "row buffer is zeroed with 16-byte stores");
-  for (int i = lane; i < NROWS * G / 4; i += 32) reinterpret_cast<uint4*>(B)[i] = make_uint4(0u, 0u, 0u, 0u);
-  __syncwarp();
+                                                 uint64_t word0, uint32_t grp, uint32_t W, int lane, uint32_t wi0,
+                                                 uint32_t wi1) {
   if (P.num_runs == 1 && __ldg(P.run_len) > 0 && __ldg(P.run_len) < (1 << 20)) {
     AffRun1 R;
     R.start = __ldg(P.run_start);
     R.limit = 32u * __ldg(P.run_len);
     R.lp = __ldg(P.run_lp);
     R.q = __ldg(P.run_q);
-    for (uint32_t wi = 0; wi < G; wi++) {
+    for (uint32_t wi = wi0; wi < wi1; wi++) {
       const uint32_t w = grp * G + wi;
       if (w >= W) break;
       aff_word_faults_1run<OFF16, MAXR>(T, B, wi, seed, word0 + w, lane, R);
     }
   } else {
-    for (uint32_t wi = 0; wi < G; wi++) {
+    for (uint32_t wi = wi0; wi < wi1; wi++) {
       const uint32_t w = grp * G + wi;
       if (w >= W) break;
       aff_word_faults<OFF16, MAXR>(P, T, B, wi, seed, word0 + w, lane);
     }
   }
-  __syncwarp();
 }
+
+// barrier of the two warps of pair `id` (named barriers 1..15; 0 is __syncthreads)
+__device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id + 1) : "memory"); }
 
 }  // namespace fs

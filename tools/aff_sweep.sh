@@ -1,2 +1,2 @@
-# time the affine kernel of config 1 at several warps-per-block settings (GPU box)
-for wps in ${@:-12 16 20 24}; do echo "warps=$wps"; FS_AFF_WARPS=$wps python tools/aff_check.py 1 | tail -1; done
+# time the affine kernel of config 1 at several warp-pair counts per block (GPU box)
+for np in ${@:-8 10 12}; do echo "pairs=$np"; FS_AFF_PAIRS=$np python tools/aff_check.py 1 | tail -1; done
