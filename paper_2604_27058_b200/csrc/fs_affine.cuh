@@ -388,9 +388,10 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   const size_t tbl_bytes = T.size() * 4;
   // ---- launch shape: a pair of warps per 8-word group; per pair a row buffer (+ a zero row),
   // the alive masks of the post-select segments and the group's coin words
-  K.nrows = nrows + 1;
+  K.nrows = (nrows + 1 + 3) / 4 * 4;  // + zero row, padded so the 32 dump words start at a multiple of 32
   const int nblk = (n_coins + 3) / 4, cstride = (n_coins + 1) | 1;  // coin words + all-ones word (odd stride)
-  const size_t per_pair = ((size_t)K.nrows + psel_bits.size() + 1) * kAffGroup * 4 + (size_t)kAffGroup * cstride * 4;
+  const size_t per_pair =
+      ((size_t)K.nrows + psel_bits.size() + 1) * kAffGroup * 4 + 32 * 4 + (size_t)kAffGroup * cstride * 4;
   int npairs = 0;
   {
     npairs = (int)std::min<size_t>(kAffMaxPairs, tbl_bytes < smem_budget ? (smem_budget - tbl_bytes) / per_pair : 0);
@@ -484,9 +485,11 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   o << "  const uint32_t* const TERMS = tb + " << o_terms << ";\n";
   (void)o_seg;
   o << "  const int pair = wib >> 1, half = wib & 1, t64 = threadIdx.x & 63;\n";
-  o << "  uint32_t* const B = smem + " << bufw << " + pair * " << (size_t)K.nrows * G << ";\n";
-  o << "  uint32_t* const AL = smem + " << bufw + (size_t)npairs * K.nrows * G << " + pair * " << (npsel + 1) * G << ";\n";
-  o << "  uint32_t* const CW = smem + " << bufw + (size_t)npairs * (K.nrows + npsel + 1) * G << " + pair * " << G * cstride
+  o << "  uint32_t* const B = smem + " << bufw << " + pair * " << (size_t)K.nrows * G + 32 << ";\n";
+  o << "  tabs.dump = " << (size_t)K.nrows * G << ";\n";
+  const size_t bufs = (size_t)npairs * ((size_t)K.nrows * G + 32);
+  o << "  uint32_t* const AL = smem + " << bufw + bufs << " + pair * " << (npsel + 1) * G << ";\n";
+  o << "  uint32_t* const CW = smem + " << bufw + bufs + (size_t)npairs * (npsel + 1) * G << " + pair * " << G * cstride
     << ";\n";
   o << "  const uint64_t word0 = A.shot0 >> 5;\n  const uint64_t seed = A.seed;\n";
   o << "  const uint32_t ngroups = (A.W + " << G - 1 << ") / " << G << ";\n";

@@ -126,6 +126,7 @@ struct AffTabs {
   const double* cls_scale;  // nc / p: first guess of the case index
   const double2* lntab;
   int cw;
+  uint32_t dump;  // first of 32 scratch words after the row buffer (multiple of 32)
   __device__ __forceinline__ uint32_t off(int c) const {
     return OFF16 ? (uint32_t)reinterpret_cast<const uint16_t*>(crow_off)[c] : crow_off[c];
   }
@@ -159,9 +160,14 @@ __device__ __forceinline__ void aff_apply(const AffTabs<OFF16>& T, uint32_t* B, 
   const int cs = (int)T.site_case[site] + c;
   const uint32_t bit = 1u << fl;
   const uint32_t j0 = T.off(cs), n = T.off(cs + 1) - j0;
+  // branch-free: slots past the case's list go to the lane's own dump word (B[dump + lane], never
+  // read), so every lane issues the same MAXR shared atomics without divergence
+  const uint32_t dl = T.dump + (threadIdx.x & 31);
 #pragma unroll
-  for (int t = 0; t < MAXR; t++)
-    if ((uint32_t)t < n) atomicXor(B + ((uint32_t)T.crows[j0 + t] ^ wi), bit);
+  for (int t = 0; t < MAXR; t++) {
+    const uint32_t e = (uint32_t)t < n ? (uint32_t)T.crows[j0 + t] : dl;
+    atomicXor(B + (e ^ wi), bit);
+  }
   for (uint32_t t = MAXR; t < n; t++) atomicXor(B + ((uint32_t)T.crows[j0 + t] ^ wi), bit);
 }
 
