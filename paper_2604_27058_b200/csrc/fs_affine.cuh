@@ -25,6 +25,7 @@
 //     and masks later rows exactly like the interpreter (fs_frame.cuh).
 #pragma once
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <sstream>
@@ -501,7 +502,18 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   o << "    fs::pair_sync(pair);\n";
   uint32_t maxr = 0;
   for (int c = 0; c < d.num_cases; c++) maxr = std::max(maxr, crow_off[c + 1] - crow_off[c]);
-  o << "    fs::aff_group_faults<" << G << ", " << (off16 ? "true" : "false") << ", " << std::min<uint32_t>(maxr, 16)
+  // uniform classes: every cum[i] within (i, i + 2) bins of the grid i * p / nc, with margin for rounding
+  bool uniform = true;
+  for (int c = 0; c < ncls; c++) {
+    const double sc = cls_prob[c] > 0.0 ? (double)cls_nc[c] / cls_prob[c] : 0.0;
+    for (int i = 0; i + 1 < cls_nc[c]; i++) {
+      const double gpos = cls_cum[c][i] * sc;  // ideal i + 1
+      if (!(std::fabs(gpos - (i + 1)) < 0.25)) uniform = false;
+    }
+  }
+  if (getenv("FS_AFF_NONUNIFORM")) uniform = false;
+  o << "    fs::aff_group_faults<" << G << ", " << (off16 ? "true" : "false") << ", " << std::min<uint32_t>(maxr, 16) << ", "
+    << (uniform ? "true" : "false")
     << ">(P, tabs, B, seed, word0, grp, A.W, lane, half * " << G / 2 << ", half * " << G / 2 << " + " << G / 2 << ");\n";
   if (n_coins > 0) {  // coin blocks of the warp's 4 words: lane = (block % 8, word)
     o << "    for (int cb = lane >> 2; cb < " << nblk << "; cb += 8) {\n";

@@ -136,7 +136,7 @@ struct AffTabs {
 // then its shot bit XORed into the case's rows of word wi.  Row r of word wi lives at
 // slot(r, wi) = r * G + (wi ^ sw(r)) = slot(r, 0) ^ wi (fs_affine.cuh aff_sw): the lanes working on
 // one word spread over all 32 banks (shared atomics: two lanes may flip the same row).
-template <bool OFF16, int MAXR>
+template <bool OFF16, int MAXR, bool UNIFORM>
 __device__ __forceinline__ void aff_apply(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, int site, int cls, int fl,
                                           double x) {
   const int nc = T.cls_nc[cls];
@@ -148,7 +148,9 @@ __device__ __forceinline__ void aff_apply(const AffTabs<OFF16>& T, uint32_t* B, 
     c = min((int)(x * T.cls_scale[cls]), nc - 1);
     c -= (c > 0 && x < cum[c - 1]) ? 1 : 0;
     c += (c < nc - 1 && !(x < cum[c])) ? 1 : 0;
-    if ((c > 0 && x < cum[c - 1]) || (c < nc - 1 && !(x < cum[c]))) {
+    // classes whose cumulative probabilities sit within one bin of the uniform grid (the host
+    // checks; e.g. DEPOLARIZE1/2) are exact after the one-step correction
+    if (!UNIFORM && ((c > 0 && x < cum[c - 1]) || (c < nc - 1 && !(x < cum[c])))) {
       int lo = 0, hi = nc;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -168,7 +170,8 @@ __device__ __forceinline__ void aff_apply(const AffTabs<OFF16>& T, uint32_t* B, 
     const uint32_t e = (uint32_t)t < n ? (uint32_t)T.crows[j0 + t] : dl;
     atomicXor(B + (e ^ wi), bit);
   }
-  for (uint32_t t = MAXR; t < n; t++) atomicXor(B + ((uint32_t)T.crows[j0 + t] ^ wi), bit);
+  if (MAXR == 16)  // lists longer than the unrolled part (MAXR < 16 covers every case of the program)
+    for (uint32_t t = MAXR; t < n; t++) atomicXor(B + ((uint32_t)T.crows[j0 + t] ^ wi), bit);
 }
 
 // Faults of one 32-shot word, warp-cooperatively: lane j evaluates step st + j of the word's
@@ -176,7 +179,7 @@ __device__ __forceinline__ void aff_apply(const AffTabs<OFF16>& T, uint32_t* B, 
 // positions of a run are an inclusive warp scan of the per-step advances 1 + floor(ln(U) * lp), and
 // the first step past the run's last cell ends it (the following lanes start the next run).
 // Generic over runs (certain sites, several probabilities).
-template <bool OFF16, int MAXR>
+template <bool OFF16, int MAXR, bool UNIFORM>
 __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi,
                                                 uint64_t seed, uint64_t wabs, int lane) {
   const int nruns = P.num_runs;
@@ -236,7 +239,7 @@ __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<
           first = 32;
         }
       }
-      if (site >= 0) aff_apply<OFF16, MAXR>(T, B, wi, site, cls, fl, x);
+      if (site >= 0) aff_apply<OFF16, MAXR, UNIFORM>(T, B, wi, site, cls, fl, x);
     }
     st += 32;
   }
@@ -251,7 +254,7 @@ struct AffRun1 {
   double lp, q;
 };
 
-template <bool OFF16, int MAXR>
+template <bool OFF16, int MAXR, bool UNIFORM>
 __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, uint64_t seed,
                                                      uint64_t wabs, int lane, const AffRun1& R) {
   uint32_t st = 0;
@@ -273,7 +276,7 @@ __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, ui
       const int s = R.start + (pos >> 5);
       const double x = __dmul_rn(u2, R.q);
       const int k = T.site_cls[s];
-      if (x < T.cls_prob[k]) aff_apply<OFF16, MAXR>(T, B, wi, s, k, pos & 31, x);  // thinning: p_site < q
+      if (x < T.cls_prob[k]) aff_apply<OFF16, MAXR, UNIFORM>(T, B, wi, s, k, pos & 31, x);  // thinning: p_site < q
     }
     if (endm) return;
     c = __shfl_sync(0xFFFFFFFFu, pos, 31);
@@ -282,7 +285,7 @@ __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, ui
 }
 
 // faults of words [wi0, wi1) of group grp (row buffer B of the group, zeroed by the caller)
-template <int G, bool OFF16, int MAXR>
+template <int G, bool OFF16, int MAXR, bool UNIFORM>
 __device__ __forceinline__ void aff_group_faults(const DevProg& P, const AffTabs<OFF16>& T, uint32_t* B, uint64_t seed,
                                                  uint64_t word0, uint32_t grp, uint32_t W, int lane, uint32_t wi0,
                                                  uint32_t wi1) {
@@ -295,13 +298,13 @@ __device__ __forceinline__ void aff_group_faults(const DevProg& P, const AffTabs
     for (uint32_t wi = wi0; wi < wi1; wi++) {
       const uint32_t w = grp * G + wi;
       if (w >= W) break;
-      aff_word_faults_1run<OFF16, MAXR>(T, B, wi, seed, word0 + w, lane, R);
+      aff_word_faults_1run<OFF16, MAXR, UNIFORM>(T, B, wi, seed, word0 + w, lane, R);
     }
   } else {
     for (uint32_t wi = wi0; wi < wi1; wi++) {
       const uint32_t w = grp * G + wi;
       if (w >= W) break;
-      aff_word_faults<OFF16, MAXR>(P, T, B, wi, seed, word0 + w, lane);
+      aff_word_faults<OFF16, MAXR, UNIFORM>(P, T, B, wi, seed, word0 + w, lane);
     }
   }
 }
