@@ -36,6 +36,7 @@ namespace fsjit {
 
 constexpr int kAffGroup = 8;              // 32-shot words per group (one 32 B sector of every output row)
 constexpr int kAffChunk = 32 / kAffGroup;  // rows per copy-out instruction
+constexpr int kAffMaxParents = 2;         // rows a copied-out row may be rebuilt from
 constexpr int kAffMaxPairs = 12;          // warp pairs per block (one block per SM; 85 registers per thread)
 // buffer slot of row r for word wi: r * G + (wi ^ sw(r)), sw(r) = (r / kAffChunk) % G (bank spread)
 inline int aff_sw(int r) { return (r / kAffChunk) % kAffGroup; }
@@ -83,14 +84,15 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     }
   }
   if (n_coins > kAffMaxCoins) { K.why = "too many coins"; return K; }
-  // buffer rows: user records [0, U), detectors [U4, U4 + D), ObservableIns rows from U4 + D4,
-  // then hidden bits read by PostSelect (U4, D4 = U, D rounded up to 4: the copy-out writes 4 rows
-  // of one kind per instruction)
+  // buffer rows: detectors [0, D), user records [D4, D4 + U), ObservableIns rows from D4 + U4, then
+  // hidden bits read by PostSelect (D4, U4 = D, U rounded up to the copy-out chunk: it writes
+  // kAffChunk rows of one kind per instruction).  Detectors come first so that record rows can be
+  // rebuilt from them (below).
   const int U4 = (U + kAffChunk - 1) / kAffChunk * kAffChunk, D4 = (D + kAffChunk - 1) / kAffChunk * kAffChunk;
   std::vector<int> bit_row(R + D, -1);  // record / detector id -> buffer row
   for (int r = 0; r < R; r++)
-    if (record_out[r] >= 0) bit_row[r] = record_out[r];
-  for (int j = 0; j < D; j++) bit_row[R + j] = U4 + j;
+    if (record_out[r] >= 0) bit_row[r] = D4 + record_out[r];
+  for (int j = 0; j < D; j++) bit_row[R + j] = j;
   int nrows = U4 + D4 + n_obs_ins;
   for (int b : psel_bits)
     if (bit_row[b] < 0) bit_row[b] = nrows++;
@@ -183,12 +185,13 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   for (int b = 0; b < R + D; b++)
     if (bit_row[b] >= 0) std::copy(RB(b), RB(b) + NW, rowb.data() + (size_t)bit_row[b] * NW);
   // ---- sparser rows by differencing: a copied-out row r may be stored as y_r = v_r ^ v_p for a
-  // parent row p in an earlier 4-row chunk of the copy-out (p < (r & ~3)); the copy-out then
-  // rebuilds v_r = B[r] ^ v_p in order.  For memory experiments the record of ancilla a in round t
+  // set of up to kAffMaxParents parent rows p (greedy, each the one removing the most elements)
+  // in earlier chunks of the same warp's copy-out; the copy-out then rebuilds
+  // v_r = B[r] ^ v_p1 ^ v_p2 ^ ... in order.  For memory experiments the record of ancilla a in round t
   // differs from its round t-1 record by one detector's worth of faults, so record rows shrink
   // to about the size of detector rows.  Rows read before the copy-out (PostSelect, observables)
   // are never differenced.
-  std::vector<int> parent(nrows, -1);
+  std::vector<std::vector<int>> parents(nrows);
   {
     std::vector<uint8_t> fixed_row(nrows, 0);
     for (int r = U4 + D4; r < nrows; r++) fixed_row[r] = 1;
@@ -215,34 +218,44 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     }
     std::vector<int> ov(nrows, 0);
     std::vector<int> cand;
-    const bool nodiff = getenv("FS_AFF_NO_DIFF") != nullptr;
+    int kp = kAffMaxParents;
+    if (getenv("FS_AFF_NO_DIFF")) kp = 0;
+    if (const char* e = getenv("FS_AFF_PARENTS")) kp = std::max(0, std::min(kAffMaxParents, atoi(e)));
     std::vector<uint64_t> y((size_t)nrows * NW);
     std::copy(rowb.begin(), rowb.end(), y.begin());
-    for (int r = 0; r < nrows && !nodiff; r++) {
-      if (fixed_row[r] || sz[r] == 0) continue;
-      const uint64_t* v = rowb.data() + (size_t)r * NW;
-      cand.clear();
-      for (size_t t = 0; t < NW; t++)
-        for (uint64_t m = v[t]; m; m &= m - 1) {
-          const size_t src = t * 64 + __builtin_ctzll(m);
-          if (src < (size_t)el0) continue;
-          for (int q : orows[src - el0]) {
-            if (q >= r - r % kAffChunk) break;
-            if ((q / kAffChunk) % 2 != (r / kAffChunk) % 2) continue;  // copied out by the other warp
-            if (ov[q]++ == 0) cand.push_back(q);
+    for (int r = 0; r < D4; r++) fixed_row[r] = 1;  // detectors stay as they are (sparse; any warp may read them)
+    for (int r = 0; r < nrows; r++) {
+      if (fixed_row[r]) continue;
+      uint64_t* cur = y.data() + (size_t)r * NW;
+      size_t csz = sz[r];
+      for (int round = 0; round < kp && csz > 0; round++) {
+        cand.clear();
+        for (size_t t = 0; t < NW; t++)
+          for (uint64_t m = cur[t]; m; m &= m - 1) {
+            const size_t src = t * 64 + __builtin_ctzll(m);
+            if (src < (size_t)el0) continue;
+            for (int q : orows[src - el0]) {
+              if (q >= r - r % kAffChunk) break;
+              // a differenced parent must be rebuilt earlier by the same warp of the pair
+              if (!fixed_row[q] && (q / kAffChunk) % 2 != (r / kAffChunk) % 2) continue;
+              if (q >= U4 + D4) continue;  // observable / post-select rows: not parents
+              if (ov[q]++ == 0) cand.push_back(q);
+            }
           }
+        int best = -1;
+        size_t bsz = csz;
+        for (int q : cand) {
+          const size_t dsz = csz + sz[q] - 2 * (size_t)ov[q];
+          if (dsz < bsz && std::find(parents[r].begin(), parents[r].end(), q) == parents[r].end()) {
+            bsz = dsz;
+            best = q;
+          }
+          ov[q] = 0;
         }
-      int best = -1;
-      size_t bsz = sz[r];
-      for (int q : cand) {
-        const size_t dsz = sz[r] + sz[q] - 2 * (size_t)ov[q];
-        if (dsz < bsz) { bsz = dsz; best = q; }
-        ov[q] = 0;
-      }
-      if (best >= 0) {
-        parent[r] = best;
-        uint64_t* yr = y.data() + (size_t)r * NW;
-        xr(yr, rowb.data() + (size_t)best * NW);
+        if (best < 0) break;
+        parents[r].push_back(best);
+        xr(cur, rowb.data() + (size_t)best * NW);
+        csz = bsz;
       }
     }
     rowb.swap(y);
@@ -356,14 +369,15 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
       default: break;
     }
   }
-  const size_t o_ps = sec((size_t)(nrows + 1) * 2);
-  {
+  size_t o_ps[kAffMaxParents];
+  for (int k = 0; k < kAffMaxParents; k++) {
+    o_ps[k] = sec((size_t)(nrows + 1) * 2);
     std::vector<uint16_t> ps(nrows + 1);
     for (int r = 0; r <= nrows; r++) {
-      const int pr = r < nrows && parent[r] >= 0 ? parent[r] : zrow;
+      const int pr = r < nrows && (int)parents[r].size() > k ? parents[r][k] : zrow;
       ps[r] = (uint16_t)(pr * kAffGroup | aff_sw(pr));
     }
-    memcpy(T.data() + o_ps, ps.data(), ps.size() * 2);
+    memcpy(T.data() + o_ps[k], ps.data(), ps.size() * 2);
   }
   const size_t o_seg = sec((size_t)(nrows + 1) * 2);
   {
@@ -481,7 +495,8 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   o << "  tabs.lntab = reinterpret_cast<const double2*>(tb + " << o_ln << ");\n";
   o << "  tabs.cls_scale = reinterpret_cast<const double*>(tb + " << o_cs << ");\n";
   o << "  tabs.cw = " << cw << ";\n";
-  o << "  const uint16_t* const PS = reinterpret_cast<const uint16_t*>(tb + " << o_ps << ");\n";
+  for (int k = 0; k < kAffMaxParents; k++)
+    o << "  const uint16_t* const PS" << k << " = reinterpret_cast<const uint16_t*>(tb + " << o_ps[k] << ");\n";
   o << "  const uint16_t* const SEG = reinterpret_cast<const uint16_t*>(tb + " << o_seg << ");\n";
   o << "  const uint32_t* const TERMS = tb + " << o_terms << ";\n";
   (void)o_seg;
@@ -557,49 +572,28 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   int cur_half = 0;
   auto emit_copy = [&](int r0, int cnt, const char* base, int rbase) {
     const int RC = kAffChunk;
-    auto sel = [&](const std::vector<std::string>& v) {  // value for this lane's row r + j4
-      bool same = true;
-      for (auto& x : v) same &= x == v[0];
-      if (same) return v[0];
-      std::string e = v[RC - 1];
-      for (int q = RC - 2; q >= 0; q--) e = "(j4 == " + std::to_string(q) + " ? " + v[q] + " : " + e + ")";
-      return e;
-    };
     for (int r = r0; r < r0 + cnt; r += RC) {
       if (r / RC % 2 != cur_half) continue;  // the other warp of the pair copies this chunk
-      // rows r..r+RC-1 (r a multiple of RC): lane row r + j4 at slot (r + j4) * G + (wi ^ sw(r));
-      // a differenced row adds its (already rebuilt) parent and is written back for later children
+      // rows r..r+RC-1 (r a multiple of RC): lane row r + j4 at slot (r + j4) * G + (wi ^ sw(r)); a
+      // differenced row adds its (already rebuilt) parents and is written back for later children
       const int rem = std::min(RC, r0 + cnt - r);
-      std::vector<std::string> mv(RC), pv(RC);
-      bool anyp = false, same_off = true;
-      for (int q = 0; q < RC; q++) {
-        const int rr = r + q;
-        mv[q] = npsel == 0 ? "m0" : "AL[SEG[" + std::to_string(r) + " + j4] * " + std::to_string(G) + " + wi]";
-        const int pp = (q < rem && parent[rr] >= 0) ? parent[rr] : -1;
-        anyp |= pp >= 0;
-        pv[q] = std::to_string(pp >= 0 ? pp : zrow);
-        const int p0 = (parent[r] >= 0) ? parent[r] : -1;
-        same_off &= q < rem && pp >= 0 && p0 >= 0 && pp - rr == p0 - r && p0 % RC == 0;
-      }
+      size_t np = 0;
+      for (int q = 0; q < rem; q++) np = std::max(np, parents[r + q].size());
+      const std::string m = npsel == 0 ? "m0" : "AL[SEG[" + std::to_string(r) + " + j4] * " + std::to_string(G) + " + wi]";
       o << "        {";
       if (rem < RC) o << " if (j4 < " << rem << ") {";
       o << " uint32_t v = B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")];";
-      if (anyp) {
-        if (same_off)
-          o << " v ^= B[" << parent[r] * G << " + j4 * " << G << " + (wi ^ " << aff_sw(parent[r]) << ")];";
-        else
-          o << " v ^= B[PS[" << r << " + j4] ^ wi];";
-        o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")] = v;";
-      }
-      o << " " << base << "[" << (r - rbase) / RC << " * sc] = v & " << sel(mv) << ";";
+      for (size_t k = 0; k < np; k++) o << " v ^= B[PS" << k << "[" << r << " + j4] ^ wi];";
+      if (np) o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")] = v;";
+      o << " " << base << "[" << (r - rbase) / RC << " * sc] = v & " << m << ";";
       if (rem < RC) o << " }";
       o << " }\n";
     }
   };
   for (cur_half = 0; cur_half < 2; cur_half++) {
     o << "        " << (cur_half == 0 ? "if (half == 0) {" : "} else {") << "\n";
-    emit_copy(0, U, "mo", 0);
-    emit_copy(U4, D, "dout", U4);
+    emit_copy(0, D, "dout", 0);
+    emit_copy(D4, U, "mo", D4);
   }
   o << "        }\n";
   o << "      }\n    }\n";
