@@ -37,7 +37,7 @@ namespace fsjit {
 constexpr int kAffGroup = 8;              // 32-shot words per group (one 32 B sector of every output row)
 constexpr int kAffChunk = 32 / kAffGroup;  // rows per copy-out instruction
 constexpr int kAffMaxParents = 2;         // rows a copied-out row may be rebuilt from
-constexpr int kAffMaxPairs = 12;          // warp pairs per block (one block per SM; 85 registers per thread)
+constexpr int kAffMaxPairs = 15;          // warp pairs per block (one block per SM; named barriers 1..15)
 // buffer slot of row r for word wi: r * G + (wi ^ sw(r)), sw(r) = (r / kAffChunk) % G (bank spread)
 inline int aff_sw(int r) { return (r / kAffChunk) % kAffGroup; }
 constexpr int kAffMaxCoins = 128;         // coin words kept in registers
