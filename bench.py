@@ -181,7 +181,7 @@ def workload_config(cfg: int) -> dict:
             "parallelism": "replicas (shot ranges), no collective"}
 
 
-KERNEL_NAME = {"frame": "fs_jit_frame (program-specialised frame kernel)",
+KERNEL_NAME = {"frame": "fs_aff_frame (affine frame kernel: fault-effect row tables, warp-cooperative noise stream)",
                "general": "general / block kernel", "hbm": "hbm_fused_pass_kernel"}
 
 
@@ -263,7 +263,7 @@ def extra_config(c: int, fp64_tflops: float) -> dict:
     import ctypes as C
 
     steps = 1 if c == 3 else 3
-    rc = time_gpu_config(c, steps, 1, 0, warm_shots=64 if c == 3 else None)
+    rc = time_gpu_config(c, steps, 1, 0)
     P, shots = rc["P"], rc["shots"]
     ms = float(np.mean(rc["ms"]))
     rate = shots / (ms / 1e3)
