@@ -362,7 +362,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     switch (FS_OPCODE(I[0])) {
       case FS_OP_MEAS_DSTATIC:
       case FS_OP_MEAS_DRANDOM:
-        if (record_out[I[3]] >= 0) row_seg[record_out[I[3]]] = npsel;
+        if (record_out[I[3]] >= 0) row_seg[bit_row[I[3]]] = npsel;
         break;
       case FS_OP_DETECTOR: row_seg[bit_row[R + I[1]]] = npsel; break;
       case FS_OP_POSTSELECT: npsel++; break;
@@ -583,7 +583,16 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
       o << "        {";
       if (rem < RC) o << " if (j4 < " << rem << ") {";
       o << " uint32_t v = B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")];";
-      for (size_t k = 0; k < np; k++) o << " v ^= B[PS" << k << "[" << r << " + j4] ^ wi];";
+      for (size_t k = 0; k < np; k++) {
+        // parents of the chunk's rows at one common offset from a chunk-aligned row: constant slots
+        const int p0 = parents[r].size() > k ? parents[r][k] : -1;
+        bool same = p0 >= 0 && p0 % RC == 0;
+        for (int q = 1; q < rem && same; q++) same = parents[r + q].size() > k && parents[r + q][k] == p0 + q;
+        if (same)
+          o << " v ^= B[" << p0 * G << " + j4 * " << G << " + (wi ^ " << aff_sw(p0) << ")];";
+        else
+          o << " v ^= B[PS" << k << "[" << r << " + j4] ^ wi];";
+      }
       if (np) o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")] = v;";
       o << " " << base << "[" << (r - rbase) / RC << " * sc] = v & " << m << ";";
       if (rem < RC) o << " }";

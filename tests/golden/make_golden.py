@@ -272,6 +272,54 @@ def main(which=("configs", "random", "toys")):
                         payload[f"{fmt}_{int(keep)}"] = np.frombuffer(open(opath, "rb").read(), dtype=np.uint8)
             np.savez_compressed(fdir / f"{name}.npz", **payload)
             print(f"formats/{name:20s} ({time.time() - t0:.1f}s)", flush=True)
+    if "affine" in which:  # frame-only programs exercising the affine frame kernel's paths
+        rng_a = np.random.default_rng(77)
+        # repetition memory with post-selected early detectors and an observable across them
+        rep = []
+        d, rounds = 5, 4
+        data, anc = list(range(0, 2 * d - 1, 2)), list(range(1, 2 * d - 1, 2))
+        for r in range(rounds):
+            rep.append("DEPOLARIZE1(0.01) " + " ".join(map(str, data)))
+            for a in anc:
+                rep.append(f"CX {a - 1} {a}\nCX {a + 1} {a}")
+            rep.append("X_ERROR(0.02) " + " ".join(map(str, anc)))
+            rep.append("M " + " ".join(map(str, anc)))
+            for j in range(len(anc)):
+                k = len(anc) - j
+                rep.append(f"DETECTOR rec[-{k}]" + (f" rec[-{k + len(anc)}]" if r else ""))
+            rep.append("R " + " ".join(map(str, anc)))
+        rep.append("X_ERROR(0.02) " + " ".join(map(str, data)))
+        rep.append("M " + " ".join(map(str, data)))
+        rep.append("OBSERVABLE_INCLUDE(0) rec[-1]")
+        # mixed noise: several probabilities (runs), near-equal ones (thinning), certain sites,
+        # Y/Z errors, MX/MY, resets, detectors and in-circuit POSTSELECT
+        mix = []
+        n = 6
+        for layer in range(8):
+            for q in range(n):
+                mix.append(["H", "S", "S_DAG", "X", "Y", "Z"][int(rng_a.integers(6))] + f" {q}")
+            perm = rng_a.permutation(n)
+            mix.append("CX " + " ".join(str(int(x)) for x in perm))
+            mix.append(f"DEPOLARIZE2(0.03) " + " ".join(str(int(x)) for x in perm))
+            mix.append(f"Y_ERROR(0.02) {layer % n}\nZ_ERROR(0.02) {(layer + 1) % n}")
+            mix.append(f"X_ERROR({0.02 * (1 + 1e-12)!r}) {(layer + 2) % n}")
+            if layer == 3:
+                mix.append("X_ERROR(1.0) 2\nDEPOLARIZE1(1.0) 4")
+            if layer % 2 == 1:
+                mix.append(f"MX {layer % n}\nMY {(layer + 3) % n}\nDETECTOR rec[-1] rec[-2]\nR {layer % n} {(layer + 3) % n}")
+            if layer == 5:
+                mix.append("M 1\nPOSTSELECT rec[-1]")
+        mix.append("M " + " ".join(map(str, range(n))))
+        mix.append("DETECTOR rec[-1] rec[-2]\nOBSERVABLE_INCLUDE(0) rec[-3] rec[-6]\nOBSERVABLE_INCLUDE(1) rec[-4]")
+        aff = {
+            "aff_rep_psel": ("\n".join(rep) + "\n", (0, 1, 2, 3, 5, 6)),
+            "aff_rep": ("\n".join(rep) + "\n", ()),
+            "aff_mixed": ("\n".join(mix) + "\n", ()),
+        }
+        for name, (text, ps) in aff.items():
+            prog = compile_circuit(text, optimize=True, postselect_detectors=ps)
+            assert prog.k_max == 0, name
+            write_case(name, prog, text, free_shots=512, trace_shots=16, boost=5.0)
     if "stratum" in which:  # stratified importance sampling (runtime.py:886-945)
         from framesim.runtime import StratumSpec
         from framesim import cli as fcli
