@@ -136,9 +136,8 @@ struct AffTabs {
 // then its shot bit XORed into the case's rows of word wi.  Row r of word wi lives at
 // slot(r, wi) = r * G + (wi ^ sw(r)) = slot(r, 0) ^ wi (fs_affine.cuh aff_sw): the lanes working on
 // one word spread over all 32 banks (shared atomics: two lanes may flip the same row).
-template <bool OFF16, int MAXR, bool UNIFORM>
-__device__ __forceinline__ void aff_apply(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, int site, int cls, int fl,
-                                          double x) {
+template <bool OFF16, bool UNIFORM>
+__device__ __forceinline__ int aff_case(const AffTabs<OFF16>& T, int site, int cls, double x) {
   const int nc = T.cls_nc[cls];
   int c = 0;
   if (nc > 1) {
@@ -159,19 +158,21 @@ __device__ __forceinline__ void aff_apply(const AffTabs<OFF16>& T, uint32_t* B, 
       c = lo < nc - 1 ? lo : nc - 1;
     }
   }
-  const int cs = (int)T.site_case[site] + c;
-  const uint32_t bit = 1u << fl;
-  const uint32_t j0 = T.off(cs), n = T.off(cs + 1) - j0;
-  // branch-free: slots past the case's list go to the lane's own dump word (B[dump + lane], never
-  // read), so every lane issues the same MAXR shared atomics without divergence
+  return (int)T.site_case[site] + c;
+}
+
+// All lanes together (converged): lane l XORs `bit` into the n rows crows[j0 .. j0 + n) of word wi
+// (n = 0: no fault).  The trip count is the warp's largest n; slots past a lane's list go to its own
+// dump word (B[dump + lane], never read), so the shared atomics issue without divergence.
+template <bool OFF16>
+__device__ __forceinline__ void aff_rows(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, uint32_t j0, uint32_t n,
+                                         uint32_t bit) {
+  const uint32_t nmax = __reduce_max_sync(0xFFFFFFFFu, n);
   const uint32_t dl = T.dump + (threadIdx.x & 31);
-#pragma unroll
-  for (int t = 0; t < MAXR; t++) {
-    const uint32_t e = (uint32_t)t < n ? (uint32_t)T.crows[j0 + t] : dl;
+  for (uint32_t t = 0; t < nmax; t++) {
+    const uint32_t e = t < n ? (uint32_t)T.crows[j0 + t] : dl;
     atomicXor(B + (e ^ wi), bit);
   }
-  if (MAXR == 16)  // lists longer than the unrolled part (MAXR < 16 covers every case of the program)
-    for (uint32_t t = MAXR; t < n; t++) atomicXor(B + ((uint32_t)T.crows[j0 + t] ^ wi), bit);
 }
 
 // Faults of one 32-shot word, warp-cooperatively: lane j evaluates step st + j of the word's
@@ -239,7 +240,13 @@ __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<
           first = 32;
         }
       }
-      if (site >= 0) aff_apply<OFF16, MAXR, UNIFORM>(T, B, wi, site, cls, fl, x);
+      uint32_t j0 = 0, n = 0;
+      if (site >= 0) {
+        const int cs = aff_case<OFF16, UNIFORM>(T, site, cls, x);
+        j0 = T.off(cs);
+        n = T.off(cs + 1) - j0;
+      }
+      aff_rows<OFF16>(T, B, wi, j0, n, 1u << fl);
     }
     st += 32;
   }
@@ -272,12 +279,18 @@ __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, ui
     const int pos = c + inc;
     const bool in = pos < (int)R.limit;
     const uint32_t endm = __ballot_sync(0xFFFFFFFFu, !in);
+    uint32_t j0 = 0, n = 0;
     if (in) {
       const int s = R.start + (pos >> 5);
       const double x = __dmul_rn(u2, R.q);
       const int k = T.site_cls[s];
-      if (x < T.cls_prob[k]) aff_apply<OFF16, MAXR, UNIFORM>(T, B, wi, s, k, pos & 31, x);  // thinning: p_site < q
+      if (x < T.cls_prob[k]) {  // thinning: p_site < q
+        const int cs = aff_case<OFF16, UNIFORM>(T, s, k, x);
+        j0 = T.off(cs);
+        n = T.off(cs + 1) - j0;
+      }
     }
+    aff_rows<OFF16>(T, B, wi, j0, n, 1u << (pos & 31));
     if (endm) return;
     c = __shfl_sync(0xFFFFFFFFu, pos, 31);
     st += 32;
