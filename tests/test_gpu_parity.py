@@ -171,6 +171,24 @@ def test_gpu_jit_equals_interpreter(cuda, name, monkeypatch):
     _same(b, c)
 
 
+@pytest.mark.parametrize("name", ["config1", "aff_mixed", "aff_rep_psel", "toy_certain", "rand06"])
+@pytest.mark.parametrize("env", [{"FS_AFF_GLOBAL_TABLES": "1"}, {"FS_AFF_PAIRS": "1"}, {"FS_AFF_NONUNIFORM": "1"},
+                                 {"FS_AFF_NO_DIFF": "1"}, {"FS_AFF_PARENTS": "1"}])
+def test_gpu_affine_variants_match_oracle(cuda, name, env, monkeypatch):
+    """Affine frame kernel variants (fault tables in global memory, one warp pair per block, the
+    exact-bisect case pick, no / single-parent row differencing) == oracle, bit for bit; odd shot
+    count and offset so the tail word and partial groups are exercised."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    P = load(name)["prog"]
+    dp = _dev(P)  # a fresh program handle: the kernel is generated at its first sample call
+    n = 3 * 256 + 37
+    _, g, _ = dp.sample_host(n, seed=19, shot0=32 * 5, flags=FS_RNG_PHILOX)
+    assert "affine: ready" in dp.jit_status(), dp.jit_status()
+    _, o, _ = oracle.sample(P, n, seed=19, shot0=32 * 5, flags=FS_RNG_PHILOX)
+    _same(g, o)
+
+
 @pytest.mark.parametrize("name", [c for c in CASES if 0 < load(c)["prog"].k_max <= 7 and not load(c)["prog"].has_postselect
                                   and not (set((load(c)["prog"].instrs[:, 0] & 0xFF).tolist()) & {7, 9})])
 def test_gpu_general_jit_equals_interpreter(cuda, name):
