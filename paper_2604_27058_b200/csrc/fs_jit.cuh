@@ -389,7 +389,9 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
   else
     o << "    AR[0] = make_double2(1.0, 0.0);\n";
   o << "    uint4 cb = make_uint4(0u, 0u, 0u, 0u);\n";
-  o << "    const uint32_t nt_ = ntot[w];\n    const bool fover = nt_ == 0xFFFFFFFFu;\n    uint32_t fcur = 0;\n";
+  // no NoiseBlock: no fault lists (the launcher skips their kernel)
+  if (K.nblocks) o << "    const uint32_t nt_ = ntot[w];\n    const bool fover = nt_ == 0xFFFFFFFFu;\n    uint32_t fcur = 0;\n";
+  else o << "    const bool fover = false;\n    uint32_t fcur = 0;\n";
   o << "    fs::WordFaultGen gen;\n    int psite = -1, plane = 0, pcase = 0;\n    if (fover) gen.init(seed, wabs);\n";
   auto put_record = [&](int rec, const std::string& expr) {
     const int col = record_out[rec], sl = bit_slot[rec];

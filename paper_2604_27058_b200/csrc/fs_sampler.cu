@@ -1965,7 +1965,7 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     uint32_t *fent = nullptr, *bcount = nullptr, *ntot = nullptr;
     int rc = alloc_fault_lists(p, a.W, &fent, &bcount, &ntot);
     if (rc) return rc;
-    if ((rc = run_fault_lists(p, a, 0, a.W, fent, bcount, ntot, stream))) return rc;
+    if (p->jit_nblocks && (rc = run_fault_lists(p, a, 0, a.W, fent, bcount, ntot, stream))) return rc;
     fsjit::Api& J = fsjit::api();
     int occ = 1;
     J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->jit.fn, p->gjit_threads, p->gjit_smem);
