@@ -196,6 +196,10 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 cmul_f(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x));
 }
+// cmul_f(u, a) for a u with a zero imaginary (cmul_re) or real (cmul_im) part: the vanishing
+// products drop out of the FMAs exactly, so these give the same doubles with two multiplies
+__device__ __forceinline__ double2 cmul_re(double ux, double2 a) { return make_double2(__dmul_rn(ux, a.x), __dmul_rn(ux, a.y)); }
+__device__ __forceinline__ double2 cmul_im(double uy, double2 a) { return make_double2(-__dmul_rn(uy, a.y), __dmul_rn(uy, a.x)); }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
 // python complex * float (runtime.py: `buf[i] * scale`): real-scaled, no FMA contraction

@@ -499,18 +499,28 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
           else o << "    " << f(Z(q)) << " ^= " << f(X(q)) << ";\n";
         }
         const int fo = I[5];
+        // complex products with a compile-time-real (or imaginary) factor: the zero component's
+        // products vanish from cmul_f exactly, so two multiplies give the same doubles
+        auto cm = [&](int uoff, const std::string& u, const std::string& a) -> std::string {
+          if (fparams[uoff + 1] == 0.0) return "fs::cmul_re(" + u + ".x, " + a + ")";
+          if (fparams[uoff] == 0.0) return "fs::cmul_im(" + u + ".y, " + a + ")";
+          return "cmul(" + u + ", " + a + ")";
+        };
+        const bool k0re = fparams[fo + 1] == 0.0 && fparams[fo + 5] == 0.0;
+        const bool k1re = fparams[fo + 3] == 0.0 && fparams[fo + 7] == 0.0;
         o << "    {\n      const double2 u00 = " << C(fo) << ", u01 = " << C(fo + 2) << ", u10 = " << C(fo + 4)
           << ", u11 = " << C(fo + 6) << ";\n";
         o << "      const int parity = (" << f(X(virt)) << " >> lane) & 1;\n";
         o << "      double p1 = 0.0, p_all = 0.0;\n";
         if (size == 2) {
-          o << "      { const double2 b0 = cadd(cmul(u00, " << A(0) << "), cmul(u01, " << A(1) << ")); const double2 b1 = cadd(cmul(u10, "
-            << A(0) << "), cmul(u11, " << A(1) << ")); p1 = cnorm2(b1); p_all = __dadd_rn(p1, cnorm2(b0)); }\n";
+          o << "      { const double2 b0 = cadd(" << cm(fo, "u00", A(0)) << ", " << cm(fo + 2, "u01", A(1)) << "); const double2 b1 = cadd("
+            << cm(fo + 4, "u10", A(0)) << ", " << cm(fo + 6, "u11", A(1)) << "); p1 = cnorm2(b1); p_all = __dadd_rn(p1, cnorm2(b0)); }\n";
         } else if (size <= 16) {
           for (int j = 0; j < size; j++)
             if (!((j >> a) & 1))
               o << "      { const double2 a0_ = " << A(j) << ", a1_ = " << A(j + st)
-                << "; const double q1 = cnorm2(cadd(cmul(u10, a0_), cmul(u11, a1_))); const double2 b0 = cadd(cmul(u00, a0_), cmul(u01, a1_)); "
+                << "; const double q1 = cnorm2(cadd(" << cm(fo + 4, "u10", "a0_") << ", " << cm(fo + 6, "u11", "a1_")
+                << ")); const double2 b0 = cadd(" << cm(fo, "u00", "a0_") << ", " << cm(fo + 2, "u01", "a1_") << "); "
                    "p1 = __dadd_rn(p1, q1); p_all = __dadd_rn(p_all, __dadd_rn(q1, cnorm2(b0))); }\n";
         } else {
           for (int j = 0; j < size; j++)
@@ -529,7 +539,8 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
         o << "      const double2 k1 = br == 0 ? cscale(u01, scale) : cscale(u11, scale);\n";
         for (int j = 0; j < half; j++) {
           const int i0 = ((j >> a) << (a + 1)) | (j & (st - 1));
-          o << "      " << A(j) << " = cadd(cmul(k0, " << A(i0) << "), cmul(k1, " << A(i0 + st) << "));\n";
+          o << "      " << A(j) << " = cadd(" << (k0re ? "fs::cmul_re(k0.x, " + A(i0) + ")" : "cmul(k0, " + A(i0) + ")") << ", "
+            << (k1re ? "fs::cmul_re(k1.x, " + A(i0 + st) + ")" : "cmul(k1, " + A(i0 + st) + ")") << ");\n";
         }
         o << "      const uint32_t badw = __ballot_sync(0xFFFFFFFFu, bad && ((alive >> lane) & 1));\n";
         o << "      errm |= badw; alive &= ~badw;\n";
