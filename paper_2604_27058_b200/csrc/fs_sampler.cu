@@ -130,7 +130,7 @@ struct fs_prog {
   std::string aff_error;
   fsjit::Compiled aff;
   uint32_t* d_aff_tables = nullptr;
-  int aff_threads = 0, aff_rows = 0;
+  int aff_threads = 0, aff_rows = 0, aff_occ = 0;
   size_t aff_smem = 0;
   // stratified sampling: suffix Poisson-binomial table of stratum w, per-chunk modes + outputs
   int strat_w = -1;
@@ -698,10 +698,14 @@ int ensure_aff(fs_prog* p) {
 
 int launch_aff(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   fsjit::Api& J = fsjit::api();
-  int occ = 1;
-  J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->aff.fn, p->aff_threads, p->aff_smem);
-  const size_t blocks = (a.W + p->aff_threads - 1) / p->aff_threads;
-  const size_t grid = std::min<size_t>(blocks, (size_t)p->num_sms * std::max(occ, 1));
+  if (p->aff_occ == 0) {  // once per program: the launch path stays free of driver queries
+    int occ = 1;
+    J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->aff.fn, p->aff_threads, p->aff_smem);
+    p->aff_occ = std::max(occ, 1);
+  }
+  const size_t groups = (a.W + 7) / 8, pairs = p->aff_threads / 64;  // one 8-word group per warp pair
+  const size_t blocks = (groups + pairs - 1) / pairs;
+  const size_t grid = std::min<size_t>(std::max<size_t>(blocks, 1), (size_t)p->num_sms * p->aff_occ);
   fs::DevProg dpv = p->dp;
   const uint32_t* tb = p->d_aff_tables;
   void* args[] = {&dpv, &a, &tb};

@@ -8,3 +8,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 ncu --set full --clock-control none --import-source on -k regex:fs_aff_frame -c 1 -o gpurun_out/prof_c1_aff \
   python tools/one_call.py 1 10000000 > gpurun_out/ncu_aff.log 2>&1
 ls -la gpurun_out/*.ncu-rep gpurun_out/launches.csv
+ncu --set full --clock-control none --import-source on -k regex:fs_jit_general -c 1 -o gpurun_out/prof_c2_gjit \
+  python tools/one_call.py 2 10000000 > gpurun_out/ncu_c2.log 2>&1
