@@ -36,7 +36,7 @@ namespace fsjit {
 
 constexpr int kAffGroup = 8;              // 32-shot words per group (one 32 B sector of every output row)
 constexpr int kAffChunk = 32 / kAffGroup;  // rows per copy-out instruction
-constexpr int kAffMaxParents = 2;         // rows a copied-out row may be rebuilt from
+constexpr int kAffMaxParents = 6;         // rows a copied-out row may be rebuilt from
 constexpr int kAffMaxPairs = 15;          // warp pairs per block (one block per SM; named barriers 1..15)
 // buffer slot of row r for word wi: r * G + (wi ^ sw(r)), sw(r) = (r / kAffChunk) % G (bank spread)
 inline int aff_sw(int r) { return (r / kAffChunk) % kAffGroup; }
@@ -184,10 +184,12 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   }
   for (int b = 0; b < R + D; b++)
     if (bit_row[b] >= 0) std::copy(RB(b), RB(b) + NW, rowb.data() + (size_t)bit_row[b] * NW);
-  // ---- sparser rows by differencing: a copied-out row r may be stored as y_r = v_r ^ v_p for a
-  // set of up to kAffMaxParents parent rows p (greedy, each the one removing the most elements)
-  // in earlier chunks of the same warp's copy-out; the copy-out then rebuilds
-  // v_r = B[r] ^ v_p1 ^ v_p2 ^ ... in order.  For memory experiments the record of ancilla a in round t
+  // ---- sparser rows by differencing: a copied-out record row r may be stored as y_r = v_r ^ v_p1
+  // ^ ... for up to kAffMaxParents parent rows (greedy: each round the detector row that most
+  // lowers the row's expected fault atomics, sum over cases of P(case) [case flips the row]); the
+  // copy-out rebuilds v_r = B[r] ^ B[p1] ^ ... from rows that are never rebuilt themselves, so its
+  // chunks carry no shared-memory write-back / re-read chains (FS_AFF_ANY_PARENTS also allows
+  // earlier rebuilt rows of the same warp).  For memory experiments the record of ancilla a in round t
   // differs from its round t-1 record by one detector's worth of faults, so record rows shrink
   // to about the size of detector rows.  Rows read before the copy-out (PostSelect, observables)
   // are never differenced.
@@ -216,9 +218,47 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
           if (src >= (size_t)el0) orows[src - el0].push_back(r);
         }
     }
+    // cost of a row vector = expected shared atomics it causes: sum over fault cases c of
+    // P(case c) [the case flips the row], i.e. of cases with an odd number of the row's elements
+    std::vector<std::vector<int>> el_cases(NE);
+    std::vector<double> cw(d.num_cases, 0.0);
+    for (int st = 0; st < E; st++)
+      for (int c = site_case_off[st]; c < site_case_off[st + 1]; c++) {
+        cw[c] = case_cum[c] - (c > site_case_off[st] ? case_cum[c - 1] : 0.0);
+        if (!(cw[c] > 0.0)) cw[c] = 1e-30;
+        for (int j = case_pauli_off[c]; j < case_pauli_off[c + 1]; j++)
+          if (case_el[j] >= 0) el_cases[case_el[j]].push_back(c);
+      }
+    std::vector<uint8_t> cpar(d.num_cases, 0);
+    std::vector<int> ctouch;
+    auto toggle = [&](const uint64_t* v) {
+      for (size_t t = 0; t < NW; t++)
+        for (uint64_t m = v[t]; m; m &= m - 1) {
+          const size_t src = t * 64 + __builtin_ctzll(m);
+          if (src < (size_t)el0) continue;
+          for (int c : el_cases[src - el0]) {
+            if (!cpar[c]) ctouch.push_back(c);
+            cpar[c] ^= 2;  // bit 1 = parity, bit 0 unused (touched list keeps duplicates harmless)
+          }
+        }
+    };
+    auto cost2 = [&](const uint64_t* a, const uint64_t* b) {  // cost of a ^ b (b may be null)
+      ctouch.clear();
+      toggle(a);
+      if (b) toggle(b);
+      double c = 0.0;
+      for (int k : ctouch) {
+        if (cpar[k] & 2) c += cw[k];
+        cpar[k] = 0;
+      }
+      return c;
+    };
     std::vector<int> ov(nrows, 0);
     std::vector<int> cand;
     int kp = kAffMaxParents;
+    // parents among the never-rebuilt rows only (detectors): the copy-out then has no shared-memory
+    // write-back / re-read chains between its chunks
+    const bool only_fixed = getenv("FS_AFF_ANY_PARENTS") == nullptr;
     if (getenv("FS_AFF_NO_DIFF")) kp = 0;
     if (const char* e = getenv("FS_AFF_PARENTS")) kp = std::max(0, std::min(kAffMaxParents, atoi(e)));
     std::vector<uint64_t> y((size_t)nrows * NW);
@@ -228,6 +268,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
       if (fixed_row[r]) continue;
       uint64_t* cur = y.data() + (size_t)r * NW;
       size_t csz = sz[r];
+      double ccost = cost2(cur, nullptr);
       for (int round = 0; round < kp && csz > 0; round++) {
         cand.clear();
         for (size_t t = 0; t < NW; t++)
@@ -237,25 +278,30 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
             for (int q : orows[src - el0]) {
               if (q >= r - r % kAffChunk) break;
               // a differenced parent must be rebuilt earlier by the same warp of the pair
-              if (!fixed_row[q] && (q / kAffChunk) % 2 != (r / kAffChunk) % 2) continue;
+              if (!fixed_row[q] && (only_fixed || (q / kAffChunk) % 2 != (r / kAffChunk) % 2)) continue;
               if (q >= U4 + D4) continue;  // observable / post-select rows: not parents
               if (ov[q]++ == 0) cand.push_back(q);
             }
           }
         int best = -1;
         size_t bsz = csz;
+        double bcost = ccost * (1.0 - 1e-9);
         for (int q : cand) {
           const size_t dsz = csz + sz[q] - 2 * (size_t)ov[q];
-          if (dsz < bsz && std::find(parents[r].begin(), parents[r].end(), q) == parents[r].end()) {
+          ov[q] = 0;
+          if (std::find(parents[r].begin(), parents[r].end(), q) != parents[r].end()) continue;
+          const double qc = cost2(cur, rowb.data() + (size_t)q * NW);
+          if (qc < bcost) {
+            bcost = qc;
             bsz = dsz;
             best = q;
           }
-          ov[q] = 0;
         }
         if (best < 0) break;
         parents[r].push_back(best);
         xr(cur, rowb.data() + (size_t)best * NW);
         csz = bsz;
+        ccost = bcost;
       }
     }
     rowb.swap(y);
@@ -569,6 +615,9 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   o << "        uint32_t* const mo = A.meas + (size_t)j4 * A.ostride + w;\n";
   o << "        uint32_t* const dout = A.det + (size_t)j4 * A.ostride + w;\n";
   o << "        const size_t sc = (size_t)" << kAffChunk << " * A.ostride;\n";
+  std::vector<uint8_t> is_parent(nrows + 1, 0);
+  for (int r = 0; r < nrows; r++)
+    for (int q : parents[r]) is_parent[q] = 1;
   int cur_half = 0;
   auto emit_copy = [&](int r0, int cnt, const char* base, int rbase) {
     const int RC = kAffChunk;
@@ -593,7 +642,9 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
         else
           o << " v ^= B[PS" << k << "[" << r << " + j4] ^ wi];";
       }
-      if (np) o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")] = v;";
+      bool wb = false;  // some later row rebuilds from one of these rows
+      for (int q = 0; q < rem && !wb; q++) wb = is_parent[r + q];
+      if (np && wb) o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")] = v;";
       o << " " << base << "[" << (r - rbase) / RC << " * sc] = v & " << m << ";";
       if (rem < RC) o << " }";
       o << " }\n";

@@ -130,7 +130,7 @@ struct fs_prog {
   std::string aff_error;
   fsjit::Compiled aff;
   uint32_t* d_aff_tables = nullptr;
-  int aff_threads = 0, aff_rows = 0, aff_occ = 0;
+  int aff_threads = 0, aff_rows = 0, aff_occ = 0, gjit_occ = 0;
   size_t aff_smem = 0;
   // stratified sampling: suffix Poisson-binomial table of stratum w, per-chunk modes + outputs
   int strat_w = -1;
@@ -1971,8 +1971,12 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     if (rc) return rc;
     if (p->jit_nblocks && (rc = run_fault_lists(p, a, 0, a.W, fent, bcount, ntot, stream))) return rc;
     fsjit::Api& J = fsjit::api();
-    int occ = 1;
-    J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->jit.fn, p->gjit_threads, p->gjit_smem);
+    if (p->gjit_occ == 0) {  // once per program
+      int o1 = 1;
+      J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&o1, p->jit.fn, p->gjit_threads, p->gjit_smem);
+      p->gjit_occ = std::max(o1, 1);
+    }
+    const int occ = p->gjit_occ;
     const int nw = p->gjit_threads / 32;
     const size_t blocks = (a.W + nw - 1) / nw;
     const size_t grid = std::min<size_t>(blocks, (size_t)p->num_sms * std::max(occ, 1));
