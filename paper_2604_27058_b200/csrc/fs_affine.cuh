@@ -561,8 +561,6 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   o << "    for (int i = t64; i < " << (size_t)K.nrows * G / 4
     << "; i += 64) reinterpret_cast<uint4*>(B)[i] = make_uint4(0u, 0u, 0u, 0u);\n";
   o << "    fs::pair_sync(pair);\n";
-  uint32_t maxr = 0;
-  for (int c = 0; c < d.num_cases; c++) maxr = std::max(maxr, crow_off[c + 1] - crow_off[c]);
   // uniform classes: every cum[i] within (i, i + 2) bins of the grid i * p / nc, with margin for rounding
   bool uniform = true;
   for (int c = 0; c < ncls; c++) {
@@ -573,8 +571,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     }
   }
   if (getenv("FS_AFF_NONUNIFORM")) uniform = false;
-  o << "    fs::aff_group_faults<" << G << ", " << (off16 ? "true" : "false") << ", " << std::min<uint32_t>(maxr, 16) << ", "
-    << (uniform ? "true" : "false")
+  o << "    fs::aff_group_faults<" << G << ", " << (off16 ? "true" : "false") << ", " << (uniform ? "true" : "false")
     << ">(P, tabs, B, seed, word0, grp, A.W, lane, half * " << G / 2 << ", half * " << G / 2 << " + " << G / 2 << ");\n";
   if (n_coins > 0) {  // coin blocks of the warp's 4 words: lane = (block % 8, word)
     o << "    for (int cb = lane >> 2; cb < " << nblk << "; cb += 8) {\n";

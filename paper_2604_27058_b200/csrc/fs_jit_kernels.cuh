@@ -180,7 +180,7 @@ __device__ __forceinline__ void aff_rows(const AffTabs<OFF16>& T, uint32_t* B, u
 // positions of a run are an inclusive warp scan of the per-step advances 1 + floor(ln(U) * lp), and
 // the first step past the run's last cell ends it (the following lanes start the next run).
 // Generic over runs (certain sites, several probabilities).
-template <bool OFF16, int MAXR, bool UNIFORM>
+template <bool OFF16, bool UNIFORM>
 __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi,
                                                 uint64_t seed, uint64_t wabs, int lane) {
   const int nruns = P.num_runs;
@@ -261,7 +261,7 @@ struct AffRun1 {
   double lp, q;
 };
 
-template <bool OFF16, int MAXR, bool UNIFORM>
+template <bool OFF16, bool UNIFORM>
 __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, uint64_t seed,
                                                      uint64_t wabs, int lane, const AffRun1& R) {
   uint32_t st = 0;
@@ -298,7 +298,7 @@ __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, ui
 }
 
 // faults of words [wi0, wi1) of group grp (row buffer B of the group, zeroed by the caller)
-template <int G, bool OFF16, int MAXR, bool UNIFORM>
+template <int G, bool OFF16, bool UNIFORM>
 __device__ __forceinline__ void aff_group_faults(const DevProg& P, const AffTabs<OFF16>& T, uint32_t* B, uint64_t seed,
                                                  uint64_t word0, uint32_t grp, uint32_t W, int lane, uint32_t wi0,
                                                  uint32_t wi1) {
@@ -311,13 +311,13 @@ __device__ __forceinline__ void aff_group_faults(const DevProg& P, const AffTabs
     for (uint32_t wi = wi0; wi < wi1; wi++) {
       const uint32_t w = grp * G + wi;
       if (w >= W) break;
-      aff_word_faults_1run<OFF16, MAXR, UNIFORM>(T, B, wi, seed, word0 + w, lane, R);
+      aff_word_faults_1run<OFF16, UNIFORM>(T, B, wi, seed, word0 + w, lane, R);
     }
   } else {
     for (uint32_t wi = wi0; wi < wi1; wi++) {
       const uint32_t w = grp * G + wi;
       if (w >= W) break;
-      aff_word_faults<OFF16, MAXR, UNIFORM>(P, T, B, wi, seed, word0 + w, lane);
+      aff_word_faults<OFF16, UNIFORM>(P, T, B, wi, seed, word0 + w, lane);
     }
   }
 }

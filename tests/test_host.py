@@ -145,3 +145,28 @@ def test_unpack_layout():
     bits = _abi.HostOutputs.unpack(words, 64)
     assert bits.shape == (64, 1)
     assert bits[:4, 0].tolist() == [1, 1, 0, 1] and bits[63, 0] == 1 and bits[4:63, 0].sum() == 0
+
+
+@pytest.mark.parametrize("name", ["config1", "aff_mixed", "aff_rep_psel", "toy_certain", "mirror00", "rand06"])
+def test_affine_kernel_source_compiles(name, tmp_path):
+    """The affine frame kernel generated for a frame-only program (fs_affine.cuh) compiles for
+    sm_100a without a GPU (nvcc -cubin): the GPU tests then only exercise its behaviour."""
+    from paper_2604_27058_b200 import _lib
+    from paper_2604_27058_b200._abi import DescHolder
+
+    P = load(name)["prog"]
+    h = DescHolder(P)
+    L = _lib.lib()
+    L.fs_debug_aff_source.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
+    n = L.fs_debug_aff_source(C.byref(h.desc), None, 0)
+    assert n > 0, n
+    buf = C.create_string_buffer(n + 1)
+    L.fs_debug_aff_source(C.byref(h.desc), buf, n + 1)
+    src = tmp_path / f"aff_{name}.cu"
+    src.write_text(buf.value.decode())
+    inc = ROOT / "paper_2604_27058_b200" / "csrc"
+    r = subprocess.run(["nvcc", "-cubin", "-arch=sm_100a", "-std=c++17", "-I", str(inc), "-I", str(ROOT / "include"),
+                        "-o", str(tmp_path / "k.cubin"), str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    sass = subprocess.run(["cuobjdump", "-sass", str(tmp_path / "k.cubin")], capture_output=True, text=True).stdout
+    assert "fs_aff_frame" in sass
