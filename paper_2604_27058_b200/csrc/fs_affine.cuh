@@ -515,6 +515,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     }
   }
   std::ostringstream o;
+  if (const char* dg = getenv("FS_AFF_DIAG")) o << "#define FS_AFF_DIAG " << atoi(dg) << "\n";  // profiling only
   o << "#include \"fs_jit_kernels.cuh\"\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << K.threads << ", 1) fs_aff_frame(fs::DevProg P, fs::RunArgs A, "
        "const uint32_t* __restrict__ tbl) {\n";
@@ -634,10 +635,11 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
         const int p0 = parents[r].size() > k ? parents[r][k] : -1;
         bool same = p0 >= 0 && p0 % RC == 0;
         for (int q = 1; q < rem && same; q++) same = parents[r + q].size() > k && parents[r + q][k] == p0 + q;
-        if (same)
+        if (same) {
           o << " v ^= B[" << p0 * G << " + j4 * " << G << " + (wi ^ " << aff_sw(p0) << ")];";
-        else
+        } else {
           o << " v ^= B[PS" << k << "[" << r << " + j4] ^ wi];";
+        }
       }
       bool wb = false;  // some later row rebuilds from one of these rows
       for (int q = 0; q < rem && !wb; q++) wb = is_parent[r + q];
@@ -647,10 +649,13 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
       o << " }\n";
     }
   };
+  const int diag = getenv("FS_AFF_DIAG") ? atoi(getenv("FS_AFF_DIAG")) : 0;  // profiling only
   for (cur_half = 0; cur_half < 2; cur_half++) {
     o << "        " << (cur_half == 0 ? "if (half == 0) {" : "} else {") << "\n";
-    emit_copy(0, D, "dout", 0);
-    emit_copy(D4, U, "mo", D4);
+    if (diag != 4 && diag != 6) {
+      emit_copy(0, D, "dout", 0);
+      emit_copy(D4, U, "mo", D4);
+    }
   }
   o << "        }\n";
   o << "      }\n    }\n";

@@ -167,11 +167,17 @@ __device__ __forceinline__ int aff_case(const AffTabs<OFF16>& T, int site, int c
 template <bool OFF16>
 __device__ __forceinline__ void aff_rows(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, uint32_t j0, uint32_t n,
                                          uint32_t bit) {
+#if defined(FS_AFF_DIAG) && FS_AFF_DIAG == 1
+  return;  // diagnostic: no row application
+#endif
   const uint32_t nmax = __reduce_max_sync(0xFFFFFFFFu, n);
   const uint32_t dl = T.dump + (threadIdx.x & 31);
-  for (uint32_t t = 0; t < nmax; t++) {
-    const uint32_t e = t < n ? (uint32_t)T.crows[j0 + t] : dl;
-    atomicXor(B + (e ^ wi), bit);
+  // two rows per trip (the odd tail's second XOR goes to the dump word): half the loop overhead
+  for (uint32_t t = 0; t < nmax; t += 2) {
+    const uint32_t e0 = t < n ? (uint32_t)T.crows[j0 + t] : dl;
+    const uint32_t e1 = t + 1 < n ? (uint32_t)T.crows[j0 + t + 1] : dl;
+    atomicXor(B + (e0 ^ wi), bit);
+    atomicXor(B + (e1 ^ wi), bit);
   }
 }
 
@@ -302,6 +308,9 @@ template <int G, bool OFF16, bool UNIFORM>
 __device__ __forceinline__ void aff_group_faults(const DevProg& P, const AffTabs<OFF16>& T, uint32_t* B, uint64_t seed,
                                                  uint64_t word0, uint32_t grp, uint32_t W, int lane, uint32_t wi0,
                                                  uint32_t wi1) {
+#if defined(FS_AFF_DIAG) && (FS_AFF_DIAG == 3 || FS_AFF_DIAG == 6)
+  return;  // diagnostic: no fault pass
+#endif
   if (P.num_runs == 1 && __ldg(P.run_len) > 0 && __ldg(P.run_len) < (1 << 20)) {
     AffRun1 R;
     R.start = __ldg(P.run_start);
