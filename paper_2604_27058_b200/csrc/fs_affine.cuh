@@ -438,6 +438,9 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     for (int c = 0; c < n_coins; c++)
       if ((v[(1 + c) >> 6] >> ((1 + c) & 63)) & 1ull) terms_tab.push_back(sl | (uint32_t)c << 16);
   }
+  // coin-major order: the 4 terms one warp instruction applies then hit distinct rows (a row's
+  // coins are consecutive in row-major order and would collide on one shared word)
+  std::stable_sort(terms_tab.begin(), terms_tab.end(), [](uint32_t a, uint32_t b) { return (a >> 16) < (b >> 16); });
   if (terms_tab.size() > kAffMaxTerms) { K.why = "noiseless part too large"; return K; }
   const size_t o_terms = sec(terms_tab.size() * 4);
   if (!terms_tab.empty()) memcpy(T.data() + o_terms, terms_tab.data(), terms_tab.size() * 4);
