@@ -1104,7 +1104,7 @@ int ensure_gjit(fs_prog* p) {
                                                            p->h_case_pauli_off, p->h_site_case_off, p->h_fparams);
   const int nw = K.arr_regs ? 4 : 2;
   const size_t fs_words = (size_t)(2 * p->dp.n + 3) / 4 * 4;
-  const size_t smem = nw * fs_words * 4 + (K.arr_regs ? 0 : (size_t)nw * 32 * 16 * ((size_t)1 << K.cap_log2));
+  const size_t smem = nw * fs_words * 4 + (K.arr_regs ? 0 : (size_t)nw * 32 * 16 * (((size_t)1 << K.cap_log2) - K.nreg));
   if (smem > kSmemBudget) { p->jit_error = "program too large for the specialised general kernel"; return FS_ERR_ARG; }
   std::string err = fsjit::compile(K.src, fsjit::self_dir() + "/../csrc", p->jit, "fs_jit_general");
   if (!err.empty()) { p->jit_error = err; return set_error(FS_ERR_ARG, err); }
