@@ -370,7 +370,9 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
   o << "#include \"fs_jit_kernels.cuh\"\n";
   o << "#define cmul fs::cmul_f\nusing fs::cadd; using fs::csub; using fs::cscale; using fs::cnorm2;\n";
   const char* gmb = getenv("FS_GJIT_MB");
-  o << "extern \"C\" __global__ void __launch_bounds__(" << (K.arr_regs ? 128 : 64) << ", " << (gmb ? atoi(gmb) : (K.arr_regs ? 3 : 1))
+  // register arrays: 4 blocks of 4 warps per SM (config 2: 2.38 -> 2.30 ms; 3 blocks leave 168
+  // registers, 5 and more spill)
+  o << "extern \"C\" __global__ void __launch_bounds__(" << (K.arr_regs ? 128 : 64) << ", " << (gmb ? atoi(gmb) : (K.arr_regs ? 4 : 1))
     << ") fs_jit_general(fs::DevProg P, fs::RunArgs A, const uint16_t* __restrict__ pslot, "
        "const uint32_t* __restrict__ fent, const uint32_t* __restrict__ bcount, const uint32_t* __restrict__ ntot) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem[];\n";

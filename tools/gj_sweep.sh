@@ -1,1 +1,1 @@
-for v in "FS_GJIT_NREG=32" "FS_GJIT_NREG=40" "FS_GJIT_NREG=48" "FS_GJIT_NREG=24" "FS_GJIT_NREG=32"; do echo "$v"; env $v python tools/gjit_check.py 0 | tail -1; done
+for v in "FS_GJIT_MB=4" "FS_GJIT_MB=5" "FS_GJIT_MB=6" "FS_GJIT_MB=8"; do echo "$v"; env $v python tools/gjit_check.py 2 | tail -1; done
