@@ -311,7 +311,11 @@ def main(which=("configs", "random", "toys")):
                 mix.append("M 1\nPOSTSELECT rec[-1]")
         mix.append("M " + " ".join(map(str, range(n))))
         mix.append("DETECTOR rec[-1] rec[-2]\nOBSERVABLE_INCLUDE(0) rec[-3] rec[-6]\nOBSERVABLE_INCLUDE(1) rec[-4]")
+        from paper_2604_27058_b200.configs import rotated_surface_code
         aff = {
+            # a larger frame-only program: ~1000 output rows, ~10^4 fault elements (table sizes,
+            # shared-memory budget and launch shape of the affine kernel away from config 1's)
+            "aff_surface_d7": (rotated_surface_code(7, 7, 2e-3), ()),
             "aff_rep_psel": ("\n".join(rep) + "\n", (0, 1, 2, 3, 5, 6)),
             "aff_rep": ("\n".join(rep) + "\n", ()),
             "aff_mixed": ("\n".join(mix) + "\n", ()),
