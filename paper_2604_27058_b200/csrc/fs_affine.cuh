@@ -13,16 +13,22 @@
 // rows(site, case) by propagating one symbolic source per constant / coin / (site, qubit, X|Z)
 // element through the program with bitsets, and emits a kernel that never simulates the frame:
 //
-//   * a warp owns a group of kAffGroup = 8 consecutive 32-shot words (one 32-byte sector of
-//     every output row) and a shared-memory row buffer B[row][8] for them;
-//   * faults: for each word of the group the 32 lanes evaluate 32 consecutive steps of that
-//     word's noise stream at once (WordFaultGen's process -- the engine stream, so every engine
-//     draws the same faults: one Philox block per step, geometric gap floor(ln(U) / log1p(-q)),
-//     thinning, case pick), place them with a warp prefix sum of the gaps, and XOR each fault's
-//     lane bit into its rows with shared atomics;
-//   * outputs: lanes 0..7 (one word each) draw their coin words and write every row once as
-//     (const ^ coins ^ B[row]) & alive, in program order, so PostSelect reads the full noisy bit
-//     and masks later rows exactly like the interpreter (fs_frame.cuh).
+//   * a pair of warps owns a group of kAffGroup = 8 consecutive 32-shot words (one 32-byte sector
+//     of every output row) and a bank-swizzled shared-memory row buffer B[row][8] for them;
+//     named barriers (bar.sync id, 64) order the pair's phases;
+//   * faults: each warp takes 4 of the words; for one word the 32 lanes evaluate 32 consecutive
+//     steps of its noise stream at once (WordFaultGen's process -- the engine stream, so every
+//     engine draws the same faults: one Philox block per step, geometric gap
+//     floor(ln(U) / log1p(-q)), thinning, case pick), place them with a warp prefix sum of the
+//     gaps, and XOR each fault's lane bit into the rows of its case with shared atomics (the
+//     case tables live in shared memory when they fit);
+//   * coins (Philox, all lanes) and the noiseless (row, coin) terms, XORed in with atomics;
+//   * PostSelect / observables in program order (lanes 0..7 of the first warp, one word each),
+//     keeping the alive mask of every post-select segment;
+//   * copy-out by both warps, 4 rows x 8 words per store: record rows are stored relative to up to
+//     kAffMaxParents detector rows (a record's faults are mostly its detectors' faults) and
+//     rebuilt here, each row masked with the alive mask in effect at its write.
+// Results are bit-identical to the frame interpreter (fs_frame.cuh) and the oracle.
 #pragma once
 #include <algorithm>
 #include <cmath>
