@@ -171,7 +171,7 @@ def test_gpu_jit_equals_interpreter(cuda, name, monkeypatch):
     _same(b, c)
 
 
-@pytest.mark.parametrize("name", ["config1", "aff_mixed", "aff_rep_psel", "toy_certain", "rand06"])
+@pytest.mark.parametrize("name", ["config1", "aff_mixed", "aff_rep_psel", "toy_certain", "rand06", "aff_surface_d7"])
 @pytest.mark.parametrize("env", [{"FS_AFF_GLOBAL_TABLES": "1"}, {"FS_AFF_PAIRS": "1"}, {"FS_AFF_NONUNIFORM": "1"},
                                  {"FS_AFF_NO_DIFF": "1"}, {"FS_AFF_PARENTS": "1"}, {"FS_AFF_ANY_PARENTS": "1"}])
 def test_gpu_affine_variants_match_oracle(cuda, name, env, monkeypatch):

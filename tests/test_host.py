@@ -147,7 +147,7 @@ def test_unpack_layout():
     assert bits[:4, 0].tolist() == [1, 1, 0, 1] and bits[63, 0] == 1 and bits[4:63, 0].sum() == 0
 
 
-@pytest.mark.parametrize("name", ["config1", "aff_mixed", "aff_rep_psel", "toy_certain", "mirror00", "rand06"])
+@pytest.mark.parametrize("name", ["config1", "aff_mixed", "aff_rep_psel", "toy_certain", "mirror00", "rand06", "aff_surface_d7"])
 def test_affine_kernel_source_compiles(name, tmp_path):
     """The affine frame kernel generated for a frame-only program (fs_affine.cuh) compiles for
     sm_100a without a GPU (nvcc -cubin): the GPU tests then only exercise its behaviour."""
