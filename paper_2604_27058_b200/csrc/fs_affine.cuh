@@ -46,7 +46,7 @@ constexpr int kAffMaxParents = 6;         // rows a copied-out row may be rebuil
 constexpr int kAffMaxPairs = 15;          // warp pairs per block (one block per SM; named barriers 1..15)
 // buffer slot of row r for word wi: r * G + (wi ^ sw(r)), sw(r) = (r / kAffChunk) % G (bank spread)
 inline int aff_sw(int r) { return (r / kAffChunk) % kAffGroup; }
-constexpr int kAffMaxCoins = 128;         // coin words kept in registers
+constexpr int kAffMaxCoins = 512;         // coin words per 32-shot word (shared memory, 2 KB per word at the limit)
 constexpr size_t kAffMaxTerms = 1 << 16;  // coin XOR terms over all rows (code size)
 
 struct AffineKernelSource {
