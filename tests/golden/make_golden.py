@@ -316,6 +316,11 @@ def main(which=("configs", "random", "toys")):
             # a larger frame-only program: ~1000 output rows, ~10^4 fault elements (table sizes,
             # shared-memory budget and launch shape of the affine kernel away from config 1's)
             "aff_surface_d7": (rotated_surface_code(7, 7, 2e-3), ()),
+            # > 128 coins: 20 qubits measured in a random basis 12 times (240 random outcomes)
+            "aff_many_coins": ("".join(f"H {' '.join(map(str, range(20)))}\nDEPOLARIZE1(0.01) {' '.join(map(str, range(20)))}\n"
+                                       f"M {' '.join(map(str, range(20)))}\nDETECTOR rec[-1] rec[-2]\n"
+                                       f"R {' '.join(map(str, range(20)))}\n" for _ in range(12))
+                               + "OBSERVABLE_INCLUDE(0) rec[-1] rec[-3]\n", ()),
             "aff_rep_psel": ("\n".join(rep) + "\n", (0, 1, 2, 3, 5, 6)),
             "aff_rep": ("\n".join(rep) + "\n", ()),
             "aff_mixed": ("\n".join(mix) + "\n", ()),
