@@ -127,16 +127,20 @@ def cpu_reference_rate(cfg: int, target_s: float = 8.0, cores: int | None = None
     oracle.build()
     path = PROGS / f"c{cfg}.npz"
     cores = cores or os.cpu_count() or 1
-    # calibrate on one core
-    probe = 256
-    while True:
-        dt, _ = _oracle_worker((path, 1, 0, probe))
-        if dt > 0.5 or probe >= 1 << 20:
-            break
-        probe *= 4
-    rate1 = probe / dt
-    per_core = max(32, int(rate1 * target_s) // 32 * 32)
-    jobs = [(path, 7, c * per_core, per_core) for c in range(cores)]
+    if target_s <= 0.0:  # one 32-shot word per core (config 3: seconds per shot)
+        per_core = 32 if Program.load(path).k_max < 16 else 1
+    else:
+        # calibrate on one core
+        probe = 256
+        while True:
+            dt, _ = _oracle_worker((path, 1, 0, probe))
+            if dt > 0.5 or probe >= 1 << 20:
+                break
+            probe *= 4
+        rate1 = probe / dt
+        per_core = max(32, int(rate1 * target_s) // 32 * 32)
+    stride = (per_core + 31) // 32 * 32  # shot ranges start on 32-shot words
+    jobs = [(path, 7, c * stride, per_core) for c in range(cores)]
     t0 = time.perf_counter()
     with mp.get_context("fork").Pool(cores) as pool:
         res = pool.map(_oracle_worker, jobs)
@@ -182,7 +186,9 @@ def workload_config(cfg: int) -> dict:
 
 
 KERNEL_NAME = {"frame": "fs_aff_frame (affine frame kernel: fault-effect row tables, warp-cooperative noise stream)",
-               "general": "general / block kernel", "hbm": "hbm_fused_pass_kernel"}
+               "general": "fs_jit_general (program-specialised general kernel, NVRTC)",
+               "segmented": "general_kernel<SEG> / block_kernel (post-select segments)",
+               "hbm": "fs_pass_<i> (program-specialised fused tile passes, NVRTC)"}
 
 
 def algorithmic_bytes_per_shot(P: Program) -> float:
@@ -258,8 +264,10 @@ def segment_work(P: Program) -> list[tuple[int, int, int]]:
     return out
 
 
-def extra_config(c: int, fp64_tflops: float) -> dict:
-    """Side measurement of another BASELINE config with its own roofline."""
+def extra_config(c: int, fp64_tflops: float, cpu: bool = True) -> dict:
+    """Side measurement of another BASELINE config: device-timed shots/s with its own
+    roofline, the same metric end to end through fs_sample_host (D2H inside the timed region), and
+    the reference algorithm on the host cores (oracle port, all cores, bounded sample)."""
     import ctypes as C
 
     steps = 1 if c == 3 else 3
@@ -267,8 +275,19 @@ def extra_config(c: int, fp64_tflops: float) -> dict:
     P, shots = rc["P"], rc["shots"]
     ms = float(np.mean(rc["ms"]))
     rate = shots / (ms / 1e3)
-    d = {"shots_per_s": rate, "ms_per_step": ms, "shots": shots, "k_max": P.k_max, "engine": rc["engine"],
-         "status": rc["status"]}
+    engine = rc["engine"]
+    if engine == "general" and P.has_postselect:
+        engine = "segmented"
+    d = {"shots_per_s": rate, "ms_per_step": ms, "shots": shots, "k_max": P.k_max, "engine": engine,
+         "kernel": KERNEL_NAME.get(engine, engine), "status": rc["status"]}
+    e2e_steps = 1 if c in (3, 4) else 2
+    e = time_e2e(rc["dp"], P, shots, 0, e2e_steps)
+    d["e2e"] = {"value": shots * e2e_steps / e["seconds"], "unit": "shots/s",
+                "h2d_bytes_per_step": e["h2d_bytes_per_step"], "d2h_bytes_per_step": e["d2h_bytes_per_step"]}
+    if cpu:
+        d["cpu_baseline"] = cpu_reference_rate(c, target_s=3.0 if c != 3 else 0.0)
+        d["vs_cpu"] = {"device": rate / d["cpu_baseline"]["value"],
+                       "e2e": d["e2e"]["value"] / d["cpu_baseline"]["value"]}
     d["gpu_launches_per_step"] = rc["launches"] / steps
     d["dominant_kernel_share"] = rc["kernel_ms"] / (ms * steps)
     if c == 3:  # fused tile passes: each reads + writes the live array of every shot once
@@ -282,7 +301,7 @@ def extra_config(c: int, fp64_tflops: float) -> dict:
         pk = peaks()["hbm_gbs"]
         W = P.work()
         d["roofline"] = {"bound": "hbm", "unit": "GB/s", "achieved": ach, "peak": pk, "frac": ach / pk,
-                         "kernel": "hbm_fused_pass_kernel", "passes": npass,
+                         "kernel": KERNEL_NAME["hbm"], "passes": npass,
                          "bytes_per_shot": pass_bytes / (shots * steps),
                          "unfused_algorithmic_bytes_per_shot": 32.0 * W,
                          "note": "bytes = one complex128 read + write of the live array per fused pass; "
@@ -448,7 +467,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "shots/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": avg_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32 (bit-sliced frames) / f64", "data": "synthetic",
-            "config": workload_config(args.config) | {"engine": r["engine"]},
+            "config": workload_config(args.config),
+            "engine": r["engine"],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_launch,

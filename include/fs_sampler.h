@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 1
+#define FS_ABI_VERSION 2
 
 /* ---- serialized program (paper_2604_27058_b200/program.py) ------------------------------ */
 
@@ -109,13 +109,21 @@ typedef struct fs_prog_desc {
 #define FS_FORCE_GENERAL 4u  /* testing: force the general per-shot-lane interpreter */
 #define FS_FORCE_HBM    8u   /* testing: force the large-k (HBM-resident array) engine */
 #define FS_NO_JIT       16u  /* testing: frame engine interpreter instead of the program-specialised kernel */
+#define FS_FORCE_SEGMENTED 32u /* testing: post-selected programs run segment by segment (survivor
+                                  compaction, warp/CTA-per-shot block engine) also in trace mode */
 
-/* trace mode: every random choice may be supplied (SURVEY §8(d) "trace mode") */
+/* trace mode: every random choice may be supplied (SURVEY §8(d) "trace mode"), and the state can
+ * be read back at the end and at a list of checkpoints in ONE call (run_shot(..., trace=)
+ * runtime.py:731-751 calls its callback after every instruction, :745-748). */
 typedef struct fs_trace_in {
   const int16_t* fault_modes; /* [nshots][E] runtime.py:587-601 encoding: 0 sample, 1 trigger with
                                  random case, 2 off, 3+c case c.  NULL = free hazard sampling. */
   const int8_t* forced;       /* [nshots][R]: -1 free, 0/1 forced outcome.  NULL = all free. */
   int32_t stop;               /* execute instructions [0, stop); <0 = whole program */
+  int32_t ncheckpoints;       /* number of checkpoints (0 = none) */
+  const int32_t* checkpoints; /* HOST memory, [ncheckpoints] strictly ascending instruction counts
+                                 in [0, stop]: checkpoint c = the state after instructions [0, c),
+                                 i.e. what the reference trace callback sees after instrs[c-1] */
 } fs_trace_in;
 
 typedef struct fs_trace_out {  /* any member may be NULL */
@@ -124,6 +132,15 @@ typedef struct fs_trace_out {  /* any member may be NULL */
   double* gamma;      /* [nshots][2] */
   double* amps;       /* [nshots][2^k_stop][2] active array at the stop point */
   uint32_t* draws;    /* [nshots] random draws consumed (FS_RNG_SPLITMIX) */
+  uint8_t* records;   /* [nshots][R] every record bit, user and hidden (ShotState.records) */
+  /* per checkpoint j (fs_trace_in.checkpoints[j]); a shot that halted (PostSelect) or raised
+     before the checkpoint has cp_valid 0 and unspecified state there */
+  uint8_t* cp_valid;    /* [ncp][nshots] */
+  uint8_t* cp_frame_x;  /* [ncp][nshots][n] */
+  uint8_t* cp_frame_z;  /* [ncp][nshots][n] */
+  double* cp_gamma;     /* [ncp][nshots][2] */
+  double* cp_amps;      /* checkpoint blocks back to back: block j = [nshots][2^k_j][2] with
+                           k_j = schedule[checkpoints[j] - 1] (0 when checkpoints[j] == 0) */
 } fs_trace_out;
 
 typedef struct fs_sample_out {
@@ -164,7 +181,8 @@ int fs_sample_host(fs_prog* prog, uint64_t seed, uint64_t shot0, uint64_t nshots
                    const fs_trace_in* tin, const fs_sample_out* out, const fs_trace_out* tout);
 
 /* counts (device int64): [U] meas, [D] det, [O] obs, then accepted; sums over ACCEPTED shots
- * (runtime.py:857-865) */
+ * (runtime.py:857-865).  Returns FS_OK, or FS_ERR_SHOT_* when some shot raised ShotError (the
+ * reference's sample_accumulate propagates it); reading that status synchronizes the stream. */
 int fs_accumulate(fs_prog* prog, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t flags,
                   int64_t* counts, void* stream);
 

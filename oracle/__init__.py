@@ -23,10 +23,9 @@ _lib = None
 
 def build(force: bool = False) -> Path:
     """Compile the C restatement (gcc, no FMA contraction, like CPython's arithmetic)."""
-    src = _HERE / "fs_oracle.c"
-    if force or not LIB_PATH.exists() or LIB_PATH.stat().st_mtime < src.stat().st_mtime:
-        LIB_PATH.parent.mkdir(exist_ok=True)
-        subprocess.check_call(["make", "-s", "-C", str(_HERE)])
+    # make does the dependency check (fs_oracle.c and the headers it shares with the engine)
+    LIB_PATH.parent.mkdir(exist_ok=True)
+    subprocess.check_call(["make", "-s", "-C", str(_HERE)] + (["-B"] if force else []))
     return LIB_PATH
 
 

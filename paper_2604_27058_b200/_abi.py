@@ -10,13 +10,14 @@ import ctypes as C
 
 import numpy as np
 
-FS_ABI_VERSION = 1
+FS_ABI_VERSION = 2
 FS_RNG_PHILOX = 0
 FS_RNG_SPLITMIX = 1
 FS_NO_RENORM = 2
 FS_FORCE_GENERAL = 4
 FS_FORCE_HBM = 8
 FS_NO_JIT = 16
+FS_FORCE_SEGMENTED = 32
 
 FS_OK = 0
 FS_ERR_ARG = -1
@@ -47,12 +48,14 @@ class FsProgDesc(C.Structure):
 
 class FsTraceIn(C.Structure):
     _fields_ = [("fault_modes", C.POINTER(C.c_int16)), ("forced", C.POINTER(C.c_int8)),
-                ("stop", C.c_int32)]
+                ("stop", C.c_int32), ("ncheckpoints", C.c_int32), ("checkpoints", C.POINTER(C.c_int32))]
 
 
 class FsTraceOut(C.Structure):
     _fields_ = [("frame_x", C.POINTER(C.c_uint8)), ("frame_z", C.POINTER(C.c_uint8)),
-                ("gamma", _f64p), ("amps", _f64p), ("draws", _u32p)]
+                ("gamma", _f64p), ("amps", _f64p), ("draws", _u32p), ("records", C.POINTER(C.c_uint8)),
+                ("cp_valid", C.POINTER(C.c_uint8)), ("cp_frame_x", C.POINTER(C.c_uint8)),
+                ("cp_frame_z", C.POINTER(C.c_uint8)), ("cp_gamma", _f64p), ("cp_amps", _f64p)]
 
 
 class FsSampleOut(C.Structure):
@@ -171,7 +174,7 @@ class TraceBuffers:
     """Host trace inputs/outputs (trace mode)."""
 
     def __init__(self, prog, nshots: int, fault_modes=None, forced=None, stop: int = -1,
-                 want_state: bool = True):
+                 want_state: bool = True, checkpoints=None):
         self.fault_modes = None if fault_modes is None else np.ascontiguousarray(fault_modes, dtype=np.int16)
         self.forced = None if forced is None else np.ascontiguousarray(forced, dtype=np.int8)
         if self.fault_modes is not None:
@@ -185,6 +188,16 @@ class TraceBuffers:
         self.tin = ti
         stop_eff = prog.num_instrs if stop < 0 or stop > prog.num_instrs else stop
         self.k_stop = int(prog.schedule[stop_eff - 1]) if stop_eff > 0 else 0
+        self.nshots = nshots
+        self.n = prog.n
+        self.checkpoints = None if checkpoints is None else np.ascontiguousarray(checkpoints, dtype=np.int32)
+        ncp = 0 if self.checkpoints is None else int(self.checkpoints.size)
+        if ncp:
+            if np.any(np.diff(self.checkpoints) <= 0) or self.checkpoints[0] < 0 or self.checkpoints[-1] > stop_eff:
+                raise ValueError("checkpoints must be strictly ascending within [0, stop]")
+            ti.ncheckpoints = ncp
+            ti.checkpoints = _ptr(self.checkpoints, C.c_int32)
+            want_state = True
         self.tout = None
         if want_state:
             n = prog.n
@@ -199,6 +212,22 @@ class TraceBuffers:
             to.gamma = _ptr(self.gamma, C.c_double)
             to.amps = _ptr(self.amps, C.c_double)
             to.draws = _ptr(self.draws, C.c_uint32)
+            self.records = np.zeros((nshots, max(prog.record_count, 1)), dtype=np.uint8)
+            to.records = _ptr(self.records, C.c_uint8)
+            if ncp:
+                ks = [int(prog.schedule[c - 1]) if c > 0 else 0 for c in self.checkpoints.tolist()]
+                self.cp_k = ks
+                self.cp_off = np.concatenate([[0], np.cumsum([nshots << k for k in ks])]).astype(np.int64)
+                self.cp_valid = np.zeros((ncp, nshots), dtype=np.uint8)
+                self.cp_fx = np.zeros((ncp, nshots, max(n, 1)), dtype=np.uint8)
+                self.cp_fz = np.zeros((ncp, nshots, max(n, 1)), dtype=np.uint8)
+                self.cp_gamma = np.zeros((ncp, nshots, 2), dtype=np.float64)
+                self.cp_amps = np.zeros((int(self.cp_off[-1]), 2), dtype=np.float64)
+                to.cp_valid = _ptr(self.cp_valid, C.c_uint8)
+                to.cp_frame_x = _ptr(self.cp_fx, C.c_uint8)
+                to.cp_frame_z = _ptr(self.cp_fz, C.c_uint8)
+                to.cp_gamma = _ptr(self.cp_gamma, C.c_double)
+                to.cp_amps = _ptr(self.cp_amps, C.c_double)
             self.tout = to
 
     def gamma_c(self):
@@ -206,6 +235,15 @@ class TraceBuffers:
 
     def amps_c(self):
         return self.amps[..., 0] + 1j * self.amps[..., 1]
+
+    def checkpoint(self, j: int) -> dict:
+        """State at checkpoint j: valid [nshots], frame_x / frame_z [nshots][n], gamma [nshots],
+        amps [nshots][2^k_j] (complex); entries of invalid shots are unspecified."""
+        a = self.cp_amps[self.cp_off[j]:self.cp_off[j + 1]]
+        a = (a[:, 0] + 1j * a[:, 1]).reshape(self.nshots, 1 << self.cp_k[j])
+        return {"valid": self.cp_valid[j].astype(bool), "frame_x": self.cp_fx[j, :, :self.n],
+                "frame_z": self.cp_fz[j, :, :self.n], "gamma": self.cp_gamma[j, :, 0] + 1j * self.cp_gamma[j, :, 1],
+                "amps": a, "k": self.cp_k[j]}
 
 # output formats (include/fs_sampler.h fs_format; cli.py:94-109)
 FS_FMT_01 = 0

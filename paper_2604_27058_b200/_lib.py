@@ -11,7 +11,7 @@ import subprocess
 import threading
 from pathlib import Path
 
-from ._abi import FsProgDesc, FsSampleOut, FsTraceIn, FsTraceOut
+from ._abi import FS_ABI_VERSION, FsProgDesc, FsSampleOut, FsTraceIn, FsTraceOut
 
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "_build" / "libfs_sampler.so"
@@ -31,7 +31,8 @@ _lib = None
 
 
 def sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [INCLUDE / "fs_sampler.h"]
+    return (sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h"))
+            + [INCLUDE / "fs_sampler.h"])
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -109,7 +110,7 @@ def lib():
             L.fs_probe.restype = C.c_int
             L.fs_probe.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, C.c_uint64, C.c_int32,
                                    C.POINTER(C.c_double), C.c_void_p]
-            if L.fs_abi_version() != 1:
+            if L.fs_abi_version() != FS_ABI_VERSION:
                 raise EngineUnavailable("ABI version mismatch")
             _lib = L
     return _lib

@@ -45,6 +45,23 @@ struct BlockCtx {
   int branch;
   int coin_blk;  // Philox coin block of ordinals 4b..4b+3, reused across coins
   uint4 coin_b;
+  // trace mode (interpreter only): supplied draws, state dumps
+  const int16_t* fmodes;  // [E] this shot's forced fault modes or NULL
+  const int8_t* forced;   // [R] this shot's forced outcomes or NULL
+  int cpi;                // next checkpoint
+  int halt_i;             // instruction at which the shot halted (PostSelect), else -1
+
+  __device__ __forceinline__ void put_rec(int rec, uint32_t bit) {
+    const int col = __ldg(P.record_out + rec);
+    if (col >= 0 && bit) out_bit(A.meas + (size_t)col * A.W);
+    const int sl = __ldg(P.bit_slot + rec);
+    if (sl >= 0) slots[sl] = bit;
+    if (A.t_rec) A.t_rec[si * P.R + rec] = (uint8_t)bit;
+  }
+  __device__ __forceinline__ void fail(int code) {
+    sh_err = code;
+    sh_alive = 0;
+  }
 
   __device__ __forceinline__ void bar() {
     if (G == 32) __syncwarp();
@@ -72,13 +89,17 @@ struct BlockCtx {
       case FS_OP_MEAS_DSTATIC:
       case FS_OP_MEAS_DRANDOM: {
         const int virt = ins[1], rec = ins[3];
+        const int fo = forced ? (int)forced[rec] : -1;
         uint32_t bit;
         if (op == FS_OP_MEAS_DSTATIC) {
           bit = fx[virt] ^ (uint32_t)flip;
+          if (fo >= 0 && (uint32_t)fo != bit) { fail(FS_ERR_SHOT_FORCED); break; }
         } else {
           const uint32_t pz = fz[virt];
           uint32_t coin;
-          if (SPLITMIX) {
+          if (fo >= 0) {
+            coin = (uint32_t)(fo ^ (int)pz ^ flip);
+          } else if (SPLITMIX) {
             coin = (uint32_t)sm.bit();
           } else {
             if ((ins[2] >> 2) != coin_blk) {
@@ -95,17 +116,23 @@ struct BlockCtx {
           fz[virt] = t;
           gamma = cscale(gamma, kInvSqrt2);
         }
-        const int col = __ldg(P.record_out + rec);
-        if (col >= 0 && bit) out_bit(A.meas + (size_t)col * A.W);
-        const int sl = __ldg(P.bit_slot + rec);
-        if (sl >= 0) slots[sl] = bit;
+        put_rec(rec, bit);
         break;
       }
       case FS_OP_COND_FRAME:
         if (slots[__ldg(P.bit_slot + ins[3])]) xor_paulis<false>(P, fx, fz, ins[1], ins[2], 1u);
         break;
       case FS_OP_NOISE:
-        if (SPLITMIX) {
+        if (fmodes) {  // forced modes (runtime.py:587-601), draws as in the general engine
+          ShotDraws d;
+          d.splitmix = SPLITMIX;
+          d.seed = A.seed;
+          d.shot = shot;
+          if (SPLITMIX) d.sm = sm;
+          d.begin(i, TAG_FORCED);
+          forced_faults_shot(P, fx, fz, 1u, ins, fmodes, d, 1, false);
+          if (SPLITMIX) sm = d.sm;
+        } else if (SPLITMIX) {
           hazard_shot(P, fx, fz, 1u, ins, sm, 1, false);
         } else {
           const int hi = ins[2];
@@ -138,7 +165,10 @@ struct BlockCtx {
       }
       case FS_OP_POSTSELECT: {
         const int bid = ins[1] == 0 ? P.R + ins[2] : ins[2];
-        if ((int)slots[__ldg(P.bit_slot + bid)] != ins[3]) sh_alive = 0;
+        if ((int)slots[__ldg(P.bit_slot + bid)] != ins[3]) {
+          sh_alive = 0;
+          halt_i = i;
+        }
         break;
       }
       default: break;
@@ -299,24 +329,30 @@ struct BlockCtx {
       if (collapse || !renorm) p1 = p_all > 0 ? __ddiv_rn(p1, p_all) : 0.0;
       if (p1 < 0.0) p1 = 0.0;
       else if (p1 > 1.0) p1 = 1.0;
-      double u;
-      if (SPLITMIX) u = sm.uniform();
-      else {
-        const uint4 o = philox((uint32_t)shot, (uint32_t)(shot >> 32), (uint32_t)i, TAG_BORN << 24, A.seed);
-        u = u64_to_unit(((uint64_t)o.y << 32) | o.x);
+      const int fo = forced ? (int)forced[rec] : -1;
+      int br;
+      double pb;
+      if (fo < 0) {
+        double u;
+        if (SPLITMIX) u = sm.uniform();
+        else {
+          const uint4 o = philox((uint32_t)shot, (uint32_t)(shot >> 32), (uint32_t)i, TAG_BORN << 24, A.seed);
+          u = u64_to_unit(((uint64_t)o.y << 32) | o.x);
+        }
+        br = u < p1 ? 1 : 0;
+        pb = br ? p1 : __dsub_rn(1.0, p1);
+        if (pb < kBranchFloor) { br ^= 1; pb = __dsub_rn(1.0, pb); }
+      } else {  // forced outcome (runtime.py:383-386, :476-479)
+        br = fo ^ parity ^ flip;
+        pb = br ? p1 : __dsub_rn(1.0, p1);
+        if (!bad && pb < kBranchFloor) bad = FS_ERR_SHOT_FORCED;
       }
-      int br = u < p1 ? 1 : 0;
-      double pb = br ? p1 : __dsub_rn(1.0, p1);
-      if (pb < kBranchFloor) { br ^= 1; pb = __dsub_rn(1.0, pb); }
       if (bad) {
         sh_err = bad;
         sh_alive = 0;
       } else {
         const uint32_t recbit = (uint32_t)(br ^ parity ^ flip);
-        const int col = __ldg(P.record_out + rec);
-        if (col >= 0 && recbit) out_bit(A.meas + (size_t)col * A.W);
-        const int sl = __ldg(P.bit_slot + rec);
-        if (sl >= 0) slots[sl] = recbit;
+        put_rec(rec, recbit);
         if (collapse) {
           const double scale = renorm ? __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(pb, p_all))) : 1.0;
           sh_k0 = br == 0 ? cscale(u00, scale) : cscale(u10, scale);
@@ -400,11 +436,42 @@ struct BlockCtx {
     bar();
   }
 
+  // trace: state after instructions [0, cp_at[j]) (all threads: amplitudes; thread 0: scalars)
+  __device__ void dump_cp(int j) {
+    const size_t cs = (size_t)j * A.nshots + si;
+    const int c = __ldg(A.cp_at + j);
+    const uint32_t sz = 1u << (c > 0 ? __ldg(P.schedule + c - 1) : 0);
+    double* dst = A.cp_amps + 2 * (__ldg(A.cp_off + j) + si * sz);
+    for (uint32_t e = tid; e < sz; e += G) {
+      dst[2 * e] = amp[e].x;
+      dst[2 * e + 1] = amp[e].y;
+    }
+    for (int q = tid; q < P.n; q += G) {
+      A.cp_fx[cs * P.n + q] = (uint8_t)(fx[q] & 1u);
+      A.cp_fz[cs * P.n + q] = (uint8_t)(fz[q] & 1u);
+    }
+    if (tid == 0) {
+      A.cp_valid[cs] = 1;
+      A.cp_gamma[2 * cs] = gamma.x;
+      A.cp_gamma[2 * cs + 1] = gamma.y;
+    }
+  }
+  __device__ __forceinline__ void dump_cps_at(int i) {
+    bool any = false;
+    while (cpi < A.ncp && __ldg(A.cp_at + cpi) == i) {
+      dump_cp(cpi++);
+      any = true;
+    }
+    if (any) bar();
+  }
+
   // the interpreter: instructions [seg_begin, seg_end) of the segment
   __device__ void interpret() {
     for (int i = S.seg_begin; i < S.seg_end; i++) {
       if (!sh_alive) break;
-      const int j = min(__ldg(P.next_array + i), S.seg_end);
+      if (A.ncp) dump_cps_at(i);
+      int j = min(__ldg(P.next_array + i), S.seg_end);
+      if (cpi < A.ncp) j = min(j, max(__ldg(A.cp_at + cpi), i));  // scalar runs stop at checkpoints
       if (j > i) {  // a run of scalar instructions
         scalar_run(i, j);
         i = j - 1;
@@ -427,6 +494,29 @@ struct BlockCtx {
         case FS_OP_RETIRE: retire(ins[1], ins[2], 1u << ins[6]); break;
         default: break;
       }
+    }
+    if (A.ncp && sh_alive) dump_cps_at(S.seg_end);
+  }
+
+  // trace: final state of a shot that ended (halted, raised or finished) in this segment
+  __device__ void dump_final(int upto) {
+    const int kst = A.stop > 0 ? __ldg(P.schedule + A.stop - 1) : 0;
+    const int kcur = upto > 0 ? __ldg(P.schedule + upto - 1) : 0;
+    const uint32_t sz = 1u << kst, cur = 1u << kcur;
+    if (A.t_amps)
+      for (uint32_t e = tid; e < sz; e += G) {
+        const double2 v = e < cur ? amp[e] : make_double2(0.0, 0.0);
+        A.t_amps[(si * sz + e) * 2] = v.x;
+        A.t_amps[(si * sz + e) * 2 + 1] = v.y;
+      }
+    if (A.t_fx)
+      for (int q = tid; q < P.n; q += G) {
+        A.t_fx[si * P.n + q] = (uint8_t)(fx[q] & 1u);
+        A.t_fz[si * P.n + q] = (uint8_t)(fz[q] & 1u);
+      }
+    if (tid == 0) {
+      if (A.t_gamma) { A.t_gamma[2 * si] = gamma.x; A.t_gamma[2 * si + 1] = gamma.y; }
+      if (A.t_draws) A.t_draws[si] = SPLITMIX ? sm.count : 0u;
     }
   }
 };
@@ -463,6 +553,14 @@ __device__ __forceinline__ void block_run(const DevProg& P, const RunArgs& A, co
     c.branch = 0;
     c.coin_blk = -1;
     c.coin_b = make_uint4(0, 0, 0, 0);
+    c.fmodes = A.fault_modes ? A.fault_modes + si * (size_t)P.E : nullptr;
+    c.forced = A.forced ? A.forced + si * (size_t)P.R : nullptr;
+    c.halt_i = -1;
+    c.cpi = 0;
+    if (A.ncp) {
+      const int lo = S.seg_begin == 0 ? 0 : S.seg_begin + 1;
+      while (c.cpi < A.ncp && __ldg(A.cp_at + c.cpi) < lo) c.cpi++;
+    }
     if (tid == 0) {
       c.sh_alive = 1;
       c.sh_err = 0;
@@ -499,6 +597,17 @@ __device__ __forceinline__ void block_run(const DevProg& P, const RunArgs& A, co
     c.bar();
     const bool alive = c.sh_alive != 0;
     const bool errored = c.sh_err != 0;
+    if ((S.last || !alive) && (A.t_fx || A.t_gamma || A.t_amps || A.t_draws)) {
+      c.halt_i = __shfl_sync(0xFFFFFFFFu, c.halt_i, 0);  // thread 0's (G >= 32: lane 0 of warp 0)
+      if (G == 256) {
+        __shared__ int sh_halt;
+        if (tid == 0) sh_halt = c.halt_i;
+        c.bar();
+        c.halt_i = sh_halt;
+      }
+      c.dump_final(c.halt_i >= 0 ? c.halt_i : (S.last && alive ? A.stop : S.seg_end));
+      c.bar();
+    }
     if (tid == 0) {
       if (errored) {
         atomicOr(A.error + (si >> 5), 1u << (si & 31));

@@ -80,6 +80,16 @@ struct RunArgs {
   double* t_gamma;
   double* t_amps;
   uint32_t* t_draws;
+  uint8_t* t_rec;       // [nshots][R] every record bit (trace)
+  // checkpoints (trace): state after instructions [0, cp_at[j]) for j < ncp
+  int ncp;
+  const int* cp_at;          // device [ncp], ascending
+  const uint64_t* cp_off;    // device [ncp]: offset (complex elements) of checkpoint j's amplitude block
+  uint8_t* cp_valid;         // [ncp][nshots]
+  uint8_t* cp_fx;            // [ncp][nshots][n]
+  uint8_t* cp_fz;
+  double* cp_gamma;          // [ncp][nshots][2]
+  double* cp_amps;           // blocks [nshots][2^k_j][2] at cp_off[j]
   const uint32_t* draw0;  // [nshots] reference-stream draws consumed before the program
                           // (stratified sampling: StratumSpec.draw_forced), NULL = 0
   // general engine: per-resident-warp array storage when it does not fit in shared memory

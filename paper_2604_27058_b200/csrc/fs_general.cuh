@@ -360,6 +360,7 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp, SegArgs S) {
       }
     };
     auto put_record = [&](int r, uint32_t word) {
+      if (A.t_rec && ((alive >> lane) & 1)) A.t_rec[si * P.R + r] = (uint8_t)((word >> lane) & 1);
       const int col = __ldg(P.record_out + r);
       if (col >= 0) put_out(A.meas + (size_t)col * A.W, word);
       if (lane == 0) {
@@ -400,8 +401,36 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp, SegArgs S) {
       }
     };
 
+    // checkpoint j: state after instructions [0, cp_at[j]) of the shots still running (a value
+    // equal to a segment start was dumped at the end of the previous segment)
+    auto dump_cp = [&](int j) {
+      if (!((alive >> lane) & 1)) return;
+      const size_t cs = (size_t)j * A.nshots + si;
+      A.cp_valid[cs] = 1;
+      for (int q = 0; q < P.n; q++) {
+        A.cp_fx[cs * P.n + q] = (fx[q] >> lane) & 1;
+        A.cp_fz[cs * P.n + q] = (fz[q] >> lane) & 1;
+      }
+      A.cp_gamma[2 * cs] = gamma.x;
+      A.cp_gamma[2 * cs + 1] = gamma.y;
+      const int c = __ldg(A.cp_at + j);
+      const uint32_t sz = 1u << (c > 0 ? __ldg(P.schedule + c - 1) : 0);
+      double* dst = A.cp_amps + 2 * (__ldg(A.cp_off + j) + si * sz);
+      for (uint32_t e = 0; e < sz; e++) {
+        const double2 v = AMP(e);
+        dst[2 * e] = v.x;
+        dst[2 * e + 1] = v.y;
+      }
+    };
+    int cpi = 0;
+    if (A.ncp) {
+      const int lo = i_begin == 0 ? 0 : i_begin + 1;
+      while (cpi < A.ncp && __ldg(A.cp_at + cpi) < lo) cpi++;
+    }
+
     for (int i = i_begin; i < i_end; i++) {
       if (alive == 0 && A.prezeroed) break;
+      while (cpi < A.ncp && __ldg(A.cp_at + cpi) == i) dump_cp(cpi++);
       const int4 I0 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i);
       const int4 I1 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i + 1);
       const int ins[8] = {I0.x, I0.y, I0.z, I0.w, I1.x, I1.y, I1.z, I1.w};
@@ -722,6 +751,7 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp, SegArgs S) {
       }
     }
     __syncwarp();
+    while (cpi < A.ncp && __ldg(A.cp_at + cpi) == i_end) dump_cp(cpi++);
     if (!SEG) {
       if (lane == 0) {
         for (int o = 0; o < P.O; o++) A.obs[(size_t)o * A.W + w] = obsw[o] & validmask;
@@ -740,6 +770,7 @@ general_kernel(DevProg P, RunArgs A, int smem_words_per_warp, SegArgs S) {
         if ((errmask >> lane) & 1) atomicOr(A.error + (si >> 5), 1u << (si & 31));
       }
       if (lane == 0 && errmask) atomicMax(A.status, errcode);
+      if (A.t_fx || A.t_gamma || A.t_amps || A.t_draws) dump_trace(ended & ~dumped, S.last ? stop : i_end);
       if (!S.last) {  // compact the survivors into the output store
         const uint32_t surv = alive & validmask;
         uint32_t base = 0;

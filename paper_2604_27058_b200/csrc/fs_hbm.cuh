@@ -206,6 +206,9 @@ __global__ void __launch_bounds__(128) hbm_scalar_kernel(DevProg P, RunArgs A, H
         if (col >= 0) A.meas[(size_t)col * A.W + gw] = recw & alive;
         const int sl = __ldg(P.bit_slot + rec);
         if (sl >= 0) SL(sl) = recw;
+        if (A.t_rec)
+          for (int b = 0; b < 32; b++)
+            if ((alive >> b) & 1) A.t_rec[(si0 + b) * P.R + rec] = (uint8_t)((recw >> b) & 1);
         break;
       }
       case FS_OP_MEAS_ACTIVE:
@@ -290,6 +293,9 @@ __global__ void __launch_bounds__(128) hbm_scalar_kernel(DevProg P, RunArgs A, H
         if (col >= 0) A.meas[(size_t)col * A.W + gw] = recw & alive;
         const int sl = __ldg(P.bit_slot + rec);
         if (sl >= 0) SL(sl) = recw;
+        if (A.t_rec)
+          for (int b = 0; b < 32; b++)
+            if ((alive >> b) & 1) A.t_rec[(si0 + b) * P.R + rec] = (uint8_t)((recw >> b) & 1);
         break;
       }
       case FS_OP_COND_FRAME: {
@@ -403,6 +409,28 @@ __global__ void hbm_finish_kernel(DevProg P, RunArgs A, HbmState H, uint64_t bat
       }
     if (A.t_gamma) { A.t_gamma[2 * si] = H.gamma[bs].x; A.t_gamma[2 * si + 1] = H.gamma[bs].y; }
     if (A.t_draws) A.t_draws[si] = H.smcount[bs];
+  }
+}
+
+// trace checkpoint j: frames, gamma and validity of the shots still running (amplitudes: gather)
+__global__ void hbm_cp_kernel(DevProg P, RunArgs A, HbmState H, uint64_t batch0, uint32_t W, int j) {
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= W) return;
+  const uint64_t si0 = batch0 + (uint64_t)w * 32;
+  const uint64_t nleft = A.nshots - si0;
+  const uint32_t validmask = nleft >= 32 ? kFull : ((1u << nleft) - 1u);
+  const uint32_t alive = H.alive[w] & validmask;
+  for (int b = 0; b < 32; b++) {
+    if (!((alive >> b) & 1)) continue;
+    const uint64_t si = si0 + b, bs = (uint64_t)w * 32 + b;
+    const size_t cs = (size_t)j * A.nshots + si;
+    A.cp_valid[cs] = 1;
+    for (int q = 0; q < P.n; q++) {
+      A.cp_fx[cs * P.n + q] = (H.fx[(size_t)q * W + w] >> b) & 1;
+      A.cp_fz[cs * P.n + q] = (H.fz[(size_t)q * W + w] >> b) & 1;
+    }
+    A.cp_gamma[2 * cs] = H.gamma[bs].x;
+    A.cp_gamma[2 * cs + 1] = H.gamma[bs].y;
   }
 }
 
@@ -563,9 +591,9 @@ __global__ void hbm_init_amps_kernel(HbmState H, uint32_t nshots_batch) {
   if (shot < nshots_batch) H.amps[(size_t)shot * H.cap] = make_double2(1.0, 0.0);
 }
 
-// trace: gather the valid elements of each shot in logical order
+// trace: gather the valid elements of each shot in logical order into dst [nshots][2^k][2]
 __global__ void hbm_gather_kernel(DevProg P, RunArgs A, HbmState H, uint64_t batch0, uint32_t nshots_batch,
-                                  int k, DevAxisMap map) {
+                                  int k, DevAxisMap map, double* dst) {
   const uint32_t shot = blockIdx.y;
   if (shot >= nshots_batch) return;
   const uint64_t sz = 1ull << k;
@@ -575,8 +603,8 @@ __global__ void hbm_gather_kernel(DevProg P, RunArgs A, HbmState H, uint64_t bat
     uint64_t p = 0;
     for (int b = 0; b < k; b++) p |= ((l >> b) & 1ull) << map.phys[b];
     const double2 v = A_[p];
-    A.t_amps[(si * sz + l) * 2] = v.x;
-    A.t_amps[(si * sz + l) * 2 + 1] = v.y;
+    dst[(si * sz + l) * 2] = v.x;
+    dst[(si * sz + l) * 2 + 1] = v.y;
   }
 }
 

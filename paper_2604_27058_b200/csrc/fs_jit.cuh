@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include <sstream>
 #include <string>
@@ -31,6 +32,7 @@ typedef int CUresult;
 typedef void* CUmodule;
 typedef void* CUfunction;
 typedef void* CUstream;
+typedef void* CUcontext;
 
 struct Api {
   bool ok = false;
@@ -51,6 +53,7 @@ struct Api {
   CUresult (*cuLaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                              CUstream, void**, void**);
   CUresult (*cuOccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t);
+  CUresult (*cuCtxGetCurrent)(CUcontext*);
 };
 
 inline void* try_open(const std::vector<std::string>& names) {
@@ -71,11 +74,8 @@ inline std::string self_dir() {
   return ".";
 }
 
-inline Api& api() {
-  static Api a;
-  static bool init = false;
-  if (init) return a;
-  init = true;
+inline Api load_api() {
+  Api a;
   void* nv = try_open({"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"});
   void* cu = try_open({"libcuda.so.1", "libcuda.so"});
   if (!nv || !cu) {
@@ -98,8 +98,15 @@ inline Api& api() {
   LOAD(cu, cuFuncSetAttribute);
   LOAD(cu, cuLaunchKernel);
   LOAD(cu, cuOccupancyMaxActiveBlocksPerMultiprocessor);
+  LOAD(cu, cuCtxGetCurrent);
 #undef LOAD
   a.ok = true;
+  return a;
+}
+
+// loaded once, thread-safely (C++11 magic static); callers check .ok before any driver call
+inline Api& api() {
+  static Api a = load_api();
   return a;
 }
 
@@ -318,7 +325,13 @@ inline FrameKernelSource gen_frame_kernel(const fs_prog_desc& d, const std::vect
 // uses the same rounding sequence as the interpreter (bit-identical results).
 inline std::string hexd(double v) {
   char b[64];
-  snprintf(b, sizeof b, "%a", v);
+  if (v != v || v - v != 0.0) {  // NaN / inf: spelled by their bits (NVRTC has no literal for them)
+    unsigned long long u;
+    memcpy(&u, &v, sizeof u);
+    snprintf(b, sizeof b, "__longlong_as_double(0x%016llxULL)", u);
+  } else {
+    snprintf(b, sizeof b, "%a", v);
+  }
   return b;
 }
 

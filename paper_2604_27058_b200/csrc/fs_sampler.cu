@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -48,6 +49,19 @@ int set_error(int code, const std::string& msg) {
 constexpr size_t kSmemBudget = 200 * 1024;  // per block, leaves room for L1
 constexpr size_t kAffSmemBudget = 208 * 1024;  // affine frame kernel: row buffers of one block per SM
 
+// every entry point runs on the device the program was created on (its allocations and NVRTC
+// modules live in that device's primary context), whatever device the calling thread has current
+struct DeviceGuard {
+  int prev = -1, want;
+  explicit DeviceGuard(int dev) : want(dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != want) cudaSetDevice(want);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Stage {  // carve-out of one device allocation
@@ -65,8 +79,10 @@ struct Stage {  // carve-out of one device allocation
 }  // namespace
 
 struct HbmStep {
-  enum Kind { SCALAR, ARR, PASS, MEAS } kind;
+  enum Kind { SCALAR, ARR, PASS, MEAS, DUMP } kind;
   int i0, i1;
+  int cp;               // DUMP: checkpoint index
+  fs::DevAxisMap map;   // DUMP: logical -> physical axes at the checkpoint
   fs::ArrOp op;
   uint64_t count;
   int pass;
@@ -77,6 +93,7 @@ struct HbmStep {
 struct HbmPlan {
   bool built = false, fused = false;
   int stop = -1;
+  std::vector<int> cuts;               // checkpoints (instruction counts) the plan dumps at
   std::vector<HbmStep> steps;
   std::vector<fs::PassDesc> passes;
   std::vector<fs::TileOp> tileops;
@@ -91,8 +108,33 @@ constexpr int kBlockK = 9;   // segment active dimension at which a shot gets a 
 constexpr int kChunks = 4;   // max word chunks of the fault-list | frame-kernel pipeline; default 1 (2-4 measured 10-27 % slower), FS_JIT_CHUNKS overrides
 }  // namespace
 
+// testing / experiment switches, read once at fs_program_create (never on a launch path)
+struct EnvSwitches {
+  bool no_affine = false;      // FS_NO_AFFINE: frame-only programs use the fault-list frame kernel
+  bool block_no_jit = false;   // FS_BLOCK_NO_JIT: segmented engine interprets every segment
+  bool block_jit_warp = false; // FS_BLOCK_JIT_WARP: also specialise warp-per-shot segments
+  int block_k = 0;             // FS_BLOCK_K: segment k at which a shot gets a warp / CTA (0 = default)
+  bool hbm_fused = false;      // FS_HBM_FUSED: fused tile passes also under FS_FORCE_HBM
+  bool hbm_unfused = false;    // FS_HBM_UNFUSED: per-instruction large-k kernels only
+  bool hbm_no_jit = false;     // FS_HBM_NO_JIT: pass microcode interpreter instead of fs_pass_<i>
+  int jit_chunks = 1;          // FS_JIT_CHUNKS: fault-list | frame-kernel pipeline depth
+  uint64_t stratum_chunk = 0;  // FS_STRATUM_CHUNK: stratified-sampling chunk (tests)
+  void read() {
+    no_affine = getenv("FS_NO_AFFINE") != nullptr;
+    block_no_jit = getenv("FS_BLOCK_NO_JIT") != nullptr;
+    block_jit_warp = getenv("FS_BLOCK_JIT_WARP") != nullptr;
+    if (const char* e = getenv("FS_BLOCK_K")) block_k = std::max(1, atoi(e));
+    hbm_fused = getenv("FS_HBM_FUSED") != nullptr;
+    hbm_unfused = getenv("FS_HBM_UNFUSED") != nullptr;
+    hbm_no_jit = getenv("FS_HBM_NO_JIT") != nullptr;
+    if (const char* e = getenv("FS_JIT_CHUNKS")) jit_chunks = std::max(1, std::min(kChunks, atoi(e)));
+    if (const char* e = getenv("FS_STRATUM_CHUNK")) stratum_chunk = std::max<uint64_t>(32, (uint64_t)atoll(e) / 32 * 32);
+  }
+};
+
 struct fs_prog {
   fs_prog_desc desc;  // scalar fields only (pointers refer to host memory of the creator)
+  EnvSwitches env;
   fs::DevProg dp;
   void* dbuf = nullptr;
   int device = 0;
@@ -170,6 +212,10 @@ struct fs_prog {
   std::vector<int32_t> h_next_array, h_frame_mat_off;
   std::map<int, fsjit::CUfunction> seg_fn;
   std::string seg_jit_err;
+  void* d_cp = nullptr;  // checkpoint instruction counts + amplitude offsets of the current call
+  size_t cp_bytes = 0;
+  std::vector<int> cp_list;        // the current call's checkpoints (host copy, large-k planner)
+  std::vector<uint64_t> cp_offs;   // their amplitude offsets (complex elements)
   void* hbm = nullptr;
   size_t hbm_bytes = 0;
   uint64_t hbm_B = 0;
@@ -189,6 +235,7 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   auto* p = new fs_prog();
   p->desc = *d;
   p->device = dev;
+  p->env.read();
   FS_CUDA_TRY(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev));
 
   // pack every table into one device allocation (16 B aligned sections)
@@ -362,6 +409,7 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
 
 extern "C" void fs_program_destroy(fs_prog* p) {
   if (!p) return;
+  DeviceGuard dg(p->device);
   cudaFree(p->dbuf);
   cudaFree(p->scratch);
   cudaFree(p->d_status);
@@ -387,6 +435,7 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->flist);
   cudaFree(p->d_site_block);
   cudaFree(p->d_aff_tables);
+  cudaFree(p->d_cp);
   if (p->aff.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->aff.mod);
   if (p->jit.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->jit.mod);
   delete p;
@@ -394,10 +443,11 @@ extern "C" void fs_program_destroy(fs_prog* p) {
 
 static bool wants_hbm(const fs_prog* p, uint32_t flags) { return p->dp.k_max >= kLargeK || (flags & FS_FORCE_HBM); }
 
-static bool wants_general(const fs_prog* p, uint32_t flags, const fs_trace_out* tout) {
+static bool wants_general(const fs_prog* p, uint32_t flags, const fs_trace_in* tin, const fs_trace_out* tout) {
   if (p->dp.k_max > 0) return true;
   if (flags & (FS_RNG_SPLITMIX | FS_FORCE_GENERAL)) return true;
-  if (tout && (tout->gamma || tout->amps || tout->draws)) return true;
+  if (tout && (tout->gamma || tout->amps || tout->draws || tout->records)) return true;
+  if (tin && tin->ncheckpoints > 0) return true;
   return false;
 }
 
@@ -504,7 +554,7 @@ extern "C" int fs_debug_gjit_source(fs_prog* p, char* buf, size_t len) {
 }
 
 namespace {
-int plan_hbm(fs_prog* p, int stop, bool fused);
+int plan_hbm(fs_prog* p, int stop, bool fused, const std::vector<int>& cuts = {});
 }
 // large-k plan statistics: [steps, passes, fused ops, unfused array kernels, measurements]
 extern "C" int fs_debug_hbm_plan(fs_prog* p, int64_t* out) {
@@ -613,7 +663,7 @@ extern "C" const char* fs_debug_jit_status(fs_prog* p) {
 extern "C" int fs_program_engine(const fs_prog* p, uint32_t flags) {
   if (!p) return set_error(FS_ERR_ARG, "null program");
   if (wants_hbm(p, flags)) return 2;
-  return wants_general(p, flags, nullptr) ? 0 : 1;
+  return wants_general(p, flags, nullptr, nullptr) ? 0 : 1;
 }
 
 namespace {
@@ -896,17 +946,21 @@ int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector
     // ran ~2x slower specialised than interpreted (instruction-fetch stalls: every scalar run and
     // measurement inlines the scalar VM; out-of-line calls cost more than they saved) and keep
     // the interpreter unless FS_BLOCK_JIT_WARP is set
-    if (karr < block_k || (karr <= 10 && !getenv("FS_BLOCK_JIT_WARP"))) continue;
+    if (karr < block_k || (karr <= 10 && !p->env.block_jit_warp)) continue;
     gen_segment(o, p, bounds[s], bounds[s + 1], karr, karr <= 10 ? 32 : 256);
     begins.push_back(bounds[s]);
   }
   if (begins.empty()) { p->seg_jit = 1; return FS_OK; }
-  static std::mutex mu;
-  static std::map<std::string, fsjit::CUmodule> cache;
+  static std::mutex mu;  // modules belong to a context: key (current context, source)
+  static std::map<std::pair<fsjit::CUcontext, std::string>, fsjit::CUmodule> cache;
   std::lock_guard<std::mutex> g(mu);
   const std::string src = o.str();
+  if (!fsjit::api().ok) { p->seg_jit_err = fsjit::api().why; return FS_ERR_ARG; }
+  fsjit::CUcontext ctx = nullptr;
+  fsjit::api().cuCtxGetCurrent(&ctx);
+  const auto key = std::make_pair(ctx, src);
   fsjit::CUmodule mod = nullptr;
-  auto it = cache.find(src);
+  auto it = cache.find(key);
   if (it != cache.end()) {
     mod = it->second;
   } else {
@@ -914,7 +968,7 @@ int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector
     std::string err = fsjit::compile(src, fsjit::self_dir() + "/../csrc", c, ("fs_seg_" + std::to_string(begins[0])).c_str());
     if (!err.empty()) { p->seg_jit_err = err; return FS_ERR_ARG; }
     mod = c.mod;
-    cache[src] = mod;
+    cache[key] = mod;
   }
   for (int b : begins) {
     fsjit::CUfunction f = nullptr;
@@ -947,7 +1001,8 @@ int launch_block_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cu
   const size_t blocks_needed = (S.n_in + ngroups - 1) / ngroups;
   const size_t grid = std::max<size_t>(1, std::min<size_t>(blocks_needed, (size_t)p->num_sms * occ));
   auto fit = p->seg_fn.find(S.seg_begin);
-  if (!sm && p->seg_jit == 1 && fit != p->seg_fn.end() && !getenv("FS_BLOCK_NO_JIT")) {  // specialised kernel
+  const bool trace = a.fault_modes || a.forced || a.t_fx || a.t_gamma || a.t_amps || a.t_draws || a.t_rec || a.ncp;
+  if (!sm && !trace && p->seg_jit == 1 && fit != p->seg_fn.end() && !p->env.block_no_jit) {  // specialised kernel
     fsjit::Api& J = fsjit::api();
     if (J.cuFuncSetAttribute(fit->second, 8, (int)smem) != 0) return set_error(FS_ERR_CUDA, "cuFuncSetAttribute(fs_seg)");
     fs::DevProg dpv = dp;
@@ -1022,8 +1077,8 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   uint32_t* d_nout = reinterpret_cast<uint32_t*>(p->d_counts);
   p->seg_counts.clear();
   int block_k = kBlockK;
-  if (const char* e = getenv("FS_BLOCK_K")) block_k = std::max(1, atoi(e));  // experiments
-  if (!(a.flags & FS_RNG_SPLITMIX) && !getenv("FS_BLOCK_NO_JIT") && p->seg_jit == 0) {
+  if (p->env.block_k) block_k = p->env.block_k;  // experiments
+  if (!(a.flags & FS_RNG_SPLITMIX) && !p->env.block_no_jit && p->seg_jit == 0) {
     std::vector<int> karrs;
     for (int sgi = 0; sgi < nseg; sgi++) {
       int kk = bounds[sgi] > 0 ? sched[bounds[sgi] - 1] : 0;
@@ -1244,12 +1299,13 @@ void compile_pass_code(std::vector<fs::TileOp>& pops, const std::vector<int>& T,
 // Host walk of the program (shot-independent): logical->physical axis map, the scalar
 // segments, per-instruction array kernels, measurements, and -- when the live dimension is at
 // least fs::kTileBits -- fused tile passes (fs_hbm_fused.cuh).
-int plan_hbm(fs_prog* p, int stop, bool fused) {
+int plan_hbm(fs_prog* p, int stop, bool fused, const std::vector<int>& cuts) {
   HbmPlan& PL = p->hplan;
-  if (PL.built && PL.stop == stop && PL.fused == fused) return FS_OK;
+  if (PL.built && PL.stop == stop && PL.fused == fused && PL.cuts == cuts) return FS_OK;
   PL = HbmPlan{};
   PL.stop = stop;
   PL.fused = fused;
+  PL.cuts = cuts;
   p->pass_jit = 0;
   p->pass_fn.clear();
   const fs::DevProg& dp = p->dp;
@@ -1357,7 +1413,29 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
     st.count = count;
     PL.steps.push_back(st);
   };
+  // checkpoint c (state after instructions [0, c)): every step before it is complete, then a
+  // DUMP step records the frames / gamma / active array with the axis map of that point
+  size_t next_cut = 0;
+  auto dump_at = [&](int pos) {
+    while (next_cut < cuts.size() && cuts[next_cut] == pos) {
+      flush();
+      HbmStep st{};
+      st.kind = HbmStep::DUMP;
+      st.i0 = pos;
+      st.cp = (int)next_cut;
+      st.i1 = (int)live.size();
+      for (int b = 0; b < (int)live.size(); b++) st.map.phys[b] = (int8_t)live[b];
+      PL.steps.push_back(st);
+      next_cut++;
+    }
+  };
+  auto next_cut_after = [&](int pos) {
+    for (size_t c = next_cut; c < cuts.size(); c++)
+      if (cuts[c] > pos) return cuts[c];
+    return INT_MAX;
+  };
   int i = 0;
+  dump_at(0);
   while (i < stop) {
     int j = i;
     while (j < stop) {
@@ -1365,6 +1443,10 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
       if (op == FS_OP_MEAS_ACTIVE || op == FS_OP_MEAS_COLLAPSE) break;
       j++;
     }
+    // a checkpoint inside [i, j) ends this range there (the rest is the next iteration's)
+    const int jc = std::min(j, next_cut_after(i));
+    const bool cut_here = jc < j;
+    j = jc;
     if (j > i) {
       HbmStep st{};
       st.kind = HbmStep::SCALAR;
@@ -1456,6 +1538,12 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
       }
     }
     flush();
+    if (cut_here) {
+      dump_at(j);
+      i = j;
+      continue;
+    }
+    dump_at(j);
     if (j >= stop) { i = j; break; }
     const int* I = ins_all + (size_t)j * FS_INS_WORDS;
     const int op = FS_OPCODE(I[0]);
@@ -1474,6 +1562,7 @@ int plan_hbm(fs_prog* p, int stop, bool fused) {
     PL.steps.push_back(st);
     if (st.collapse) live.erase(live.begin() + I[2]);
     i = j + 1;
+    dump_at(i);
   }
   const int kst = stop > 0 ? p->h_sched[stop - 1] : 0;
   if ((int)live.size() != kst) return set_error(FS_ERR_ARG, "internal: axis map out of sync with schedule");
@@ -1650,12 +1739,17 @@ int ensure_pass_jit(fs_prog* p) {
   const HbmPlan& PL = p->hplan;
   const std::string src = gen_pass_source(PL);
   // one module per distinct source per process (tests and benches create many programs)
+  // (modules belong to a context: the key is (current context, source))
   static std::mutex mu;
-  static std::map<std::string, fsjit::CUmodule> cache;
+  static std::map<std::pair<fsjit::CUcontext, std::string>, fsjit::CUmodule> cache;
   std::lock_guard<std::mutex> g(mu);
   fsjit::Api& J = fsjit::api();
+  if (!J.ok) { p->pass_jit_err = J.why; return FS_ERR_ARG; }
+  fsjit::CUcontext ctx = nullptr;
+  J.cuCtxGetCurrent(&ctx);
+  const auto key = std::make_pair(ctx, src);
   fsjit::CUmodule mod = nullptr;
-  auto it = cache.find(src);
+  auto it = cache.find(key);
   if (it != cache.end()) {
     mod = it->second;
   } else {
@@ -1663,7 +1757,7 @@ int ensure_pass_jit(fs_prog* p) {
     std::string err = fsjit::compile(src, fsjit::self_dir() + "/../csrc", c, "fs_pass_0");
     if (!err.empty()) { p->pass_jit_err = err; return FS_ERR_ARG; }
     mod = c.mod;
-    cache[src] = mod;
+    cache[key] = mod;
   }
   p->pass_fn.assign(PL.passes.size(), nullptr);
   for (size_t i = 0; i < PL.passes.size(); i++) {
@@ -1744,12 +1838,13 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
     FS_CUDA_TRY(cudaGetLastError());
     return FS_OK;
   };
-  const bool fused = !(a.flags & FS_FORCE_HBM) || getenv("FS_HBM_FUSED");
-  int rc0 = plan_hbm(p, a.stop, fused && !getenv("FS_HBM_UNFUSED"));
+  const bool fused = !(a.flags & FS_FORCE_HBM) || p->env.hbm_fused;
+  static const std::vector<int> no_cuts;
+  int rc0 = plan_hbm(p, a.stop, fused && !p->env.hbm_unfused, a.ncp ? p->cp_list : no_cuts);
   if (rc0) return rc0;
   const HbmPlan& PL = p->hplan;
   const size_t pass_smem = fs::kPassSmem;
-  const bool use_pass_jit = !PL.passes.empty() && !getenv("FS_HBM_NO_JIT") && ensure_pass_jit(p) == FS_OK;
+  const bool use_pass_jit = !PL.passes.empty() && !p->env.hbm_no_jit && ensure_pass_jit(p) == FS_OK;
   if (!PL.passes.empty())
     FS_CUDA_TRY(cudaFuncSetAttribute(fs::hbm_fused_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem));
   for (uint64_t batch0 = 0; batch0 < a.nshots; batch0 += B) {
@@ -1797,6 +1892,16 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
           FS_CUDA_TRY(cudaGetLastError());
           break;
         }
+        case HbmStep::DUMP: {
+          fs::hbm_cp_kernel<<<(W + 127) / 128, 128, 0, stream>>>(dp, a, H, batch0, W, st.cp);
+          const uint64_t sz = 1ull << st.i1;
+          const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>((sz + 255) / 256, 1024));
+          fs::hbm_gather_kernel<<<dim3((unsigned)gx, (unsigned)nb), 256, 0, stream>>>(
+              dp, a, H, batch0, (uint32_t)nb, st.i1, st.map, a.cp_amps + 2 * p->cp_offs[st.cp]);
+          p->launches += 2;
+          FS_CUDA_TRY(cudaGetLastError());
+          break;
+        }
         case HbmStep::MEAS: {
           const int nbu = (int)std::max<uint64_t>(1, std::min<uint64_t>(nblk, (st.count + 2047) / 2048));
           fs::hbm_reduce_kernel<<<dim3(nbu, (unsigned)nb), 256, 0, stream>>>(st.op, H, st.count, st.collapse, st.u10, st.u11);
@@ -1825,7 +1930,8 @@ int launch_hbm(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
       for (int b = 0; b < kst; b++) m.phys[b] = (int8_t)PL.final_live[b];
       const uint64_t sz = 1ull << kst;
       const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>((sz + 255) / 256, 1024));
-      fs::hbm_gather_kernel<<<dim3((unsigned)gx, (unsigned)nb), 256, 0, stream>>>(dp, a, H, batch0, (uint32_t)nb, kst, m);
+      fs::hbm_gather_kernel<<<dim3((unsigned)gx, (unsigned)nb), 256, 0, stream>>>(dp, a, H, batch0, (uint32_t)nb, kst, m,
+                                                                                  a.t_amps);
       p->launches++;
       FS_CUDA_TRY(cudaGetLastError());
     }
@@ -1868,7 +1974,48 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     a.t_gamma = tout->gamma;
     a.t_amps = tout->amps;
     a.t_draws = tout->draws;
+    a.t_rec = tout->records;
     if ((a.t_fx == nullptr) != (a.t_fz == nullptr)) return set_error(FS_ERR_ARG, "frame_x/frame_z must both be set");
+    if (a.t_rec && dp.R) FS_CUDA_TRY(cudaMemsetAsync(a.t_rec, 0, nshots * (size_t)dp.R, stream));
+  }
+  if (tin && tin->ncheckpoints > 0) {  // checkpoint list (host) -> device, with amplitude offsets
+    const int ncp = tin->ncheckpoints;
+    if (!tin->checkpoints) return set_error(FS_ERR_ARG, "checkpoints is NULL");
+    if (!tout || !tout->cp_valid || !tout->cp_frame_x || !tout->cp_frame_z || !tout->cp_gamma || !tout->cp_amps)
+      return set_error(FS_ERR_ARG, "checkpoints need cp_valid, cp_frame_x/z, cp_gamma and cp_amps outputs");
+    std::vector<int> at(tin->checkpoints, tin->checkpoints + ncp);
+    std::vector<uint64_t> off(ncp);
+    uint64_t o = 0;
+    for (int j = 0; j < ncp; j++) {
+      if (at[j] < 0 || at[j] > a.stop || (j && at[j] <= at[j - 1]))
+        return set_error(FS_ERR_ARG, "checkpoints must be strictly ascending within [0, stop]");
+      off[j] = o;
+      o += nshots << (at[j] > 0 ? p->h_sched[at[j] - 1] : 0);
+    }
+    const size_t need = align_up(4 * (size_t)ncp, 16) + 8 * (size_t)ncp;
+    if (need > p->cp_bytes) {
+      cudaFree(p->d_cp);
+      p->d_cp = nullptr;
+      p->cp_bytes = 0;
+      FS_CUDA_TRY(cudaMalloc(&p->d_cp, need));
+      p->cp_bytes = need;
+    }
+    int* d_at = static_cast<int*>(p->d_cp);
+    uint64_t* d_off = reinterpret_cast<uint64_t*>(static_cast<unsigned char*>(p->d_cp) + align_up(4 * (size_t)ncp, 16));
+    FS_CUDA_TRY(cudaMemcpyAsync(d_at, at.data(), 4 * (size_t)ncp, cudaMemcpyHostToDevice, stream));
+    FS_CUDA_TRY(cudaMemcpyAsync(d_off, off.data(), 8 * (size_t)ncp, cudaMemcpyHostToDevice, stream));
+    FS_CUDA_TRY(cudaStreamSynchronize(stream));  // the host vectors go out of scope
+    p->cp_list = at;
+    p->cp_offs = off;
+    a.ncp = ncp;
+    a.cp_at = d_at;
+    a.cp_off = d_off;
+    a.cp_valid = tout->cp_valid;
+    a.cp_fx = tout->cp_frame_x;
+    a.cp_fz = tout->cp_frame_z;
+    a.cp_gamma = tout->cp_gamma;
+    a.cp_amps = tout->cp_amps;
+    FS_CUDA_TRY(cudaMemsetAsync(a.cp_valid, 0, (size_t)ncp * nshots, stream));
   }
   a.arr_log2 = dp.k_max;
   a.draw0 = draw0;
@@ -1881,10 +2028,10 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     if (dp.D) FS_CUDA_TRY(cudaMemsetAsync(a.det, 0, sizeof(uint32_t) * dp.D * W, stream));
     a.prezeroed = 1;
   }
-  const bool general = wants_general(p, flags, tout);
+  const bool general = wants_general(p, flags, tin, tout);
   const bool trace_in = tin && (tin->fault_modes || tin->forced);
   if (!general && !trace_in && !(tout && tout->frame_x) && !(flags & FS_NO_JIT) && a.stop == dp.num_instrs &&
-      !getenv("FS_NO_AFFINE") && ensure_aff(p) == FS_OK)
+      !p->env.no_affine && ensure_aff(p) == FS_OK)
     return launch_aff(p, a, stream);
   if (!general && !trace_in && !(tout && tout->frame_x) && !(flags & FS_NO_JIT) && a.stop == dp.num_instrs) {
     int rc = ensure_jit(p);
@@ -1904,7 +2051,7 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
         for (int c = 0; c < kChunks + 1; c++) FS_CUDA_TRY(cudaEventCreateWithFlags(&p->ev[c], cudaEventDisableTiming));
       }
       int nch_req = 1;
-      if (const char* ce = getenv("FS_JIT_CHUNKS")) nch_req = std::max(1, std::min(kChunks, atoi(ce)));
+      nch_req = p->env.jit_chunks;
       const int nch = W >= (size_t)nch_req * 4096 ? nch_req : 1;
       const size_t per = (W + nch - 1) / nch;
       FS_CUDA_TRY(cudaEventRecord(p->ev[kChunks], stream));
@@ -1962,8 +2109,9 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
     return FS_OK;
   }
   // general engine
-  const bool trace = (tin && (tin->fault_modes || tin->forced)) || tout;
-  if (dp.has_psel && !trace && a.stop == dp.num_instrs) return launch_segmented(p, a, stream);
+  const bool trace = (tin && (tin->fault_modes || tin->forced || tin->ncheckpoints > 0)) || tout;
+  if (dp.has_psel && (!trace || (flags & FS_FORCE_SEGMENTED)) && a.stop == dp.num_instrs)
+    return launch_segmented(p, a, stream);
   if (!(a.flags & (FS_RNG_SPLITMIX | FS_NO_RENORM | FS_NO_JIT | FS_FORCE_GENERAL)) && !trace &&
       a.stop == dp.num_instrs && gjit_supported(p) && ensure_gjit(p) == FS_OK) {
     uint32_t *fent = nullptr, *bcount = nullptr, *ntot = nullptr;
@@ -2025,6 +2173,7 @@ extern "C" int fs_sample(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nsh
                          void* stream) {
   if (!p) return set_error(FS_ERR_ARG, "null program");
   std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard dg(p->device);
   return launch(p, seed, shot0, nshots, flags, tin, out, tout, static_cast<cudaStream_t>(stream));
 }
 
@@ -2034,17 +2183,13 @@ extern "C" int fs_sample_host(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_
   if (!p || !out) return set_error(FS_ERR_ARG, "null argument");
   if (nshots == 0) return FS_OK;
   std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard dg(p->device);
   const fs::DevProg& dp = p->dp;
   const size_t W = (nshots + 31) / 32;
   int stop = dp.num_instrs;
   if (tin && tin->stop >= 0 && tin->stop < dp.num_instrs) stop = tin->stop;
   int k_stop = 0;
-  if (stop > 0) {
-    // schedule lives on the device; the host copy was not retained -> fetch one int
-    int ks = 0;
-    FS_CUDA_TRY(cudaMemcpy(&ks, dp.schedule + stop - 1, sizeof(int), cudaMemcpyDeviceToHost));
-    k_stop = ks;
-  }
+  if (stop > 0) k_stop = p->h_sched[stop - 1];
   const size_t n = (size_t)dp.n;
   // sizes
   size_t need = 0;
@@ -2053,11 +2198,23 @@ extern "C" int fs_sample_host(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_
   const bool has_fm = tin && tin->fault_modes, has_fo = tin && tin->forced;
   if (has_fm) acc(2 * nshots * dp.E);
   if (has_fo) acc(nshots * dp.R);
+  const int ncp = (tin && tin->ncheckpoints > 0 && tin->checkpoints) ? tin->ncheckpoints : 0;
+  size_t cp_amp_elems = 0;  // complex elements of all checkpoint blocks
+  for (int j = 0; j < ncp; j++) {
+    const int c = tin->checkpoints[j];
+    if (c < 0 || c > stop) return set_error(FS_ERR_ARG, "checkpoints must be strictly ascending within [0, stop]");
+    cp_amp_elems += nshots << (c > 0 ? p->h_sched[c - 1] : 0);
+  }
   if (tout) {
     if (tout->frame_x) { acc(nshots * n); acc(nshots * n); }
     if (tout->gamma) acc(16 * nshots);
     if (tout->amps) acc(16 * nshots * ((size_t)1 << k_stop));
     if (tout->draws) acc(4 * nshots);
+    if (tout->records) acc(nshots * (size_t)dp.R);
+    if (ncp) {
+      acc(ncp * nshots); acc(ncp * nshots * n); acc(ncp * nshots * n); acc(16 * ncp * nshots);
+      acc(16 * cp_amp_elems);
+    }
   }
   if (need > p->stage_bytes) {
     cudaFree(p->stage);
@@ -2081,6 +2238,8 @@ extern "C" int fs_sample_host(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_
   fs_trace_in* ptin = nullptr;
   if (tin) {
     dtin.stop = tin->stop;
+    dtin.ncheckpoints = tin->ncheckpoints;  // host list, read by launch()
+    dtin.checkpoints = tin->checkpoints;
     if (has_fm) {
       int16_t* d = st.take<int16_t>(nshots * dp.E);
       FS_CUDA_TRY(cudaMemcpyAsync(d, tin->fault_modes, 2 * nshots * dp.E, cudaMemcpyHostToDevice, s));
@@ -2100,6 +2259,14 @@ extern "C" int fs_sample_host(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_
     if (tout->gamma) dtout.gamma = st.take<double>(2 * nshots);
     if (tout->amps) dtout.amps = st.take<double>(2 * nshots * ((size_t)1 << k_stop));
     if (tout->draws) dtout.draws = st.take<uint32_t>(nshots);
+    if (tout->records) dtout.records = st.take<uint8_t>(nshots * (size_t)dp.R);
+    if (ncp) {
+      dtout.cp_valid = st.take<uint8_t>(ncp * nshots);
+      dtout.cp_frame_x = st.take<uint8_t>(ncp * nshots * n);
+      dtout.cp_frame_z = st.take<uint8_t>(ncp * nshots * n);
+      dtout.cp_gamma = st.take<double>(2 * ncp * nshots);
+      dtout.cp_amps = st.take<double>(2 * cp_amp_elems);
+    }
     ptout = &dtout;
   }
   int rc = launch(p, seed, shot0, nshots, flags, ptin, &dout, ptout, s);
@@ -2120,6 +2287,15 @@ extern "C" int fs_sample_host(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_
     if (tout->amps)
       FS_CUDA_TRY(cudaMemcpyAsync(tout->amps, dtout.amps, 16 * nshots * ((size_t)1 << k_stop), cudaMemcpyDeviceToHost, s));
     if (tout->draws) FS_CUDA_TRY(cudaMemcpyAsync(tout->draws, dtout.draws, 4 * nshots, cudaMemcpyDeviceToHost, s));
+    if (tout->records && dp.R)
+      FS_CUDA_TRY(cudaMemcpyAsync(tout->records, dtout.records, nshots * (size_t)dp.R, cudaMemcpyDeviceToHost, s));
+    if (ncp) {
+      if (tout->cp_valid) FS_CUDA_TRY(cudaMemcpyAsync(tout->cp_valid, dtout.cp_valid, ncp * nshots, cudaMemcpyDeviceToHost, s));
+      if (tout->cp_frame_x) FS_CUDA_TRY(cudaMemcpyAsync(tout->cp_frame_x, dtout.cp_frame_x, ncp * nshots * n, cudaMemcpyDeviceToHost, s));
+      if (tout->cp_frame_z) FS_CUDA_TRY(cudaMemcpyAsync(tout->cp_frame_z, dtout.cp_frame_z, ncp * nshots * n, cudaMemcpyDeviceToHost, s));
+      if (tout->cp_gamma) FS_CUDA_TRY(cudaMemcpyAsync(tout->cp_gamma, dtout.cp_gamma, 16 * ncp * nshots, cudaMemcpyDeviceToHost, s));
+      if (tout->cp_amps) FS_CUDA_TRY(cudaMemcpyAsync(tout->cp_amps, dtout.cp_amps, 16 * cp_amp_elems, cudaMemcpyDeviceToHost, s));
+    }
   }
   FS_CUDA_TRY(cudaStreamSynchronize(s));
   if (out->status) *out->status = status;
@@ -2130,10 +2306,23 @@ extern "C" int fs_sample_host(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_
   return status;
 }
 
+namespace {
+// device status of a whole call -> host (synchronizes the stream); sets the error text
+int finish_status(const int32_t* status_d, cudaStream_t stream) {
+  int32_t status = 0;
+  FS_CUDA_TRY(cudaMemcpyAsync(&status, status_d, 4, cudaMemcpyDeviceToHost, stream));
+  FS_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (status == FS_ERR_SHOT_NAN) g_last_error = "NaN amplitude encountered at an active measurement";
+  else if (status) g_last_error = "forced outcome has probability below BRANCH_FLOOR";
+  return status;
+}
+}  // namespace
+
 extern "C" int fs_accumulate(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t flags,
                              int64_t* counts, void* stream_) {
   if (!p || !counts) return set_error(FS_ERR_ARG, "null argument");
   std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard dg(p->device);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   const fs::DevProg& dp = p->dp;
   const int nrows = dp.U + dp.D + dp.O;
@@ -2148,6 +2337,10 @@ extern "C" int fs_accumulate(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t
     FS_CUDA_TRY(cudaMalloc(&p->stage, need));
     p->stage_bytes = need;
   }
+  // shots that raised (NaN / impossible forced outcome) are not silently counted as rejected:
+  // the call returns their status like fs_sample (the reference propagates ShotError)
+  int32_t* status_d = reinterpret_cast<int32_t*>(static_cast<unsigned char*>(p->stage) + 4 * Wc * (nrows + 2));
+  FS_CUDA_TRY(cudaMemsetAsync(status_d, 0, 4, stream));
   for (uint64_t s0 = 0; s0 < nshots; s0 += chunk) {
     const uint64_t ns = std::min<uint64_t>(chunk, nshots - s0);
     const uint32_t W = (uint32_t)((ns + 31) / 32);
@@ -2160,6 +2353,7 @@ extern "C" int fs_accumulate(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t
     o.obs = rows + (size_t)W * (dp.U + dp.D);
     o.accepted = rows + (size_t)W * nrows;
     o.error = rows + (size_t)W * (nrows + 1);
+    o.status = status_d;  // accumulates (atomicMax) over every chunk of the call
     int rc = launch(p, seed, shot0 + s0, ns, flags, nullptr, &o, nullptr, stream);
     if (rc != FS_OK) return rc;
     dim3 grid(std::min<uint32_t>((W + 255) / 256, 64), nrows + 1);
@@ -2167,7 +2361,7 @@ extern "C" int fs_accumulate(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t
     p->launches++;
     FS_CUDA_TRY(cudaGetLastError());
   }
-  return FS_OK;
+  return finish_status(status_d, stream);
 }
 
 // ------------------------------------------------------------------ output formats (cli.py)
@@ -2201,6 +2395,7 @@ extern "C" int fs_format(fs_prog* p, const fs_sample_out* words, uint64_t nshots
   if (nkept) *nkept = 0;
   if (nshots == 0) return FS_OK;
   std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard dg(p->device);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   const fs::DevProg& dp = p->dp;
   const char* wt = weight_text ? weight_text : "1";
@@ -2314,7 +2509,7 @@ int sample_stratum_impl(fs_prog* p, uint32_t w, uint64_t seed, uint64_t shot0, u
   const size_t W = (nshots + 31) / 32;
   const int rows = dp.U + dp.D + dp.O + 2;
   uint64_t chunk = std::max<uint64_t>(32, ((uint64_t)1 << 30) / (2 * E) / 32 * 32);
-  if (const char* e = getenv("FS_STRATUM_CHUNK")) chunk = std::max<uint64_t>(32, (uint64_t)atoll(e) / 32 * 32);  // tests
+  if (p->env.stratum_chunk) chunk = p->env.stratum_chunk;  // tests
   chunk = std::min<uint64_t>(chunk, (nshots + 31) / 32 * 32);
   const size_t Wc = chunk / 32;
   const size_t need = align_up(2 * E * chunk, 256) + align_up(4 * chunk, 256) + align_up(4 * Wc * rows, 256) + 256;
@@ -2381,6 +2576,7 @@ int sample_stratum_impl(fs_prog* p, uint32_t w, uint64_t seed, uint64_t shot0, u
 extern "C" int fs_stratum_weight(fs_prog* p, uint32_t w, double* weight) {
   if (!p || !weight) return set_error(FS_ERR_ARG, "null argument");
   std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard dg(p->device);
   if (int rc = stratum_prepare(p, w)) return rc;
   *weight = p->strat_weight;
   return FS_OK;
@@ -2391,6 +2587,7 @@ extern "C" int fs_sample_stratum(fs_prog* p, uint32_t w, uint64_t seed, uint64_t
   if (!p || !out) return set_error(FS_ERR_ARG, "null argument");
   if (nshots == 0) return FS_OK;
   std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard dg(p->device);
   return sample_stratum_impl(p, w, seed, shot0, nshots, flags, out, static_cast<cudaStream_t>(stream));
 }
 
@@ -2399,6 +2596,7 @@ extern "C" int fs_sample_stratum_host(fs_prog* p, uint32_t w, uint64_t seed, uin
   if (!p || !out) return set_error(FS_ERR_ARG, "null argument");
   if (nshots == 0) return FS_OK;
   std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard dg(p->device);
   const fs::DevProg& dp = p->dp;
   const size_t W = (nshots + 31) / 32;
   const size_t rows = (size_t)dp.U + dp.D + dp.O + 2;
@@ -2442,6 +2640,7 @@ extern "C" int fs_accumulate_stratum(fs_prog* p, uint32_t w, uint64_t seed, uint
                                      uint32_t flags, int64_t* counts, void* stream_) {
   if (!p || !counts) return set_error(FS_ERR_ARG, "null argument");
   std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard dg(p->device);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   const fs::DevProg& dp = p->dp;
   const int nrows = dp.U + dp.D + dp.O;
@@ -2456,6 +2655,10 @@ extern "C" int fs_accumulate_stratum(fs_prog* p, uint32_t w, uint64_t seed, uint
     FS_CUDA_TRY(cudaMalloc(&p->stage, need));
     p->stage_bytes = need;
   }
+  // shots that raised (NaN / impossible forced outcome) are not silently counted as rejected:
+  // the call returns their status like fs_sample (the reference propagates ShotError)
+  int32_t* status_d = reinterpret_cast<int32_t*>(static_cast<unsigned char*>(p->stage) + 4 * Wc * (nrows + 2));
+  FS_CUDA_TRY(cudaMemsetAsync(status_d, 0, 4, stream));
   for (uint64_t s0 = 0; s0 < nshots; s0 += chunk) {
     const uint64_t ns = std::min<uint64_t>(chunk, nshots - s0);
     const uint32_t W = (uint32_t)((ns + 31) / 32);
@@ -2466,6 +2669,7 @@ extern "C" int fs_accumulate_stratum(fs_prog* p, uint32_t w, uint64_t seed, uint
     o.obs = rows + (size_t)W * (dp.U + dp.D);
     o.accepted = rows + (size_t)W * nrows;
     o.error = rows + (size_t)W * (nrows + 1);
+    o.status = status_d;
     int rc = sample_stratum_impl(p, w, seed, shot0 + s0, ns, flags, &o, stream);
     if (rc != FS_OK) return rc;
     dim3 grid(std::min<uint32_t>((W + 255) / 256, 64), nrows + 1);
@@ -2473,7 +2677,7 @@ extern "C" int fs_accumulate_stratum(fs_prog* p, uint32_t w, uint64_t seed, uint
     p->launches++;
     FS_CUDA_TRY(cudaGetLastError());
   }
-  return FS_OK;
+  return finish_status(status_d, stream);
 }
 
 // ------------------------------------------------------------------ expectation probe

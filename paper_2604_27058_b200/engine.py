@@ -62,14 +62,23 @@ class DeviceProgram:
         f.argtypes = [C.c_void_p]
         return f(self._h).decode()
 
+    def segment_counts(self) -> list[int]:
+        """Diagnostics of the last segmented call: shots entering each post-select segment."""
+        buf = (C.c_uint32 * 4096)()
+        f = self._lib.fs_debug_seg_counts
+        f.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.c_int]
+        n = f(self._h, buf, 4096)
+        return [int(buf[i]) for i in range(min(max(n, 0), 4096))]
+
     def engine(self, flags: int = 0) -> str:
         return {0: "general", 1: "frame", 2: "hbm"}[self._lib.fs_program_engine(self._h, flags)]
 
     # -- host buffers (C-ABI does H2D/D2H) ----------------------------------------------
     def sample_host(self, nshots: int, seed: int = 0, shot0: int = 0, flags: int = 0,
                     fault_modes=None, forced=None, stop: int = -1, want_state: bool = False,
-                    check: bool = True):
-        """Returns (status, HostOutputs, TraceBuffers|None)."""
+                    check: bool = True, checkpoints=None):
+        """Returns (status, HostOutputs, TraceBuffers|None).  ``checkpoints``: instruction counts
+        at which the state is also recorded (TraceBuffers.checkpoint(j))."""
         if nshots < 1:
             raise ValueError("shots must be >= 1")
         out = HostOutputs(self.prog, nshots)
@@ -77,8 +86,9 @@ class DeviceProgram:
         out.struct.status = status.ctypes.data_as(C.POINTER(C.c_int32))
         tb = None
         tin = tout = None
-        if fault_modes is not None or forced is not None or stop >= 0 or want_state:
-            tb = TraceBuffers(self.prog, nshots, fault_modes, forced, stop, want_state=want_state)
+        if fault_modes is not None or forced is not None or stop >= 0 or want_state or checkpoints is not None:
+            tb = TraceBuffers(self.prog, nshots, fault_modes, forced, stop, want_state=want_state,
+                              checkpoints=checkpoints)
             tin = C.byref(tb.tin)
             tout = C.byref(tb.tout) if tb.tout is not None else None
         rc = self._lib.fs_sample_host(self._h, seed, shot0, nshots, flags, tin, C.byref(out.struct), tout)

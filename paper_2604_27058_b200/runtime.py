@@ -407,9 +407,11 @@ def run_shot(prog, state: ShotState | None = None, shot: int = 0, seed: int = 0,
              forced_outcomes=None, weight: float = 1.0, trace=None, rng: str = "reference") -> ShotRecord:
     """Execute one shot on the GPU; ``state`` receives its final state (runtime.py:731-751).
 
-    ``trace(state, ins)`` is called after every instruction like the reference;
-    each call re-executes the program prefix on the device (the engine does
-    not stop mid-kernel), so traced runs are for validation, not speed.
+    ``trace(state, ins)`` is called after every instruction like the reference (a post-selected
+    shot stops before the halting instruction's callback, runtime.py:749).  The states it sees
+    come from the device's checkpoint dumps (fs_trace_in.checkpoints): one device call returns
+    the state after every instruction, split into a few calls only when the active arrays of all
+    checkpoints would exceed ``_TRACE_BYTES``.
     """
     if state is None:
         state = ShotState(prog, seed=seed)
@@ -423,46 +425,112 @@ def run_shot(prog, state: ShotState | None = None, shot: int = 0, seed: int = 0,
     state.forced_faults = forced_faults
     state.forced_outcomes = forced_outcomes
     state.weight = weight
+    # a 1-shot call at absolute shot index `shot`: pad the word so the Philox word matches
+    n = lane + 1
+    fmn = None if fm is None else np.repeat(fm, n, axis=0)
+    fon = None if fo is None else np.repeat(fo, n, axis=0)
+    if fon is not None:
+        fon[:lane] = -1
 
-    def run(stop: int):
-        # a 1-shot call at absolute shot index `shot`: pad the word so the Philox word matches
-        n = lane + 1
-        fmn = None if fm is None else np.repeat(fm, n, axis=0)
-        fon = None if fo is None else np.repeat(fo, n, axis=0)
-        if fon is not None:
-            fon[:lane] = -1
-        st, out, tb = dp.sample_host(n, seed=state.seed, shot0=base, flags=flags,
-                                     fault_modes=fmn, forced=fon, stop=stop, want_state=True, check=False)
-        if st not in (0,) and st > 0:
-            # errors of padding lanes are impossible (no forced outcomes there); ours raises
-            if out.error_bits()[lane]:
-                from .engine import raise_for_status
+    def call(stop: int, checkpoints=None):
+        st, out, tb = dp.sample_host(n, seed=state.seed, shot0=base, flags=flags, fault_modes=fmn, forced=fon,
+                                     stop=stop, want_state=True, check=False, checkpoints=checkpoints)
+        if st > 0 and out.error_bits()[lane]:
+            from .engine import raise_for_status
 
-                raise_for_status(st)
-        _copy_state(state, P, out, tb, lane, stop)
-        return out
+            raise_for_status(st)  # errors of padding lanes are impossible (nothing forced there)
+        elif st < 0:
+            from .engine import raise_for_status
+
+            raise_for_status(st)
+        return out, tb
 
     if trace is None:
-        out = run(-1)
+        out, tb = call(-1)
+        _copy_state(state, P, out, tb, lane)
     else:
         instrs = getattr(prog, "instrs", None)
         names = {v: k for k, v in OP_NAMES.items()}
-        out = None
-        for i in range(P.num_instrs):
-            out = run(i + 1)
-            ins = instrs[i] if instrs is not None else names[int(P.instrs[i, 0] & 0xFF)]
-            if not state.accepted:
-                break  # the halting post-select raises before its trace callback (runtime.py:749)
-            trace(state, ins)
-        if out is None:
-            out = run(-1)
+        writers = _writers(P)
+        N = P.num_instrs
+        out = tb = None
+        i = 0
+        while i < N:  # checkpoints i+1 .. j, one device call
+            j, nbytes = i, 0
+            while j < N and (j == i or nbytes + (16 * n << int(P.schedule[j])) <= _TRACE_BYTES):
+                nbytes += 16 * n << int(P.schedule[j])
+                j += 1
+            out, tb = call(j, checkpoints=np.arange(i + 1, j + 1, dtype=np.int32))
+            halted = False
+            for c in range(i + 1, j + 1):
+                cp = tb.checkpoint(c - i - 1)
+                if not cp["valid"][lane]:
+                    halted = True  # halted / raised before the end of instruction c-1
+                    break
+                _copy_checkpoint(state, P, tb, cp, lane, c, writers)
+                ins = instrs[c - 1] if instrs is not None else names[int(P.instrs[c - 1, 0] & 0xFF)]
+                trace(state, ins)
+            if halted:
+                break
+            i = j
+        out, tb = call(-1)
+        _copy_state(state, P, out, tb, lane)
     return ShotRecord(measurements=out.measurements()[lane].copy(),
                       detectors=out.detectors()[lane].copy(),
                       observables=out.observables()[lane].copy(),
                       accepted=bool(out.accepted_bits()[lane]), weight=weight)
 
 
-def _copy_state(state: ShotState, P: Program, out, tb, lane: int, stop: int) -> None:
+_TRACE_BYTES = 1 << 30  # active-array bytes of the checkpoints one traced device call returns
+
+
+def _writers(P: Program) -> dict:
+    """Instruction index writing each record / detector, and the observable contributions (for
+    the records / detectors / observables a trace callback sees mid-program)."""
+    rec_w = np.full(P.record_count, P.num_instrs, np.int64)
+    det_w = np.full(P.num_detectors, P.num_instrs, np.int64)
+    obs_c = []  # (instr, observable, records)
+    ops = P.instrs[:, 0] & 0xFF
+    for i in range(P.num_instrs):
+        op = int(ops[i])
+        if op in (5, 6, 7, 8):  # MeasDormantStatic/Random, MeasActive, MeasCollapse: w3 = record
+            rec_w[int(P.instrs[i, 3])] = i
+        elif op == 12:
+            det_w[int(P.instrs[i, 1])] = i
+        elif op == 13:
+            off, cnt = int(P.instrs[i, 2]), int(P.instrs[i, 3])
+            obs_c.append((i, int(P.instrs[i, 1]), P.reclists[off:off + cnt].astype(np.int64)))
+    return {"rec": rec_w, "det": det_w, "obs": obs_c}
+
+
+def _copy_checkpoint(state: ShotState, P: Program, tb, cp: dict, lane: int, c: int, writers: dict) -> None:
+    """State after instructions [0, c) (device checkpoint) into ``state``."""
+    state.frame_x[:] = cp["frame_x"][lane]
+    state.frame_z[:] = cp["frame_z"][lane]
+    state.gamma = complex(cp["gamma"][lane])
+    state.k = cp["k"]
+    state.buf[: 1 << cp["k"]] = cp["amps"][lane]
+    final = tb.records[lane, : P.record_count]
+    state.records[:] = np.where(writers["rec"] < c, final, 0)
+    if P.num_detectors:
+        dets = np.zeros(P.num_detectors, np.uint8)
+        for d in np.flatnonzero(writers["det"] < c):
+            off, cnt = _det_list(P, int(writers["det"][d]))
+            dets[d] = np.bitwise_xor.reduce(final[P.reclists[off:off + cnt]]) if cnt else 0
+        state.detectors[:] = dets
+    if P.num_observables:
+        obs = np.zeros(P.num_observables, np.uint8)
+        for i, o, recs in writers["obs"]:
+            if i < c and recs.size:
+                obs[o] ^= np.bitwise_xor.reduce(final[recs])
+        state.observables[:] = obs
+
+
+def _det_list(P: Program, i: int):
+    return int(P.instrs[i, 2]), int(P.instrs[i, 3])
+
+
+def _copy_state(state: ShotState, P: Program, out, tb, lane: int) -> None:
     state.frame_x[:] = tb.frame_x[lane, : P.n]
     state.frame_z[:] = tb.frame_z[lane, : P.n]
     state.gamma = complex(tb.gamma_c()[lane])
@@ -470,9 +538,7 @@ def _copy_state(state: ShotState, P: Program, out, tb, lane: int, stop: int) -> 
     state.buf[: 1 << tb.k_stop] = tb.amps_c()[lane]
     state.accepted = bool(out.accepted_bits()[lane])
     state.draws = int(tb.draws[lane])
-    meas = out.measurements()[lane]
-    state.records[:] = 0
-    state.records[P.user_records] = meas
+    state.records[:] = tb.records[lane, : P.record_count]  # user and hidden records (ShotState.records)
     if P.num_detectors:
         state.detectors[:] = out.detectors()[lane]
     if P.num_observables:

@@ -66,7 +66,7 @@ def trace_golden(prog, shots, seed, boost, rng, checkpoints=()):
     rand_records = {ins.record for ins in prog.instrs if type(ins).__name__ in RANDOM_KINDS}
     modes = np.full((shots, E), 2, dtype=np.int16)
     forced = np.full((shots, R), -1, dtype=np.int8)
-    rows = {k: [] for k in ("meas", "det", "obs", "acc", "fx", "fz", "gamma", "k", "amps", "draws")}
+    rows = {k: [] for k in ("meas", "det", "obs", "acc", "fx", "fz", "gamma", "k", "amps", "draws", "rec")}
     cps = {c: {"fx": [], "fz": [], "gamma": [], "amps": []} for c in checkpoints}
     for s in range(shots):
         for site, tab in enumerate(prog.sites):
@@ -99,6 +99,7 @@ def trace_golden(prog, shots, seed, boost, rng, checkpoints=()):
         rows["k"].append(st2.k)
         rows["amps"].append(st2.active_view().copy())
         rows["draws"].append(st2.rng.draws)
+        rows["rec"].append(st2.records.copy())
         for c in checkpoints:
             if c in snap:
                 fx, fz, g, a = snap[c]
@@ -119,6 +120,7 @@ def trace_golden(prog, shots, seed, boost, rng, checkpoints=()):
         "t_fx": np.array(rows["fx"], np.uint8), "t_fz": np.array(rows["fz"], np.uint8),
         "t_gamma": np.array(rows["gamma"], np.complex128), "t_k": np.array(rows["k"], np.int32),
         "t_draws": np.array(rows["draws"], np.int64),
+        "t_rec": np.array(rows["rec"], np.uint8).reshape(shots, R),  # all records, hidden included
     }
     ks = set(rows["k"])
     if len(ks) == 1:  # every shot ends at the same k unless some halted
@@ -152,8 +154,219 @@ def write_case(name, prog, text, *, free_shots=256, free_seed=3, trace_shots=16,
           f"({time.time() - t0:.1f}s)", flush=True)
 
 
+# ------------------------------------------------------------------ round-2 fixtures
+SKETCH_VECS = 4      # <v_i, a> for v_i ~ CN(0, 1)^(2^k), default_rng(SKETCH_SEED + i)
+SKETCH_SEED = 4242
+SKETCH_ENTRIES = 1024  # sampled entries, indices default_rng(SKETCH_SEED - 1).choice(2^k, 1024)
+
+
+def sketch_vectors(k):
+    """The fixed complex vectors of the amplitude sketch (the tests regenerate them)."""
+    out = []
+    for i in range(SKETCH_VECS):
+        g = np.random.default_rng(SKETCH_SEED + i)
+        out.append(g.standard_normal(1 << k) + 1j * g.standard_normal(1 << k))
+    idx = np.sort(np.random.default_rng(SKETCH_SEED - 1).choice(1 << k, size=min(SKETCH_ENTRIES, 1 << k),
+                                                                  replace=False))
+    return out, idx
+
+
+def sketch(a, vecs, idx):
+    """(sum |a|^2, [<v_i, a>], a[idx]) of one amplitude array."""
+    a = np.asarray(a, np.complex128)
+    return (float(np.vdot(a, a).real), np.array([np.vdot(v, a) for v in vecs], np.complex128),
+            a[idx].copy())
+
+
+def deep_trace_golden(prog, shots, seed, rng, checkpoints, boost=20.0, forced_builder=None):
+    """trace_golden for arrays too large to store: the active array at each checkpoint is kept as a
+    sketch (norm, inner products with fixed seeded vectors, sampled entries).  ``forced_builder``
+    (shot, modes) -> forced outcomes dict replaces the free-run recipe (post-selected programs)."""
+    E = len(prog.sites)
+    R = prog.record_count
+    rand_records = {ins.record for ins in prog.instrs if type(ins).__name__ in RANDOM_KINDS}
+    modes = np.full((shots, E), 2, dtype=np.int16)
+    forced = np.full((shots, R), -1, dtype=np.int8)
+    sk = {c: sketch_vectors(prog.active_schedule[c]) for c in checkpoints}
+    rows = {k: [] for k in ("meas", "det", "obs", "acc", "fx", "fz", "gamma", "k", "amps", "draws", "rec")}
+    cps = {c: {"fx": [], "fz": [], "gamma": [], "norm2": [], "ip": [], "vals": []} for c in checkpoints}
+    for s in range(shots):
+        t0 = time.time()
+        if forced_builder is None:
+            for site, tab in enumerate(prog.sites):
+                if tab.case_cum and rng.random() < min(1.0, tab.prob * boost):
+                    modes[s, site] = 3 + int(rng.integers(0, len(tab.case_cum)))
+            st = ShotState(prog, seed=seed + 17)
+            run_shot(prog, st, shot=1000 + s, forced_faults=modes[s])
+            fo = {int(r): int(st.records[r]) for r in rand_records}
+        else:
+            modes[s], fo = forced_builder(s)
+        for r, b in fo.items():
+            forced[s, r] = b
+        snap = {}
+
+        def tr(state, ins, _idx=[0]):
+            i = _idx[0]
+            _idx[0] += 1
+            if i in cps:
+                vecs, idx = sk[i]
+                snap[i] = (state.frame_x.copy(), state.frame_z.copy(), complex(state.gamma),
+                           sketch(state.active_view(), vecs, idx))
+
+        st2 = ShotState(prog, seed=seed)
+        rec = run_shot(prog, st2, shot=s, forced_faults=modes[s], forced_outcomes=fo, trace=tr)
+        rows["meas"].append(rec.measurements.astype(np.uint8))
+        rows["det"].append(rec.detectors.astype(np.uint8))
+        rows["obs"].append(rec.observables.astype(np.uint8))
+        rows["acc"].append(int(rec.accepted))
+        rows["fx"].append(st2.frame_x.copy())
+        rows["fz"].append(st2.frame_z.copy())
+        rows["gamma"].append(complex(st2.gamma))
+        rows["k"].append(st2.k)
+        rows["amps"].append(st2.active_view().copy())
+        rows["draws"].append(st2.rng.draws)
+        rows["rec"].append(st2.records.copy())
+        for c in checkpoints:
+            kc = prog.active_schedule[c]
+            if c in snap:
+                fx, fz, g, (n2, ip, vals) = snap[c]
+            else:
+                fx = fz = np.zeros(prog.n, np.uint8)
+                g, n2 = complex("nan"), float("nan")
+                ip = np.full(SKETCH_VECS, np.nan + 0j)
+                vals = np.full(min(SKETCH_ENTRIES, 1 << kc), np.nan + 0j)
+            cps[c]["fx"].append(fx)
+            cps[c]["fz"].append(fz)
+            cps[c]["gamma"].append(g)
+            cps[c]["norm2"].append(n2)
+            cps[c]["ip"].append(ip)
+            cps[c]["vals"].append(vals)
+        print(f"  shot {s}: accepted={rec.accepted} ({time.time() - t0:.1f}s)", flush=True)
+    U, D, O = len(prog.user_records), prog.num_detectors, prog.num_observables
+    out = {
+        "t_modes": modes, "t_forced": forced,
+        "t_meas": np.array(rows["meas"], np.uint8).reshape(shots, U),
+        "t_det": np.array(rows["det"], np.uint8).reshape(shots, D),
+        "t_obs": np.array(rows["obs"], np.uint8).reshape(shots, O),
+        "t_acc": np.array(rows["acc"], np.uint8),
+        "t_fx": np.array(rows["fx"], np.uint8), "t_fz": np.array(rows["fz"], np.uint8),
+        "t_gamma": np.array(rows["gamma"], np.complex128), "t_k": np.array(rows["k"], np.int32),
+        "t_draws": np.array(rows["draws"], np.int64),
+        "t_rec": np.array(rows["rec"], np.uint8).reshape(shots, R),
+        "t_seed": np.array([seed]),
+        "sk_index": np.array(checkpoints, np.int32),
+        "sk_seed": np.array([SKETCH_SEED, SKETCH_VECS, SKETCH_ENTRIES]),
+    }
+    if len(set(rows["k"])) == 1:
+        out["t_amps"] = np.array(rows["amps"], np.complex128)
+    for c in checkpoints:
+        out[f"sk{c}_idx"] = sk[c][1]
+        out[f"sk{c}_fx"] = np.array(cps[c]["fx"], np.uint8)
+        out[f"sk{c}_fz"] = np.array(cps[c]["fz"], np.uint8)
+        out[f"sk{c}_gamma"] = np.array(cps[c]["gamma"], np.complex128)
+        out[f"sk{c}_norm2"] = np.array(cps[c]["norm2"], np.float64)
+        out[f"sk{c}_ip"] = np.array(cps[c]["ip"], np.complex128)
+        out[f"sk{c}_vals"] = np.array(cps[c]["vals"], np.complex128)
+    return out
+
+
+def accepted_forced_builder(prog, text, rng, boost):
+    """Forced faults + forced outcomes under which the post-selected program ACCEPTS the shot.
+
+    Pauli-frame updates are GF(2)-affine in the recorded outcomes, so with the faults fixed the
+    detector vector is an affine function of the MeasDormantRandom coins: probe it column by
+    column on the same circuit compiled WITHOUT post-selection (same records and sites), solve
+    detectors = 0 for the coin flips, then confirm on the post-selected program (a forced
+    MeasCollapse record that became impossible, or any mismatch, draws a new fault plan)."""
+    from framesim.runtime import ShotError
+
+    prog_np = compile_circuit(text)
+    assert prog_np.record_count == prog.record_count and len(prog_np.sites) == len(prog.sites)
+    E = len(prog.sites)
+    rand_records = [ins.record for ins in prog.instrs if type(ins).__name__ in RANDOM_KINDS]
+    coins = [ins.record for ins in prog_np.instrs if type(ins).__name__ == "MeasDormantRandom"]
+    D = prog.num_detectors
+
+    def dets(modes, fo, seed):
+        st = ShotState(prog_np, seed=seed)
+        rec = run_shot(prog_np, st, shot=0, forced_faults=modes, forced_outcomes=fo)
+        return np.asarray(rec.detectors, np.uint8), st
+
+    def solve(A, b):  # one random solution of A x = b over GF(2), or None
+        A = A.copy() % 2
+        b = b.copy() % 2
+        m, n = A.shape
+        piv = []
+        r = 0
+        for c in rng.permutation(n):
+            rows = [i for i in range(r, m) if A[i, c]]
+            if not rows:
+                continue
+            A[[r, rows[0]]] = A[[rows[0], r]]
+            b[[r, rows[0]]] = b[[rows[0], r]]
+            for i in range(m):
+                if i != r and A[i, c]:
+                    A[i] ^= A[r]
+                    b[i] ^= b[r]
+            piv.append((r, c))
+            r += 1
+            if r == m:
+                break
+        if any(b[i] for i in range(r, m)):
+            return None
+        x = np.zeros(n, np.uint8)
+        free = [c for c in range(n) if c not in {c for _, c in piv}]
+        x[free] = rng.integers(0, 2, len(free))
+        for row, c in reversed(piv):
+            x[c] = (b[row] + (A[row] @ x) - A[row, c] * x[c]) % 2
+        return x
+
+    cache = {}
+
+    def build(s):
+        for attempt in range(50):
+            modes = np.full(E, 2, dtype=np.int16)
+            for site, tab in enumerate(prog.sites):
+                if tab.case_cum and rng.random() < min(1.0, tab.prob * boost):
+                    modes[site] = 3 + int(rng.integers(0, len(tab.case_cum)))
+            seed = 7000 + 101 * s + attempt
+            try:
+                d0, st = dets(modes, None, seed)
+            except ShotError:
+                continue
+            base = {int(r): int(st.records[r]) for r in rand_records}
+            if "A" not in cache:  # coin -> detector columns (fault-plan independent)
+                cols = []
+                for c in coins:
+                    fo = dict(base)
+                    fo[c] ^= 1
+                    try:
+                        dc, _ = dets(modes, fo, seed)
+                    except ShotError:
+                        dc = None
+                    cols.append(np.zeros(D, np.uint8) if dc is None else dc ^ d0)
+                cache["A"] = np.array(cols, np.uint8).T
+            x = solve(cache["A"], d0)
+            if x is None:
+                continue
+            fo = dict(base)
+            for c, f in zip(coins, x):
+                fo[c] ^= int(f)
+            try:
+                st2 = ShotState(prog, seed=seed)
+                rec = run_shot(prog, st2, shot=0, forced_faults=modes, forced_outcomes=fo)
+            except ShotError:
+                continue
+            if rec.accepted:
+                return modes, fo
+        raise RuntimeError("no accepted trajectory found")
+
+    return build
+
+
 def main(which=("configs", "random", "toys")):
     OUT.mkdir(exist_ok=True)
+    (OUT / "deep").mkdir(exist_ok=True)
     PROGS.mkdir(exist_ok=True)
     if "toys" in which:
         toys = {
@@ -465,6 +678,121 @@ def main(which=("configs", "random", "toys")):
             payload["value"] = np.array([r[4] for r in rows])
             np.savez_compressed(pdir / f"{name}.npz", **payload)
             print(f"probe/{name} n={n} k={prog.k_max} probes={len(rows)}", flush=True)
+    if "c3deep" in which:  # config 3 (k = 22): 8 trace shots, sketched checkpoints at k >= 20
+        text, ps = config_text(3)
+        prog = compile_circuit(text, postselect_detectors=ps)
+        sched = list(prog.active_schedule)
+        big = [i for i, k in enumerate(sched) if k >= 20]
+        cps = (big[0], big[len(big) // 2], big[-1])
+        t0 = time.time()
+        payload = {"program": np.frombuffer(serialize(prog, name="config3_deep").to_npz_bytes(), dtype=np.uint8)}
+        payload.update(deep_trace_golden(prog, 8, seed=11, rng=np.random.default_rng(3003), checkpoints=cps))
+        np.savez_compressed(OUT / "deep" / "config3_deep.npz", **payload)
+        print(f"deep/config3_deep cps={cps} ({time.time() - t0:.1f}s)", flush=True)
+    if "c4deep" in which:  # config 4: accepted shots (all 15 post-selections pass), checkpoints at k >= 10
+        text, ps = config_text(4)
+        prog = compile_circuit(text, postselect_detectors=ps)
+        sched = list(prog.active_schedule)
+        ks = [i for i, k in enumerate(sched) if k >= 10]
+        cps = tuple(sorted({ks[0], ks[len(ks) // 3], ks[2 * len(ks) // 3], ks[-1]}))
+        t0 = time.time()
+        rng = np.random.default_rng(4004)
+        payload = {"program": np.frombuffer(serialize(prog, name="config4_deep").to_npz_bytes(), dtype=np.uint8)}
+        payload.update(deep_trace_golden(prog, 8, seed=11, rng=rng, checkpoints=cps,
+                                         forced_builder=accepted_forced_builder(prog, text, rng, boost=20.0)))
+        np.savez_compressed(OUT / "deep" / "config4_deep.npz", **payload)
+        print(f"deep/config4_deep cps={cps} ({time.time() - t0:.1f}s)", flush=True)
+    if "renorm" in which:  # renormalize=False (runtime.py:355-366, :389-404, :481)
+        rdir = OUT / "renorm"
+        rdir.mkdir(exist_ok=True)
+        from paper_2604_27058_b200.configs import random_near_clifford
+        rng = np.random.default_rng(555)
+        cases = {
+            "two_fair": ("H 0\nM 0\nH 0\nM 0\n", True),  # |gamma|^2 ||phi||^2 = 0.25 (test_runtime.py:244-249)
+            "htm": ("H 0\nT 0\nH 0\nM 0\n", True),
+            "unopt_active": ("H 0\nT 0\nH 1\nT 1\nCX 0 1\nH 0\nM 0\nH 1\nM 1\nR_X(0.3) 2\nMX 2\n", False),
+            "noise_twice": ("H 0\nT 0\nH 0\nM 0\nDEPOLARIZE1(0.3) 0\nM 0\n", True),
+            "near_clifford": (random_near_clifford(7, 6, t_cells=7, seed=21), True),
+            "near_clifford_half": (random_near_clifford(8, 5, t_cells=8, seed=22).rsplit("M ", 1)[0]
+                                   + "M 0 2 4 6\n", True),
+        }
+        for i in range(6):
+            circ = ftest.random_circuit(rng, int(rng.integers(2, 7)), int(rng.integers(8, 24)), p_noise=0.1,
+                                        measure_rate=0.25, max_noncliff=6, reset_rate=0.05)
+            cases[f"random{i}"] = (str(circ), bool(i % 3))
+        for name, (text, opt) in cases.items():
+            t0 = time.time()
+            prog = compile_circuit(text, optimize=opt)
+            payload = {"program": np.frombuffer(serialize(prog, name=name).to_npz_bytes(), dtype=np.uint8),
+                       "circuit": np.array(text)}
+            recs = list(sample(prog, 256, seed=8, renormalize=False))
+            U, D, O = len(prog.user_records), prog.num_detectors, prog.num_observables
+            payload["f_meas"] = np.array([r.measurements for r in recs], np.uint8).reshape(256, U)
+            payload["f_det"] = np.array([r.detectors for r in recs], np.uint8).reshape(256, D)
+            payload["f_obs"] = np.array([r.observables for r in recs], np.uint8).reshape(256, O)
+            payload["f_acc"] = np.array([r.accepted for r in recs], np.uint8)
+            payload["f_seed"] = np.array([8])
+            # unnormalised states of free shots: gamma, |gamma|^2 ||phi||^2 (= branch probability)
+            rows = []
+            for shot in range(16):
+                st = ShotState(prog, seed=3, renormalize=False)
+                run_shot(prog, st, shot=shot)
+                rows.append((complex(st.gamma), st.k, st.active_view().copy(), st.records.copy(),
+                             st.frame_x.copy(), st.frame_z.copy()))
+            ks = {r[1] for r in rows}
+            payload["s_gamma"] = np.array([r[0] for r in rows], np.complex128)
+            payload["s_total"] = np.array([abs(r[0]) ** 2 * float(np.linalg.norm(r[2]) ** 2) for r in rows])
+            payload["s_rec"] = np.array([r[3] for r in rows], np.uint8).reshape(16, -1)
+            payload["s_fx"] = np.array([r[4] for r in rows], np.uint8)
+            payload["s_fz"] = np.array([r[5] for r in rows], np.uint8)
+            payload["s_seed"] = np.array([3])
+            if len(ks) == 1:
+                payload["s_amps"] = np.array([r[2] for r in rows], np.complex128)
+            np.savez_compressed(rdir / f"{name}.npz", **payload)
+            print(f"renorm/{name:20s} k_max={prog.k_max} ({time.time() - t0:.1f}s)", flush=True)
+    if "accept" in which:  # reference acceptance criterion 3 inputs (test_acceptance.py:131-152)
+        from framesim.oracle import dense_run
+        from framesim.testing import noise_sites_of, random_fault_plan
+        from framesim.circuit import flatten
+        t0 = time.time()
+        rng = np.random.default_rng(33)
+        payload = {}
+        for i in range(200):
+            n = int(rng.integers(1, 7))
+            circ = ftest.random_circuit(rng, n, int(rng.integers(4, 16)), p_noise=0.3, measure_rate=0.25,
+                                        max_noncliff=6, reset_rate=0.05, feedforward_rate=0.08)
+            plan = random_fault_plan(circ, rng)
+            flat = flatten(circ)
+            dense = dense_run(flat, fault_plan=plan, seed=9000 + i)
+            outcome_plan = {j: int(b) for j, b in enumerate(dense.records)}
+            n_sites = len(noise_sites_of(flat))
+            modes = np.full(max(n_sites, 0), 2, np.int16)
+            for site, case in (plan or {}).items():
+                modes[site] = case + 3
+            prog = compile_circuit(flat)
+            st = ShotState(prog, seed=9000 + i)
+            rec = run_shot(prog, st, shot=0, forced_faults=modes if n_sites else None, forced_outcomes=outcome_plan)
+            forced = np.full(prog.record_count, -1, np.int8)
+            for r, b in outcome_plan.items():
+                if r < prog.record_count:
+                    forced[r] = b
+            key = f"c{i:03d}_"
+            payload[key + "program"] = np.frombuffer(serialize(prog, name=f"accept{i:03d}").to_npz_bytes(), dtype=np.uint8)
+            payload[key + "modes"] = modes
+            payload[key + "forced"] = forced
+            payload[key + "seed"] = np.array([9000 + i])
+            payload[key + "meas"] = np.asarray(rec.measurements, np.uint8)
+            payload[key + "det"] = np.asarray(rec.detectors, np.uint8)
+            payload[key + "obs"] = np.asarray(rec.observables, np.uint8)
+            payload[key + "oracle_meas"] = np.asarray(dense.user_records, np.uint8)
+            payload[key + "rec"] = st.records.copy()
+            payload[key + "fx"] = st.frame_x.copy()
+            payload[key + "fz"] = st.frame_z.copy()
+            payload[key + "gamma"] = np.array([complex(st.gamma)])
+            payload[key + "amps"] = st.active_view().copy()
+        (OUT / "accept").mkdir(exist_ok=True)
+        np.savez_compressed(OUT / "accept" / "criterion3.npz", **payload)
+        print(f"accept/criterion3.npz: 200 circuits ({time.time() - t0:.1f}s)", flush=True)
     if "configs" in which:
         for i in range(5):
             text, ps = config_text(i)

@@ -29,3 +29,51 @@ def rel_err(a, b) -> float:
     b = np.asarray(b)
     den = max(float(np.linalg.norm(b)), 1e-300)
     return float(np.linalg.norm(a - b)) / den
+
+
+def _load_path(path: Path) -> dict:
+    with np.load(path, allow_pickle=False) as z:
+        d = {k: z[k] for k in z.files}
+    if "program" in d:
+        d["prog"] = Program.load(io.BytesIO(d["program"].tobytes()))
+    return d
+
+
+@lru_cache(maxsize=None)
+def load_renorm(name: str) -> dict:
+    """renormalize=False fixtures (make_golden.py "renorm")."""
+    return _load_path(GOLDEN / "renorm" / f"{name}.npz")
+
+
+def renorm_names() -> list[str]:
+    return sorted(p.stem for p in (GOLDEN / "renorm").glob("*.npz"))
+
+
+@lru_cache(maxsize=None)
+def load_deep(name: str) -> dict:
+    """Deep trace fixtures with sketched checkpoints (make_golden.py "c3deep" / "c4deep")."""
+    return _load_path(GOLDEN / "deep" / f"{name}.npz")
+
+
+@lru_cache(maxsize=None)
+def load_accept() -> list[dict]:
+    """The 200 forced-trajectory circuits of the reference's acceptance criterion 3."""
+    with np.load(GOLDEN / "accept" / "criterion3.npz", allow_pickle=False) as z:
+        raw = {k: z[k] for k in z.files}
+    out = []
+    for i in range(200):
+        key = f"c{i:03d}_"
+        d = {k[len(key):]: v for k, v in raw.items() if k.startswith(key)}
+        d["prog"] = Program.load(io.BytesIO(d["program"].tobytes()))
+        out.append(d)
+    return out
+
+
+def sketch_vectors(k: int, seed: int, nvec: int, nent: int):
+    """make_golden.sketch_vectors: fixed seeded complex vectors + sampled entry indices."""
+    vecs = []
+    for i in range(nvec):
+        g = np.random.default_rng(seed + i)
+        vecs.append(g.standard_normal(1 << k) + 1j * g.standard_normal(1 << k))
+    idx = np.sort(np.random.default_rng(seed - 1).choice(1 << k, size=min(nent, 1 << k), replace=False))
+    return vecs, idx

@@ -162,10 +162,11 @@ def test_gpu_jit_equals_interpreter(cuda, name, monkeypatch):
     n = 70_000
     _, a, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX)
     assert "affine: ready" in dp.jit_status(), dp.jit_status()
-    monkeypatch.setenv("FS_NO_AFFINE", "1")
-    _, b, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX)
-    assert dp.jit_status().startswith("ready"), dp.jit_status()
+    monkeypatch.setenv("FS_NO_AFFINE", "1")  # switches are read when a program handle is created
+    dp2 = _dev(P)
     monkeypatch.delenv("FS_NO_AFFINE")
+    _, b, _ = dp2.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX)
+    assert dp2.jit_status().startswith("ready"), dp2.jit_status()
     _, c, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX | FS_NO_JIT)
     _same(a, c)
     _same(b, c)

@@ -90,13 +90,26 @@ def test_run_shot_forced_matches_reference(cuda):
 
 
 def test_gamma_squared_is_branch_probability(cuda):
-    # reference test_runtime.py:252-256 ("H 0; M 0; H 0; M 0": two fair branches)
-    from paper_2604_27058_b200.program import Program
+    # reference test_runtime.py:252-256: "H 0; M 0; H 0; M 0" has two fair branches -> |gamma|^2 = 1/4
+    from goldens import load_renorm
 
-    P = load("toy_noise_twice")["prog"]
-    st = R.ShotState(P)
-    R.run_shot(P, st, shot=0)
-    assert abs(abs(st.gamma) ** 2 * np.linalg.norm(st.active_view()) ** 2) > 0
+    P = load_renorm("two_fair")["prog"]
+    for shot in range(8):
+        st = R.ShotState(P)
+        R.run_shot(P, st, shot=shot)
+        assert abs(abs(st.gamma) ** 2 - 0.25) < 1e-12
+
+
+def test_subnormalized_mode_tracks_branch_probability(cuda):
+    # reference test_runtime.py:244-249: renormalize=False keeps |gamma|^2 ||phi||^2 = 1/4
+    from goldens import load_renorm
+
+    P = load_renorm("two_fair")["prog"]
+    for shot in range(8):
+        st = R.ShotState(P, renormalize=False)
+        R.run_shot(P, st, shot=shot)
+        total = abs(st.gamma) ** 2 * float(np.linalg.norm(st.active_view()) ** 2)
+        assert abs(total - 0.25) < 1e-12
 
 
 def test_sample_accumulate_matches_reference_marginals(cuda):

@@ -7,9 +7,8 @@ from paper_2604_27058_b200.program import Program
 from paper_2604_27058_b200.engine import DeviceProgram
 from paper_2604_27058_b200.configs import CONFIGS
 
-def run(dp, shots, seed, aff):
-    if aff: os.environ.pop('FS_NO_AFFINE', None)
-    else: os.environ['FS_NO_AFFINE'] = '1'
+def run(dps, shots, seed, aff):
+    dp = dps[0] if aff else dps[1]  # FS_NO_AFFINE is read when a program handle is created
     out = dp.alloc_device_outputs(shots)
     dp.sample_device(shots, out, seed=seed); torch.cuda.synchronize()
     ms = []
@@ -21,10 +20,14 @@ def run(dp, shots, seed, aff):
 
 for cfg in [int(c) for c in sys.argv[1:]] or [1]:
     P = Program.load(f'paper_2604_27058_b200/programs/c{cfg}.npz')
+    os.environ.pop('FS_NO_AFFINE', None)
     dp = DeviceProgram(P)
+    os.environ['FS_NO_AFFINE'] = '1'
+    dp2 = DeviceProgram(P)
+    os.environ.pop('FS_NO_AFFINE', None)
     for shots in (1000, 100003, CONFIGS[cfg]['shots']):
-        a, ta = run(dp, shots, 7, True)
-        b, tb = run(dp, shots, 7, False)
+        a, ta = run((dp, dp2), shots, 7, True)
+        b, tb = run((dp, dp2), shots, 7, False)
         same = all(torch.equal(a[k], b[k]) for k in a if k != 'status' and a[k] is not None)
         print(json.dumps({"cfg": cfg, "shots": shots, "equal": same, "aff_ms": ta, "old_ms": tb,
                           "aff_shots_per_s": shots / ta * 1e3}), flush=True)
