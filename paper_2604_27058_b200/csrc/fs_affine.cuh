@@ -483,6 +483,17 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     fprintf(stderr, "\n");
     size_t el_total = 0;
     for (auto& v : el_rows) el_total += v.size();
+    {
+      std::vector<int> hit(nrows, 0), npar(kAffMaxParents + 1, 0);
+      for (auto& v : el_rows)
+        for (int r : v) hit[r] = 1;
+      int nhit = 0, nhit_det = 0;
+      for (int r = 0; r < nrows; r++) { nhit += hit[r]; if (r < D4) nhit_det += hit[r]; }
+      for (int r = 0; r < nrows; r++) npar[parents[r].size()]++;
+      fprintf(stderr, "aff: rows with fault residual %d (detector rows %d of %d); parents histogram:", nhit, nhit_det, D);
+      for (int k = 0; k <= kAffMaxParents; k++) fprintf(stderr, " %d:%d", k, npar[k]);
+      fprintf(stderr, "\n");
+    }
     fprintf(stderr,
             "aff: rows %d coins %d elements %zu element-rows %zu cases %d case-rows %zu classes %d tables %zu B "
             "(%s) warps %d\n",
@@ -525,6 +536,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   }
   std::ostringstream o;
   if (const char* dg = getenv("FS_AFF_DIAG")) o << "#define FS_AFF_DIAG " << atoi(dg) << "\n";  // profiling only
+  if (getenv("FS_AFF_UNBALANCED")) o << "#define FS_AFF_ROWS aff_rows\n";  // A/B: every lane loops to the warp's max
   o << "#include \"fs_jit_kernels.cuh\"\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << K.threads << ", 1) fs_aff_frame(fs::DevProg P, fs::RunArgs A, "
        "const uint32_t* __restrict__ tbl) {\n";

@@ -181,6 +181,45 @@ __device__ __forceinline__ void aff_rows(const AffTabs<OFF16>& T, uint32_t* B, u
   }
 }
 
+// Load-balanced form of aff_rows: the warp's fault rows (sum of n over lanes, ~3.7 per fault) are
+// spread over the lanes 32 at a time instead of every lane looping to the warp's largest n.  Entry
+// t of the concatenated lists belongs to the last lane whose exclusive start is <= t (a lane with
+// n = 0 never is: the next lane has the same start); the owner is found by a 5-step binary search
+// over the lanes' starts (shuffles).  Same XORs as aff_rows, in another order (XOR commutes).
+template <bool OFF16>
+__device__ __forceinline__ void aff_rows_bal(const AffTabs<OFF16>& T, uint32_t* B, uint32_t wi, uint32_t j0, uint32_t n,
+                                             uint32_t bit) {
+#if defined(FS_AFF_DIAG) && FS_AFF_DIAG == 1
+  return;  // diagnostic: no row application
+#endif
+  const int lane = threadIdx.x & 31;
+  uint32_t e = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, e, o);
+    if (lane >= o) e += t;
+  }
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, e, 31);
+  const uint32_t s = e - n;                  // exclusive start of this lane's rows
+  const uint32_t base = j0 - s;              // row-list index of entry t = base(owner) + t
+  for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+    const uint32_t t = t0 + (uint32_t)lane;
+    int l = 0;
+#pragma unroll
+    for (int step = 16; step; step >>= 1) {
+      const uint32_t sv = __shfl_sync(0xFFFFFFFFu, s, l + step);
+      if (sv <= t) l += step;
+    }
+    const uint32_t b = __shfl_sync(0xFFFFFFFFu, base, l);
+    const uint32_t bv = __shfl_sync(0xFFFFFFFFu, bit, l);
+    if (t < total) atomicXor(B + ((uint32_t)T.crows[b + t] ^ wi), bv);
+  }
+}
+
+#ifndef FS_AFF_ROWS
+#define FS_AFF_ROWS aff_rows_bal
+#endif
+
 // Faults of one 32-shot word, warp-cooperatively: lane j evaluates step st + j of the word's
 // noise stream (the WordFaultGen process, step by step the same draws and decisions), the cell
 // positions of a run are an inclusive warp scan of the per-step advances 1 + floor(ln(U) * lp), and
@@ -252,7 +291,7 @@ __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<
         j0 = T.off(cs);
         n = T.off(cs + 1) - j0;
       }
-      aff_rows<OFF16>(T, B, wi, j0, n, 1u << fl);
+      FS_AFF_ROWS<OFF16>(T, B, wi, j0, n, 1u << fl);
     }
     st += 32;
   }
@@ -296,7 +335,7 @@ __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, ui
         n = T.off(cs + 1) - j0;
       }
     }
-    aff_rows<OFF16>(T, B, wi, j0, n, 1u << (pos & 31));
+    FS_AFF_ROWS<OFF16>(T, B, wi, j0, n, 1u << (pos & 31));
     if (endm) return;
     c = __shfl_sync(0xFFFFFFFFu, pos, 31);
     st += 32;

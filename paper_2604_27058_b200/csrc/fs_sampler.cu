@@ -540,6 +540,23 @@ extern "C" int fs_debug_seg_counts(fs_prog* p, uint32_t* out, int cap) {
   return n;
 }
 
+// the same generator from a descriptor (no device needed: source inspection / offline SASS checks)
+extern "C" int fs_debug_gjit_source_desc(const fs_prog_desc* d, char* buf, size_t len) {
+  if (!d) return -1;
+  auto vec = [](const auto* ptr, size_t n) { return std::vector<std::remove_cv_t<std::remove_pointer_t<decltype(ptr)>>>(ptr, ptr + n); };
+  std::vector<int32_t> ins = vec(d->instrs, (size_t)d->num_instrs * FS_INS_WORDS);
+  fsjit::GeneralKernelSource K = fsjit::gen_general_kernel(
+      *d, ins, vec(d->gates, d->num_gates), vec(d->paulis, d->num_paulis), vec(d->reclists, d->num_reclists),
+      vec(d->record_out, d->record_count), vec(d->bit_slot, d->record_count + d->num_detectors),
+      vec(d->case_pauli_off, d->num_cases + 1), vec(d->site_case_off, d->num_sites + 1), vec(d->fparams, d->num_fparams));
+  if (buf && len) {
+    size_t m = std::min(len - 1, K.src.size());
+    std::memcpy(buf, K.src.data(), m);
+    buf[m] = 0;
+  }
+  return (int)K.src.size();
+}
+
 extern "C" int fs_debug_gjit_source(fs_prog* p, char* buf, size_t len) {
   if (!p) return -1;
   fsjit::GeneralKernelSource K = fsjit::gen_general_kernel(p->desc, p->h_instrs, p->h_gates, p->h_paulis,

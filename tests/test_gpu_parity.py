@@ -174,7 +174,8 @@ def test_gpu_jit_equals_interpreter(cuda, name, monkeypatch):
 
 @pytest.mark.parametrize("name", ["config1", "aff_mixed", "aff_rep_psel", "toy_certain", "rand06", "aff_surface_d7"])
 @pytest.mark.parametrize("env", [{"FS_AFF_GLOBAL_TABLES": "1"}, {"FS_AFF_PAIRS": "1"}, {"FS_AFF_NONUNIFORM": "1"},
-                                 {"FS_AFF_NO_DIFF": "1"}, {"FS_AFF_PARENTS": "1"}, {"FS_AFF_ANY_PARENTS": "1"}])
+                                 {"FS_AFF_NO_DIFF": "1"}, {"FS_AFF_PARENTS": "1"}, {"FS_AFF_ANY_PARENTS": "1"},
+                                 {"FS_AFF_UNBALANCED": "1"}])
 def test_gpu_affine_variants_match_oracle(cuda, name, env, monkeypatch):
     """Affine frame kernel variants (fault tables in global memory, one warp pair per block, the
     exact-bisect case pick, no / single-parent row differencing) == oracle, bit for bit; odd shot
