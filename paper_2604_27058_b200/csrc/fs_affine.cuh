@@ -536,7 +536,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   }
   std::ostringstream o;
   if (const char* dg = getenv("FS_AFF_DIAG")) o << "#define FS_AFF_DIAG " << atoi(dg) << "\n";  // profiling only
-  if (getenv("FS_AFF_UNBALANCED")) o << "#define FS_AFF_ROWS aff_rows\n";  // A/B: every lane loops to the warp's max
+  if (getenv("FS_AFF_BALANCED")) o << "#define FS_AFF_ROWS aff_rows_bal\n";  // A/B: load-balanced row loop
   o << "#include \"fs_jit_kernels.cuh\"\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << K.threads << ", 1) fs_aff_frame(fs::DevProg P, fs::RunArgs A, "
        "const uint32_t* __restrict__ tbl) {\n";

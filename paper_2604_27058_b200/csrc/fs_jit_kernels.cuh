@@ -217,7 +217,7 @@ __device__ __forceinline__ void aff_rows_bal(const AffTabs<OFF16>& T, uint32_t* 
 }
 
 #ifndef FS_AFF_ROWS
-#define FS_AFF_ROWS aff_rows_bal
+#define FS_AFF_ROWS aff_rows  // measured: the balanced form's shuffles cost more MIO than they save
 #endif
 
 // Faults of one 32-shot word, warp-cooperatively: lane j evaluates step st + j of the word's

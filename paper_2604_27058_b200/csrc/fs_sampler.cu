@@ -113,7 +113,7 @@ constexpr int kChunks = 4;   // max word chunks of the fault-list | frame-kernel
 // testing / experiment switches, read once at fs_program_create (never on a launch path)
 struct EnvSwitches {
   bool no_affine = false;      // FS_NO_AFFINE: frame-only programs use the fault-list frame kernel
-  bool aff_v1 = false;         // FS_AFF_V1: the warp-pair affine kernel instead of the lane-per-word one
+  bool aff2 = false;           // FS_AFF2: the lane-per-word affine kernel (measured slower; kept for A/B)
   bool block_no_jit = false;   // FS_BLOCK_NO_JIT: segmented engine interprets every segment
   bool block_jit_warp = false; // FS_BLOCK_JIT_WARP: also specialise warp-per-shot segments
   int block_k = 0;             // FS_BLOCK_K: segment k at which a shot gets a warp / CTA (0 = default)
@@ -124,7 +124,7 @@ struct EnvSwitches {
   uint64_t stratum_chunk = 0;  // FS_STRATUM_CHUNK: stratified-sampling chunk (tests)
   void read() {
     no_affine = getenv("FS_NO_AFFINE") != nullptr;
-    aff_v1 = getenv("FS_AFF_V1") != nullptr;
+    aff2 = getenv("FS_AFF2") != nullptr;
     block_no_jit = getenv("FS_BLOCK_NO_JIT") != nullptr;
     block_jit_warp = getenv("FS_BLOCK_JIT_WARP") != nullptr;
     if (const char* e = getenv("FS_BLOCK_K")) block_k = std::max(1, atoi(e));
@@ -801,7 +801,9 @@ int ensure_aff(fs_prog* p) {
   return FS_OK;
 }
 
-// lane-per-word affine frame kernel (fs_affine2.cuh), the default for frame-only programs
+// lane-per-word affine frame kernel (fs_affine2.cuh), FS_AFF2 only: at one warp per 32 words its
+// column buffers hold 8x the shots of a warp pair's, so 9 warps fit an SM instead of 28 and the
+// latency-bound noise chains run at IPC 1.3 (0.42 vs 0.21 ms per 1e7 shots, profiles/r2_c1_aff2_ncu.md)
 int ensure_aff2(fs_prog* p) {
   if (p->aff2_state == 1) return FS_OK;
   if (p->aff2_state == -1) return FS_ERR_ARG;
@@ -2135,7 +2137,7 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
   const bool trace_in = tin && (tin->fault_modes || tin->forced);
   const bool frame_free = !general && !trace_in && !(tout && tout->frame_x) && !(flags & FS_NO_JIT) &&
                           a.stop == dp.num_instrs && !p->env.no_affine;
-  if (frame_free && !p->env.aff_v1 && ensure_aff2(p) == FS_OK) return launch_aff2(p, a, stream);
+  if (frame_free && p->env.aff2 && ensure_aff2(p) == FS_OK) return launch_aff2(p, a, stream);
   if (frame_free && ensure_aff(p) == FS_OK) return launch_aff(p, a, stream);
   if (!general && !trace_in && !(tout && tout->frame_x) && !(flags & FS_NO_JIT) && a.stop == dp.num_instrs) {
     int rc = ensure_jit(p);
