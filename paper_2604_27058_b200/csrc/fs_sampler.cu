@@ -120,6 +120,7 @@ struct EnvSwitches {
   bool hbm_fused = false;      // FS_HBM_FUSED: fused tile passes also under FS_FORCE_HBM
   bool hbm_unfused = false;    // FS_HBM_UNFUSED: per-instruction large-k kernels only
   bool hbm_no_jit = false;     // FS_HBM_NO_JIT: pass microcode interpreter instead of fs_pass_<i>
+  bool pass_no_tma = false;    // FS_PASS_NO_TMA: fs_pass_<i> stage tiles with cp.async instead of TMA bulk copies
   int jit_chunks = 1;          // FS_JIT_CHUNKS: fault-list | frame-kernel pipeline depth
   uint64_t stratum_chunk = 0;  // FS_STRATUM_CHUNK: stratified-sampling chunk (tests)
   void read() {
@@ -131,6 +132,7 @@ struct EnvSwitches {
     hbm_fused = getenv("FS_HBM_FUSED") != nullptr;
     hbm_unfused = getenv("FS_HBM_UNFUSED") != nullptr;
     hbm_no_jit = getenv("FS_HBM_NO_JIT") != nullptr;
+    pass_no_tma = getenv("FS_PASS_NO_TMA") != nullptr;
     if (const char* e = getenv("FS_JIT_CHUNKS")) jit_chunks = std::max(1, std::min(kChunks, atoi(e)));
     if (const char* e = getenv("FS_STRATUM_CHUNK")) stratum_chunk = std::max<uint64_t>(32, (uint64_t)atoll(e) / 32 * 32);
   }
@@ -1703,7 +1705,7 @@ int plan_hbm(fs_prog* p, int stop, bool fused, const std::vector<int>& cuts) {
 // Each fused pass's microcode compiled to straight-line code (NVRTC): masks, register bits,
 // exchange partners and address deposits become constants; the interpreter
 // (fs_hbm_fused.cuh hbm_fused_pass_kernel) remains the fallback (FS_HBM_NO_JIT).
-std::string gen_pass_source(const HbmPlan& PL) {
+std::string gen_pass_source(const HbmPlan& PL, bool tma_ok) {
   std::ostringstream o;
   o << "#include \"fs_hbm_fused.cuh\"\nusing namespace fs;\n";
   auto hexu = [](uint32_t x) {
@@ -1713,6 +1715,8 @@ std::string gen_pass_source(const HbmPlan& PL) {
   };
   for (size_t pi = 0; pi < PL.passes.size(); pi++) {
     const fs::PassDesc& D = PL.passes[pi];
+    // TMA staging when the tile's three lowest bits are physical axes 0..2 (128-byte runs)
+    const bool tma = tma_ok && D.T[0] == 0 && D.T[1] == 1 && D.T[2] == 2;
     // smem: exchange half-buffer (32 KiB) | next-tile staging (64 KiB) | resolved constants
     o << "extern \"C\" __global__ void __launch_bounds__(256, 2) fs_pass_" << pi
       << "(HbmState H, const PassConst* __restrict__ consts, uint32_t W) {\n"
@@ -1741,10 +1745,23 @@ std::string gen_pass_source(const HbmPlan& PL) {
       return d.str();
     };
     auto prefetch = [&](const char* basevar) {  // this thread's 16 elements of a tile -> its Sg slots
+      if (tma) {  // segments tid and tid + 256 (128 B each: local index s * 8 + [0, 8))
+        o << "      if (tid == 0) mbar_expect_tx(&bar, " << (16u << fs::kTileBits) << "u);\n"
+          << "      fence_proxy_async_smem();\n"
+          << "      bulk_g2s(Sg + tid * 8, A + (" << basevar << " | seg_lo), 128u, &bar);\n"
+          << "      bulk_g2s(Sg + (tid + 256) * 8, A + (" << basevar << " | seg_lo | " << hexu(1u << D.T[11]) << "), 128u, &bar);\n";
+        return;
+      }
       for (int j = 0; j < fs::kTileElems; j++)
         o << "      cp_async16(Sg + tid + " << 256 * j << ", A + (" << basevar << " | dep_lo | " << hexu(D.dep_hi[j]) << "));\n";
       o << "      cp_async_commit();\n";
     };
+    if (tma) {  // segment s = tid (+256): its local bits 3..11 = s bits 0..8 on axes T[3..11]
+      o << ";\n  const uint32_t seg_lo = 0u";
+      for (int i = 0; i < 8; i++) o << " | (((tid >> " << i << ") & 1u) << " << (int)D.T[3 + i] << ")";
+      o << ";\n  __shared__ uint64_t bar;\n  uint32_t phase = 0u;\n"
+        << "  if (tid == 0) { mbar_init(&bar, 1u); asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\"); }\n";
+    }
     o << ";\n  __syncthreads();\n"
       << "  double2* __restrict__ A = H.amps + (size_t)shot * H.cap;\n"
       << "  double2 v[16];\n"
@@ -1754,9 +1771,11 @@ std::string gen_pass_source(const HbmPlan& PL) {
     o << "  }\n"
       << "  for (uint32_t ti = blockIdx.x; ti < NT; ti += gridDim.x) {\n"
       << "    const uint64_t base = " << deposit("ti") << ";\n"
-      << "    const uint32_t X0 = tid | (ti << " << fs::kTileBits << ");\n"
-      << "    cp_async_wait_all();\n";
+      << "    const uint32_t X0 = tid | (ti << " << fs::kTileBits << ");\n";
+    if (tma) o << "    mbar_wait(&bar, phase);\n    phase ^= 1u;\n";
+    else o << "    cp_async_wait_all();\n";
     for (int j = 0; j < fs::kTileElems; j++) o << "    v[" << j << "] = Sg[tid + " << 256 * j << "];\n";
+    if (tma) o << "    __syncthreads();  // every read of Sg before the next tile's bulk copies overwrite it\n";
     o << "    if (ti + gridDim.x < NT) {\n      const uint32_t tn = ti + gridDim.x;\n      const uint64_t bn = " << deposit("tn") << ";\n";
     prefetch("bn");
     o << "    }\n";
@@ -1842,7 +1861,7 @@ int ensure_pass_jit(fs_prog* p) {
   if (p->pass_jit == -1) return FS_ERR_ARG;
   p->pass_jit = -1;
   const HbmPlan& PL = p->hplan;
-  const std::string src = gen_pass_source(PL);
+  const std::string src = gen_pass_source(PL, !p->env.pass_no_tma);
   // one module per distinct source per process (tests and benches create many programs)
   // (modules belong to a context: the key is (current context, source))
   static std::mutex mu;
