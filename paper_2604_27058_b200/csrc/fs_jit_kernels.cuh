@@ -39,6 +39,29 @@ __device__ __noinline__ void gjit_noise_fallback(const DevProg& P, uint32_t* Fs,
   }
 }
 
+// The same regeneration for the ballot form of the general kernel's NoiseBlocks: every lane runs
+// the word's generator (same state in all lanes) and keeps the faults of ITS shot as a mask over
+// the block's touched slots (tidx: touched-slot index per Pauli entry).
+__device__ __noinline__ uint64_t gjit_noise_mask(const DevProg& P, const uint16_t* __restrict__ tidx, WordFaultGen& gen,
+                                                 int& psite, int& plane, int& pcase, int hi, int lane) {
+  uint64_t fm = 0ull;
+  for (;;) {
+    if (psite < 0) {
+      int st_, ln_, cs_;
+      const int r_ = gen.step(P, st_, ln_, cs_);
+      if (r_ == 2) { psite = 0x7FFFFFFF; break; }
+      if (r_ == 0) continue;
+      psite = st_; plane = ln_; pcase = cs_;
+    }
+    if (psite >= hi) break;
+    if (plane == lane)
+      for (int j = __ldg(P.case_pauli_off + pcase); j < __ldg(P.case_pauli_off + pcase + 1); j++)
+        fm ^= 1ull << __ldg(tidx + j);
+    psite = -1;
+  }
+  return fm;
+}
+
 // Noise for the specialised frame kernel.  fault_list_kernel generates each 32-shot word's
 // faults (WordFaultGen: the engine stream; lane = word) and writes one entry per fault,
 // ent[i][W] = pauli_off << 10 | pauli_cnt << 5 | shot_bit, plus per-NoiseBlock counts

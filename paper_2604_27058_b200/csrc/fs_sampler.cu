@@ -120,7 +120,7 @@ struct EnvSwitches {
   bool hbm_fused = false;      // FS_HBM_FUSED: fused tile passes also under FS_FORCE_HBM
   bool hbm_unfused = false;    // FS_HBM_UNFUSED: per-instruction large-k kernels only
   bool hbm_no_jit = false;     // FS_HBM_NO_JIT: pass microcode interpreter instead of fs_pass_<i>
-  bool pass_no_tma = false;    // FS_PASS_NO_TMA: fs_pass_<i> stage tiles with cp.async instead of TMA bulk copies
+  bool pass_tma = false;       // FS_PASS_TMA: fs_pass_<i> stage tiles with TMA bulk copies instead of cp.async
   int jit_chunks = 1;          // FS_JIT_CHUNKS: fault-list | frame-kernel pipeline depth
   uint64_t stratum_chunk = 0;  // FS_STRATUM_CHUNK: stratified-sampling chunk (tests)
   void read() {
@@ -132,7 +132,7 @@ struct EnvSwitches {
     hbm_fused = getenv("FS_HBM_FUSED") != nullptr;
     hbm_unfused = getenv("FS_HBM_UNFUSED") != nullptr;
     hbm_no_jit = getenv("FS_HBM_NO_JIT") != nullptr;
-    pass_no_tma = getenv("FS_PASS_NO_TMA") != nullptr;
+    pass_tma = getenv("FS_PASS_TMA") != nullptr;
     if (const char* e = getenv("FS_JIT_CHUNKS")) jit_chunks = std::max(1, std::min(kChunks, atoi(e)));
     if (const char* e = getenv("FS_STRATUM_CHUNK")) stratum_chunk = std::max<uint64_t>(32, (uint64_t)atoll(e) / 32 * 32);
   }
@@ -1715,8 +1715,12 @@ std::string gen_pass_source(const HbmPlan& PL, bool tma_ok) {
   };
   for (size_t pi = 0; pi < PL.passes.size(); pi++) {
     const fs::PassDesc& D = PL.passes[pi];
-    // TMA staging when the tile's three lowest bits are physical axes 0..2 (128-byte runs)
-    const bool tma = tma_ok && D.T[0] == 0 && D.T[1] == 1 && D.T[2] == 2;
+    // TMA staging when the tile's lowest L >= 3 bits are physical axes 0..L-1: the tile is
+    // 2^(12-L) contiguous runs of 2^L amplitudes (16 << L bytes), one bulk copy each
+    int L = 0;
+    while (L < 8 && D.T[L] == L) L++;
+    const bool tma = tma_ok && L >= 3;
+    const int nseg = 1 << (fs::kTileBits - L), segb = 16 << L;
     // smem: exchange half-buffer (32 KiB) | next-tile staging (64 KiB) | resolved constants
     o << "extern \"C\" __global__ void __launch_bounds__(256, 2) fs_pass_" << pi
       << "(HbmState H, const PassConst* __restrict__ consts, uint32_t W) {\n"
@@ -1745,20 +1749,28 @@ std::string gen_pass_source(const HbmPlan& PL, bool tma_ok) {
       return d.str();
     };
     auto prefetch = [&](const char* basevar) {  // this thread's 16 elements of a tile -> its Sg slots
-      if (tma) {  // segments tid and tid + 256 (128 B each: local index s * 8 + [0, 8))
+      if (tma) {  // segment s (local index s << L + [0, 2^L)): threads tid < nseg, s = tid + 256 r
         o << "      if (tid == 0) mbar_expect_tx(&bar, " << (16u << fs::kTileBits) << "u);\n"
-          << "      fence_proxy_async_smem();\n"
-          << "      bulk_g2s(Sg + tid * 8, A + (" << basevar << " | seg_lo), 128u, &bar);\n"
-          << "      bulk_g2s(Sg + (tid + 256) * 8, A + (" << basevar << " | seg_lo | " << hexu(1u << D.T[11]) << "), 128u, &bar);\n";
+          << "      fence_proxy_async_smem();\n";
+        if (nseg < 256) o << "      if (tid < " << nseg << "u) ";
+        else o << "      ";
+        o << "bulk_g2s(Sg + (tid << " << L << "), A + (" << basevar << " | seg_lo), " << segb << "u, &bar);\n";
+        for (int r = 1; r < nseg / 256; r++) {  // segments tid + 256 r: local bits L + 8.. from r
+          uint32_t hi = 0;
+          for (int b = 0; L + 8 + b < fs::kTileBits; b++)
+            if ((r >> b) & 1) hi |= 1u << D.T[L + 8 + b];
+          o << "      bulk_g2s(Sg + ((tid + " << 256 * r << "u) << " << L << "), A + (" << basevar << " | seg_lo | " << hexu(hi)
+            << "), " << segb << "u, &bar);\n";
+        }
         return;
       }
       for (int j = 0; j < fs::kTileElems; j++)
         o << "      cp_async16(Sg + tid + " << 256 * j << ", A + (" << basevar << " | dep_lo | " << hexu(D.dep_hi[j]) << "));\n";
       o << "      cp_async_commit();\n";
     };
-    if (tma) {  // segment s = tid (+256): its local bits 3..11 = s bits 0..8 on axes T[3..11]
+    if (tma) {  // segment s: local bits L.. = s bits on axes T[L..]; tid supplies s bits 0..7
       o << ";\n  const uint32_t seg_lo = 0u";
-      for (int i = 0; i < 8; i++) o << " | (((tid >> " << i << ") & 1u) << " << (int)D.T[3 + i] << ")";
+      for (int i = 0; i < 8 && L + i < fs::kTileBits; i++) o << " | (((tid >> " << i << ") & 1u) << " << (int)D.T[L + i] << ")";
       o << ";\n  __shared__ uint64_t bar;\n  uint32_t phase = 0u;\n"
         << "  if (tid == 0) { mbar_init(&bar, 1u); asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\"); }\n";
     }
@@ -1861,7 +1873,7 @@ int ensure_pass_jit(fs_prog* p) {
   if (p->pass_jit == -1) return FS_ERR_ARG;
   p->pass_jit = -1;
   const HbmPlan& PL = p->hplan;
-  const std::string src = gen_pass_source(PL, !p->env.pass_no_tma);
+  const std::string src = gen_pass_source(PL, p->env.pass_tma);
   // one module per distinct source per process (tests and benches create many programs)
   // (modules belong to a context: the key is (current context, source))
   static std::mutex mu;
