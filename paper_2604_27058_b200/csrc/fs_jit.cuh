@@ -595,12 +595,14 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
             }
         std::sort(touched.begin(), touched.end());
         touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
-        // ballot form (<= 64 touched slots): every lane scans the block's fault entries of its
+        // ballot form (<= 64 touched slots, FS_GJIT_NOISE_BALLOT): every lane scans the block's fault entries of its
         // word (broadcast loads), folds the entries of ITS shot into a mask over the touched slots
         // (per-entry slot index table after pslot), and each touched slot word takes the ballot of
         // that bit -- no shared-memory staging, no lane-0 serial loop.  Overflowed fault lists
         // (rare) keep the lane-0 path through shared memory.
-        const bool ballot = touched.size() <= 64 && !getenv("FS_GJIT_NOISE_SMEM");
+        // measured on config 2: 2.92 vs 2.31 ms per 1e7 shots (the ballots add ~4 instructions per
+        // touched slot to a kernel bound by instruction issue) -> opt-in FS_GJIT_NOISE_BALLOT
+        const bool ballot = touched.size() <= 64 && getenv("FS_GJIT_NOISE_BALLOT");
         if (ballot)
           for (int s2 = I[1]; s2 < I[2]; s2++)
             for (int c = site_case_off[s2]; c < site_case_off[s2 + 1]; c++)

@@ -203,8 +203,12 @@ def test_gpu_affine_variants_match_oracle(cuda, name, env, monkeypatch):
 
 @pytest.mark.parametrize("name", [c for c in CASES if 0 < load(c)["prog"].k_max <= 7 and not load(c)["prog"].has_postselect
                                   and not (set((load(c)["prog"].instrs[:, 0] & 0xFF).tolist()) & {7, 9})])
-def test_gpu_general_jit_equals_interpreter(cuda, name):
-    """Program-specialised general kernel (NVRTC) == general interpreter, bit for bit."""
+@pytest.mark.parametrize("env", [{}, {"FS_GJIT_NOISE_BALLOT": "1"}])
+def test_gpu_general_jit_equals_interpreter(cuda, name, env, monkeypatch):
+    """Program-specialised general kernel (NVRTC; NoiseBlocks through shared memory or by ballots)
+    == general interpreter, bit for bit."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     P = load(name)["prog"]
     dp = _dev(P)
     n = 20_000
