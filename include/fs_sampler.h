@@ -172,8 +172,10 @@ void fs_program_destroy(fs_prog* prog);
    2 = large-k engine (active arrays in HBM) */
 int fs_program_engine(const fs_prog* prog, uint32_t flags);
 
-/* shot0 must be a multiple of 32 (shot words are absolute).  Returns FS_OK, or
- * FS_ERR_SHOT_* when some shot raised (see out->error), or a negative error. */
+/* shot0 must be a multiple of 32: the Philox stream keys coins and noise by the absolute 32-shot
+ * word (shot / 32) and Born draws by the absolute shot, so any split of a run into calls at
+ * multiples of 32 reproduces it exactly (FS_RNG_SPLITMIX is keyed per shot, like framesim).
+ * Returns FS_OK, or FS_ERR_SHOT_* when some shot raised (see out->error), or a negative error. */
 int fs_sample(fs_prog* prog, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t flags,
               const fs_trace_in* tin, const fs_sample_out* out, const fs_trace_out* tout,
               void* stream);

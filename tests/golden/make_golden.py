@@ -793,6 +793,44 @@ def main(which=("configs", "random", "toys")):
         (OUT / "accept").mkdir(exist_ok=True)
         np.savez_compressed(OUT / "accept" / "criterion3.npz", **payload)
         print(f"accept/criterion3.npz: 200 circuits ({time.time() - t0:.1f}s)", flush=True)
+    if "frameref" in which:  # the reference's independent Pauli-frame sampler (oracle.py:407-516)
+        from framesim.oracle import pauli_frame_reference_sample
+        from framesim.circuit import flatten, parse_circuit
+        from paper_2604_27058_b200.configs import rotated_surface_code
+        fdir = OUT / "frameref"
+        fdir.mkdir(exist_ok=True)
+        cases = {
+            "config1": (config_text(1)[0], 200_000),                       # config 1 check
+            "surface_d5_p5e-3": (rotated_surface_code(5, 5, 5e-3), 200_000),  # boosted rates
+            "repetition_d3_r5": (str(ftest.repetition_code_circuit(3, 5, 1e-3)), 1_000_000),  # criterion 4
+        }
+        for name, (text, shots) in cases.items():
+            t0 = time.time()
+            circ = flatten(parse_circuit(text))
+            prog = compile_circuit(circ)
+            det = np.zeros(prog.num_detectors, np.int64)
+            obs = np.zeros(prog.num_observables, np.int64)
+            chunk = 50_000
+            for c0 in range(0, shots, chunk):
+                _, d, o = pauli_frame_reference_sample(circ, min(chunk, shots - c0), seed=90404 + c0)
+                det += np.asarray(d, np.int64).reshape(-1, prog.num_detectors).sum(0)
+                if prog.num_observables:
+                    obs += np.asarray(o, np.int64).reshape(-1, prog.num_observables).sum(0)
+            np.savez_compressed(fdir / f"{name}.npz",
+                                program=np.frombuffer(serialize(prog, name=name).to_npz_bytes(), dtype=np.uint8),
+                                det_counts=det, obs_counts=obs, shots=np.array([shots]))
+            print(f"frameref/{name}: {shots} frame-sampler shots ({time.time() - t0:.1f}s)", flush=True)
+    if "mirrors50" in which:  # acceptance criterion 2 (test_acceptance.py:110-128): 50 exact mirrors
+        rng = np.random.default_rng(2024)
+        payload = {}
+        for i in range(50):
+            n = int(rng.integers(1, 9))
+            circ = ftest.random_mirror_circuit(rng, n, int(rng.integers(1, 13)))
+            prog = compile_circuit(circ)
+            payload[f"m{i:02d}"] = np.frombuffer(serialize(prog, name=f"mirror{i:02d}").to_npz_bytes(), dtype=np.uint8)
+        (OUT / "accept").mkdir(exist_ok=True)
+        np.savez_compressed(OUT / "accept" / "criterion2_mirrors.npz", **payload)
+        print("accept/criterion2_mirrors.npz: 50 programs", flush=True)
     if "configs" in which:
         for i in range(5):
             text, ps = config_text(i)

@@ -77,3 +77,31 @@ def sketch_vectors(k: int, seed: int, nvec: int, nent: int):
         vecs.append(g.standard_normal(1 << k) + 1j * g.standard_normal(1 << k))
     idx = np.sort(np.random.default_rng(seed - 1).choice(1 << k, size=min(nent, 1 << k), replace=False))
     return vecs, idx
+
+
+def frameref_names() -> list[str]:
+    return sorted(p.stem for p in (GOLDEN / "frameref").glob("*.npz"))
+
+
+@lru_cache(maxsize=None)
+def load_frameref(name: str) -> dict:
+    """Detector / observable counts of the reference's independent Pauli-frame sampler
+    (framesim/oracle.py:407-516) for a Clifford program (make_golden.py "frameref")."""
+    return _load_path(GOLDEN / "frameref" / f"{name}.npz")
+
+
+@lru_cache(maxsize=None)
+def load_mirrors50() -> list:
+    """The 50 exact mirror programs of the reference's acceptance criterion 2."""
+    with np.load(GOLDEN / "accept" / "criterion2_mirrors.npz", allow_pickle=False) as z:
+        return [Program.load(io.BytesIO(z[k].tobytes())) for k in sorted(z.files)]
+
+
+def max_two_sample_z(a, b, na: int, nb: int) -> float:
+    """Largest two-sample binomial |z| (pooled sigma, each side's own n) over paired counts
+    (test_acceptance.py:163-169)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    p = (a + b) / (na + nb)
+    sig = np.sqrt(np.maximum(p * (1 - p), 1e-12) * (1.0 / na + 1.0 / nb))
+    return float(np.max(np.abs(a / na - b / nb) / sig)) if a.size else 0.0

@@ -11,7 +11,9 @@
 * renormalize=False (free sampling + unnormalised states), every engine;
 * ShotState.records holds hidden records too (trace outputs), vs reference and oracle;
 * NaN injected into an Expand phase raises ShotError("NaN") on every engine (reference
-  test_runtime.py:274-281), also through sample_accumulate.
+  test_runtime.py:274-281), also through sample_accumulate;
+* detector / observable rates vs the reference's independent Pauli-frame sampler (config 1, SURVEY
+  §8(d); acceptance criterion 4) and the 50 exact mirrors of acceptance criterion 2.
 """
 from __future__ import annotations
 
@@ -21,7 +23,8 @@ import numpy as np
 import pytest
 
 import oracle
-from goldens import case_names, load, load_accept, load_deep, load_renorm, rel_err, renorm_names
+from goldens import (case_names, frameref_names, load, load_accept, load_deep, load_frameref, load_mirrors50,
+                     load_renorm, max_two_sample_z, rel_err, renorm_names)
 from paper_2604_27058_b200._abi import (FS_FORCE_GENERAL, FS_FORCE_HBM, FS_FORCE_SEGMENTED, FS_NO_JIT,
                                         FS_NO_RENORM, FS_RNG_PHILOX, FS_RNG_SPLITMIX)
 from test_oracle_pins import check_sketch
@@ -311,3 +314,27 @@ def test_gpu_nan_raises_through_run_shot(cuda):
         R.run_shot(Q, shot=0)
     with pytest.raises(R.ShotError, match="NaN"):
         R.sample_accumulate(Q, 1000, seed=0)
+
+
+# ---------------------------------------------------------------------------- independent references
+
+@pytest.mark.parametrize("name", frameref_names())
+@pytest.mark.parametrize("flags,n", [(FS_RNG_PHILOX, 10_000_000), (FS_RNG_SPLITMIX, 1_000_000)])
+def test_gpu_rates_match_reference_frame_sampler(cuda, name, flags, n):
+    """Detector / observable rates of the engine (the bench's affine kernel for Philox) vs the
+    reference's independent Pauli-frame sampler (oracle.py:407-516), |z| < 5."""
+    g = load_frameref(name)
+    dp = _dev(g["prog"])
+    acc = dp.accumulate(n, seed=123, flags=flags)
+    ns = int(g["shots"][0])
+    assert max_two_sample_z(acc["detectors"], g["det_counts"], n, ns) < 5.0
+    assert max_two_sample_z(acc["observables"], g["obs_counts"], n, ns) < 5.0
+
+
+@pytest.mark.parametrize("flags", [FS_RNG_PHILOX, FS_RNG_SPLITMIX])
+def test_gpu_fifty_mirrors_are_deterministic(cuda, flags):
+    """Acceptance criterion 2 (test_acceptance.py:110-128): 50 exact U U^dagger circuits x 10^4
+    shots, every record 0."""
+    for i, P in enumerate(load_mirrors50()):
+        acc = _dev(P).accumulate(10_000, seed=i, flags=flags)
+        assert not acc["measurements"].any(), i

@@ -8,7 +8,9 @@
   reference stream bit-exact, and the unnormalised states of free shots (gamma,
   |gamma|^2 ||phi||^2, records, frames, amplitudes);
 * ``deep/config4_deep`` -- accepted config-4 trajectories (all 15 post-selections pass): final
-  state and the sketched checkpoints at k >= 10.
+  state and the sketched checkpoints at k >= 10;
+* ``frameref/*`` -- detector / observable rates against the reference's independent Pauli-frame
+  sampler (oracle.py:407-516; config 1, a boosted surface code, criterion 4's repetition code).
 """
 from __future__ import annotations
 
@@ -16,7 +18,8 @@ import numpy as np
 import pytest
 
 import oracle
-from goldens import load_accept, load_deep, load_renorm, rel_err, renorm_names, sketch_vectors
+from goldens import (frameref_names, load_accept, load_deep, load_frameref, load_renorm, max_two_sample_z,
+                     rel_err, renorm_names, sketch_vectors)
 from paper_2604_27058_b200._abi import FS_NO_RENORM, FS_RNG_SPLITMIX
 
 TOL = 1e-10
@@ -108,3 +111,18 @@ def test_oracle_config4_deep_trajectories():
         np.testing.assert_array_equal(tb.frame_x[:, :P.n], g[f"sk{c}_fx"])
         assert rel_err(tb.gamma_c(), g[f"sk{c}_gamma"]) < TOL
         check_sketch(tb.amps_c(), g, c, valid)
+
+
+@pytest.mark.parametrize("name", frameref_names())
+def test_oracle_rates_match_reference_frame_sampler(name):
+    """The reference VM (oracle restatement, reference stream) vs the reference's independent
+    Pauli-frame sampler (oracle.py:407-516): every detector / observable rate within 5 sigma
+    (the config-1 check; acceptance criterion 4 for the repetition code)."""
+    g = load_frameref(name)
+    P = g["prog"]
+    n = 200_000
+    st, acc = oracle.accumulate(P, n, seed=77, flags=FS_RNG_SPLITMIX)
+    assert st == 0
+    ns = int(g["shots"][0])
+    assert max_two_sample_z(acc["detectors"], g["det_counts"], n, ns) < 5.0
+    assert max_two_sample_z(acc["observables"], g["obs_counts"], n, ns) < 5.0
