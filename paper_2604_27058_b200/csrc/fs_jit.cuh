@@ -362,8 +362,7 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
   // memory (config 0, k = 6: 0.053 -> 0.040 ms per 1e5 shots; 16 or 48 registers-resident: 0.042 / 0.041)
   K.nreg = K.arr_regs ? (1 << d.k_max) : std::min(32, (1 << d.k_max) / 2);
   if (const char* e = getenv("FS_GJIT_NREG")) if (!K.arr_regs) K.nreg = std::max(0, std::min(atoi(e), (1 << d.k_max) - 1));
-  const size_t tidx0 = paulis.size() + 1;  // second half of pslot: touched-slot index per Pauli entry
-  K.pslot.assign(2 * tidx0, 0);
+  K.pslot.assign(paulis.size() + 1, 0);
   K.site_block.assign(d.num_sites + 1, 0);
   for (int i = 0, b = 0; i < d.num_instrs; i++)
     if (FS_OPCODE(ins_all[(size_t)i * FS_INS_WORDS]) == FS_OP_NOISE) {
@@ -595,39 +594,7 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
             }
         std::sort(touched.begin(), touched.end());
         touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
-        // ballot form (<= 64 touched slots, FS_GJIT_NOISE_BALLOT): every lane scans the block's fault entries of its
-        // word (broadcast loads), folds the entries of ITS shot into a mask over the touched slots
-        // (per-entry slot index table after pslot), and each touched slot word takes the ballot of
-        // that bit -- no shared-memory staging, no lane-0 serial loop.  Overflowed fault lists
-        // (rare) keep the lane-0 path through shared memory.
-        // measured on config 2: 2.92 vs 2.31 ms per 1e7 shots (the ballots add ~4 instructions per
-        // touched slot to a kernel bound by instruction issue) -> opt-in FS_GJIT_NOISE_BALLOT
-        const bool ballot = touched.size() <= 64 && getenv("FS_GJIT_NOISE_BALLOT");
-        if (ballot)
-          for (int s2 = I[1]; s2 < I[2]; s2++)
-            for (int c = site_case_off[s2]; c < site_case_off[s2 + 1]; c++)
-              for (int j = case_pauli_off[c]; j < case_pauli_off[c + 1]; j++)
-                K.pslot[tidx0 + j] = (uint16_t)(std::lower_bound(touched.begin(), touched.end(), (int)K.pslot[j]) - touched.begin());
         o << "    {\n";
-        if (ballot) {
-          o << "      uint64_t fm = 0ull;\n";
-          o << "      if (fover) {\n";
-          o << "        fm = fs::gjit_noise_mask(P, pslot + " << tidx0 << ", gen, psite, plane, pcase, " << I[2] << ", lane);\n";
-          o << "      } else {\n";
-          o << "        const uint32_t nb_ = __ldg(bcount + (size_t)" << nblk << " * A.ostride + w);\n";
-          o << "        for (uint32_t t = 0; t < nb_; t++) {\n";
-          o << "          const uint32_t e = __ldg(fent + (size_t)(fcur + t) * A.ostride + w);\n";
-          o << "          if ((int)(e & 31u) == lane) {\n";
-          o << "            const int off = (int)(e >> 10), cnt = (int)((e >> 5) & 31u);\n";
-          o << "            for (int j = 0; j < cnt; j++) fm ^= 1ull << __ldg(pslot + " << tidx0 << " + off + j);\n";
-          o << "          }\n        }\n        fcur += nb_;\n      }\n";
-          o << "      if (__any_sync(0xFFFFFFFFu, fm != 0ull)) {\n";
-          for (size_t t = 0; t < touched.size(); t++)
-            o << "        " << f(touched[t]) << " ^= __ballot_sync(0xFFFFFFFFu, (uint32_t)(fm >> " << t << ") & 1u);\n";
-          o << "      }\n    }\n";
-          nblk++;
-          break;
-        }
         for (int sl : touched) o << "      Fs[" << sl << "] = " << f(sl) << ";\n";
         o << "      __syncwarp();\n      if (lane == 0) {\n";
         o << "        if (!fover) {\n          const uint32_t nb_ = __ldg(bcount + (size_t)" << nblk << " * A.ostride + w);\n";

@@ -39,29 +39,6 @@ __device__ __noinline__ void gjit_noise_fallback(const DevProg& P, uint32_t* Fs,
   }
 }
 
-// The same regeneration for the ballot form of the general kernel's NoiseBlocks: every lane runs
-// the word's generator (same state in all lanes) and keeps the faults of ITS shot as a mask over
-// the block's touched slots (tidx: touched-slot index per Pauli entry).
-__device__ __noinline__ uint64_t gjit_noise_mask(const DevProg& P, const uint16_t* __restrict__ tidx, WordFaultGen& gen,
-                                                 int& psite, int& plane, int& pcase, int hi, int lane) {
-  uint64_t fm = 0ull;
-  for (;;) {
-    if (psite < 0) {
-      int st_, ln_, cs_;
-      const int r_ = gen.step(P, st_, ln_, cs_);
-      if (r_ == 2) { psite = 0x7FFFFFFF; break; }
-      if (r_ == 0) continue;
-      psite = st_; plane = ln_; pcase = cs_;
-    }
-    if (psite >= hi) break;
-    if (plane == lane)
-      for (int j = __ldg(P.case_pauli_off + pcase); j < __ldg(P.case_pauli_off + pcase + 1); j++)
-        fm ^= 1ull << __ldg(tidx + j);
-    psite = -1;
-  }
-  return fm;
-}
-
 // Noise for the specialised frame kernel.  fault_list_kernel generates each 32-shot word's
 // faults (WordFaultGen: the engine stream; lane = word) and writes one entry per fault,
 // ent[i][W] = pauli_off << 10 | pauli_cnt << 5 | shot_bit, plus per-NoiseBlock counts
@@ -390,143 +367,6 @@ __device__ __forceinline__ void aff_group_faults(const DevProg& P, const AffTabs
       if (w >= W) break;
       aff_word_faults<OFF16, UNIFORM>(P, T, B, wi, seed, word0 + w, lane);
     }
-  }
-}
-
-// ------------------------------------------------------------------ lane-per-word affine kernel
-// (fs_affine2.cuh).  Tables in shared memory: buffer rows per case and pass, site -> (first case,
-// class), class -> (case count, p, cumulative case probabilities), the ln table of the gap draws.
-struct Aff2Tabs {
-  const uint16_t* rows;      // [case][pass] lists of pass-local buffer rows
-  const uint32_t* coff;      // [case + 1] first entry of the case's lists (u16 entries when coff16)
-  bool coff16;
-  const uint8_t* cnp;        // [case][npass] list lengths
-  const uint32_t* site_case;
-  const uint16_t* site_cls;
-  const int* cls_nc;
-  const double* cls_prob;
-  const double* cls_cum;
-  const double* cls_scale;
-  const double2* lntab;
-  int cw;
-};
-
-template <bool UNIFORM>
-__device__ __forceinline__ int aff2_case(const Aff2Tabs& T, int site, int cls, double x) {
-  const int nc = T.cls_nc[cls];
-  int c = 0;
-  if (nc > 1) {  // bisect_right(cum, x) clamped to nc - 1 (as aff_case)
-    const double* cum = T.cls_cum + cls * T.cw;
-    c = min((int)(x * T.cls_scale[cls]), nc - 1);
-    c -= (c > 0 && x < cum[c - 1]) ? 1 : 0;
-    c += (c < nc - 1 && !(x < cum[c])) ? 1 : 0;
-    if (!UNIFORM && ((c > 0 && x < cum[c - 1]) || (c < nc - 1 && !(x < cum[c])))) {
-      int lo = 0, hi = nc;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (x < cum[mid]) hi = mid; else lo = mid + 1;
-      }
-      c = lo < nc - 1 ? lo : nc - 1;
-    }
-  }
-  return (int)T.site_case[site] + c;
-}
-
-// queue entry k of this lane: shared memory below QCAP, spill column beyond
-constexpr int kAff2Spill = 128;  // spill slots per lane beyond the shared-memory queue
-template <int QCAP>
-__device__ __forceinline__ void aff2_push(uint32_t* Q, uint32_t* ovf, size_t ovs, int& qn, int lane, uint32_t e) {
-  if (qn < QCAP) Q[qn * 32 + lane] = e;
-  else if (qn < QCAP + kAff2Spill) ovf[(size_t)(qn - QCAP) * ovs] = e;
-  else return;  // unreachable in practice: QCAP = mean + 8 sigma of the word's fault count, + 128
-  qn++;
-}
-template <int QCAP>
-__device__ __forceinline__ uint32_t aff2_entry(const uint32_t* Q, const uint32_t* ovf, size_t ovs, int k, int lane) {
-  return k < QCAP ? Q[k * 32 + lane] : ovf[(size_t)(k - QCAP) * ovs];
-}
-
-// The word's noise stream, one lane per word, step after step: WordFaultGen's process (same
-// Philox block per step, gap floor(ln(U) * lp), thinning, case) -- the one-run form keeps the run
-// parameters in registers (aff_word_faults_1run's arithmetic), the generic form is WordFaultGen
-// itself.  Faults are queued as (case << 5 | shot bit); returns the count.
-template <bool RUN1, bool UNIFORM, int QCAP>
-__device__ __forceinline__ int aff2_word_faults(const DevProg& P, const Aff2Tabs& T, uint32_t* Q, uint32_t* ovf,
-                                                size_t ovs, uint64_t seed, uint64_t wabs, int lane) {
-  int qn = 0;
-  if (RUN1) {
-    const int start = __ldg(P.run_start);
-    const int limit = 32 * __ldg(P.run_len);
-    const double lp = __ldg(P.run_lp), q = __ldg(P.run_q);
-    if (limit == 0) {  // a certain site run cannot be RUN1 (host checks run_len > 0)
-      return 0;
-    }
-    int c = -1;
-    for (uint32_t st = 0;; st++) {
-      const uint4 b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), 0u, (TAG_NOISE << 24) | st, seed);
-      const double g = floor(__dmul_rn(ln_unit_t(((uint64_t)b.y << 32) | b.x, T.lntab), lp));
-      const int inc = g < 33554432.0 ? (int)g + 1 : 33554432;
-      c += inc;
-      if (c >= limit) break;
-      const double u2 = u64_to_unit(((uint64_t)b.w << 32) | b.z);
-      const int s = start + (c >> 5);
-      const double x = __dmul_rn(u2, q);
-      const int k = T.site_cls[s];
-      if (x < T.cls_prob[k]) {  // thinning: p_site < q
-        const int cs = aff2_case<UNIFORM>(T, s, k, x);
-        aff2_push<QCAP>(Q, ovf, ovs, qn, lane, ((uint32_t)cs << 5) | (uint32_t)(c & 31));
-      }
-    }
-  } else {
-    WordFaultGen gen;
-    gen.init(seed, wabs);
-    int site = 0, fl = 0, cs = 0;
-    for (;;) {
-      const int r = gen.step(P, site, fl, cs);
-      if (r == 2) break;
-      if (r == 1) aff2_push<QCAP>(Q, ovf, ovs, qn, lane, ((uint32_t)cs << 5) | (uint32_t)fl);
-    }
-  }
-  return qn;
-}
-
-// XOR every queued fault's shot bit into its rows of pass `pass` (this lane's column of the row
-// buffer: plain load / store, no other lane touches it).  The lane walks its queue with a cursor;
-// up to four rows of the current case per trip keep several independent loads in flight.
-template <int NPASS, int QCAP, int DUMP>
-__device__ __forceinline__ void aff2_apply(const Aff2Tabs& T, uint32_t* B, const uint32_t* Q, const uint32_t* ovf,
-                                           size_t ovs, int qn, int pass, int lane) {
-#if defined(FS_AFF_DIAG) && FS_AFF_DIAG == 1
-  return;
-#endif
-  int k = 0;
-  uint32_t j = 0, jend = 0, bit = 0;
-  for (;;) {
-    while (j == jend) {  // next case with rows in this pass
-      if (k == qn) return;
-      const uint32_t e = aff2_entry<QCAP>(Q, ovf, ovs, k++, lane);
-      const uint32_t c = e >> 5;
-      bit = 1u << (e & 31);
-      j = T.coff16 ? (uint32_t)reinterpret_cast<const uint16_t*>(T.coff)[c] : T.coff[c];
-      const uint8_t* np = T.cnp + (size_t)c * NPASS;
-#pragma unroll
-      for (int p = 0; p < NPASS; p++)
-        if (p < pass) j += np[p];
-      jend = j + np[pass];
-    }
-    // up to four distinct rows of one case: all loads before the stores (the rows of a case are
-    // distinct), the missing ones on the dump row
-    const uint32_t m = jend - j;
-    uint32_t* const p0 = B + (uint32_t)T.rows[j] * 32 + lane;
-    uint32_t* const p1 = B + (m > 1 ? (uint32_t)T.rows[j + 1] : (uint32_t)DUMP) * 32 + lane;
-    uint32_t* const p2 = B + (m > 2 ? (uint32_t)T.rows[j + 2] : (uint32_t)DUMP) * 32 + lane;
-    uint32_t* const p3 = B + (m > 3 ? (uint32_t)T.rows[j + 3] : (uint32_t)DUMP) * 32 + lane;
-    j += m < 4 ? m : 4;
-    const uint32_t a0 = *p0, a1 = *p1, a2 = *p2, a3 = *p3;
-    *p0 = a0 ^ bit;
-    *p1 = a1 ^ bit;
-    *p2 = a2 ^ bit;
-    *p3 = a3 ^ bit;
   }
 }
 

@@ -26,7 +26,6 @@
 #include "fs_block.cuh"
 #include "fs_jit.cuh"
 #include "fs_affine.cuh"
-#include "fs_affine2.cuh"
 #include "fs_jit_kernels.cuh"
 #include "fs_format.cuh"
 #include "fs_stratum.cuh"
@@ -49,7 +48,6 @@ int set_error(int code, const std::string& msg) {
 
 constexpr size_t kSmemBudget = 200 * 1024;  // per block, leaves room for L1
 constexpr size_t kAffSmemBudget = 208 * 1024;  // affine frame kernel: row buffers of one block per SM
-constexpr size_t kAff2SmemBudget = 226 * 1024; // lane-per-word affine kernel: tables + per-warp buffers
 
 // every entry point runs on the device the program was created on (its allocations and NVRTC
 // modules live in that device's primary context), whatever device the calling thread has current
@@ -113,7 +111,6 @@ constexpr int kChunks = 4;   // max word chunks of the fault-list | frame-kernel
 // testing / experiment switches, read once at fs_program_create (never on a launch path)
 struct EnvSwitches {
   bool no_affine = false;      // FS_NO_AFFINE: frame-only programs use the fault-list frame kernel
-  bool aff2 = false;           // FS_AFF2: the lane-per-word affine kernel (measured slower; kept for A/B)
   bool block_no_jit = false;   // FS_BLOCK_NO_JIT: segmented engine interprets every segment
   bool block_jit_warp = false; // FS_BLOCK_JIT_WARP: also specialise warp-per-shot segments
   int block_k = 0;             // FS_BLOCK_K: segment k at which a shot gets a warp / CTA (0 = default)
@@ -125,7 +122,6 @@ struct EnvSwitches {
   uint64_t stratum_chunk = 0;  // FS_STRATUM_CHUNK: stratified-sampling chunk (tests)
   void read() {
     no_affine = getenv("FS_NO_AFFINE") != nullptr;
-    aff2 = getenv("FS_AFF2") != nullptr;
     block_no_jit = getenv("FS_BLOCK_NO_JIT") != nullptr;
     block_jit_warp = getenv("FS_BLOCK_JIT_WARP") != nullptr;
     if (const char* e = getenv("FS_BLOCK_K")) block_k = std::max(1, atoi(e));
@@ -180,16 +176,6 @@ struct fs_prog {
   uint32_t* d_aff_tables = nullptr;
   int aff_threads = 0, aff_rows = 0, aff_occ = 0, gjit_occ = 0;
   size_t aff_smem = 0;
-  // lane-per-word affine kernel (fs_affine2.cuh): 0 not tried, 1 ready, -1 not applicable / failed
-  int aff2_state = 0;
-  std::string aff2_error;
-  fsjit::Compiled aff2;
-  uint32_t* d_aff2_tables = nullptr;
-  uint32_t* d_aff2_ovf = nullptr;
-  size_t aff2_ovf_bytes = 0;
-  int aff2_threads = 0, aff2_occ = 0;
-  size_t aff2_smem = 0;
-  bool h_run1 = false;  // one geometric noise run (run_len > 0): the kernel's register fast path
   // stratified sampling: suffix Poisson-binomial table of stratum w, per-chunk modes + outputs
   int strat_w = -1;
   double strat_weight = 0.0;
@@ -306,7 +292,6 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
     site += len;
   }
   const int nruns = (int)run_start.size();
-  p->h_run1 = nruns == 1 && run_len[0] > 0 && 32LL * run_len[0] < (1LL << 25);
   size_t o_rs = add(run_start.data(), sizeof(int32_t) * nruns);
   size_t o_rl2 = add(run_len.data(), sizeof(int32_t) * nruns);
   size_t o_rlp = add(run_lp.data(), sizeof(double) * nruns);
@@ -452,10 +437,7 @@ extern "C" void fs_program_destroy(fs_prog* p) {
   cudaFree(p->flist);
   cudaFree(p->d_site_block);
   cudaFree(p->d_aff_tables);
-  cudaFree(p->d_aff2_tables);
-  cudaFree(p->d_aff2_ovf);
   cudaFree(p->d_cp);
-  if (p->aff2.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->aff2.mod);
   if (p->aff.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->aff.mod);
   if (p->jit.mod && fsjit::api().ok) fsjit::api().cuModuleUnload(p->jit.mod);
   delete p;
@@ -532,23 +514,6 @@ extern "C" int fs_debug_jit_source(const fs_prog_desc* d, char* buf, size_t len)
 }
 
 // source of the affine frame kernel (fs_affine.cuh); negative if not applicable
-extern "C" int fs_debug_aff2_source(const fs_prog_desc* d, int run1, char* buf, size_t len) {
-  if (!d) return -1;
-  auto vec = [](const auto* ptr, size_t n) { return std::vector<std::remove_cv_t<std::remove_pointer_t<decltype(ptr)>>>(ptr, ptr + n); };
-  fsjit::Affine2KernelSource K = fsjit::gen_affine2_kernel(
-      *d, vec(d->instrs, (size_t)d->num_instrs * FS_INS_WORDS), vec(d->gates, d->num_gates), vec(d->paulis, d->num_paulis),
-      vec(d->reclists, d->num_reclists), vec(d->record_out, d->record_count), vec(d->case_pauli_off, d->num_cases + 1),
-      vec(d->site_case_off, d->num_sites + 1), vec(d->site_prob, d->num_sites), vec(d->case_cum, d->num_cases),
-      run1 ? 1 : 2, kAff2SmemBudget);
-  const std::string& src = K.why.empty() ? K.src : K.why;
-  if (buf && len) {
-    size_t m = std::min(len - 1, src.size());
-    std::memcpy(buf, src.data(), m);
-    buf[m] = 0;
-  }
-  return K.why.empty() ? (int)src.size() : -2;
-}
-
 extern "C" int fs_debug_aff_source(const fs_prog_desc* d, char* buf, size_t len) {
   if (!d) return -1;
   const int R = d->record_count, D = d->num_detectors, E = d->num_sites;
@@ -711,9 +676,6 @@ extern "C" const char* fs_debug_jit_status(fs_prog* p) {
                         : (p->jit_state == 0 ? "not built" : "failed: " + p->jit_error);
   s += p->aff_state == 1 ? "; affine: ready threads=" + std::to_string(p->aff_threads)
                          : (p->aff_state == 0 ? "; affine: not built" : "; affine: n/a (" + p->aff_error + ")");
-  s += p->aff2_state == 1 ? "; affine2: ready threads=" + std::to_string(p->aff2_threads) +
-                                " smem=" + std::to_string(p->aff2_smem)
-                          : (p->aff2_state == 0 ? "; affine2: not built" : "; affine2: n/a (" + p->aff2_error + ")");
   return s.c_str();
 }
 
@@ -800,56 +762,6 @@ int ensure_aff(fs_prog* p) {
   p->aff_rows = K.nrows;
   p->aff_smem = K.smem;
   p->aff_state = 1;
-  return FS_OK;
-}
-
-// lane-per-word affine frame kernel (fs_affine2.cuh), FS_AFF2 only: at one warp per 32 words its
-// column buffers hold 8x the shots of a warp pair's, so 9 warps fit an SM instead of 28 and the
-// latency-bound noise chains run at IPC 1.3 (0.42 vs 0.21 ms per 1e7 shots, profiles/r2_c1_aff2_ncu.md)
-int ensure_aff2(fs_prog* p) {
-  if (p->aff2_state == 1) return FS_OK;
-  if (p->aff2_state == -1) return FS_ERR_ARG;
-  p->aff2_state = -1;
-  fsjit::Affine2KernelSource K = fsjit::gen_affine2_kernel(
-      p->desc, p->h_instrs, p->h_gates, p->h_paulis, p->h_reclists, p->h_record_out, p->h_case_pauli_off,
-      p->h_site_case_off, p->h_site_prob, p->h_case_cum, p->h_run1 ? 1 : 2, kAff2SmemBudget);
-  if (!K.why.empty()) { p->aff2_error = K.why; return FS_ERR_ARG; }
-  std::string err = fsjit::compile(K.src, fsjit::self_dir() + "/../csrc", p->aff2, "fs_aff2_frame");
-  if (!err.empty()) { p->aff2_error = err; return set_error(FS_ERR_ARG, err); }
-  fsjit::Api& J = fsjit::api();
-  if (J.cuFuncSetAttribute(p->aff2.fn, 8 /* MAX_DYNAMIC_SHARED_SIZE_BYTES */, (int)K.smem) != 0) {
-    p->aff2_error = "cuFuncSetAttribute failed";
-    return FS_ERR_ARG;
-  }
-  FS_CUDA_TRY(cudaMalloc(&p->d_aff2_tables, sizeof(uint32_t) * K.tables.size()));
-  FS_CUDA_TRY(cudaMemcpy(p->d_aff2_tables, K.tables.data(), sizeof(uint32_t) * K.tables.size(), cudaMemcpyHostToDevice));
-  p->aff2_threads = K.threads;
-  p->aff2_smem = K.smem;
-  int occ = 1;
-  J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->aff2.fn, p->aff2_threads, p->aff2_smem);
-  p->aff2_occ = std::max(occ, 1);
-  // spill columns of the fault queues: one per thread of the grid
-  p->aff2_ovf_bytes = (size_t)p->num_sms * p->aff2_occ * p->aff2_threads * fs::kAff2Spill * 4;
-  FS_CUDA_TRY(cudaMalloc(&p->d_aff2_ovf, p->aff2_ovf_bytes));
-  p->aff2_state = 1;
-  return FS_OK;
-}
-
-int launch_aff2(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
-  fsjit::Api& J = fsjit::api();
-  const size_t groups = (a.W + 31) / 32, wpb = p->aff2_threads / 32;  // one 32-word group per warp
-  const size_t blocks = (groups + wpb - 1) / wpb;
-  const size_t grid = std::min<size_t>(std::max<size_t>(blocks, 1), (size_t)p->num_sms * p->aff2_occ);
-  fs::DevProg dpv = p->dp;
-  const uint32_t* tb = p->d_aff2_tables;
-  uint32_t* ovf = p->d_aff2_ovf;
-  void* args[] = {&dpv, &a, &tb, &ovf};
-  kt_begin(p, stream);
-  int r = J.cuLaunchKernel(p->aff2.fn, (unsigned)grid, 1, 1, (unsigned)p->aff2_threads, 1, 1, (unsigned)p->aff2_smem,
-                           stream, args, nullptr);
-  kt_end(p, stream);
-  p->launches++;
-  if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_aff2_frame) failed: " + std::to_string(r));
   return FS_OK;
 }
 
@@ -2168,7 +2080,6 @@ int launch(fs_prog* p, uint64_t seed, uint64_t shot0, uint64_t nshots, uint32_t 
   const bool trace_in = tin && (tin->fault_modes || tin->forced);
   const bool frame_free = !general && !trace_in && !(tout && tout->frame_x) && !(flags & FS_NO_JIT) &&
                           a.stop == dp.num_instrs && !p->env.no_affine;
-  if (frame_free && p->env.aff2 && ensure_aff2(p) == FS_OK) return launch_aff2(p, a, stream);
   if (frame_free && ensure_aff(p) == FS_OK) return launch_aff(p, a, stream);
   if (!general && !trace_in && !(tout && tout->frame_x) && !(flags & FS_NO_JIT) && a.stop == dp.num_instrs) {
     int rc = ensure_jit(p);

@@ -161,13 +161,8 @@ def test_gpu_jit_equals_interpreter(cuda, name, monkeypatch):
     dp = _dev(P)
     n = 70_000
     _, a, _ = dp.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX)
-    assert "affine2: ready" in dp.jit_status() or "affine: ready" in dp.jit_status(), dp.jit_status()
-    monkeypatch.setenv("FS_AFF2", "1")  # switches are read when a program handle is created
-    dpv1 = _dev(P)
-    monkeypatch.delenv("FS_AFF2")
-    _, a1, _ = dpv1.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX)
-    _same(a, a1)
-    monkeypatch.setenv("FS_NO_AFFINE", "1")
+    assert "affine: ready" in dp.jit_status(), dp.jit_status()
+    monkeypatch.setenv("FS_NO_AFFINE", "1")  # switches are read when a program handle is created
     dp2 = _dev(P)
     monkeypatch.delenv("FS_NO_AFFINE")
     _, b, _ = dp2.sample_host(n, seed=11, shot0=32 * 7, flags=FS_RNG_PHILOX)
@@ -181,34 +176,26 @@ def test_gpu_jit_equals_interpreter(cuda, name, monkeypatch):
                                   "aff_many_coins"])
 @pytest.mark.parametrize("env", [{}, {"FS_AFF_GLOBAL_TABLES": "1"}, {"FS_AFF_PAIRS": "1"}, {"FS_AFF_NONUNIFORM": "1"},
                                  {"FS_AFF_NO_DIFF": "1"}, {"FS_AFF_PARENTS": "1"}, {"FS_AFF_ANY_PARENTS": "1"},
-                                 {"FS_AFF_BALANCED": "1"}, {"FS_AFF2": "1"}, {"FS_AFF2": "1", "FS_AFF2_MINWARPS": "16"},
-                                 {"FS_AFF2": "1", "FS_AFF2_MINWARPS": "28"}, {"FS_AFF2": "1", "FS_AFF_NONUNIFORM": "1"}])
+                                 {"FS_AFF_BALANCED": "1"}])
 def test_gpu_affine_variants_match_oracle(cuda, name, env, monkeypatch):
-    """Affine kernel variants (warp-pair kernel: fault tables in global memory, one warp pair per
-    block, exact-bisect case pick, no / single-parent row differencing, load-balanced row loop;
-    lane-per-word kernel FS_AFF2: one pass, multi-pass buffers) == oracle, bit for bit; odd shot
-    count and offset so the tail word and partial groups are exercised."""
+    """Affine frame kernel variants (fault tables in global memory, one warp pair per block, the
+    exact-bisect case pick, no / single-parent row differencing, load-balanced row loop) == oracle,
+    bit for bit; odd shot count and offset so the tail word and partial groups are exercised."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     P = load(name)["prog"]
     dp = _dev(P)  # a fresh program handle: the kernel is generated at its first sample call
-    n = 3 * 1024 + 37
+    n = 3 * 256 + 37
     _, g, _ = dp.sample_host(n, seed=19, shot0=32 * 5, flags=FS_RNG_PHILOX)
-    st = dp.jit_status()
-    v1 = "FS_AFF2" not in env or name in ("aff_many_coins", "aff_surface_d7")  # the latter two: beyond aff2 limits
-    assert ("affine: ready" in st) if v1 else ("affine2: ready" in st), st
+    assert "affine: ready" in dp.jit_status(), dp.jit_status()
     _, o, _ = oracle.sample(P, n, seed=19, shot0=32 * 5, flags=FS_RNG_PHILOX)
     _same(g, o)
 
 
 @pytest.mark.parametrize("name", [c for c in CASES if 0 < load(c)["prog"].k_max <= 7 and not load(c)["prog"].has_postselect
                                   and not (set((load(c)["prog"].instrs[:, 0] & 0xFF).tolist()) & {7, 9})])
-@pytest.mark.parametrize("env", [{}, {"FS_GJIT_NOISE_BALLOT": "1"}])
-def test_gpu_general_jit_equals_interpreter(cuda, name, env, monkeypatch):
-    """Program-specialised general kernel (NVRTC; NoiseBlocks through shared memory or by ballots)
-    == general interpreter, bit for bit."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+def test_gpu_general_jit_equals_interpreter(cuda, name):
+    """Program-specialised general kernel (NVRTC) == general interpreter, bit for bit."""
     P = load(name)["prog"]
     dp = _dev(P)
     n = 20_000
@@ -232,10 +219,14 @@ def _hbm_plan(dp):
 
 
 @pytest.mark.parametrize("name", [c for c in FUSED if "t_modes" in load(c)])
-def test_gpu_fused_passes_trace_match_reference(cuda, name, monkeypatch):
-    """Large-k engine with fused tile passes (FS_HBM_FUSED) on every k_max >= 12 golden: trace
-    records, frames, gamma, final amplitudes and checkpoints against the REFERENCE."""
+@pytest.mark.parametrize("tma", [False, True])
+def test_gpu_fused_passes_trace_match_reference(cuda, name, tma, monkeypatch):
+    """Large-k engine with fused tile passes (FS_HBM_FUSED; tiles staged by cp.async or by TMA bulk
+    copies) on every k_max >= 12 golden: trace records, frames, gamma, final amplitudes and
+    checkpoints against the REFERENCE."""
     monkeypatch.setenv("FS_HBM_FUSED", "1")
+    if tma:
+        monkeypatch.setenv("FS_PASS_TMA", "1")
     g = load(name)
     P = g["prog"]
     dp = _dev(P)

@@ -61,7 +61,7 @@ def _check_final(P, g, out, tb):
 
 
 # ---------------------------------------------------------------------------- config 3
-@pytest.mark.parametrize("env", [{}, {"FS_HBM_NO_JIT": "1"}])
+@pytest.mark.parametrize("env", [{}, {"FS_HBM_NO_JIT": "1"}, {"FS_PASS_TMA": "1"}])
 def test_gpu_config3_trace_checkpoints_match_reference(cuda, env, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
