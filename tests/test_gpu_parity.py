@@ -177,7 +177,8 @@ def test_gpu_jit_equals_interpreter(cuda, name, monkeypatch):
 @pytest.mark.parametrize("env", [{}, {"FS_AFF_GLOBAL_TABLES": "1"}, {"FS_AFF_PAIRS": "1"}, {"FS_AFF_NONUNIFORM": "1"},
                                  {"FS_AFF_NO_DIFF": "1"}, {"FS_AFF_PARENTS": "1"}, {"FS_AFF_ANY_PARENTS": "1"},
                                  {"FS_AFF_BALANCED": "1"}, {"FS_AFF_W2": "1"}, {"FS_AFF_W2": "1", "FS_AFF_ANY_PARENTS": "1"}])
-def test_gpu_affine_variants_match_oracle(cuda, name, env, monkeypatch):
+@pytest.mark.parametrize("n", [3 * 256 + 37, 3 * 256 + 69])  # even / odd output stride (26 / 27 words)
+def test_gpu_affine_variants_match_oracle(cuda, name, env, n, monkeypatch):
     """Affine frame kernel variants (fault tables in global memory, one warp pair per block, the
     exact-bisect case pick, no / single-parent row differencing, load-balanced row loop, 64-bit
     copy-out of word pairs) == oracle, bit for bit; odd shot count and offset so the tail word,
@@ -186,7 +187,6 @@ def test_gpu_affine_variants_match_oracle(cuda, name, env, monkeypatch):
         monkeypatch.setenv(k, v)
     P = load(name)["prog"]
     dp = _dev(P)  # a fresh program handle: the kernel is generated at its first sample call
-    n = 3 * 256 + 37
     _, g, _ = dp.sample_host(n, seed=19, shot0=32 * 5, flags=FS_RNG_PHILOX)
     assert "affine: ready" in dp.jit_status(), dp.jit_status()
     _, o, _ = oracle.sample(P, n, seed=19, shot0=32 * 5, flags=FS_RNG_PHILOX)
