@@ -44,9 +44,8 @@ constexpr int kAffGroup = 8;              // 32-shot words per group (one 32 B s
 constexpr int kAffChunk = 32 / kAffGroup;  // rows per copy-out instruction
 constexpr int kAffMaxParents = 6;         // rows a copied-out row may be rebuilt from
 constexpr int kAffMaxPairs = 15;          // warp pairs per block (one block per SM; named barriers 1..15)
-// buffer slot of row r for word wi: r * G + (wi ^ sw(r)) with sw(r) = (r / kAffChunk) % G (bank
-// spread of the fault atomics), or ((r / 8) % 4) * 2 for the FS_AFF_W2 copy-out (word pairs stay
-// contiguous: 64-bit loads and stores)
+// buffer slot of row r for word wi: r * G + (wi ^ sw(r)), sw(r) = (r / kAffChunk) % G (bank spread)
+inline int aff_sw(int r) { return (r / kAffChunk) % kAffGroup; }
 constexpr int kAffMaxCoins = 512;         // coin words per 32-shot word (shared memory, 2 KB per word at the limit)
 constexpr size_t kAffMaxTerms = 1 << 16;  // coin XOR terms over all rows (code size)
 
@@ -72,11 +71,6 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
                                                   const std::vector<double>& case_cum, size_t smem_budget) {
   AffineKernelSource K;
   const int n = d.n, R = d.record_count, U = d.num_user_records, D = d.num_detectors, E = d.num_sites;
-  // copy-out form: 4 rows x 8 words of 32 bits per instruction, or (FS_AFF_W2) 8 rows x 4 word
-  // PAIRS (64-bit loads / stores; the slot swizzle keeps each pair contiguous)
-  const bool w2 = getenv("FS_AFF_W2") != nullptr;
-  const int RCH = w2 ? 8 : kAffChunk;  // rows per copy-out instruction
-  auto aff_sw = [&](int r) { return w2 ? ((r / 8) % 4) * 2 : (r / kAffChunk) % kAffGroup; };
   (void)bit_slot;
   if (d.k_max != 0) { K.why = "not frame-only"; return K; }
   // ---- rows: user records (col), detectors, one per ObservableIns, hidden bits read by PostSelect
@@ -100,7 +94,7 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   // hidden bits read by PostSelect (D4, U4 = D, U rounded up to the copy-out chunk: it writes
   // kAffChunk rows of one kind per instruction).  Detectors come first so that record rows can be
   // rebuilt from them (below).
-  const int U4 = (U + RCH - 1) / RCH * RCH, D4 = (D + RCH - 1) / RCH * RCH;
+  const int U4 = (U + kAffChunk - 1) / kAffChunk * kAffChunk, D4 = (D + kAffChunk - 1) / kAffChunk * kAffChunk;
   std::vector<int> bit_row(R + D, -1);  // record / detector id -> buffer row
   for (int r = 0; r < R; r++)
     if (record_out[r] >= 0) bit_row[r] = D4 + record_out[r];
@@ -288,9 +282,9 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
             const size_t src = t * 64 + __builtin_ctzll(m);
             if (src < (size_t)el0) continue;
             for (int q : orows[src - el0]) {
-              if (q >= r - r % RCH) break;
+              if (q >= r - r % kAffChunk) break;
               // a differenced parent must be rebuilt earlier by the same warp of the pair
-              if (!fixed_row[q] && (only_fixed || (q / RCH) % 2 != (r / RCH) % 2)) continue;
+              if (!fixed_row[q] && (only_fixed || (q / kAffChunk) % 2 != (r / kAffChunk) % 2)) continue;
               if (q >= U4 + D4) continue;  // observable / post-select rows: not parents
               if (ov[q]++ == 0) cand.push_back(q);
             }
@@ -634,62 +628,17 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   o << "    }\n";
   o << "    fs::pair_sync(pair);\n";
   o << "    {\n";
-  if (w2) {
-    o << "      const int j8 = lane >> 2, wp2 = (lane & 3) * 2;\n";
-    o << "      const uint32_t w = grp * " << G << " + wp2;\n";
-    o << "      const bool ev = !(A.ostride & 1u), w1ok = w + 1 < A.W;\n";
-    o << "      if (w < A.W) {\n";
-    if (npsel == 0) o << "        const uint2 m0 = *reinterpret_cast<const uint2*>(AL + wp2);\n";
-    o << "        uint32_t* const mo = A.meas + (size_t)j8 * A.ostride + w;\n";
-    o << "        uint32_t* const dout = A.det + (size_t)j8 * A.ostride + w;\n";
-    o << "        const size_t sc = (size_t)" << RCH << " * A.ostride;\n";
-  } else {
-    o << "      const uint32_t w = grp * " << G << " + wi;\n";
-    o << "      if (w < A.W) {\n";
-    if (npsel == 0) o << "        const uint32_t m0 = AL[wi];\n";
-    o << "        uint32_t* const mo = A.meas + (size_t)j4 * A.ostride + w;\n";
-    o << "        uint32_t* const dout = A.det + (size_t)j4 * A.ostride + w;\n";
-    o << "        const size_t sc = (size_t)" << kAffChunk << " * A.ostride;\n";
-  }
+  o << "      const uint32_t w = grp * " << G << " + wi;\n";
+  o << "      if (w < A.W) {\n";
+  if (npsel == 0) o << "        const uint32_t m0 = AL[wi];\n";
+  o << "        uint32_t* const mo = A.meas + (size_t)j4 * A.ostride + w;\n";
+  o << "        uint32_t* const dout = A.det + (size_t)j4 * A.ostride + w;\n";
+  o << "        const size_t sc = (size_t)" << kAffChunk << " * A.ostride;\n";
   std::vector<uint8_t> is_parent(nrows + 1, 0);
   for (int r = 0; r < nrows; r++)
     for (int q : parents[r]) is_parent[q] = 1;
   int cur_half = 0;
-  auto emit_copy2 = [&](int r0, int cnt, const char* base, int rbase) {  // FS_AFF_W2 form
-    const int RC = RCH;
-    auto slot = [&](int row, const char* jv) {
-      return "B + " + std::to_string(row * G) + " + " + jv + " * " + std::to_string(G) + " + (wp2 ^ " +
-             std::to_string(aff_sw(row)) + ")";
-    };
-    for (int r = r0; r < r0 + cnt; r += RC) {
-      if (r / RC % 2 != cur_half) continue;
-      const int rem = std::min(RC, r0 + cnt - r);
-      size_t np = 0;
-      for (int q = 0; q < rem; q++) np = std::max(np, parents[r + q].size());
-      const std::string m = npsel == 0 ? "m0" : "(*reinterpret_cast<const uint2*>(AL + SEG[" + std::to_string(r) +
-                                                    " + j8] * " + std::to_string(G) + " + wp2))";
-      o << "        {";
-      if (rem < RC) o << " if (j8 < " << rem << ") {";
-      o << " uint2 v = *reinterpret_cast<const uint2*>(" << slot(r, "j8") << ");";
-      for (size_t k = 0; k < np; k++) {
-        const int p0 = parents[r].size() > k ? parents[r][k] : -1;
-        bool same = p0 >= 0 && p0 % RC == 0;
-        for (int q = 1; q < rem && same; q++) same = parents[r + q].size() > k && parents[r + q][k] == p0 + q;
-        if (same) o << " { const uint2 p = *reinterpret_cast<const uint2*>(" << slot(p0, "j8") << "); v.x ^= p.x; v.y ^= p.y; }";
-        else o << " { const uint2 p = *reinterpret_cast<const uint2*>(B + (PS" << k << "[" << r << " + j8] ^ wp2)); v.x ^= p.x; v.y ^= p.y; }";
-      }
-      bool wb = false;
-      for (int q = 0; q < rem && !wb; q++) wb = is_parent[r + q];
-      if (np && wb) o << " *reinterpret_cast<uint2*>(" << slot(r, "j8") << ") = v;";
-      o << " { const uint2 mm = " << m << "; uint32_t* const dst = " << base << " + " << (r - rbase) / RC << " * sc;"
-        << " if (ev) *reinterpret_cast<uint2*>(dst) = make_uint2(v.x & mm.x, v.y & mm.y);"
-        << " else { dst[0] = v.x & mm.x; if (w1ok) dst[1] = v.y & mm.y; } }";
-      if (rem < RC) o << " }";
-      o << " }\n";
-    }
-  };
   auto emit_copy = [&](int r0, int cnt, const char* base, int rbase) {
-    if (w2) { emit_copy2(r0, cnt, base, rbase); return; }
     const int RC = kAffChunk;
     for (int r = r0; r < r0 + cnt; r += RC) {
       if (r / RC % 2 != cur_half) continue;  // the other warp of the pair copies this chunk

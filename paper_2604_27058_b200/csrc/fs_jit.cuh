@@ -404,8 +404,12 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
   for (int sl = 0; sl < 2 * n; sl++) o << "    uint32_t " << f(sl) << " = 0u;\n";
   for (int sl = 0; sl < d.num_slots; sl++) o << "    uint32_t r" << sl << " = 0u;\n";
   for (int j = 0; j < d.num_observables; j++) o << "    uint32_t ob" << j << " = 0u;\n";
-  for (int i = 0; i < K.nreg; i++) o << "    double2 a" << i << " = make_double2(" << (i == 0 ? "1.0" : "0.0") << ", 0.0);\n";
-  if (K.nreg == 0) o << "    AR[0] = make_double2(1.0, 0.0);\n";
+  // the initial amplitude 1 is opaque to the compiler (asm): the array work of a noiseless
+  // prefix (config 0: the six Expands before the first random draw) is executed per shot, never
+  // constant-folded into the kernel
+  o << "    double one_;\n    asm volatile(\"mov.b64 %0, 0x3FF0000000000000;\" : \"=d\"(one_));\n";
+  for (int i = 0; i < K.nreg; i++) o << "    double2 a" << i << " = make_double2(" << (i == 0 ? "one_" : "0.0") << ", 0.0);\n";
+  if (K.nreg == 0) o << "    AR[0] = make_double2(one_, 0.0);\n";
   o << "    uint4 cb = make_uint4(0u, 0u, 0u, 0u);\n";
   // no NoiseBlock: no fault lists (the launcher skips their kernel)
   if (K.nblocks) o << "    const uint32_t nt_ = ntot[w];\n    const bool fover = nt_ == 0xFFFFFFFFu;\n    uint32_t fcur = 0;\n";
