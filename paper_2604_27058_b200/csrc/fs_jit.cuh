@@ -360,7 +360,9 @@ inline GeneralKernelSource gen_general_kernel(const fs_prog_desc& d, const std::
   if (const char* e = getenv("FS_GJIT_SMEM")) K.arr_regs = K.arr_regs && atoi(e) == 0;  // tuning
   // larger arrays: the low half (at most 32) of the amplitudes stays in registers, the rest in shared
   // memory (config 0, k = 6: 0.053 -> 0.040 ms per 1e5 shots; 16 or 48 registers-resident: 0.042 / 0.041)
-  K.nreg = K.arr_regs ? (1 << d.k_max) : std::min(32, (1 << d.k_max) / 2);
+  // (with the noiseless prefix executed per shot, config 0 at k = 6: 32 register-resident -> 0.077
+  // ms per 1e5 shots (spills), 24 -> 0.057, 16 -> 0.059, 8 -> 0.070)
+  K.nreg = K.arr_regs ? (1 << d.k_max) : std::min(24, (1 << d.k_max) / 2);
   if (const char* e = getenv("FS_GJIT_NREG")) if (!K.arr_regs) K.nreg = std::max(0, std::min(atoi(e), (1 << d.k_max) - 1));
   K.pslot.assign(paulis.size() + 1, 0);
   K.site_block.assign(d.num_sites + 1, 0);
