@@ -70,7 +70,7 @@ struct BlockCtx {
   __device__ __forceinline__ void out_bit(uint32_t* row) { atomicOr(row + (si >> 5), 1u << (si & 31)); }
 
   // one scalar instruction of this shot (thread 0 only)
-  __device__ void scalar_step(int i) {
+  __device__ __forceinline__ void scalar_step(int i) {
     const int4 I0 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i);
     const int4 I1 = __ldg(reinterpret_cast<const int4*>(P.instrs) + 2 * i + 1);
     const int ins[8] = {I0.x, I0.y, I0.z, I0.w, I1.x, I1.y, I1.z, I1.w};
@@ -437,7 +437,7 @@ struct BlockCtx {
   }
 
   // trace: state after instructions [0, cp_at[j]) (all threads: amplitudes; thread 0: scalars)
-  __device__ void dump_cp(int j) {
+  __device__ __forceinline__ void dump_cp(int j) {
     const size_t cs = (size_t)j * A.nshots + si;
     const int c = __ldg(A.cp_at + j);
     const uint32_t sz = 1u << (c > 0 ? __ldg(P.schedule + c - 1) : 0);
@@ -466,7 +466,7 @@ struct BlockCtx {
   }
 
   // the interpreter: instructions [seg_begin, seg_end) of the segment
-  __device__ void interpret() {
+  __device__ __forceinline__ void interpret() {
     for (int i = S.seg_begin; i < S.seg_end; i++) {
       if (!sh_alive) break;
       if (A.ncp) dump_cps_at(i);
@@ -499,7 +499,7 @@ struct BlockCtx {
   }
 
   // trace: final state of a shot that ended (halted, raised or finished) in this segment
-  __device__ void dump_final(int upto) {
+  __device__ __forceinline__ void dump_final(int upto) {
     const int kst = A.stop > 0 ? __ldg(P.schedule + A.stop - 1) : 0;
     const int kcur = upto > 0 ? __ldg(P.schedule + upto - 1) : 0;
     const uint32_t sz = 1u << kst, cur = 1u << kcur;

@@ -338,3 +338,34 @@ def test_gpu_fifty_mirrors_are_deterministic(cuda, flags):
     for i, P in enumerate(load_mirrors50()):
         acc = _dev(P).accumulate(10_000, seed=i, flags=flags)
         assert not acc["measurements"].any(), i
+
+
+# ---------------------------------------------------------------------------- block engines
+_PSEL = [c for c in case_names() if load(c)["prog"].has_postselect and "t_modes" in load(c)]
+
+
+@pytest.mark.parametrize("name", _PSEL)
+@pytest.mark.parametrize("env", [{"FS_BLOCK_K": "1"}, {"FS_BLOCK_K": "1", "FS_BLOCK_SMEM": "1"}, {}])
+def test_gpu_block_engines_match_reference_and_oracle(cuda, name, env, monkeypatch):
+    """Every segment of a post-selected program through the warp-per-shot block engine
+    (FS_BLOCK_K=1: registers-resident arrays, or FS_BLOCK_SMEM: shared memory): trace against the
+    reference (records, frames, gamma, amplitudes), Philox free sampling against the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = load(name)
+    P = g["prog"]
+    dp = _dev(P)
+    out, tb = _trace_all(dp, g, FS_RNG_SPLITMIX | FS_FORCE_SEGMENTED)
+    np.testing.assert_array_equal(out.measurements(), g["t_meas"])
+    np.testing.assert_array_equal(out.detectors(), g["t_det"])
+    np.testing.assert_array_equal(out.accepted_bits(), g["t_acc"])
+    np.testing.assert_array_equal(tb.frame_x[:, :P.n], g["t_fx"])
+    assert rel_err(tb.gamma_c(), g["t_gamma"]) < TOL
+    if "t_amps" in g and g["t_acc"].all():
+        assert rel_err(tb.amps_c(), g["t_amps"]) < TOL
+    n = 8192
+    _, a, _ = dp.sample_host(n, seed=41, shot0=32 * 3, flags=FS_RNG_PHILOX)
+    _, b, _ = oracle.sample(P, n, seed=41, shot0=32 * 3, flags=FS_RNG_PHILOX)
+    np.testing.assert_array_equal(a.measurements(), b.measurements())
+    np.testing.assert_array_equal(a.detectors(), b.detectors())
+    np.testing.assert_array_equal(a.accepted_bits(), b.accepted_bits())
