@@ -24,7 +24,6 @@
 #include "fs_hbm.cuh"
 #include "fs_hbm_fused.cuh"
 #include "fs_block.cuh"
-#include "fs_block_reg.cuh"
 #include "fs_jit.cuh"
 #include "fs_affine.cuh"
 #include "fs_jit_kernels.cuh"
@@ -113,7 +112,6 @@ constexpr int kChunks = 4;   // max word chunks of the fault-list | frame-kernel
 struct EnvSwitches {
   bool no_affine = false;      // FS_NO_AFFINE: frame-only programs use the fault-list frame kernel
   bool block_no_jit = false;   // FS_BLOCK_NO_JIT: segmented engine interprets every segment
-  bool block_smem = false;     // FS_BLOCK_SMEM: warp-per-shot segments keep the array in shared memory
   bool block_jit_warp = false; // FS_BLOCK_JIT_WARP: also specialise warp-per-shot segments
   int block_k = 0;             // FS_BLOCK_K: segment k at which a shot gets a warp / CTA (0 = default)
   bool hbm_fused = false;      // FS_HBM_FUSED: fused tile passes also under FS_FORCE_HBM
@@ -125,7 +123,6 @@ struct EnvSwitches {
   void read() {
     no_affine = getenv("FS_NO_AFFINE") != nullptr;
     block_no_jit = getenv("FS_BLOCK_NO_JIT") != nullptr;
-    block_smem = getenv("FS_BLOCK_SMEM") != nullptr;
     block_jit_warp = getenv("FS_BLOCK_JIT_WARP") != nullptr;
     if (const char* e = getenv("FS_BLOCK_K")) block_k = std::max(1, atoi(e));
     hbm_fused = getenv("FS_HBM_FUSED") != nullptr;
@@ -1004,42 +1001,8 @@ int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector
   return FS_OK;
 }
 
-// warp-per-shot segment with the active array in registers (fs_block_reg.cuh)
-template <bool SM>
-int launch_block_reg(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cudaStream_t stream) {
-  const fs::DevProg& dp = p->dp;
-  const int nr = karr <= 5 ? 1 : 1 << (karr - 5);
-  void (*kern)(fs::DevProg, fs::RunArgs, fs::SegArgs, int, int) = nullptr;
-  int maxg = fs::kBlockMaxGroups;
-  switch (nr) {
-    case 1: kern = fs::block_reg_kernel<SM, 1>; maxg = fs::block_reg_groups<1>(); break;
-    case 2: kern = fs::block_reg_kernel<SM, 2>; maxg = fs::block_reg_groups<2>(); break;
-    case 4: kern = fs::block_reg_kernel<SM, 4>; maxg = fs::block_reg_groups<4>(); break;
-    case 8: kern = fs::block_reg_kernel<SM, 8>; maxg = fs::block_reg_groups<8>(); break;
-    case 16: kern = fs::block_reg_kernel<SM, 16>; maxg = fs::block_reg_groups<16>(); break;
-    default: kern = fs::block_reg_kernel<SM, 32>; maxg = fs::block_reg_groups<32>(); break;
-  }
-  const size_t group_bytes = align_up((size_t)4 * (2 * dp.n + dp.num_slots + dp.O + 4), 16);
-  const int ngroups = (int)std::max<size_t>(1, std::min<size_t>(maxg, (220 * 1024) / group_bytes));
-  const int nt = 32 * ngroups;
-  const size_t smem = group_bytes * ngroups;
-  FS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int occ = occupancy_blocks(kern, nt, smem);
-  const size_t blocks_needed = (S.n_in + ngroups - 1) / ngroups;
-  const size_t grid = std::max<size_t>(1, std::min<size_t>(blocks_needed, (size_t)p->num_sms * occ));
-  kt_begin(p, stream);
-  kern<<<(unsigned)grid, nt, smem, stream>>>(dp, a, S, karr, (int)group_bytes);
-  kt_end(p, stream);
-  p->launches++;
-  FS_CUDA_TRY(cudaGetLastError());
-  return FS_OK;
-}
-
 int launch_block_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cudaStream_t stream) {
   const fs::DevProg& dp = p->dp;
-  if (karr <= 10 && !p->env.block_smem)  // warp per shot: the array in registers
-    return (a.flags & FS_RNG_SPLITMIX) ? launch_block_reg<true>(p, a, S, karr, stream)
-                                       : launch_block_reg<false>(p, a, S, karr, stream);
   const size_t group_bytes = align_up(((size_t)16 << karr) + (size_t)4 * (2 * dp.n + dp.num_slots + dp.O + 4), 16);
   if (group_bytes > kSmemBudget) return set_error(FS_ERR_ARG, "active array too large for the block engine");
   const bool warp_mode = karr <= 10;

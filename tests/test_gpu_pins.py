@@ -345,11 +345,12 @@ _PSEL = [c for c in case_names() if load(c)["prog"].has_postselect and "t_modes"
 
 
 @pytest.mark.parametrize("name", _PSEL)
-@pytest.mark.parametrize("env", [{"FS_BLOCK_K": "1"}, {"FS_BLOCK_K": "1", "FS_BLOCK_SMEM": "1"}, {}])
+@pytest.mark.parametrize("env", [{"FS_BLOCK_K": "1"}, {"FS_BLOCK_K": "11"}, {}])
 def test_gpu_block_engines_match_reference_and_oracle(cuda, name, env, monkeypatch):
-    """Every segment of a post-selected program through the warp-per-shot block engine
-    (FS_BLOCK_K=1: registers-resident arrays, or FS_BLOCK_SMEM: shared memory): trace against the
-    reference (records, frames, gamma, amplitudes), Philox free sampling against the oracle."""
+    """Post-selected programs with every segment through the block engine (FS_BLOCK_K=1: warp or
+    CTA per shot from k = 1), through lane-per-shot segments up to k = 10 (FS_BLOCK_K=11), and by
+    default: trace against the reference (records, frames, gamma, amplitudes), Philox free
+    sampling against the oracle."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     g = load(name)
