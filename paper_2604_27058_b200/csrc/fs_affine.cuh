@@ -537,6 +537,26 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   std::ostringstream o;
   if (const char* dg = getenv("FS_AFF_DIAG")) o << "#define FS_AFF_DIAG " << atoi(dg) << "\n";  // profiling only
   if (getenv("FS_AFF_BALANCED")) o << "#define FS_AFF_ROWS aff_rows_bal\n";  // A/B: load-balanced row loop
+  if (!getenv("FS_AFF_CLS_TABLES")) {
+    if (ncls <= 4) {  // class probabilities, case counts and scales as constants (no table loads)
+      o << "#define FS_AFF_CLS_CONST 1\n";
+      o << "__device__ __forceinline__ int fs_aff_cls_nc(int k) { return ";
+      for (int c = 0; c + 1 < ncls; c++) o << "k == " << c << " ? " << cls_nc[c] << " : ";
+      o << (ncls ? cls_nc[ncls - 1] : 0) << "; }\n";
+      o << "__device__ __forceinline__ double fs_aff_cls_prob(int k) { return ";
+      for (int c = 0; c + 1 < ncls; c++) o << "k == " << c << " ? " << hexd(cls_prob[c]) << " : ";
+      o << hexd(ncls ? cls_prob[ncls - 1] : 0.0) << "; }\n";
+      o << "__device__ __forceinline__ double fs_aff_cls_scale(int k) { return ";
+      for (int c = 0; c + 1 < ncls; c++) {
+        const double sc = cls_prob[c] > 0.0 ? (double)cls_nc[c] / cls_prob[c] : 0.0;
+        o << "k == " << c << " ? " << hexd(sc) << " : ";
+      }
+      {
+        const double sc = ncls && cls_prob[ncls - 1] > 0.0 ? (double)cls_nc[ncls - 1] / cls_prob[ncls - 1] : 0.0;
+        o << hexd(sc) << "; }\n";
+      }
+    }
+  }
   o << "#include \"fs_jit_kernels.cuh\"\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << K.threads << ", 1) fs_aff_frame(fs::DevProg P, fs::RunArgs A, "
        "const uint32_t* __restrict__ tbl) {\n";

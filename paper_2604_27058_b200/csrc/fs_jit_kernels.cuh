@@ -138,13 +138,21 @@ struct AffTabs {
 // one word spread over all 32 banks (shared atomics: two lanes may flip the same row).
 template <bool OFF16, bool UNIFORM>
 __device__ __forceinline__ int aff_case(const AffTabs<OFF16>& T, int site, int cls, double x) {
+#ifdef FS_AFF_CLS_CONST  // class case counts and scales as generated constants (no table loads)
+  const int nc = fs_aff_cls_nc(cls);
+#else
   const int nc = T.cls_nc[cls];
+#endif
   int c = 0;
   if (nc > 1) {
     // bisect_right(cum, x) clamped to nc - 1 == the first c < nc - 1 with x < cum[c], else nc - 1:
     // the uniform-case guess x * nc / p corrected by one step each way, exact bisect if still off
     const double* cum = T.cls_cum + cls * T.cw;
+#ifdef FS_AFF_CLS_CONST
+    c = min((int)(x * fs_aff_cls_scale(cls)), nc - 1);
+#else
     c = min((int)(x * T.cls_scale[cls]), nc - 1);
+#endif
     c -= (c > 0 && x < cum[c - 1]) ? 1 : 0;
     c += (c < nc - 1 && !(x < cum[c])) ? 1 : 0;
     // classes whose cumulative probabilities sit within one bin of the uniform grid (the host
@@ -247,7 +255,11 @@ __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<
           site = start;
           fl = cl + lane - first;
           cls = T.site_cls[site];
+#ifdef FS_AFF_CLS_CONST
+          x = u2 * fs_aff_cls_prob(cls);
+#else
           x = u2 * T.cls_prob[cls];
+#endif
         }
         cl += take;
         first += take;
@@ -269,7 +281,11 @@ __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<
           const int s = start + (int)(pos >> 5);
           const double xs = __dmul_rn(u2, __ldg(P.run_q + run));
           const int k = T.site_cls[s];
+#ifdef FS_AFF_CLS_CONST
+          if (xs < fs_aff_cls_prob(k)) {  // thinning: p_site < q
+#else
           if (xs < T.cls_prob[k]) {  // thinning: p_site < q
+#endif
             site = s;
             fl = (int)(pos & 31);
             cls = k;
@@ -329,7 +345,11 @@ __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, ui
       const int s = R.start + (pos >> 5);
       const double x = __dmul_rn(u2, R.q);
       const int k = T.site_cls[s];
+#ifdef FS_AFF_CLS_CONST  // thinning bound from the generated class constants
+      if (x < fs_aff_cls_prob(k)) {
+#else
       if (x < T.cls_prob[k]) {  // thinning: p_site < q
+#endif
         const int cs = aff_case<OFF16, UNIFORM>(T, s, k, x);
         j0 = T.off(cs);
         n = T.off(cs + 1) - j0;
