@@ -16,9 +16,7 @@
 namespace fs {
 
 // G threads per shot: G = 32 (warp per shot, several shots per CTA) or G = 256 (CTA per shot)
-constexpr int kBlockMaxGroups = 24;  // warp-per-shot groups per CTA (bounded by shared memory): static arrays
-constexpr int kBlockGroupsWide = 24; // launch bound of the k <= 9 warp-per-shot kernel (8 KB shots: 24 fit)
-constexpr int kBlockGroupsNarrow = 16;  // launch bound of the k = 10 kernel (16 KB shots: 13 fit; 128 registers)
+constexpr int kBlockMaxGroups = 16;  // warp-per-shot groups per CTA (bounded by shared memory)
 
 template <bool SPLITMIX, int G>
 struct BlockCtx {
@@ -659,10 +657,10 @@ __device__ __forceinline__ void block_run(const DevProg& P, const RunArgs& A, co
   }
 }
 
-template <bool SPLITMIX, int G, int NG = (G == 32 ? kBlockGroupsNarrow : 1)>
-// warp groups: shared memory admits one CTA per SM at the k >= 9 this form runs (13 groups of 16 KB
-// at k = 10: 128 registers per thread; 24 groups of 8 KB at k = 9: 80 registers)
-__global__ void __launch_bounds__(G == 32 ? 32 * NG : 256, G == 32 ? 1 : 4)
+template <bool SPLITMIX, int G>
+// warp groups: shared memory admits one CTA per SM at the k >= 9 this form runs (13-16 groups),
+// so the register budget is 128 per thread
+__global__ void __launch_bounds__(G == 32 ? 32 * kBlockMaxGroups : 256, G == 32 ? 1 : 4)
     block_kernel(DevProg P, RunArgs A, SegArgs S, int karr, int group_bytes) {
   block_run<SPLITMIX, G>(P, A, S, karr, group_bytes, [](BlockCtx<SPLITMIX, G>& c) { c.interpret(); });
 }

@@ -112,7 +112,6 @@ constexpr int kChunks = 4;   // max word chunks of the fault-list | frame-kernel
 struct EnvSwitches {
   bool no_affine = false;      // FS_NO_AFFINE: frame-only programs use the fault-list frame kernel
   bool block_no_jit = false;   // FS_BLOCK_NO_JIT: segmented engine interprets every segment
-  bool block_narrow = false;   // FS_BLOCK_NARROW: at most 16 warp-per-shot groups per CTA (A/B)
   bool block_jit_warp = false; // FS_BLOCK_JIT_WARP: also specialise warp-per-shot segments
   int block_k = 0;             // FS_BLOCK_K: segment k at which a shot gets a warp / CTA (0 = default)
   bool hbm_fused = false;      // FS_HBM_FUSED: fused tile passes also under FS_FORCE_HBM
@@ -124,7 +123,6 @@ struct EnvSwitches {
   void read() {
     no_affine = getenv("FS_NO_AFFINE") != nullptr;
     block_no_jit = getenv("FS_BLOCK_NO_JIT") != nullptr;
-    block_narrow = getenv("FS_BLOCK_NARROW") != nullptr;
     block_jit_warp = getenv("FS_BLOCK_JIT_WARP") != nullptr;
     if (const char* e = getenv("FS_BLOCK_K")) block_k = std::max(1, atoi(e));
     hbm_fused = getenv("FS_HBM_FUSED") != nullptr;
@@ -850,7 +848,7 @@ int launch_general_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, bool seg, 
 void gen_segment(std::ostringstream& o, const fs_prog* p, int b, int e, int karr, int G) {
   const int* IN = p->h_instrs.data();
   const int lg = G == 32 ? 5 : 8;
-  o << "extern \"C\" __global__ void __launch_bounds__(" << (G == 32 ? 32 * fs::kBlockGroupsNarrow : 256) << ", "
+  o << "extern \"C\" __global__ void __launch_bounds__(" << (G == 32 ? 32 * fs::kBlockMaxGroups : 256) << ", "
     << (G == 32 ? 1 : 4) << ") fs_seg_" << b << "(DevProg P, RunArgs A, SegArgs S, int group_bytes) {\n"
     << "  block_run<false, " << G << ">(P, A, S, " << karr << ", group_bytes, [&](BlockCtx<false, " << G
     << ">& c) {\n    double2* __restrict__ am = c.amp;\n    const uint32_t tid = (uint32_t)c.tid;\n";
@@ -1010,16 +1008,12 @@ int launch_block_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cu
   const bool warp_mode = karr <= 10;
   // as many warp groups as fit next to the static shared arrays (a k = 10 shot is ~17 KB)
   const size_t dyn_budget = 220 * 1024;
-  // wide form (24 groups, 80 registers) when more than 16 shots' arrays fit (k <= 9)
-  const bool wide = warp_mode && !p->env.block_narrow && dyn_budget / group_bytes > (size_t)fs::kBlockGroupsNarrow;
-  const int maxg = wide ? fs::kBlockGroupsWide : fs::kBlockGroupsNarrow;
-  const int ngroups = warp_mode ? (int)std::max<size_t>(1, std::min<size_t>(maxg, dyn_budget / group_bytes)) : 1;
+  const int ngroups = warp_mode ? (int)std::max<size_t>(1, std::min<size_t>(fs::kBlockMaxGroups, dyn_budget / group_bytes)) : 1;
   const int nt = warp_mode ? 32 * ngroups : 256;
   const size_t smem = group_bytes * ngroups;
   void (*kern)(fs::DevProg, fs::RunArgs, fs::SegArgs, int, int);
   const bool sm = a.flags & FS_RNG_SPLITMIX;
-  if (warp_mode && wide) kern = sm ? fs::block_kernel<true, 32, fs::kBlockGroupsWide> : fs::block_kernel<false, 32, fs::kBlockGroupsWide>;
-  else if (warp_mode) kern = sm ? fs::block_kernel<true, 32> : fs::block_kernel<false, 32>;
+  if (warp_mode) kern = sm ? fs::block_kernel<true, 32> : fs::block_kernel<false, 32>;
   else kern = sm ? fs::block_kernel<true, 256> : fs::block_kernel<false, 256>;
   FS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int occ = occupancy_blocks(kern, nt, smem);
