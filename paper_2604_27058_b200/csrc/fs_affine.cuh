@@ -43,7 +43,8 @@ namespace fsjit {
 constexpr int kAffGroup = 8;              // 32-shot words per group (one 32 B sector of every output row)
 constexpr int kAffChunk = 32 / kAffGroup;  // rows per copy-out instruction
 constexpr int kAffMaxParents = 6;         // rows a copied-out row may be rebuilt from
-constexpr int kAffMaxPairs = 15;          // warp pairs per block (one block per SM; named barriers 1..15)
+constexpr int kAffMaxPairs = 16;          // warp pairs per block (one block per SM; named barriers 0..15)
+constexpr int kAffDefaultPairs = 14;      // measured best for config 1 (below)
 // buffer slot of row r for word wi: r * G + (wi ^ sw(r)), sw(r) = (r / kAffChunk) % G (bank spread)
 inline int aff_sw(int r) { return (r / kAffChunk) % kAffGroup; }
 constexpr int kAffMaxCoins = 512;         // coin words per 32-shot word (shared memory, 2 KB per word at the limit)
@@ -200,6 +201,13 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   // to about the size of detector rows.  Rows read before the copy-out (PostSelect, observables)
   // are never differenced.
   std::vector<std::vector<int>> parents(nrows);
+  // register parents: record rows rebuilt earlier by the same thread of the copy-out (rows r and q
+  // with q = r (mod 8) fall to the same warp of the pair and the same lane row j4), whose rebuilt
+  // value is still in a register -- no shared-memory write-back or re-read (a stabilizer's record
+  // in round t against its round t-1 record: the residual is one detector's worth of faults)
+  std::vector<std::vector<int>> rparents(nrows);
+  const bool reg_parents = getenv("FS_AFF_DET_PARENTS") == nullptr && getenv("FS_AFF_ANY_PARENTS") == nullptr;
+  auto full_chunk = [&](int q) { return q >= D4 && q < D4 + U && q - q % kAffChunk + kAffChunk <= D4 + U; };
   {
     std::vector<uint8_t> fixed_row(nrows, 0);
     for (int r = U4 + D4; r < nrows; r++) fixed_row[r] = 1;
@@ -283,9 +291,11 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
             if (src < (size_t)el0) continue;
             for (int q : orows[src - el0]) {
               if (q >= r - r % kAffChunk) break;
-              // a differenced parent must be rebuilt earlier by the same warp of the pair
-              if (!fixed_row[q] && (only_fixed || (q / kAffChunk) % 2 != (r / kAffChunk) % 2)) continue;
               if (q >= U4 + D4) continue;  // observable / post-select rows: not parents
+              const bool regp = reg_parents && !fixed_row[q] && q % (2 * kAffChunk) == r % (2 * kAffChunk) &&
+                                full_chunk(q) && r >= D4 && r < D4 + U;
+              // a differenced parent must be rebuilt earlier by the same warp of the pair
+              if (!fixed_row[q] && !regp && (only_fixed || (q / kAffChunk) % 2 != (r / kAffChunk) % 2)) continue;
               if (ov[q]++ == 0) cand.push_back(q);
             }
           }
@@ -295,7 +305,9 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
         for (int q : cand) {
           const size_t dsz = csz + sz[q] - 2 * (size_t)ov[q];
           ov[q] = 0;
-          if (std::find(parents[r].begin(), parents[r].end(), q) != parents[r].end()) continue;
+          if (std::find(parents[r].begin(), parents[r].end(), q) != parents[r].end() ||
+              std::find(rparents[r].begin(), rparents[r].end(), q) != rparents[r].end())
+            continue;
           const double qc = cost2(cur, rowb.data() + (size_t)q * NW);
           if (qc < bcost) {
             bcost = qc;
@@ -304,7 +316,8 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
           }
         }
         if (best < 0) break;
-        parents[r].push_back(best);
+        if (reg_parents && !fixed_row[best]) rparents[r].push_back(best);
+        else parents[r].push_back(best);
         xr(cur, rowb.data() + (size_t)best * NW);
         csz = bsz;
         ccost = bcost;
@@ -369,10 +382,10 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
     site_cls[st] = (uint16_t)it->second;
   }
   if (cls_prob.size() >= 65535) { K.why = "too many site classes"; return K; }
+  const int ncls = (int)cls_prob.size();
   // ---- table blob (u32 words, 16 B sections): crows u16 | crow_off u16 or u32 | site_case u32 |
   // site_cls u16 | cls_nc i32 | cls_prob f64 | cls_cum f64 [ncls][cw]
   const bool off16 = crows.size() < 65536;
-  const int ncls = (int)cls_prob.size();
   auto& T = K.tables;
   auto sec = [&](size_t bytes) {
     size_t w = T.size();
@@ -464,14 +477,17 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
       ((size_t)K.nrows + psel_bits.size() + 1) * kAffGroup * 4 + 32 * 4 + (size_t)kAffGroup * cstride * 4;
   int npairs = 0;
   {
-    npairs = (int)std::min<size_t>(kAffMaxPairs, tbl_bytes < smem_budget ? (smem_budget - tbl_bytes) / per_pair : 0);
-    if (const char* e = getenv("FS_AFF_PAIRS")) npairs = std::min(npairs, std::max(1, atoi(e)));
+    // at most 14 pairs by default: config 1 measured 0.198 ms at 14 pairs (28 warps / SM), 0.201 at
+    // 16 and 0.206 at 12 (FS_AFF_PAIRS overrides, up to kAffMaxPairs)
+    const char* ep = getenv("FS_AFF_PAIRS");
+    const size_t cap = ep ? (size_t)std::max(1, std::min(kAffMaxPairs, atoi(ep))) : (size_t)kAffDefaultPairs;
+    npairs = (int)std::min<size_t>(cap, tbl_bytes < smem_budget ? (smem_budget - tbl_bytes) / per_pair : 0);
     K.tables_smem = npairs >= 4 && !getenv("FS_AFF_GLOBAL_TABLES");
-    if (!K.tables_smem) {
-      npairs = (int)std::min<size_t>(kAffMaxPairs, smem_budget / per_pair);
-      if (const char* e = getenv("FS_AFF_PAIRS")) npairs = std::min(npairs, std::max(1, atoi(e)));
-    }
+    if (!K.tables_smem) npairs = (int)std::min<size_t>(cap, smem_budget / per_pair);
     if (npairs < 1) { K.why = "row buffer does not fit shared memory"; return K; }
+    // an even pair count puts the same number of warps on each of the SM's four schedulers (the
+    // kernel is issue-bound: 15 pairs = 8/8/7/7 warps ran slower than 14 pairs = 7/7/7/7)
+    if (npairs > 1 && !ep) npairs &= ~1;
     K.threads = npairs * 64;
     K.smem = per_pair * npairs + (K.tables_smem ? tbl_bytes : 0);
   }
@@ -489,7 +505,10 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
         for (int r : v) hit[r] = 1;
       int nhit = 0, nhit_det = 0;
       for (int r = 0; r < nrows; r++) { nhit += hit[r]; if (r < D4) nhit_det += hit[r]; }
-      for (int r = 0; r < nrows; r++) npar[parents[r].size()]++;
+      for (int r = 0; r < nrows; r++) npar[std::min<size_t>(kAffMaxParents, parents[r].size() + rparents[r].size())]++;
+      int nreg = 0;
+      for (int r = 0; r < nrows; r++) nreg += (int)rparents[r].size();
+      fprintf(stderr, "aff: register parents %d\n", nreg);
       fprintf(stderr, "aff: rows with fault residual %d (detector rows %d of %d); parents histogram:", nhit, nhit_det, D);
       for (int k = 0; k <= kAffMaxParents; k++) fprintf(stderr, " %d:%d", k, npar[k]);
       fprintf(stderr, "\n");
@@ -540,6 +559,23 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   if (!getenv("FS_AFF_CLS_TABLES")) {
     if (ncls <= 4) {  // class probabilities, case counts and scales as constants (no table loads)
       o << "#define FS_AFF_CLS_CONST 1\n";
+      if (!getenv("FS_AFF_NO_SAFEZONE")) {
+        // eps(k) > max_i |cum[i] * nc / p - (i + 1)| (+ margin for the rounding of x * nc / p): a
+        // y = x * nc / p at least eps from every integer has floor(y) == bisect_right(cum, x)
+        o << "#define FS_AFF_SAFEZONE 1\n";
+        o << "__device__ __forceinline__ double fs_aff_cls_eps(int k) { return ";
+        for (int c = 0; c < ncls; c++) {
+          const double sc = cls_prob[c] > 0.0 ? (double)cls_nc[c] / cls_prob[c] : 0.0;
+          double e = 0.0;
+          for (int i = 0; i + 1 < cls_nc[c]; i++) e = std::max(e, std::fabs(cls_cum[c][i] * sc - (i + 1)));
+          e = e * 2.0 + 1e-9;
+          if (!(e < 0.25)) e = 2.0;  // not near-uniform: always the exact path
+          if (c + 1 < ncls) o << "k == " << c << " ? " << hexd(e) << " : ";
+          else o << hexd(e);
+        }
+        if (ncls == 0) o << "2.0";
+        o << "; }\n";
+      }
       o << "__device__ __forceinline__ int fs_aff_cls_nc(int k) { return ";
       for (int c = 0; c + 1 < ncls; c++) o << "k == " << c << " ? " << cls_nc[c] << " : ";
       o << (ncls ? cls_nc[ncls - 1] : 0) << "; }\n";
@@ -654,9 +690,11 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
   o << "        uint32_t* const mo = A.meas + (size_t)j4 * A.ostride + w;\n";
   o << "        uint32_t* const dout = A.det + (size_t)j4 * A.ostride + w;\n";
   o << "        const size_t sc = (size_t)" << kAffChunk << " * A.ostride;\n";
-  std::vector<uint8_t> is_parent(nrows + 1, 0);
-  for (int r = 0; r < nrows; r++)
+  std::vector<uint8_t> is_parent(nrows + 1, 0), is_rparent(nrows + 1, 0);
+  for (int r = 0; r < nrows; r++) {
     for (int q : parents[r]) is_parent[q] = 1;
+    for (int q : rparents[r]) is_rparent[q] = 1;
+  }
   int cur_half = 0;
   auto emit_copy = [&](int r0, int cnt, const char* base, int rbase) {
     const int RC = kAffChunk;
@@ -668,26 +706,50 @@ inline AffineKernelSource gen_affine_frame_kernel(const fs_prog_desc& d, const s
       size_t np = 0;
       for (int q = 0; q < rem; q++) np = std::max(np, parents[r + q].size());
       const std::string m = npsel == 0 ? "m0" : "AL[SEG[" + std::to_string(r) + " + j4] * " + std::to_string(G) + " + wi]";
-      o << "        {";
+      // a full chunk some later row uses as a register parent keeps its value in v<r>
+      bool rkeep = false;
+      for (int q = 0; q < rem && !rkeep; q++) rkeep = is_rparent[r + q];
+      const std::string V = rkeep ? "v" + std::to_string(r) : std::string("v");
+      o << "        ";
+      if (!rkeep) o << "{";
       if (rem < RC) o << " if (j4 < " << rem << ") {";
-      o << " uint32_t v = B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")];";
+      o << " uint32_t " << V << " = B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")];";
+      size_t nr = 0;
+      for (int q = 0; q < rem; q++) nr = std::max(nr, rparents[r + q].size());
+      for (size_t k = 0; k < nr; k++) {
+        const int p0 = rparents[r].size() > k ? rparents[r][k] : -1;
+        bool same = rem == RC && p0 >= 0 && p0 % RC == 0;
+        for (int q = 1; q < rem && same; q++) same = rparents[r + q].size() > k && rparents[r + q][k] == p0 + q;
+        if (same) {
+          o << " " << V << " ^= v" << p0 << ";";
+        } else {  // lane row j4 = q holds row p of chunk p - q (p = r + q mod 8)
+          o << " " << V << " ^= ";
+          for (int q = 0; q < rem; q++) {
+            const std::string x = rparents[r + q].size() > k ? "v" + std::to_string(rparents[r + q][k] - q) : "0u";
+            if (q + 1 < rem) o << "j4 == " << q << " ? " << x << " : ";
+            else o << x;
+          }
+          o << ";";
+        }
+      }
       for (size_t k = 0; k < np; k++) {
         // parents of the chunk's rows at one common offset from a chunk-aligned row: constant slots
         const int p0 = parents[r].size() > k ? parents[r][k] : -1;
         bool same = p0 >= 0 && p0 % RC == 0;
         for (int q = 1; q < rem && same; q++) same = parents[r + q].size() > k && parents[r + q][k] == p0 + q;
         if (same) {
-          o << " v ^= B[" << p0 * G << " + j4 * " << G << " + (wi ^ " << aff_sw(p0) << ")];";
+          o << " " << V << " ^= B[" << p0 * G << " + j4 * " << G << " + (wi ^ " << aff_sw(p0) << ")];";
         } else {
-          o << " v ^= B[PS" << k << "[" << r << " + j4] ^ wi];";
+          o << " " << V << " ^= B[PS" << k << "[" << r << " + j4] ^ wi];";
         }
       }
       bool wb = false;  // some later row rebuilds from one of these rows
       for (int q = 0; q < rem && !wb; q++) wb = is_parent[r + q];
-      if (np && wb) o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")] = v;";
-      o << " " << base << "[" << (r - rbase) / RC << " * sc] = v & " << m << ";";
+      if ((np || nr) && wb) o << " B[" << r * G << " + j4 * " << G << " + (wi ^ " << aff_sw(r) << ")] = " << V << ";";
+      o << " " << base << "[" << (r - rbase) / RC << " * sc] = " << V << " & " << m << ";";
       if (rem < RC) o << " }";
-      o << " }\n";
+      if (!rkeep) o << " }";
+      o << "\n";
     }
   };
   const int diag = getenv("FS_AFF_DIAG") ? atoi(getenv("FS_AFF_DIAG")) : 0;  // profiling only

@@ -149,24 +149,40 @@ __device__ __forceinline__ int aff_case(const AffTabs<OFF16>& T, int site, int c
     // the uniform-case guess x * nc / p corrected by one step each way, exact bisect if still off
     const double* cum = T.cls_cum + cls * T.cw;
 #ifdef FS_AFF_CLS_CONST
-    c = min((int)(x * fs_aff_cls_scale(cls)), nc - 1);
+    const double y = x * fs_aff_cls_scale(cls);
 #else
-    c = min((int)(x * T.cls_scale[cls]), nc - 1);
+    const double y = x * T.cls_scale[cls];
 #endif
-    c -= (c > 0 && x < cum[c - 1]) ? 1 : 0;
-    c += (c < nc - 1 && !(x < cum[c])) ? 1 : 0;
-    // classes whose cumulative probabilities sit within one bin of the uniform grid (the host
-    // checks; e.g. DEPOLARIZE1/2) are exact after the one-step correction
-    if (!UNIFORM && ((c > 0 && x < cum[c - 1]) || (c < nc - 1 && !(x < cum[c])))) {
-      int lo = 0, hi = nc;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (x < cum[mid]) hi = mid; else lo = mid + 1;
+    c = min((int)y, nc - 1);
+#ifdef FS_AFF_SAFEZONE
+    // every cum[i] * nc / p lies within eps(k) of i + 1 (host-checked, eps >= 1 for classes that do
+    // not): a y at least eps away from every integer is already exact, without table loads
+    const double fr = y - (double)(int)y;
+    if (!(fr >= fs_aff_cls_eps(cls) && fr <= 1.0 - fs_aff_cls_eps(cls)))
+#endif
+    {
+      c -= (c > 0 && x < cum[c - 1]) ? 1 : 0;
+      c += (c < nc - 1 && !(x < cum[c])) ? 1 : 0;
+      // classes whose cumulative probabilities sit within one bin of the uniform grid (the host
+      // checks; e.g. DEPOLARIZE1/2) are exact after the one-step correction
+      if (!UNIFORM && ((c > 0 && x < cum[c - 1]) || (c < nc - 1 && !(x < cum[c])))) {
+        int lo = 0, hi = nc;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (x < cum[mid]) hi = mid; else lo = mid + 1;
+        }
+        c = lo < nc - 1 ? lo : nc - 1;
       }
-      c = lo < nc - 1 ? lo : nc - 1;
     }
   }
   return (int)T.site_case[site] + c;
+}
+
+// case cs -> its row list crows[j0 .. j0 + n)
+template <bool OFF16>
+__device__ __forceinline__ void aff_case_rows(const AffTabs<OFF16>& T, int cs, uint32_t& j0, uint32_t& n) {
+  j0 = T.off(cs);
+  n = T.off(cs + 1) - j0;
 }
 
 // All lanes together (converged): lane l XORs `bit` into the n rows crows[j0 .. j0 + n) of word wi
@@ -302,11 +318,7 @@ __device__ __forceinline__ void aff_word_faults(const DevProg& P, const AffTabs<
         }
       }
       uint32_t j0 = 0, n = 0;
-      if (site >= 0) {
-        const int cs = aff_case<OFF16, UNIFORM>(T, site, cls, x);
-        j0 = T.off(cs);
-        n = T.off(cs + 1) - j0;
-      }
+      if (site >= 0) aff_case_rows(T, aff_case<OFF16, UNIFORM>(T, site, cls, x), j0, n);
       FS_AFF_ROWS<OFF16>(T, B, wi, j0, n, 1u << fl);
     }
     st += 32;
@@ -350,9 +362,7 @@ __device__ __forceinline__ void aff_word_faults_1run(const AffTabs<OFF16>& T, ui
 #else
       if (x < T.cls_prob[k]) {  // thinning: p_site < q
 #endif
-        const int cs = aff_case<OFF16, UNIFORM>(T, s, k, x);
-        j0 = T.off(cs);
-        n = T.off(cs + 1) - j0;
+        aff_case_rows(T, aff_case<OFF16, UNIFORM>(T, s, k, x), j0, n);
       }
     }
     FS_AFF_ROWS<OFF16>(T, B, wi, j0, n, 1u << (pos & 31));
@@ -390,7 +400,8 @@ __device__ __forceinline__ void aff_group_faults(const DevProg& P, const AffTabs
   }
 }
 
-// barrier of the two warps of pair `id` (named barriers 1..15; 0 is __syncthreads)
-__device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id + 1) : "memory"); }
+// barrier of the two warps of pair `id` (named barriers 0..15; barrier 0 serves the block-wide
+// __syncthreads of the table load only before any pair uses it)
+__device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
 }  // namespace fs

@@ -47,7 +47,7 @@ int set_error(int code, const std::string& msg) {
   } while (0)
 
 constexpr size_t kSmemBudget = 200 * 1024;  // per block, leaves room for L1
-constexpr size_t kAffSmemBudget = 208 * 1024;  // affine frame kernel: row buffers of one block per SM
+constexpr size_t kAffSmemBudget = 224 * 1024;  // affine frame kernel: row buffers of one block per SM
 
 // every entry point runs on the device the program was created on (its allocations and NVRTC
 // modules live in that device's primary context), whatever device the calling thread has current

@@ -176,12 +176,14 @@ def test_gpu_jit_equals_interpreter(cuda, name, monkeypatch):
                                   "aff_many_coins"])
 @pytest.mark.parametrize("env", [{}, {"FS_AFF_GLOBAL_TABLES": "1"}, {"FS_AFF_PAIRS": "1"}, {"FS_AFF_NONUNIFORM": "1"},
                                  {"FS_AFF_NO_DIFF": "1"}, {"FS_AFF_PARENTS": "1"}, {"FS_AFF_ANY_PARENTS": "1"},
-                                 {"FS_AFF_BALANCED": "1"}, {"FS_AFF_CLS_TABLES": "1"}])
+                                 {"FS_AFF_BALANCED": "1"}, {"FS_AFF_CLS_TABLES": "1"}, {"FS_AFF_DET_PARENTS": "1"},
+                                 {"FS_AFF_PAIRS": "16"}, {"FS_AFF_NO_SAFEZONE": "1"}])
 @pytest.mark.parametrize("n", [3 * 256 + 37, 3 * 256 + 69])  # even / odd output stride (26 / 27 words)
 def test_gpu_affine_variants_match_oracle(cuda, name, env, n, monkeypatch):
     """Affine frame kernel variants (fault tables in global memory, one warp pair per block, the
-    exact-bisect case pick, no / single-parent row differencing, load-balanced row loop, class
-    parameters from tables instead of constants) == oracle,
+    exact-bisect case pick, no / single-parent / detector-only / any-row differencing, load-balanced
+    row loop, class parameters from tables instead of constants, 16 pairs = named barrier 0, case
+    pick always through the cumulative table) == oracle,
     bit for bit; odd shot counts and an offset so the tail word, partial groups and an odd output
     stride are exercised."""
     for k, v in env.items():
