@@ -285,6 +285,78 @@ struct BlockCtx {
     bar();
   }
 
+  // v * i^p
+  static __device__ __forceinline__ double2 rot4(double2 v, uint32_t p) {
+    const double x = (p & 1u) ? v.y : v.x, y = (p & 1u) ? v.x : v.y;
+    return make_double2(((p + 1u) & 2u) ? -x : x, (p & 2u) ? -y : y);
+  }
+
+  // A star group (fs_sampler.cu fs_program_create): the ArrayGates CX(a, .), CZ(a, .), S / S_DAG(a),
+  // [H(a)], [ArrayRot] of a localisation run in one sweep.  Elements with bit a clear stay; element
+  // j with bit a set becomes i^(pw + 2 parity(j & Mz)) * old[j ^ M]; then H on a, then the
+  // ArrayRot phases.  The group's frame matrix has been applied (ArrayRot reads the parity after it).
+  __device__ __forceinline__ void star_group(int a, uint32_t M, uint32_t Mz, uint32_t pw, bool hasH, bool hasAR,
+                                             int ar_virt, int ar_axis, int ar_fp, uint32_t size) {
+    const uint32_t A_ = 1u << a;
+    double2 ph0 = make_double2(1.0, 0.0), ph1 = ph0;
+    if (hasAR) {
+      double2 e0, e1;
+      parity_phases(ar_virt, ar_fp, 0, e0, e1);
+      const int par = fx[ar_virt] & 1;
+      ph0 = par ? e1 : e0;
+      ph1 = par ? e0 : e1;
+    }
+    auto hiphase = [&](uint32_t id, double2 v) { return rot4(v, pw + 2u * ((uint32_t)__popc(id & Mz) & 1u)); };
+    auto finish = [&](uint32_t i0, double2 lo, double2 hi) {  // lo at i0, hi at i0 | A_
+      if (hasH) {
+        const double2 s = cscale(cadd(lo, hi), kInvSqrt2), d = cscale(csub(lo, hi), kInvSqrt2);
+        lo = s;
+        hi = d;
+      }
+      if (hasAR) {
+        lo = cmul(lo, ((i0 >> ar_axis) & 1u) ? ph1 : ph0);
+        hi = cmul(hi, (((i0 | A_) >> ar_axis) & 1u) ? ph1 : ph0);
+      }
+      amp[i0] = lo;
+      amp[i0 | A_] = hi;
+    };
+    const bool touch_lo = hasH || hasAR;
+    if (M == 0u) {
+      for (uint32_t j = tid; j < size / 2; j += G) {
+        const uint32_t i0 = ins0(j, a);
+        const double2 hi = hiphase(i0 | A_, amp[i0 | A_]);
+        if (touch_lo) finish(i0, amp[i0], hi);
+        else amp[i0 | A_] = hi;
+      }
+    } else {
+      const int m = __ffs((int)M) - 1;
+      const int lo_ax = a < m ? a : m, hi_ax = a < m ? m : a;
+      for (uint32_t j = tid; j < size / 4; j += G) {
+        const uint32_t i0 = ins0(ins0(j, lo_ax), hi_ax), i1 = i0 ^ M;  // bit a clear in both
+        const double2 h0 = amp[i1 | A_], h1 = amp[i0 | A_];
+        const double2 n0 = hiphase(i0 | A_, h0), n1 = hiphase(i1 | A_, h1);
+        if (touch_lo) {
+          finish(i0, amp[i0], n0);
+          finish(i1, amp[i1], n1);
+        } else {
+          amp[i0 | A_] = n0;
+          amp[i1 | A_] = n1;
+        }
+      }
+    }
+    bar();
+  }
+
+  // group gi of the descriptor table: its frame matrix, then the sweep
+  __device__ __forceinline__ int run_group(int gi) {
+    const int4 D0 = __ldg(reinterpret_cast<const int4*>(P.fuse) + 2 * gi);
+    const int4 D1 = __ldg(reinterpret_cast<const int4*>(P.fuse) + 2 * gi + 1);
+    frame_matrix(D1.w);
+    star_group(D0.y & 0xFF, (uint32_t)D0.z, (uint32_t)D0.w, (uint32_t)D1.x & 3u, (D1.x & 4) != 0, (D1.x & 8) != 0,
+               D1.y & 0xFFFF, D1.y >> 16, D1.z, 1u << (D0.y >> 8));
+    return D0.x;
+  }
+
   // fixed-order tree: element t += element t + w for w = G/2 .. 1 (same pairs either way)
   __device__ __forceinline__ void reduce2(double& s1, double& sa) {
     if (G == 32) {
@@ -484,7 +556,12 @@ struct BlockCtx {
       const int flip = FS_FLIP(I0.x);
       switch (op) {
         case FS_OP_FRAME: frame_matrix(__ldg(P.frame_mat_off + i)); break;  // next_array stops here only with a matrix
-        case FS_OP_ARRAY_GATE: gate(ins[1], ins[2], ins[3], ins[4], ins[5], 1u << ins[6]); break;
+        case FS_OP_ARRAY_GATE: {
+          const int gi = S.fuse ? __ldg(P.fuse_at + i) : -1;
+          if (gi >= 0) i += run_group(gi) - 1;
+          else gate(ins[1], ins[2], ins[3], ins[4], ins[5], 1u << ins[6]);
+          break;
+        }
         case FS_OP_EXPAND: expand(ins[1], ins[5], 1u << ins[6]); break;
         case FS_OP_ARRAY_ROT: array_rot(ins[1], ins[2], ins[5], 1u << ins[6]); break;
         case FS_OP_MEAS_ACTIVE:

@@ -57,6 +57,10 @@ struct DevProg {
   // v = (x_0..x_{n-1}, z_0..z_{n-1}) to v' with v'_r = parity(row_r & v); rows are 4 words
   const uint32_t* __restrict__ frame_mat;
   const int* __restrict__ frame_mat_off;  // [N] word offset of instruction i's rows, -1 if none
+  // star groups (block engine, fs_sampler.cu fs_program_create): fuse_at[i] = group starting at
+  // ArrayGate i or -1; fuse = 8-word descriptors
+  const int* __restrict__ fuse_at;
+  const int* __restrict__ fuse;
 };
 
 struct RunArgs {

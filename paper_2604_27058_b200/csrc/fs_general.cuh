@@ -244,6 +244,7 @@ struct SegArgs {
   StateStore in, out;
   int k_in, k_out;         // active dimension at the segment boundaries
   int nfw, nsw, now;
+  int fuse;                // block engine: star groups enabled (no checkpoint falls inside one)
 };
 
 template <bool SPLITMIX, bool ARR_SMEM, bool SEG>

@@ -113,6 +113,7 @@ struct EnvSwitches {
   bool no_affine = false;      // FS_NO_AFFINE: frame-only programs use the fault-list frame kernel
   bool block_no_jit = false;   // FS_BLOCK_NO_JIT: segmented engine interprets every segment
   bool block_jit_warp = false; // FS_BLOCK_JIT_WARP: also specialise warp-per-shot segments
+  bool block_no_fuse = false;  // FS_BLOCK_NO_FUSE: block engine runs ArrayGates one sweep each (no star groups)
   int block_k = 0;             // FS_BLOCK_K: segment k at which a shot gets a warp / CTA (0 = default)
   bool hbm_fused = false;      // FS_HBM_FUSED: fused tile passes also under FS_FORCE_HBM
   bool hbm_unfused = false;    // FS_HBM_UNFUSED: per-instruction large-k kernels only
@@ -124,6 +125,7 @@ struct EnvSwitches {
     no_affine = getenv("FS_NO_AFFINE") != nullptr;
     block_no_jit = getenv("FS_BLOCK_NO_JIT") != nullptr;
     block_jit_warp = getenv("FS_BLOCK_JIT_WARP") != nullptr;
+    block_no_fuse = getenv("FS_BLOCK_NO_FUSE") != nullptr;
     if (const char* e = getenv("FS_BLOCK_K")) block_k = std::max(1, atoi(e));
     hbm_fused = getenv("FS_HBM_FUSED") != nullptr;
     hbm_unfused = getenv("FS_HBM_UNFUSED") != nullptr;
@@ -211,7 +213,7 @@ struct fs_prog {
   std::string pass_jit_err;
   // program-specialised segment kernels of the block engine (key: segment begin), Philox stream
   int seg_jit = 0;
-  std::vector<int32_t> h_next_array, h_frame_mat_off;
+  std::vector<int32_t> h_next_array, h_frame_mat_off, h_fuse_at, h_fuse;
   std::map<int, fsjit::CUfunction> seg_fn;
   std::string seg_jit_err;
   void* d_cp = nullptr;  // checkpoint instruction counts + amplitude offsets of the current call
@@ -302,43 +304,123 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   const bool mats = n2 <= 128 && d->k_max > 0;
   std::vector<uint32_t> frame_mat;
   std::vector<int32_t> frame_mat_off(d->num_instrs + 1, -1);
-  if (mats) {
+  // one frame gate on a 0/1 vector (fx = v, fz = v + n)
+  auto frame_gate = [&](uint32_t* fx, uint32_t* fz, int g, int a, int b) {
+    uint32_t tt;
+    switch (g) {
+      case FS_G_H: tt = fx[a]; fx[a] = fz[a]; fz[a] = tt; break;
+      case FS_G_S: case FS_G_SDAG: fz[a] ^= fx[a]; break;
+      case FS_G_CX: fx[b] ^= fx[a]; fz[a] ^= fz[b]; break;
+      case FS_G_CZ: fz[b] ^= fx[a]; fz[a] ^= fx[b]; break;
+      case FS_G_SWAP:
+        tt = fx[a]; fx[a] = fx[b]; fx[b] = tt;
+        tt = fz[a]; fz[a] = fz[b]; fz[b] = tt;
+        break;
+      default: break;
+    }
+  };
+  // the frame action of instructions [i0, i1) (FrameGates lists and the frame side of ArrayGates)
+  // as one matrix appended to frame_mat; returns its word offset
+  auto build_matrix = [&](int i0, int i1) {
+    const int32_t off = (int32_t)frame_mat.size();
+    frame_mat.resize(frame_mat.size() + (size_t)n2 * 4, 0u);
     std::vector<uint32_t> v(n2);
-    for (int i = 0; i < d->num_instrs; i++) {
-      const int* I = d->instrs + (size_t)i * FS_INS_WORDS;
-      if (FS_OPCODE(I[0]) != FS_OP_FRAME) continue;
-      frame_mat_off[i] = (int32_t)frame_mat.size();
-      frame_mat.resize(frame_mat.size() + (size_t)n2 * 4, 0u);
-      uint32_t* M = frame_mat.data() + frame_mat_off[i];
-      for (int j = 0; j < n2; j++) {
-        std::fill(v.begin(), v.end(), 0u);
-        v[j] = 1u;
-        uint32_t* fx = v.data();
-        uint32_t* fz = v.data() + d->n;
-        for (int t = 0; t < I[2]; t++) {
-          const uint32_t g = d->gates[I[1] + t];
-          const int a = FS_GATE_A(g), b = FS_GATE_B(g);
-          uint32_t tt;
-          switch (FS_GATE_G(g)) {
-            case FS_G_H: tt = fx[a]; fx[a] = fz[a]; fz[a] = tt; break;
-            case FS_G_S: case FS_G_SDAG: fz[a] ^= fx[a]; break;
-            case FS_G_CX: fx[b] ^= fx[a]; fz[a] ^= fz[b]; break;
-            case FS_G_CZ: fz[b] ^= fx[a]; fz[a] ^= fx[b]; break;
-            case FS_G_SWAP:
-              tt = fx[a]; fx[a] = fx[b]; fx[b] = tt;
-              tt = fz[a]; fz[a] = fz[b]; fz[b] = tt;
-              break;
-            default: break;
+    for (int j = 0; j < n2; j++) {
+      std::fill(v.begin(), v.end(), 0u);
+      v[j] = 1u;
+      for (int i = i0; i < i1; i++) {
+        const int* I = d->instrs + (size_t)i * FS_INS_WORDS;
+        const int op = FS_OPCODE(I[0]);
+        if (op == FS_OP_FRAME) {
+          for (int t = 0; t < I[2]; t++) {
+            const uint32_t g = d->gates[I[1] + t];
+            frame_gate(v.data(), v.data() + d->n, FS_GATE_G(g), FS_GATE_A(g), FS_GATE_B(g));
           }
+        } else if (op == FS_OP_ARRAY_GATE) {
+          frame_gate(v.data(), v.data() + d->n, I[1], I[2], I[3]);
         }
-        for (int r = 0; r < n2; r++)
-          if (v[r] & 1u) M[(size_t)r * 4 + (j >> 5)] |= 1u << (j & 31);
       }
+      uint32_t* M = frame_mat.data() + off;
+      for (int r = 0; r < n2; r++)
+        if (v[r] & 1u) M[(size_t)r * 4 + (j >> 5)] |= 1u << (j & 31);
+    }
+    return off;
+  };
+  if (mats)
+    for (int i = 0; i < d->num_instrs; i++)
+      if (FS_OPCODE(d->instrs[(size_t)i * FS_INS_WORDS]) == FS_OP_FRAME) frame_mat_off[i] = build_matrix(i, i + 1);
+  // Star groups (block engine): a run of ArrayGates that all act through one pivot axis a --
+  // CX(a, b), CZ(a, c), S / S_DAG(a), then at most one H(a) -- with FrameGates in between and an
+  // optional closing ArrayRot is one sweep: elements with bit a clear keep their place, element j
+  // with bit a set becomes i^(ns + 2 (parity(j & Mz) ^ s0)) * old[j ^ M]; then the H butterfly on
+  // a and the ArrayRot phases.  The same values as the per-instruction sweeps (permutations, sign
+  // flips and multiplications by +-i are exact), one pass over the array instead of one per gate.
+  // Descriptor (8 words): len, a | k << 8, M, Mz, power | hasH << 2 | hasAR << 3,
+  // ar_virt | ar_axis << 16, ar_fp, frame matrix offset.
+  std::vector<int32_t> fuse_at(d->num_instrs + 1, -1), fuse;
+  if (mats && !p->env.block_no_fuse) {
+    for (int i = 0; i < d->num_instrs;) {
+      const int* I0 = d->instrs + (size_t)i * FS_INS_WORDS;
+      if (FS_OPCODE(I0[0]) != FS_OP_ARRAY_GATE) { i++; continue; }
+      int pivot = -1, narr = 0, end = i, ar = -1;
+      uint32_t M = 0, Mz = 0, ns = 0;
+      bool hasH = false;
+      std::vector<std::pair<int, uint32_t>> czs;  // (other axis, M at that time)
+      const int k = I0[6];
+      for (int t = i; t < d->num_instrs; t++) {
+        const int* I = d->instrs + (size_t)t * FS_INS_WORDS;
+        const int op = FS_OPCODE(I[0]);
+        if (op == FS_OP_FRAME) continue;  // absorbed if an array instruction of the group follows
+        if (op == FS_OP_ARRAY_ROT) {
+          if (I[6] == k && narr > 0) { ar = t; end = t + 1; narr++; }
+          break;
+        }
+        if (op != FS_OP_ARRAY_GATE || I[6] != k || hasH) break;
+        const int g = I[1], a = I[4], b = I[5];
+        bool ok = true;
+        if (g == FS_G_S || g == FS_G_SDAG || g == FS_G_H) {
+          if (pivot < 0) pivot = a;
+          if (a != pivot) ok = false;
+          else if (g == FS_G_H) hasH = true;
+          else ns = (ns + (g == FS_G_S ? 1u : 3u)) & 3u;
+        } else if (g == FS_G_CX) {
+          if (pivot < 0) pivot = a;
+          if (a != pivot || b == pivot) ok = false;
+          else M ^= 1u << b;
+        } else if (g == FS_G_CZ) {
+          if (pivot < 0) pivot = a;
+          const int other = a == pivot ? b : (b == pivot ? a : -1);
+          if (other < 0 || other == pivot) ok = false;
+          else { Mz ^= 1u << other; czs.push_back({other, M}); }
+        } else {
+          ok = false;
+        }
+        if (!ok) break;
+        narr++;
+        end = t + 1;
+      }
+      if (narr < 2) { i++; continue; }
+      uint32_t s0 = 0;
+      for (auto& cz : czs) s0 ^= ((M ^ cz.second) >> cz.first) & 1u;
+      const int* IA = ar >= 0 ? d->instrs + (size_t)ar * FS_INS_WORDS : nullptr;
+      fuse_at[i] = (int32_t)(fuse.size() / 8);
+      fuse.push_back(end - i);
+      fuse.push_back(pivot | (k << 8));
+      fuse.push_back((int32_t)M);
+      fuse.push_back((int32_t)Mz);
+      fuse.push_back((int32_t)(((ns + 2u * s0) & 3u) | (hasH ? 4u : 0u) | (ar >= 0 ? 8u : 0u)));
+      fuse.push_back(IA ? (IA[1] | (IA[2] << 16)) : 0);
+      fuse.push_back(IA ? IA[5] : 0);
+      fuse.push_back(build_matrix(i, end));
+      i = end;
     }
   }
+  if (fuse.empty()) fuse.assign(8, 0);
   if (frame_mat.empty()) frame_mat.push_back(0u);
   size_t o_fm = add(frame_mat.data(), sizeof(uint32_t) * frame_mat.size());
   size_t o_fmo = add(frame_mat_off.data(), sizeof(int32_t) * frame_mat_off.size());
+  size_t o_fat = add(fuse_at.data(), sizeof(int32_t) * fuse_at.size());
+  size_t o_fus = add(fuse.data(), sizeof(int32_t) * fuse.size());
   std::vector<int32_t> next_array(d->num_instrs + 1, d->num_instrs);
   for (int i = d->num_instrs - 1; i >= 0; i--) {
     const int op = FS_OPCODE(d->instrs[(size_t)i * FS_INS_WORDS]);
@@ -390,6 +472,10 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   p->h_next_array = next_array;
   p->h_frame_mat_off = frame_mat_off;
   dp.frame_mat_off = reinterpret_cast<const int*>(b + o_fmo);
+  dp.fuse_at = reinterpret_cast<const int*>(b + o_fat);
+  dp.fuse = reinterpret_cast<const int*>(b + o_fus);
+  p->h_fuse_at = fuse_at;
+  p->h_fuse = fuse;
   p->h_instrs.assign(d->instrs, d->instrs + (size_t)FS_INS_WORDS * d->num_instrs);
   p->h_sched.assign(d->schedule, d->schedule + d->num_instrs);
   if (d->num_fparams) p->h_fparams.assign(d->fparams, d->fparams + d->num_fparams);
@@ -870,6 +956,15 @@ void gen_segment(std::ostringstream& o, const fs_prog* p, int b, int e, int karr
     const int* I = IN + (size_t)i * FS_INS_WORDS;
     const int op = FS_OPCODE(I[0]), flip = FS_FLIP(I[0]);
     const uint32_t size = 1u << I[6];
+    if (op == FS_OP_ARRAY_GATE && p->h_fuse_at[i] >= 0) {  // a star group: frame matrix + one sweep
+      const int32_t* Dg = p->h_fuse.data() + (size_t)8 * p->h_fuse_at[i];
+      o << "    {  // " << i << " .. " << i + Dg[0] << "\n      c.frame_matrix(" << Dg[7] << ");\n      c.star_group("
+        << (Dg[1] & 0xFF) << ", " << (uint32_t)Dg[2] << "u, " << (uint32_t)Dg[3] << "u, " << (Dg[4] & 3) << "u, "
+        << ((Dg[4] & 4) ? "true" : "false") << ", " << ((Dg[4] & 8) ? "true" : "false") << ", " << (Dg[5] & 0xFFFF) << ", "
+        << (Dg[5] >> 16) << ", " << Dg[6] << ", " << size << "u);\n    }\n";
+      i += Dg[0];
+      continue;
+    }
     o << "    {  // " << i << "\n";
     switch (op) {
       case FS_OP_FRAME:
@@ -1091,6 +1186,12 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   S.nfw = (2 * dp.n + 31) / 32;
   S.nsw = (dp.num_slots + 31) / 32;
   S.now = (dp.O + 31) / 32;
+  // star groups run fused unless a checkpoint asks for the state inside one
+  S.fuse = 1;
+  if (a.ncp)
+    for (int c : p->cp_list)
+      for (int i = 0; i < dp.num_instrs; i++)
+        if (p->h_fuse_at[i] >= 0 && c > i && c < i + p->h_fuse[(size_t)8 * p->h_fuse_at[i]]) S.fuse = 0;
   const uint64_t chunk = (uint64_t)1 << 22;
   if (!p->d_counts) FS_CUDA_TRY(cudaMalloc(&p->d_counts, 64));
   uint32_t* d_nout = reinterpret_cast<uint32_t*>(p->d_counts);
