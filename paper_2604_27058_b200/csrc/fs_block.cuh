@@ -285,18 +285,19 @@ struct BlockCtx {
     bar();
   }
 
-  // v * i^p
-  static __device__ __forceinline__ double2 rot4(double2 v, uint32_t p) {
-    const double x = (p & 1u) ? v.y : v.x, y = (p & 1u) ? v.x : v.y;
-    return make_double2(((p + 1u) & 2u) ? -x : x, (p & 2u) ? -y : y);
+  // x with its sign bit flipped where m has bit 31 set
+  static __device__ __forceinline__ double flipsign(double x, uint32_t m) {
+    return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
   }
 
   // A star group (fs_sampler.cu fs_program_create): the ArrayGates CX(a, .), CZ(a, .), S / S_DAG(a),
   // [H(a)], [ArrayRot] of a localisation run in one sweep.  Elements with bit a clear stay; element
   // j with bit a set becomes i^(pw + 2 parity(j & Mz)) * old[j ^ M]; then H on a, then the
   // ArrayRot phases.  The group's frame matrix has been applied (ArrayRot reads the parity after it).
-  __device__ __forceinline__ void star_group(int a, uint32_t M, uint32_t Mz, uint32_t pw, bool hasH, bool hasAR,
-                                             int ar_virt, int ar_axis, int ar_fp, uint32_t size) {
+  // SWAP = pw odd (the factor is +-i: real and imaginary parts trade places).
+  template <bool SWAP>
+  __device__ __forceinline__ void star_group_t(int a, uint32_t M, uint32_t Mz, uint32_t pw, bool hasH, bool hasAR,
+                                               int ar_virt, int ar_axis, int ar_fp, uint32_t size) {
     const uint32_t A_ = 1u << a;
     double2 ph0 = make_double2(1.0, 0.0), ph1 = ph0;
     if (hasAR) {
@@ -306,7 +307,12 @@ struct BlockCtx {
       ph0 = par ? e1 : e0;
       ph1 = par ? e0 : e1;
     }
-    auto hiphase = [&](uint32_t id, double2 v) { return rot4(v, pw + 2u * ((uint32_t)__popc(id & Mz) & 1u)); };
+    // v * i^(pw + 2 par): the x sign flips iff par ^ (pw in {1, 2}), the y sign iff par ^ (pw >= 2)
+    const uint32_t cx = (pw == 1u || pw == 2u) ? 0x80000000u : 0u, cy = pw >= 2u ? 0x80000000u : 0u;
+    auto hiphase = [&](uint32_t id, double2 v) {
+      const uint32_t sg = (uint32_t)__popc(id & Mz) << 31;
+      return make_double2(flipsign(SWAP ? v.y : v.x, sg ^ cx), flipsign(SWAP ? v.x : v.y, sg ^ cy));
+    };
     auto finish = [&](uint32_t i0, double2 lo, double2 hi) {  // lo at i0, hi at i0 | A_
       if (hasH) {
         const double2 s = cscale(cadd(lo, hi), kInvSqrt2), d = cscale(csub(lo, hi), kInvSqrt2);
@@ -345,6 +351,11 @@ struct BlockCtx {
       }
     }
     bar();
+  }
+  __device__ __forceinline__ void star_group(int a, uint32_t M, uint32_t Mz, uint32_t pw, bool hasH, bool hasAR,
+                                             int ar_virt, int ar_axis, int ar_fp, uint32_t size) {
+    if (pw & 1u) star_group_t<true>(a, M, Mz, pw, hasH, hasAR, ar_virt, ar_axis, ar_fp, size);
+    else star_group_t<false>(a, M, Mz, pw, hasH, hasAR, ar_virt, ar_axis, ar_fp, size);
   }
 
   // group gi of the descriptor table: its frame matrix, then the sweep
@@ -649,12 +660,18 @@ __device__ __forceinline__ void block_run(const DevProg& P, const RunArgs& A, co
       if (tid == 0) amp[0] = make_double2(1.0, 0.0);
     } else {
       const StateStore& I = S.in;
+      // the array goes global -> shared asynchronously (16 B per request, no register staging)
+      // while the frame bits and the scalar state load
+      const uint32_t sz = 1u << S.k_in, icap = 1u << S.k_in;
+      for (uint32_t j = tid; j < sz; j += G) {
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(amp + j);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(I.amps + store_amp_index(idx, j, icap, I.shot_major)) : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
       for (int b = tid; b < 2 * P.n; b += G) fx[b] = (I.frame[(size_t)idx * S.nfw + (b >> 5)] >> (b & 31)) & 1u;
       for (int b = tid; b < P.num_slots; b += G)
         c.slots[b] = (I.slotbits[(size_t)idx * S.nsw + (b >> 5)] >> (b & 31)) & 1u;
       for (int b = tid; b < P.O; b += G) c.obsb[b] = (I.obsbits[(size_t)idx * S.now + (b >> 5)] >> (b & 31)) & 1u;
-      const uint32_t sz = 1u << S.k_in, icap = 1u << S.k_in;
-      for (uint32_t j = tid; j < sz; j += G) amp[j] = I.amps[store_amp_index(idx, j, icap, I.shot_major)];
       if (tid == 0) {
         c.gamma = I.gamma[idx];
         if (SPLITMIX) c.sm.count = I.smcount[idx];
@@ -668,6 +685,7 @@ __device__ __forceinline__ void block_run(const DevProg& P, const RunArgs& A, co
           c.gen.c = I.gen_c[idx];
         }
       }
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     c.bar();
     exec(c);
