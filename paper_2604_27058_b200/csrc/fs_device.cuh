@@ -61,6 +61,8 @@ struct DevProg {
   // ArrayGate i or -1; fuse = 8-word descriptors
   const int* __restrict__ fuse_at;
   const int* __restrict__ fuse;
+  // per-case frame masks, 4 words each (x_q at bit q, z_q at bit n + q); NULL when 2n > 128
+  const uint4* __restrict__ case_mask;
 };
 
 struct RunArgs {

@@ -113,6 +113,7 @@ struct EnvSwitches {
   bool no_affine = false;      // FS_NO_AFFINE: frame-only programs use the fault-list frame kernel
   bool block_no_jit = false;   // FS_BLOCK_NO_JIT: segmented engine interprets every segment
   bool block_jit_warp = false; // FS_BLOCK_JIT_WARP: also specialise warp-per-shot segments
+  bool block_no_wjit = false;  // FS_BLOCK_NO_WJIT: warp-per-shot segments keep the interpreter (no fs_wseg.cuh kernels)
   bool block_no_fuse = false;  // FS_BLOCK_NO_FUSE: block engine runs ArrayGates one sweep each (no star groups)
   int block_k = 0;             // FS_BLOCK_K: segment k at which a shot gets a warp / CTA (0 = default)
   bool hbm_fused = false;      // FS_HBM_FUSED: fused tile passes also under FS_FORCE_HBM
@@ -126,6 +127,7 @@ struct EnvSwitches {
     block_no_jit = getenv("FS_BLOCK_NO_JIT") != nullptr;
     block_jit_warp = getenv("FS_BLOCK_JIT_WARP") != nullptr;
     block_no_fuse = getenv("FS_BLOCK_NO_FUSE") != nullptr;
+    block_no_wjit = getenv("FS_BLOCK_NO_WJIT") != nullptr;
     if (const char* e = getenv("FS_BLOCK_K")) block_k = std::max(1, atoi(e));
     hbm_fused = getenv("FS_HBM_FUSED") != nullptr;
     hbm_unfused = getenv("FS_HBM_UNFUSED") != nullptr;
@@ -416,11 +418,25 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
     }
   }
   if (fuse.empty()) fuse.assign(8, 0);
+  // per-case frame masks (x_q at bit q, z_q at bit n + q) for the packed-frame segment kernels
+  std::vector<uint32_t> case_mask;
+  if (mats && d->num_cases > 0) {
+    case_mask.assign((size_t)4 * d->num_cases, 0u);
+    for (int c = 0; c < d->num_cases; c++)
+      for (int j = d->case_pauli_off[c]; j < d->case_pauli_off[c + 1]; j++) {
+        const uint32_t en = d->paulis[j];
+        const int bit = FS_PAULI_Z(en) ? d->n + (int)FS_PAULI_Q(en) : (int)FS_PAULI_Q(en);
+        case_mask[(size_t)4 * c + (bit >> 5)] ^= 1u << (bit & 31);
+      }
+  }
+  const bool have_masks = mats;
+  if (case_mask.empty()) case_mask.assign(4, 0u);
   if (frame_mat.empty()) frame_mat.push_back(0u);
   size_t o_fm = add(frame_mat.data(), sizeof(uint32_t) * frame_mat.size());
   size_t o_fmo = add(frame_mat_off.data(), sizeof(int32_t) * frame_mat_off.size());
   size_t o_fat = add(fuse_at.data(), sizeof(int32_t) * fuse_at.size());
   size_t o_fus = add(fuse.data(), sizeof(int32_t) * fuse.size());
+  size_t o_cm = add(case_mask.data(), sizeof(uint32_t) * case_mask.size());
   std::vector<int32_t> next_array(d->num_instrs + 1, d->num_instrs);
   for (int i = d->num_instrs - 1; i >= 0; i--) {
     const int op = FS_OPCODE(d->instrs[(size_t)i * FS_INS_WORDS]);
@@ -474,6 +490,7 @@ extern "C" int fs_program_create(const fs_prog_desc* d, fs_prog** out) {
   dp.frame_mat_off = reinterpret_cast<const int*>(b + o_fmo);
   dp.fuse_at = reinterpret_cast<const int*>(b + o_fat);
   dp.fuse = reinterpret_cast<const int*>(b + o_fus);
+  dp.case_mask = have_masks ? reinterpret_cast<const uint4*>(b + o_cm) : nullptr;
   p->h_fuse_at = fuse_at;
   p->h_fuse = fuse;
   p->h_instrs.assign(d->instrs, d->instrs + (size_t)FS_INS_WORDS * d->num_instrs);
@@ -762,6 +779,8 @@ extern "C" const char* fs_debug_jit_status(fs_prog* p) {
                         : (p->jit_state == 0 ? "not built" : "failed: " + p->jit_error);
   s += p->aff_state == 1 ? "; affine: ready threads=" + std::to_string(p->aff_threads)
                          : (p->aff_state == 0 ? "; affine: not built" : "; affine: n/a (" + p->aff_error + ")");
+  s += p->seg_jit == 1 ? "; segments: ready kernels=" + std::to_string(p->seg_fn.size())
+                       : (p->seg_jit == 0 ? "; segments: not built" : "; segments: failed (" + p->seg_jit_err + ")");
   return s.c_str();
 }
 
@@ -1046,13 +1065,143 @@ void gen_segment(std::ostringstream& o, const fs_prog* p, int b, int e, int karr
   o << "  });\n}\n";
 }
 
+// Warp-per-shot segments fully specialised (fs_wseg.cuh): scalar instructions included, the frame
+// bit-packed in registers.  Needs 2n <= 128 (frame matrices, case masks), <= 32 slots / observables.
+bool wseg_supported(const fs_prog* p) {
+  return 2 * p->dp.n <= 128 && p->dp.num_slots <= 32 && p->dp.O <= 32 && p->dp.case_mask != nullptr;
+}
+
+void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int karr) {
+  const int* IN = p->h_instrs.data();
+  const int n = p->dp.n, R = p->dp.R;
+  auto C = [&](int off) {
+    return "make_double2(" + fsjit::hexd(p->h_fparams[off]) + ", " + fsjit::hexd(p->h_fparams[off + 1]) + ")";
+  };
+  auto slot_of = [&](int bit) { return p->h_bit_slot[bit]; };
+  // mask words of a Pauli list
+  auto mask_of = [&](int off, int cnt, uint32_t m[4]) {
+    m[0] = m[1] = m[2] = m[3] = 0u;
+    for (int j = off; j < off + cnt; j++) {
+      const uint32_t en = p->h_paulis[j];
+      const int bit = FS_PAULI_Z(en) ? n + (int)FS_PAULI_Q(en) : (int)FS_PAULI_Q(en);
+      m[bit >> 5] ^= 1u << (bit & 31);
+    }
+  };
+  auto frame_gate = [&](int g, int va, int vb) {
+    switch (g) {
+      case FS_G_S: case FS_G_SDAG: o << "    c.g_s(" << va << ", " << n + va << ");\n"; break;
+      case FS_G_H: o << "    c.g_h(" << va << ", " << n + va << ");\n"; break;
+      case FS_G_CX: o << "    c.g_cx(" << va << ", " << n + va << ", " << vb << ", " << n + vb << ");\n"; break;
+      case FS_G_CZ: o << "    c.g_cz(" << va << ", " << n + va << ", " << vb << ", " << n + vb << ");\n"; break;
+      default: break;
+    }
+  };
+  o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * fs::kBlockMaxGroups << ", 1) fs_seg_" << b
+    << "(DevProg P, RunArgs A, SegArgs S, int group_bytes) {\n  wseg_run(P, A, S, group_bytes, [&](WCtx& c) {\n";
+  for (int i = b; i < e;) {
+    const int* I = IN + (size_t)i * FS_INS_WORDS;
+    const int op = FS_OPCODE(I[0]), flip = FS_FLIP(I[0]);
+    const uint32_t size = 1u << I[6];
+    o << "    // " << i << "\n";
+    if (op == FS_OP_ARRAY_GATE && p->h_fuse_at[i] >= 0) {
+      const int32_t* Dg = p->h_fuse.data() + (size_t)8 * p->h_fuse_at[i];
+      const bool hasAR = (Dg[4] & 8) != 0;
+      o << "    c.frame_mat(" << Dg[7] << ");\n    {\n";
+      if (hasAR) {
+        const int virt = Dg[5] & 0xFFFF, fp = Dg[6];
+        o << "      const uint32_t par = c.fbit(" << virt << ");\n      const double2 e0 = " << C(fp) << ", e1 = " << C(fp + 2)
+          << ";\n      const double2 ph0 = par ? e1 : e0, ph1 = par ? e0 : e1;\n";
+      } else {
+        o << "      const double2 ph0 = make_double2(1.0, 0.0), ph1 = ph0;\n";
+      }
+      o << "      c.star<" << ((Dg[4] & 1) ? "true" : "false") << ">(" << (Dg[1] & 0xFF) << ", " << (uint32_t)Dg[2] << "u, "
+        << (uint32_t)Dg[3] << "u, " << (Dg[4] & 3) << "u, " << ((Dg[4] & 4) ? "true" : "false") << ", "
+        << (hasAR ? "true" : "false") << ", " << (Dg[5] >> 16) << ", ph0, ph1, " << size << "u);\n    }\n";
+      i += Dg[0];
+      continue;
+    }
+    switch (op) {
+      case FS_OP_FRAME:
+        o << "    c.frame_mat(" << p->h_frame_mat_off[i] << ");\n";
+        break;
+      case FS_OP_ARRAY_GATE:
+        o << "    c.gate(" << I[1] << ", " << I[4] << ", " << I[5] << ", " << size << "u);\n";
+        frame_gate(I[1], I[2], I[3]);
+        break;
+      case FS_OP_EXPAND:
+        o << "    { const uint32_t par = c.fbit(" << I[1] << "); c.expand(" << size << "u, par ? " << C(I[5] + 4) << " : " << C(I[5])
+          << ", par ? " << C(I[5] + 6) << " : " << C(I[5] + 2) << "); }\n";
+        break;
+      case FS_OP_ARRAY_ROT:
+        o << "    { const uint32_t par = c.fbit(" << I[1] << "); const double2 e0 = " << C(I[5]) << ", e1 = " << C(I[5] + 2)
+          << "; c.array_rot(" << I[2] << ", " << size << "u, par ? e1 : e0, par ? e0 : e1); }\n";
+        break;
+      case FS_OP_MEAS_DSTATIC:
+        o << "    c.meas_dstatic(" << I[1] << ", " << flip << ", " << p->h_record_out[I[3]] << ", " << slot_of(I[3]) << ");\n";
+        break;
+      case FS_OP_MEAS_DRANDOM:
+        o << "    c.meas_drandom(" << I[1] << ", " << n + I[1] << ", " << I[2] << ", " << flip << ", " << p->h_record_out[I[3]] << ", "
+          << slot_of(I[3]) << ");\n";
+        break;
+      case FS_OP_MEAS_ACTIVE:
+      case FS_OP_MEAS_COLLAPSE: {
+        const bool collapse = op == FS_OP_MEAS_COLLAPSE;
+        if (collapse) {
+          const int po = I[4] >> 8, pc = I[4] & 0xFF;
+          for (int j = 0; j < pc; j++) {
+            const uint32_t g = p->h_gates[po + j];
+            frame_gate(FS_GATE_G(g), FS_GATE_A(g), FS_GATE_B(g));
+          }
+        }
+        o << "    if (!c.measure<" << (collapse ? "true" : "false") << ">(" << i << ", " << I[1] << ", " << I[2] << ", " << flip << ", "
+          << p->h_record_out[I[3]] << ", " << slot_of(I[3]) << ", " << size << "u, ";
+        if (collapse) o << C(I[5]) << ", " << C(I[5] + 2) << ", " << C(I[5] + 4) << ", " << C(I[5] + 6);
+        else o << "make_double2(1, 0), make_double2(0, 0), make_double2(0, 0), make_double2(1, 0)";
+        o << ")) return;\n";
+        break;
+      }
+      case FS_OP_RETIRE:
+        o << "    c.retire(" << I[1] << ", " << I[2] << ", " << size << "u);\n";
+        break;
+      case FS_OP_COND_FRAME: {
+        uint32_t m[4];
+        mask_of(I[1], I[2], m);
+        o << "    if ((c.slots >> " << slot_of(I[3]) << ") & 1u) c.xor_mask(" << m[0] << "u, " << m[1] << "u, " << m[2] << "u, " << m[3]
+          << "u);\n";
+        break;
+      }
+      case FS_OP_NOISE:
+        o << "    c.noise(" << I[2] << ");\n";
+        break;
+      case FS_OP_DETECTOR:
+      case FS_OP_OBSERVABLE: {
+        o << "    { const uint32_t v = (0u";
+        for (int j = 0; j < I[3]; j++) o << " ^ (c.slots >> " << slot_of(p->h_reclists[I[2] + j]) << ")";
+        o << ") & 1u; ";
+        if (op == FS_OP_DETECTOR) o << "c.detector(v, " << I[1] << ", " << slot_of(R + I[1]) << "); }\n";
+        else o << "c.obs ^= v << " << I[1] << "; }\n";
+        break;
+      }
+      case FS_OP_POSTSELECT: {
+        const int bid = I[1] == 0 ? R + I[2] : I[2];
+        o << "    if (((c.slots >> " << slot_of(bid) << ") & 1u) != " << I[3] << "u) { c.alive = 0; return; }\n";
+        break;
+      }
+      default:
+        break;  // GammaRot: the global phase is not an output of free sampling
+    }
+    i++;
+  }
+  o << "  });\n}\n";
+}
+
 // every block-engine segment of the program (Philox stream) in one NVRTC module
 int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector<int>& karrs, int block_k) {
   if (p->seg_jit == 1) return FS_OK;
   if (p->seg_jit == -1) return FS_ERR_ARG;
   p->seg_jit = -1;
   std::ostringstream o;
-  o << "#include \"fs_block.cuh\"\nusing namespace fs;\n";
+  o << "#include \"fs_wseg.cuh\"\nusing namespace fs;\n";
   std::vector<int> begins;
   for (size_t s = 0; s + 1 < bounds.size(); s++) {
     const int karr = karrs[s];
@@ -1060,8 +1209,13 @@ int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector
     // ran ~2x slower specialised than interpreted (instruction-fetch stalls: every scalar run and
     // measurement inlines the scalar VM; out-of-line calls cost more than they saved) and keep
     // the interpreter unless FS_BLOCK_JIT_WARP is set
-    if (karr < block_k || (karr <= 10 && !p->env.block_jit_warp)) continue;
-    gen_segment(o, p, bounds[s], bounds[s + 1], karr, karr <= 10 ? 32 : 256);
+    if (karr < block_k) continue;
+    if (karr <= 10 && wseg_supported(p) && !p->env.block_no_wjit) {
+      gen_segment_w(o, p, bounds[s], bounds[s + 1], karr);
+    } else {
+      if (karr <= 10 && !p->env.block_jit_warp) continue;
+      gen_segment(o, p, bounds[s], bounds[s + 1], karr, karr <= 10 ? 32 : 256);
+    }
     begins.push_back(bounds[s]);
   }
   if (begins.empty()) { p->seg_jit = 1; return FS_OK; }

@@ -1,0 +1,402 @@
+// fs_wseg.cuh -- warp-per-shot segments of the block engine, fully specialised (NVRTC).
+//
+// The interpreter form (fs_block.cuh block_kernel<.., 32>) keeps one shot's frame as one shared
+// word per bit and runs every scalar instruction (FrameGates, dormant measurements, CondFrame,
+// noise, detectors) on thread 0 between warp barriers -- at the k = 9-10 segments of config 4 that
+// scalar VM, not the array sweeps, is most of the time (profiles/r2_c4_block_ncu.md).  Here the
+// whole segment is straight-line code generated per program (fs_sampler.cu gen_segment_w):
+//
+//   * the frame of the shot is bit-packed in four registers (2n <= 128 bits: x_q at bit q, z_q at
+//     bit n + q -- the survivor store's own layout) that every lane holds: scalar instructions are
+//     executed redundantly by all 32 lanes, so there is no shared-memory frame, no barrier and no
+//     instruction decode; a CondFrame or a noise case is four XORs with a mask (immediates, or
+//     one 16-byte load from the host-built per-case table), FrameGates are their GF(2) matrix
+//     (lane r evaluates rows r, r + 32, .. and ballots assemble the new words);
+//   * record / detector slots and observables are one register each;
+//   * array sweeps are the block engine's (same per-thread order of partial sums, same tree);
+//   * the measurement decision is taken by every lane from the broadcast sums.
+//
+// Philox stream, no trace inputs or outputs (those run the interpreter).  State in and out through
+// the engine-neutral survivor store (fs_general.cuh StateStore).
+#pragma once
+#include "fs_block.cuh"
+
+namespace fs {
+
+struct WCtx {
+  const DevProg& P;
+  const RunArgs& A;
+  const SegArgs& S;
+  double2* amp;
+  int tid;
+  uint64_t si, shot, wabs;
+  int mylane;
+  bool renorm;
+  uint32_t F[4];        // packed frame
+  uint32_t slots, obs;  // packed record / detector slots, observables
+  int alive, err;
+  WordFaultGen gen;
+  int pend_site, pend_lane, pend_case;
+  int coin_blk;
+  uint4 coin_b;
+  int branch;
+
+  __device__ __forceinline__ uint32_t fbit(int b) const { return (F[b >> 5] >> (b & 31)) & 1u; }
+  __device__ __forceinline__ void fxor(int b, uint32_t v) { F[b >> 5] ^= v << (b & 31); }
+  // frame gates on bit positions (x_a, z_a, x_b, z_b are positions in the packed frame)
+  __device__ __forceinline__ void g_s(int xa, int za) { fxor(za, fbit(xa)); }
+  __device__ __forceinline__ void g_h(int xa, int za) {
+    const uint32_t t = fbit(xa) ^ fbit(za);
+    fxor(xa, t);
+    fxor(za, t);
+  }
+  __device__ __forceinline__ void g_cx(int xa, int za, int xb, int zb) {
+    fxor(xb, fbit(xa));
+    fxor(za, fbit(zb));
+  }
+  __device__ __forceinline__ void g_cz(int xa, int za, int xb, int zb) {
+    fxor(zb, fbit(xa));
+    fxor(za, fbit(xb));
+  }
+  __device__ __forceinline__ void xor_mask(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
+    F[0] ^= m0; F[1] ^= m1; F[2] ^= m2; F[3] ^= m3;
+  }
+
+  // FrameGates (or a star group's frame side) as a GF(2) matrix: v'_r = parity(row_r & v)
+  __device__ __forceinline__ void frame_mat(int mo) {
+    const int n2 = 2 * P.n;
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int r = tid + 32 * k;
+      uint32_t b = 0u;
+      if (r < n2) {
+        const uint4 row = __ldg(reinterpret_cast<const uint4*>(P.frame_mat + mo) + r);
+        b = (uint32_t)__popc((row.x & F[0]) ^ (row.y & F[1]) ^ (row.z & F[2]) ^ (row.w & F[3])) & 1u;
+      }
+      o[k] = __ballot_sync(0xFFFFFFFFu, b != 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) F[k] = o[k];
+  }
+
+  __device__ __forceinline__ void out_bit(uint32_t* row) {
+    if (tid == 0) atomicOr(row + (si >> 5), 1u << (si & 31));
+  }
+  // record bit: user column col (or -1), slot sl (or -1)
+  __device__ __forceinline__ void put_rec(int col, int sl, uint32_t bit) {
+    if (col >= 0 && bit) out_bit(A.meas + (size_t)col * A.W);
+    if (sl >= 0) slots = (slots & ~(1u << sl)) | (bit << sl);
+  }
+
+  __device__ __forceinline__ void meas_dstatic(int xq, int flip, int col, int sl) { put_rec(col, sl, fbit(xq) ^ (uint32_t)flip); }
+  __device__ __forceinline__ void meas_drandom(int xq, int zq, int ord, int flip, int col, int sl) {
+    if ((ord >> 2) != coin_blk) {
+      coin_blk = ord >> 2;
+      coin_b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), (uint32_t)coin_blk, TAG_COIN << 24, A.seed);
+    }
+    const int cj = ord & 3;
+    const uint32_t cw = cj == 0 ? coin_b.x : (cj == 1 ? coin_b.y : (cj == 2 ? coin_b.z : coin_b.w));
+    const uint32_t coin = (cw >> mylane) & 1u, px = fbit(xq), pz = fbit(zq);
+    fxor(xq, px ^ pz ^ coin);  // x <- z ^ coin
+    fxor(zq, pz ^ px);         // z <- old x
+    put_rec(col, sl, coin ^ pz ^ (uint32_t)flip);
+  }
+  __device__ __forceinline__ void detector(uint32_t v, int d, int sl) {
+    if (v) out_bit(A.det + (size_t)d * A.W);
+    if (sl >= 0) slots = (slots & ~(1u << sl)) | (v << sl);
+  }
+
+  // NoiseBlock over sites < hi: the word's fault stream, this shot's lane (fs_block.cuh scalar_step)
+  __device__ __forceinline__ void noise(int hi) {
+    for (;;) {
+      if (pend_site < 0) {
+        int st_, ln_, cs_;
+        const int r = gen.step(P, st_, ln_, cs_);
+        if (r == 2) { pend_site = 0x7FFFFFFF; break; }
+        if (r == 0) continue;
+        pend_site = st_; pend_lane = ln_; pend_case = cs_;
+      }
+      if (pend_site >= hi) break;
+      if (pend_lane == mylane) {
+        const uint4 m = __ldg(P.case_mask + pend_case);
+        xor_mask(m.x, m.y, m.z, m.w);
+      }
+      pend_site = -1;
+    }
+  }
+
+  // sweeps ------------------------------------------------------------------------------------
+  __device__ __forceinline__ void gate(int g, int a, int b, uint32_t size) {
+    if (g == FS_G_S || g == FS_G_SDAG) {
+      const double2 ph = make_double2(0.0, g == FS_G_S ? 1.0 : -1.0);
+      for (uint32_t j = tid; j < size / 2; j += 32) {
+        const uint32_t id = ins0(j, a) | (1u << a);
+        amp[id] = cmul(amp[id], ph);
+      }
+    } else if (g == FS_G_H) {
+      const uint32_t st = 1u << a;
+      for (uint32_t j = tid; j < size / 2; j += 32) {
+        const uint32_t i0 = ins0(j, a);
+        const double2 lo = amp[i0], hi = amp[i0 + st];
+        amp[i0] = cscale(cadd(lo, hi), kInvSqrt2);
+        amp[i0 + st] = cscale(csub(lo, hi), kInvSqrt2);
+      }
+    } else {
+      const int lo_ax = a < b ? a : b, hi_ax = a < b ? b : a;
+      for (uint32_t j = tid; j < size / 4; j += 32) {
+        const uint32_t id = ins0(ins0(j, lo_ax), hi_ax) | (1u << a);
+        const uint32_t jd = id | (1u << b);
+        if (g == FS_G_CX) {
+          const double2 t0 = amp[id];
+          amp[id] = amp[jd];
+          amp[jd] = t0;
+        } else {
+          const double2 v = amp[jd];
+          amp[jd] = make_double2(-v.x, -v.y);
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  __device__ __forceinline__ void expand(uint32_t size, double2 ph0, double2 ph1) {
+    for (uint32_t j = tid; j < size; j += 32) {
+      const double2 v = amp[j];
+      amp[j] = cmul(v, ph0);
+      amp[size + j] = cmul(v, ph1);
+    }
+    __syncwarp();
+  }
+
+  __device__ __forceinline__ void array_rot(int a, uint32_t size, double2 ph0, double2 ph1) {
+    for (uint32_t j = tid; j < size; j += 32) amp[j] = cmul(amp[j], ((j >> a) & 1) ? ph1 : ph0);
+    __syncwarp();
+  }
+
+  // star group (fs_block.cuh star_group_t); ph0 / ph1 = the closing ArrayRot's phases for bit 0 / 1
+  template <bool SWAP>
+  __device__ __forceinline__ void star(int a, uint32_t M, uint32_t Mz, uint32_t pw, bool hasH, bool hasAR, int ar_axis,
+                                       double2 ph0, double2 ph1, uint32_t size) {
+    const uint32_t A_ = 1u << a;
+    const uint32_t cx = (pw == 1u || pw == 2u) ? 0x80000000u : 0u, cy = pw >= 2u ? 0x80000000u : 0u;
+    auto hiphase = [&](uint32_t id, double2 v) {
+      const uint32_t sg = (uint32_t)__popc(id & Mz) << 31;
+      return make_double2(BlockCtx<false, 32>::flipsign(SWAP ? v.y : v.x, sg ^ cx),
+                          BlockCtx<false, 32>::flipsign(SWAP ? v.x : v.y, sg ^ cy));
+    };
+    auto finish = [&](uint32_t i0, double2 lo, double2 hi) {
+      if (hasH) {
+        const double2 s = cscale(cadd(lo, hi), kInvSqrt2), d = cscale(csub(lo, hi), kInvSqrt2);
+        lo = s;
+        hi = d;
+      }
+      if (hasAR) {
+        lo = cmul(lo, ((i0 >> ar_axis) & 1u) ? ph1 : ph0);
+        hi = cmul(hi, (((i0 | A_) >> ar_axis) & 1u) ? ph1 : ph0);
+      }
+      amp[i0] = lo;
+      amp[i0 | A_] = hi;
+    };
+    const bool touch_lo = hasH || hasAR;
+    if (M == 0u) {
+      for (uint32_t j = tid; j < size / 2; j += 32) {
+        const uint32_t i0 = ins0(j, a);
+        const double2 hi = hiphase(i0 | A_, amp[i0 | A_]);
+        if (touch_lo) finish(i0, amp[i0], hi);
+        else amp[i0 | A_] = hi;
+      }
+    } else {
+      const int m = __ffs((int)M) - 1;
+      const int lo_ax = a < m ? a : m, hi_ax = a < m ? m : a;
+      for (uint32_t j = tid; j < size / 4; j += 32) {
+        const uint32_t i0 = ins0(ins0(j, lo_ax), hi_ax), i1 = i0 ^ M;
+        const double2 h0 = amp[i1 | A_], h1 = amp[i0 | A_];
+        const double2 n0 = hiphase(i0 | A_, h0), n1 = hiphase(i1 | A_, h1);
+        if (touch_lo) {
+          finish(i0, amp[i0], n0);
+          finish(i1, amp[i1], n1);
+        } else {
+          amp[i0 | A_] = n0;
+          amp[i1 | A_] = n1;
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  // MeasActive / MeasCollapse (fs_block.cuh measure + meas_decide); xv = frame bit of the measured
+  // virtual qubit's X part (the collapse pre-gates have been applied by the caller).  Returns false
+  // when the shot stopped (NaN).
+  template <bool COLLAPSE>
+  __device__ __forceinline__ bool measure(int i, int xv, int a, int flip, int col, int sl, uint32_t size, double2 u00,
+                                          double2 u01, double2 u10, double2 u11) {
+    const uint32_t half = size >> 1, st = 1u << a;
+    double s1 = 0.0, sa = 0.0;
+    for (uint32_t j = tid; j < half; j += 32) {
+      const uint32_t i0 = ins0(j, a);
+      const double2 a0 = amp[i0], a1 = amp[i0 + st];
+      if (COLLAPSE) s1 = __dadd_rn(s1, cnorm2(cadd(cmul(a0, u10), cmul(u11, a1))));
+      else s1 = __dadd_rn(s1, cnorm2(a1));
+      sa = __dadd_rn(sa, __dadd_rn(cnorm2(a0), cnorm2(a1)));
+    }
+#pragma unroll
+    for (int w = 16; w; w >>= 1) {  // the block engine's tree: element t += element t + w
+      const double o1 = __shfl_down_sync(0xFFFFFFFFu, s1, w), o2 = __shfl_down_sync(0xFFFFFFFFu, sa, w);
+      if (tid < w) {
+        s1 = __dadd_rn(s1, o1);
+        sa = __dadd_rn(sa, o2);
+      }
+    }
+    double p1 = __shfl_sync(0xFFFFFFFFu, s1, 0);
+    const double p_all = __shfl_sync(0xFFFFFFFFu, sa, 0);
+    const uint32_t parity = fbit(xv);
+    if (p1 != p1) {
+      err = FS_ERR_SHOT_NAN;
+      alive = 0;
+      return false;
+    }
+    if (COLLAPSE || !renorm) p1 = p_all > 0 ? __ddiv_rn(p1, p_all) : 0.0;
+    if (p1 < 0.0) p1 = 0.0;
+    else if (p1 > 1.0) p1 = 1.0;
+    const uint4 o = philox((uint32_t)shot, (uint32_t)(shot >> 32), (uint32_t)i, TAG_BORN << 24, A.seed);
+    const double u = u64_to_unit(((uint64_t)o.y << 32) | o.x);
+    int br = u < p1 ? 1 : 0;
+    double pb = br ? p1 : __dsub_rn(1.0, p1);
+    if (pb < kBranchFloor) { br ^= 1; pb = __dsub_rn(1.0, pb); }
+    put_rec(col, sl, (uint32_t)br ^ parity ^ (uint32_t)flip);
+    branch = br;
+    if (COLLAPSE) {
+      const double scale = renorm ? __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(pb, p_all))) : 1.0;
+      const double2 k0 = br == 0 ? cscale(u00, scale) : cscale(u10, scale);
+      const double2 k1 = br == 0 ? cscale(u01, scale) : cscale(u11, scale);
+      fxor(xv, (uint32_t)br);
+      for (uint32_t b0 = 0; b0 < half; b0 += 32) {  // in place, strip by strip
+        const uint32_t j = b0 + tid;
+        double2 val = make_double2(0.0, 0.0);
+        if (j < half) {
+          const uint32_t i0 = ins0(j, a);
+          val = cadd(cmul(k0, amp[i0]), cmul(k1, amp[i0 + st]));
+        }
+        __syncwarp();
+        if (j < half) amp[j] = val;
+        __syncwarp();
+      }
+    } else {
+      const double s = renorm ? __ddiv_rn(1.0, __dsqrt_rn(pb)) : 1.0;
+      const uint32_t dead = 1u - (uint32_t)br;
+      for (uint32_t j = tid; j < size; j += 32) {
+        if (((j >> a) & 1) == dead) amp[j] = make_double2(0.0, 0.0);
+        else if (renorm) amp[j] = cscale(amp[j], s);
+      }
+      __syncwarp();
+    }
+    return true;
+  }
+
+  __device__ __forceinline__ void retire(int xv, int a, uint32_t size) {
+    const uint32_t half = size >> 1;
+    for (uint32_t b0 = 0; b0 < half; b0 += 32) {
+      const uint32_t j = b0 + tid;
+      double2 val = make_double2(0.0, 0.0);
+      if (j < half) val = amp[ins0(j, a) + ((uint32_t)branch << a)];
+      __syncwarp();
+      if (j < half) amp[j] = val;
+      __syncwarp();
+    }
+    fxor(xv, (uint32_t)branch);
+  }
+};
+
+// the shot loop of a specialised warp-per-shot segment (fs_block.cuh block_run without the shared
+// frame): one warp per shot, `group_bytes` of dynamic shared memory per warp for the array
+template <class Exec>
+__device__ __forceinline__ void wseg_run(const DevProg& P, const RunArgs& A, const SegArgs& S, int group_bytes,
+                                         Exec&& exec) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int group = threadIdx.x >> 5, ngroups = blockDim.x >> 5, tid = threadIdx.x & 31;
+  double2* amp = reinterpret_cast<double2*>(smem_raw + (size_t)group * group_bytes);
+  for (uint32_t idx = blockIdx.x * ngroups + group; idx < S.n_in; idx += gridDim.x * ngroups) {
+    const uint64_t si = S.first ? S.chunk0 + idx : S.in.shot[idx];
+    if (si >= A.nshots) continue;
+    WCtx c{P, A, S, amp, tid, si, A.shot0 + si, 0, 0, !(A.flags & FS_NO_RENORM)};
+    c.wabs = c.shot >> 5;
+    c.mylane = (int)(c.shot & 31);
+    c.alive = 1;
+    c.err = 0;
+    c.pend_site = -1;
+    c.pend_lane = 0;
+    c.pend_case = 0;
+    c.branch = 0;
+    c.coin_blk = -1;
+    c.coin_b = make_uint4(0, 0, 0, 0);
+    double2 gamma = make_double2(1.0, 0.0);
+    c.gen.init(A.seed, c.wabs);
+#pragma unroll
+    for (int k = 0; k < 4; k++) c.F[k] = 0u;
+    c.slots = 0u;
+    c.obs = 0u;
+    if (S.first) {
+      if (tid == 0) amp[0] = make_double2(1.0, 0.0);
+    } else {
+      const StateStore& I = S.in;
+      const uint32_t sz = 1u << S.k_in;
+      for (uint32_t j = tid; j < sz; j += 32) {
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(amp + j);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(I.amps + store_amp_index(idx, j, sz, I.shot_major)) : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        if (k < S.nfw) c.F[k] = I.frame[(size_t)idx * S.nfw + k];
+      if (S.nsw) c.slots = I.slotbits[(size_t)idx * S.nsw];
+      if (S.now) c.obs = I.obsbits[(size_t)idx * S.now];
+      gamma = I.gamma[idx];
+      c.gen.step_no = I.gen_i[(size_t)idx * 6];
+      c.gen.run = (int)I.gen_i[(size_t)idx * 6 + 1];
+      c.gen.cl = (int)I.gen_i[(size_t)idx * 6 + 2];
+      c.pend_site = (int)I.gen_i[(size_t)idx * 6 + 3];
+      c.pend_lane = (int)I.gen_i[(size_t)idx * 6 + 4];
+      c.pend_case = (int)I.gen_i[(size_t)idx * 6 + 5];
+      c.gen.c = I.gen_c[idx];
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncwarp();
+    exec(c);
+    __syncwarp();
+    const bool alive = c.alive != 0, errored = c.err != 0;
+    if (tid == 0 && errored) {
+      atomicOr(A.error + (si >> 5), 1u << (si & 31));
+      atomicMax(A.status, c.err);
+    }
+    if (S.last || !alive) {
+      for (int o = 0; o < P.O; o++)
+        if ((c.obs >> o) & 1u) c.out_bit(A.obs + (size_t)o * A.W);
+      if (alive && !errored) c.out_bit(A.accepted);
+    }
+    if (!S.last && alive) {  // survivor: compact into the output store
+      uint32_t slot = 0;
+      if (tid == 0) slot = atomicAdd(S.n_out, 1u);
+      slot = __shfl_sync(0xFFFFFFFFu, slot, 0);
+      const StateStore& O = S.out;
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        if (k < S.nfw && tid == k) O.frame[(size_t)slot * S.nfw + k] = c.F[k];
+      const uint32_t sz = 1u << S.k_out;
+      for (uint32_t j = tid; j < sz; j += 32) O.amps[store_amp_index(slot, j, sz, O.shot_major)] = amp[j];
+      if (tid == 0) {
+        if (S.nsw) O.slotbits[(size_t)slot * S.nsw] = c.slots;
+        if (S.now) O.obsbits[(size_t)slot * S.now] = c.obs;
+        O.shot[slot] = (uint32_t)si;
+        O.gamma[slot] = gamma;
+        uint32_t* gi = O.gen_i + (size_t)slot * 6;
+        gi[0] = c.gen.step_no; gi[1] = (uint32_t)c.gen.run; gi[2] = (uint32_t)c.gen.cl;
+        gi[3] = (uint32_t)c.pend_site; gi[4] = (uint32_t)c.pend_lane; gi[5] = (uint32_t)c.pend_case;
+        O.gen_c[slot] = c.gen.c;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace fs

@@ -346,7 +346,8 @@ _PSEL = [c for c in case_names() if load(c)["prog"].has_postselect and "t_modes"
 
 @pytest.mark.parametrize("name", _PSEL)
 @pytest.mark.parametrize("env", [{"FS_BLOCK_K": "1"}, {"FS_BLOCK_K": "11"}, {}, {"FS_BLOCK_NO_FUSE": "1"},
-                                 {"FS_BLOCK_K": "1", "FS_BLOCK_NO_FUSE": "1"}])
+                                 {"FS_BLOCK_K": "1", "FS_BLOCK_NO_FUSE": "1"}, {"FS_BLOCK_NO_WJIT": "1"},
+                                 {"FS_BLOCK_K": "1", "FS_BLOCK_NO_WJIT": "1"}])
 def test_gpu_block_engines_match_reference_and_oracle(cuda, name, env, monkeypatch):
     """Post-selected programs with every segment through the block engine (FS_BLOCK_K=1: warp or
     CTA per shot from k = 1), through lane-per-shot segments up to k = 10 (FS_BLOCK_K=11), and by
@@ -377,12 +378,13 @@ def test_gpu_block_engines_match_reference_and_oracle(cuda, name, env, monkeypat
 @pytest.mark.parametrize("k,seed", [(2, 0), (3, 1), (4, 2), (5, 3), (6, 4), (7, 5), (8, 6), (9, 7), (10, 8), (10, 9),
                                     (11, 10), (12, 11)])
 @pytest.mark.parametrize("env", [{"FS_BLOCK_K": "1"}, {"FS_BLOCK_K": "1", "FS_BLOCK_NO_JIT": "1"},
-                                 {"FS_BLOCK_K": "1", "FS_BLOCK_JIT_WARP": "1"},
+                                 {"FS_BLOCK_K": "1", "FS_BLOCK_NO_WJIT": "1"},
+                                 {"FS_BLOCK_K": "1", "FS_BLOCK_NO_WJIT": "1", "FS_BLOCK_JIT_WARP": "1"},
                                  {"FS_BLOCK_K": "1", "FS_BLOCK_NO_FUSE": "1"}])
 def test_gpu_star_groups_match_oracle(cuda, k, seed, env, monkeypatch):
     """The block engine's fused ArrayGate runs (star groups: CX / CZ / S through one pivot axis,
-    an optional H and ArrayRot, FrameGates in between; interpreter, specialised CTA- and
-    warp-per-shot kernels) against the oracle's one-sweep-per-instruction VM on hand-built
+    an optional H and ArrayRot, FrameGates in between; interpreter, specialised CTA-per-shot
+    kernels, packed-frame (fs_wseg.cuh) and shared-frame specialised warp-per-shot kernels) against the oracle's one-sweep-per-instruction VM on hand-built
     programs (tests/synth.py): records of Philox free sampling bit for bit, and the frame, gamma
     and amplitudes at checkpoints between the runs (the reference stream, trace mode)."""
     from synth import star_program
@@ -397,6 +399,9 @@ def test_gpu_star_groups_match_oracle(cuda, k, seed, env, monkeypatch):
     np.testing.assert_array_equal(a.measurements(), b.measurements())
     np.testing.assert_array_equal(a.accepted_bits(), b.accepted_bits())
     assert a.accepted_bits().all()
+    # the specialised segment kernel compiled (a failed compile would fall back to the interpreter)
+    interpreted = "FS_BLOCK_NO_JIT" in env or (k <= 10 and "FS_BLOCK_NO_WJIT" in env and "FS_BLOCK_JIT_WARP" not in env)
+    assert ("segments: ready kernels=%d" % (0 if interpreted else 1)) in dp.jit_status(), dp.jit_status()
     cuts = P.meta["cuts"]
     ns = 8
     _, g, tb = dp.sample_host(ns, seed=11, flags=FS_RNG_SPLITMIX | FS_FORCE_SEGMENTED, want_state=True,
