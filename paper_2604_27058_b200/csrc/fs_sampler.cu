@@ -15,6 +15,7 @@
 #include <functional>
 #include <map>
 #include <mutex>
+#include <set>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -114,6 +115,7 @@ struct EnvSwitches {
   bool block_no_jit = false;   // FS_BLOCK_NO_JIT: segmented engine interprets every segment
   bool block_jit_warp = false; // FS_BLOCK_JIT_WARP: also specialise warp-per-shot segments
   bool block_no_wjit = false;  // FS_BLOCK_NO_WJIT: warp-per-shot segments keep the interpreter (no fs_wseg.cuh kernels)
+  bool seg_no_ljit = false;    // FS_SEG_NO_LJIT: lane-per-shot segments keep the interpreter (no fs_lseg.cuh kernels)
   bool block_no_fuse = false;  // FS_BLOCK_NO_FUSE: block engine runs ArrayGates one sweep each (no star groups)
   int block_k = 0;             // FS_BLOCK_K: segment k at which a shot gets a warp / CTA (0 = default)
   bool hbm_fused = false;      // FS_HBM_FUSED: fused tile passes also under FS_FORCE_HBM
@@ -128,6 +130,7 @@ struct EnvSwitches {
     block_jit_warp = getenv("FS_BLOCK_JIT_WARP") != nullptr;
     block_no_fuse = getenv("FS_BLOCK_NO_FUSE") != nullptr;
     block_no_wjit = getenv("FS_BLOCK_NO_WJIT") != nullptr;
+    seg_no_ljit = getenv("FS_SEG_NO_LJIT") != nullptr;
     if (const char* e = getenv("FS_BLOCK_K")) block_k = std::max(1, atoi(e));
     hbm_fused = getenv("FS_HBM_FUSED") != nullptr;
     hbm_unfused = getenv("FS_HBM_UNFUSED") != nullptr;
@@ -215,6 +218,8 @@ struct fs_prog {
   std::string pass_jit_err;
   // program-specialised segment kernels of the block engine (key: segment begin), Philox stream
   int seg_jit = 0;
+  std::set<int> seg_lane;  // segment starts compiled as lane-per-shot kernels (fs_lseg.cuh)
+  std::map<int, int> seg_occ;  // their resident blocks per SM
   std::vector<int32_t> h_next_array, h_frame_mat_off, h_fuse_at, h_fuse;
   std::map<int, fsjit::CUfunction> seg_fn;
   std::string seg_jit_err;
@@ -779,7 +784,7 @@ extern "C" const char* fs_debug_jit_status(fs_prog* p) {
                         : (p->jit_state == 0 ? "not built" : "failed: " + p->jit_error);
   s += p->aff_state == 1 ? "; affine: ready threads=" + std::to_string(p->aff_threads)
                          : (p->aff_state == 0 ? "; affine: not built" : "; affine: n/a (" + p->aff_error + ")");
-  s += p->seg_jit == 1 ? "; segments: ready kernels=" + std::to_string(p->seg_fn.size())
+  s += p->seg_jit == 1 ? "; segments: ready kernels=" + std::to_string(p->seg_fn.size() - p->seg_lane.size()) + " lane=" + std::to_string(p->seg_lane.size())
                        : (p->seg_jit == 0 ? "; segments: not built" : "; segments: failed (" + p->seg_jit_err + ")");
   return s.c_str();
 }
@@ -1195,24 +1200,142 @@ void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int ka
   o << "  });\n}\n";
 }
 
+// Lane-per-shot segments fully specialised (fs_lseg.cuh): every lane runs one shot with its frame
+// packed in registers and its array in a per-thread array.  Same limits as the warp-per-shot form.
+constexpr int kLsegMaxK = 8;  // 2^8 amplitudes = 4 KiB of thread-local memory per shot
+
+void gen_segment_l(std::ostringstream& o, const fs_prog* p, int b, int e, int karr, int k_in, int k_out) {
+  const int* IN = p->h_instrs.data();
+  const int n = p->dp.n, R = p->dp.R;
+  auto C = [&](int off) {
+    return "make_double2(" + fsjit::hexd(p->h_fparams[off]) + ", " + fsjit::hexd(p->h_fparams[off + 1]) + ")";
+  };
+  auto slot_of = [&](int bit) { return p->h_bit_slot[bit]; };
+  auto mask_of = [&](int off, int cnt, uint32_t m[4]) {
+    m[0] = m[1] = m[2] = m[3] = 0u;
+    for (int j = off; j < off + cnt; j++) {
+      const uint32_t en = p->h_paulis[j];
+      const int bit = FS_PAULI_Z(en) ? n + (int)FS_PAULI_Q(en) : (int)FS_PAULI_Q(en);
+      m[bit >> 5] ^= 1u << (bit & 31);
+    }
+  };
+  auto frame_gate = [&](int g, int va, int vb) {
+    switch (g) {
+      case FS_G_S: case FS_G_SDAG: o << "    c.g_s(" << va << ", " << n + va << ");\n"; break;
+      case FS_G_H: o << "    c.g_h(" << va << ", " << n + va << ");\n"; break;
+      case FS_G_CX: o << "    c.g_cx(" << va << ", " << n + va << ", " << vb << ", " << n + vb << ");\n"; break;
+      case FS_G_CZ: o << "    c.g_cz(" << va << ", " << n + va << ", " << vb << ", " << n + vb << ");\n"; break;
+      default: break;
+    }
+  };
+  o << "extern \"C\" __global__ void __launch_bounds__(128) fs_seg_" << b
+    << "(DevProg P, RunArgs A, SegArgs S, int group_bytes) {\n  lseg_run<" << karr << ", " << k_in << ", " << k_out
+    << ">(P, A, S, [&](LCtx<" << karr << ">& c) {\n";
+  for (int i = b; i < e; i++) {
+    const int* I = IN + (size_t)i * FS_INS_WORDS;
+    const int op = FS_OPCODE(I[0]), flip = FS_FLIP(I[0]);
+    o << "    // " << i << "\n";
+    switch (op) {
+      case FS_OP_FRAME:
+        for (int j = 0; j < I[2]; j++) {
+          const uint32_t g = p->h_gates[I[1] + j];
+          frame_gate(FS_GATE_G(g), FS_GATE_A(g), FS_GATE_B(g));
+        }
+        break;
+      case FS_OP_ARRAY_GATE:
+        o << "    c.gate<" << I[1] << ", " << I[4] << ", " << (I[5] < 0 ? 0 : I[5]) << ", " << I[6] << ">();\n";
+        frame_gate(I[1], I[2], I[3]);
+        break;
+      case FS_OP_EXPAND:
+        o << "    { const uint32_t par = c.fbit(" << I[1] << "); c.expand<" << I[6] << ">(par ? " << C(I[5] + 4) << " : " << C(I[5])
+          << ", par ? " << C(I[5] + 6) << " : " << C(I[5] + 2) << "); }\n";
+        break;
+      case FS_OP_ARRAY_ROT:
+        o << "    { const uint32_t par = c.fbit(" << I[1] << "); const double2 e0 = " << C(I[5]) << ", e1 = " << C(I[5] + 2)
+          << "; c.array_rot<" << I[2] << ", " << I[6] << ">(par ? e1 : e0, par ? e0 : e1); }\n";
+        break;
+      case FS_OP_MEAS_DSTATIC:
+        o << "    c.meas_dstatic(" << I[1] << ", " << flip << ", " << p->h_record_out[I[3]] << ", " << slot_of(I[3]) << ");\n";
+        break;
+      case FS_OP_MEAS_DRANDOM:
+        o << "    c.meas_drandom(" << I[1] << ", " << n + I[1] << ", " << I[2] << ", " << flip << ", " << p->h_record_out[I[3]] << ", "
+          << slot_of(I[3]) << ");\n";
+        break;
+      case FS_OP_MEAS_ACTIVE:
+      case FS_OP_MEAS_COLLAPSE: {
+        const bool collapse = op == FS_OP_MEAS_COLLAPSE;
+        if (collapse) {
+          const int po = I[4] >> 8, pc = I[4] & 0xFF;
+          for (int j = 0; j < pc; j++) {
+            const uint32_t g = p->h_gates[po + j];
+            frame_gate(FS_GATE_G(g), FS_GATE_A(g), FS_GATE_B(g));
+          }
+        }
+        o << "    if (!c.measure<" << (collapse ? "true" : "false") << ", " << I[2] << ", " << I[6] << ">(" << i << ", " << I[1] << ", "
+          << flip << ", " << p->h_record_out[I[3]] << ", " << slot_of(I[3]) << ", ";
+        if (collapse) o << C(I[5]) << ", " << C(I[5] + 2) << ", " << C(I[5] + 4) << ", " << C(I[5] + 6);
+        else o << "make_double2(1, 0), make_double2(0, 0), make_double2(0, 0), make_double2(1, 0)";
+        o << ")) return;\n";
+        break;
+      }
+      case FS_OP_RETIRE:
+        o << "    c.retire<" << I[2] << ", " << I[6] << ">(" << I[1] << ");\n";
+        break;
+      case FS_OP_COND_FRAME: {
+        uint32_t m[4];
+        mask_of(I[1], I[2], m);
+        o << "    if ((c.slots >> " << slot_of(I[3]) << ") & 1u) c.xor_mask(" << m[0] << "u, " << m[1] << "u, " << m[2] << "u, " << m[3]
+          << "u);\n";
+        break;
+      }
+      case FS_OP_NOISE:
+        o << "    c.noise(" << I[2] << ");\n";
+        break;
+      case FS_OP_DETECTOR:
+      case FS_OP_OBSERVABLE: {
+        o << "    { const uint32_t v = (0u";
+        for (int j = 0; j < I[3]; j++) o << " ^ (c.slots >> " << slot_of(p->h_reclists[I[2] + j]) << ")";
+        o << ") & 1u; ";
+        if (op == FS_OP_DETECTOR) o << "c.detector(v, " << I[1] << ", " << slot_of(R + I[1]) << "); }\n";
+        else o << "c.obs ^= v << " << I[1] << "; }\n";
+        break;
+      }
+      case FS_OP_POSTSELECT: {
+        const int bid = I[1] == 0 ? R + I[2] : I[2];
+        o << "    if (((c.slots >> " << slot_of(bid) << ") & 1u) != " << I[3] << "u) { c.alive = 0; return; }\n";
+        break;
+      }
+      default:
+        break;  // GammaRot: the global phase is not an output of free sampling
+    }
+  }
+  o << "  });\n}\n";
+}
+
 // every block-engine segment of the program (Philox stream) in one NVRTC module
 int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector<int>& karrs, int block_k) {
   if (p->seg_jit == 1) return FS_OK;
   if (p->seg_jit == -1) return FS_ERR_ARG;
   p->seg_jit = -1;
   std::ostringstream o;
-  o << "#include \"fs_wseg.cuh\"\nusing namespace fs;\n";
+  o << "#include \"fs_lseg.cuh\"\nusing namespace fs;\n";
   std::vector<int> begins;
+  const int* sched = p->h_sched.data();
   for (size_t s = 0; s + 1 < bounds.size(); s++) {
     const int karr = karrs[s];
-    // CTA-per-shot segments only: measured 1.2-1.8x faster specialised.  The warp-per-shot ones
-    // ran ~2x slower specialised than interpreted (instruction-fetch stalls: every scalar run and
-    // measurement inlines the scalar VM; out-of-line calls cost more than they saved) and keep
-    // the interpreter unless FS_BLOCK_JIT_WARP is set
-    if (karr < block_k) continue;
-    if (karr <= 10 && wseg_supported(p) && !p->env.block_no_wjit) {
+    if (karr < block_k) {
+      // lane-per-shot segments: fully specialised (fs_lseg.cuh) while the array fits thread-local
+      // memory; the interpreter otherwise
+      if (karr > kLsegMaxK || !wseg_supported(p) || p->env.seg_no_ljit) continue;
+      gen_segment_l(o, p, bounds[s], bounds[s + 1], karr, bounds[s] > 0 ? sched[bounds[s] - 1] : 0, sched[bounds[s + 1] - 1]);
+      p->seg_lane.insert(bounds[s]);
+    } else if (karr <= 10 && wseg_supported(p) && !p->env.block_no_wjit) {
+      // warp-per-shot segments: fully specialised (fs_wseg.cuh)
       gen_segment_w(o, p, bounds[s], bounds[s + 1], karr);
     } else {
+      // CTA-per-shot segments: specialised sweeps around the shared scalar VM (measured 1.2-1.8x
+      // faster); warp-per-shot ones in that form ran ~2x slower than interpreted (instruction-fetch
+      // stalls) and keep the interpreter unless FS_BLOCK_JIT_WARP is set
       if (karr <= 10 && !p->env.block_jit_warp) continue;
       gen_segment(o, p, bounds[s], bounds[s + 1], karr, karr <= 10 ? 32 : 256);
     }
@@ -1290,6 +1413,39 @@ int launch_block_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cu
   kt_end(p, stream);
   p->launches++;
   FS_CUDA_TRY(cudaGetLastError());
+  return FS_OK;
+}
+
+// lane-per-shot specialised segment (fs_lseg.cuh): Philox free sampling only
+bool lseg_ready(const fs_prog* p, const fs::RunArgs& a, const fs::SegArgs& S) {
+  const bool trace = a.fault_modes || a.forced || a.t_fx || a.t_gamma || a.t_amps || a.t_draws || a.t_rec || a.ncp;
+  return !(a.flags & FS_RNG_SPLITMIX) && !trace && p->seg_jit == 1 && !p->env.block_no_jit &&
+         p->seg_lane.count(S.seg_begin) && p->seg_fn.count(S.seg_begin);
+}
+
+int launch_lane_segment(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, cudaStream_t stream) {
+  fsjit::Api& J = fsjit::api();
+  fsjit::CUfunction fn = p->seg_fn[S.seg_begin];
+  const int nt = 128;
+  int occ = 0;
+  auto oit = p->seg_occ.find(S.seg_begin);
+  if (oit != p->seg_occ.end()) occ = oit->second;
+  else {
+    if (J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nt, 0) != 0 || occ < 1) occ = 1;
+    p->seg_occ[S.seg_begin] = occ;
+  }
+  const size_t blocks_needed = ((size_t)S.n_in + nt - 1) / nt;
+  const size_t grid = std::max<size_t>(1, std::min<size_t>(blocks_needed, (size_t)p->num_sms * occ));
+  fs::DevProg dpv = p->dp;
+  fs::RunArgs av = a;
+  fs::SegArgs sv = S;
+  int gb = 0;
+  void* args[] = {&dpv, &av, &sv, &gb};
+  kt_begin(p, stream);
+  const int r = J.cuLaunchKernel(fn, (unsigned)grid, 1, 1, nt, 1, 1, 0, stream, args, nullptr);
+  kt_end(p, stream);
+  p->launches++;
+  if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_seg, lane) failed: " + std::to_string(r));
   return FS_OK;
 }
 
@@ -1397,8 +1553,10 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
         FS_CUDA_TRY(cudaMemsetAsync(d_nout, 0, 4, stream));
       }
       S.n_out = d_nout;
-      int rc = karr >= block_k ? launch_block_kernel(p, a, S, karr, stream)
-                               : launch_general_kernel(p, a, S, true, karr, (n_in + 31) / 32, stream);
+      int rc;
+      if (karr >= block_k) rc = launch_block_kernel(p, a, S, karr, stream);
+      else if (lseg_ready(p, a, S)) rc = launch_lane_segment(p, a, S, stream);
+      else rc = launch_general_kernel(p, a, S, true, karr, (n_in + 31) / 32, stream);
       if (rc) return rc;
       if (S.last) break;
       uint32_t n_out = 0;

@@ -23,15 +23,16 @@
 
 namespace fs {
 
-struct WCtx {
+// Scalar state of one shot and the scalar instructions on it (shared by the warp-per-shot segments
+// below, where all 32 lanes hold the same shot and `writer` is lane 0, and the lane-per-shot
+// segments of fs_lseg.cuh, where every lane is its own shot's writer)
+struct SCtx {
   const DevProg& P;
   const RunArgs& A;
   const SegArgs& S;
-  double2* amp;
-  int tid;
   uint64_t si, shot, wabs;
   int mylane;
-  bool renorm;
+  bool renorm, writer;
   uint32_t F[4];        // packed frame
   uint32_t slots, obs;  // packed record / detector slots, observables
   int alive, err;
@@ -40,6 +41,25 @@ struct WCtx {
   int coin_blk;
   uint4 coin_b;
   int branch;
+
+  __device__ __forceinline__ SCtx(const DevProg& P_, const RunArgs& A_, const SegArgs& S_, uint64_t si_, bool writer_)
+      : P(P_), A(A_), S(S_), si(si_), shot(A_.shot0 + si_), renorm(!(A_.flags & FS_NO_RENORM)), writer(writer_) {
+    wabs = shot >> 5;
+    mylane = (int)(shot & 31);
+    alive = 1;
+    err = 0;
+    pend_site = -1;
+    pend_lane = 0;
+    pend_case = 0;
+    branch = 0;
+    coin_blk = -1;
+    coin_b = make_uint4(0, 0, 0, 0);
+    gen.init(A.seed, wabs);
+#pragma unroll
+    for (int k = 0; k < 4; k++) F[k] = 0u;
+    slots = 0u;
+    obs = 0u;
+  }
 
   __device__ __forceinline__ uint32_t fbit(int b) const { return (F[b >> 5] >> (b & 31)) & 1u; }
   __device__ __forceinline__ void fxor(int b, uint32_t v) { F[b >> 5] ^= v << (b & 31); }
@@ -62,26 +82,8 @@ struct WCtx {
     F[0] ^= m0; F[1] ^= m1; F[2] ^= m2; F[3] ^= m3;
   }
 
-  // FrameGates (or a star group's frame side) as a GF(2) matrix: v'_r = parity(row_r & v)
-  __device__ __forceinline__ void frame_mat(int mo) {
-    const int n2 = 2 * P.n;
-    uint32_t o[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const int r = tid + 32 * k;
-      uint32_t b = 0u;
-      if (r < n2) {
-        const uint4 row = __ldg(reinterpret_cast<const uint4*>(P.frame_mat + mo) + r);
-        b = (uint32_t)__popc((row.x & F[0]) ^ (row.y & F[1]) ^ (row.z & F[2]) ^ (row.w & F[3])) & 1u;
-      }
-      o[k] = __ballot_sync(0xFFFFFFFFu, b != 0u);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; k++) F[k] = o[k];
-  }
-
   __device__ __forceinline__ void out_bit(uint32_t* row) {
-    if (tid == 0) atomicOr(row + (si >> 5), 1u << (si & 31));
+    if (writer) atomicOr(row + (si >> 5), 1u << (si & 31));
   }
   // record bit: user column col (or -1), slot sl (or -1)
   __device__ __forceinline__ void put_rec(int col, int sl, uint32_t bit) {
@@ -124,6 +126,48 @@ struct WCtx {
       }
       pend_site = -1;
     }
+  }
+
+  // survivor state in / out of the engine-neutral store (everything but the amplitudes)
+  __device__ __forceinline__ void load_scalars(const StateStore& I, uint32_t idx) {
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      if (k < S.nfw) F[k] = I.frame[(size_t)idx * S.nfw + k];
+    if (S.nsw) slots = I.slotbits[(size_t)idx * S.nsw];
+    if (S.now) obs = I.obsbits[(size_t)idx * S.now];
+    gen.step_no = I.gen_i[(size_t)idx * 6];
+    gen.run = (int)I.gen_i[(size_t)idx * 6 + 1];
+    gen.cl = (int)I.gen_i[(size_t)idx * 6 + 2];
+    pend_site = (int)I.gen_i[(size_t)idx * 6 + 3];
+    pend_lane = (int)I.gen_i[(size_t)idx * 6 + 4];
+    pend_case = (int)I.gen_i[(size_t)idx * 6 + 5];
+    gen.c = I.gen_c[idx];
+  }
+};
+
+struct WCtx : SCtx {
+  double2* amp;
+  int tid;
+
+  __device__ __forceinline__ WCtx(const DevProg& P_, const RunArgs& A_, const SegArgs& S_, double2* amp_, int tid_, uint64_t si_)
+      : SCtx(P_, A_, S_, si_, tid_ == 0), amp(amp_), tid(tid_) {}
+
+  // FrameGates (or a star group's frame side) as a GF(2) matrix: v'_r = parity(row_r & v)
+  __device__ __forceinline__ void frame_mat(int mo) {
+    const int n2 = 2 * P.n;
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int r = tid + 32 * k;
+      uint32_t b = 0u;
+      if (r < n2) {
+        const uint4 row = __ldg(reinterpret_cast<const uint4*>(P.frame_mat + mo) + r);
+        b = (uint32_t)__popc((row.x & F[0]) ^ (row.y & F[1]) ^ (row.z & F[2]) ^ (row.w & F[3])) & 1u;
+      }
+      o[k] = __ballot_sync(0xFFFFFFFFu, b != 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) F[k] = o[k];
   }
 
   // sweeps ------------------------------------------------------------------------------------
@@ -319,23 +363,8 @@ __device__ __forceinline__ void wseg_run(const DevProg& P, const RunArgs& A, con
   for (uint32_t idx = blockIdx.x * ngroups + group; idx < S.n_in; idx += gridDim.x * ngroups) {
     const uint64_t si = S.first ? S.chunk0 + idx : S.in.shot[idx];
     if (si >= A.nshots) continue;
-    WCtx c{P, A, S, amp, tid, si, A.shot0 + si, 0, 0, !(A.flags & FS_NO_RENORM)};
-    c.wabs = c.shot >> 5;
-    c.mylane = (int)(c.shot & 31);
-    c.alive = 1;
-    c.err = 0;
-    c.pend_site = -1;
-    c.pend_lane = 0;
-    c.pend_case = 0;
-    c.branch = 0;
-    c.coin_blk = -1;
-    c.coin_b = make_uint4(0, 0, 0, 0);
+    WCtx c(P, A, S, amp, tid, si);
     double2 gamma = make_double2(1.0, 0.0);
-    c.gen.init(A.seed, c.wabs);
-#pragma unroll
-    for (int k = 0; k < 4; k++) c.F[k] = 0u;
-    c.slots = 0u;
-    c.obs = 0u;
     if (S.first) {
       if (tid == 0) amp[0] = make_double2(1.0, 0.0);
     } else {
@@ -346,19 +375,8 @@ __device__ __forceinline__ void wseg_run(const DevProg& P, const RunArgs& A, con
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(I.amps + store_amp_index(idx, j, sz, I.shot_major)) : "memory");
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
-#pragma unroll
-      for (int k = 0; k < 4; k++)
-        if (k < S.nfw) c.F[k] = I.frame[(size_t)idx * S.nfw + k];
-      if (S.nsw) c.slots = I.slotbits[(size_t)idx * S.nsw];
-      if (S.now) c.obs = I.obsbits[(size_t)idx * S.now];
+      c.load_scalars(I, idx);
       gamma = I.gamma[idx];
-      c.gen.step_no = I.gen_i[(size_t)idx * 6];
-      c.gen.run = (int)I.gen_i[(size_t)idx * 6 + 1];
-      c.gen.cl = (int)I.gen_i[(size_t)idx * 6 + 2];
-      c.pend_site = (int)I.gen_i[(size_t)idx * 6 + 3];
-      c.pend_lane = (int)I.gen_i[(size_t)idx * 6 + 4];
-      c.pend_case = (int)I.gen_i[(size_t)idx * 6 + 5];
-      c.gen.c = I.gen_c[idx];
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncwarp();

@@ -347,7 +347,8 @@ _PSEL = [c for c in case_names() if load(c)["prog"].has_postselect and "t_modes"
 @pytest.mark.parametrize("name", _PSEL)
 @pytest.mark.parametrize("env", [{"FS_BLOCK_K": "1"}, {"FS_BLOCK_K": "11"}, {}, {"FS_BLOCK_NO_FUSE": "1"},
                                  {"FS_BLOCK_K": "1", "FS_BLOCK_NO_FUSE": "1"}, {"FS_BLOCK_NO_WJIT": "1"},
-                                 {"FS_BLOCK_K": "1", "FS_BLOCK_NO_WJIT": "1"}])
+                                 {"FS_BLOCK_K": "1", "FS_BLOCK_NO_WJIT": "1"}, {"FS_SEG_NO_LJIT": "1"},
+                                 {"FS_BLOCK_K": "11", "FS_SEG_NO_LJIT": "1"}])
 def test_gpu_block_engines_match_reference_and_oracle(cuda, name, env, monkeypatch):
     """Post-selected programs with every segment through the block engine (FS_BLOCK_K=1: warp or
     CTA per shot from k = 1), through lane-per-shot segments up to k = 10 (FS_BLOCK_K=11), and by
@@ -401,7 +402,7 @@ def test_gpu_star_groups_match_oracle(cuda, k, seed, env, monkeypatch):
     assert a.accepted_bits().all()
     # the specialised segment kernel compiled (a failed compile would fall back to the interpreter)
     interpreted = "FS_BLOCK_NO_JIT" in env or (k <= 10 and "FS_BLOCK_NO_WJIT" in env and "FS_BLOCK_JIT_WARP" not in env)
-    assert ("segments: ready kernels=1" in dp.jit_status()) == (not interpreted), dp.jit_status()
+    assert ("segments: ready kernels=1 " in dp.jit_status()) == (not interpreted), dp.jit_status()
     cuts = P.meta["cuts"]
     ns = 8
     _, g, tb = dp.sample_host(ns, seed=11, flags=FS_RNG_SPLITMIX | FS_FORCE_SEGMENTED, want_state=True,
