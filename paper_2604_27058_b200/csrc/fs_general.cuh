@@ -95,6 +95,40 @@ struct WordFaultGen {
     if (num_cases(P, site) > 1) cs = pick_case_x(P, site, x);
     return 1;
   }
+  // step() in two halves for a consumer that owns one lane of the word: first the candidate --
+  // (site, lane), its uniform, whether the site is a certain one -- from the same Philox block and
+  // with the same stream position as step(); the thinning test and the case pick (dependent table
+  // loads, most of a step's latency) only for the candidates the consumer keeps (resolve)
+  __device__ __forceinline__ int step_cand(const DevProg& P, int& site, int& lane, double& x, int& certain) {
+    if (run >= P.num_runs) return 2;
+    const int start = __ldg(P.run_start + run), len = __ldg(P.run_len + run);
+    const uint4 b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), 0u, (TAG_NOISE << 24) | step_no++, seed);
+    const double u2 = u64_to_unit(((uint64_t)b.w << 32) | b.z);
+    if (len == 0) {
+      site = start;
+      lane = cl++;
+      if (cl == 32) { run++; cl = 0; }
+      x = u2;
+      certain = 1;
+      return 1;
+    }
+    const double g = floor(__dmul_rn(ln_unit(((uint64_t)b.y << 32) | b.x), __ldg(P.run_lp + run)));
+    c = __dadd_rn(__dadd_rn(c, 1.0), g);
+    if (!(c < (double)(32 * len))) { run++; c = -1.0; return 0; }
+    const long long ci = (long long)c;
+    lane = (int)(ci & 31);
+    site = start + (int)(ci >> 5);
+    x = __dmul_rn(u2, __ldg(P.run_q + run));  // uniform on [0, q)
+    certain = 0;
+    return 1;
+  }
+  // the case of a candidate, or -1 when thinning drops it
+  __device__ __forceinline__ static int resolve(const DevProg& P, int site, double x, int certain) {
+    if (!certain && !(x < __ldg(P.site_prob + site))) return -1;
+    int cs = __ldg(P.site_case_off + site);
+    if (num_cases(P, site) > 1) cs = certain ? pick_case(P, site, x) : pick_case_x(P, site, x);
+    return cs;
+  }
 };
 
 template <int CAP>

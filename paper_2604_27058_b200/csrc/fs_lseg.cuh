@@ -25,9 +25,12 @@ namespace fs {
 
 constexpr int kLsegUnrollK = 4;  // arrays up to 2^4 amplitudes are unrolled into registers
 
-template <int KARR>
+template <int KARR, int NLAZY>
 struct LCtx : SCtx {
   double2* __restrict__ arr;  // the shot's array: a thread-local array of 2^KARR in lseg_run
+  // Expands after the segment's last array-reading instruction are not executed: their phase pairs
+  // (picked at their program point) wait here and are applied when the survivor is saved
+  double2 lz0[NLAZY > 0 ? NLAZY : 1], lz1[NLAZY > 0 ? NLAZY : 1];
 
   __device__ __forceinline__ LCtx(const DevProg& P_, const RunArgs& A_, const SegArgs& S_, uint64_t si_, double2* arr_)
       : SCtx(P_, A_, S_, si_, true), arr(arr_) {}
@@ -160,8 +163,9 @@ struct LCtx : SCtx {
   }
 };
 
-// the shot loop of a specialised lane-per-shot segment: array of 2^KIN in, 2^KOUT out
-template <int KARR, int KIN, int KOUT, class Exec>
+// the shot loop of a specialised lane-per-shot segment: array of 2^KIN in, 2^KOUT out, the last
+// NLAZY Expands (2^(KOUT - NLAZY) -> 2^KOUT) folded into the save
+template <int KARR, int KIN, int KOUT, int NLAZY, class Exec>
 __device__ __forceinline__ void lseg_run(const DevProg& P, const RunArgs& A, const SegArgs& S, Exec&& exec) {
   const int lane = threadIdx.x & 31;
   const uint32_t nthreads = gridDim.x * blockDim.x;
@@ -171,7 +175,7 @@ __device__ __forceinline__ void lseg_run(const DevProg& P, const RunArgs& A, con
     const uint64_t si = S.first ? S.chunk0 + idx : (valid ? S.in.shot[idx] : 0);
     valid = valid && si < A.nshots;
     double2 arr[1 << KARR];
-    LCtx<KARR> c(P, A, S, si, arr);
+    LCtx<KARR, NLAZY> c(P, A, S, si, arr);
     double2 gamma = make_double2(1.0, 0.0);
     if (valid) {
       if (S.first) {
@@ -202,6 +206,7 @@ __device__ __forceinline__ void lseg_run(const DevProg& P, const RunArgs& A, con
       if (lane == 0 && surv) base = atomicAdd(S.n_out, (uint32_t)__popc(surv));
       base = __shfl_sync(0xFFFFFFFFu, base, 0);
       if (alive) {
+        c.settle_pending();
         const uint32_t slot = base + (uint32_t)__popc(surv & ((1u << lane) - 1u));
         const StateStore& O = S.out;
 #pragma unroll
@@ -215,8 +220,17 @@ __device__ __forceinline__ void lseg_run(const DevProg& P, const RunArgs& A, con
         gi[0] = c.gen.step_no; gi[1] = (uint32_t)c.gen.run; gi[2] = (uint32_t)c.gen.cl;
         gi[3] = (uint32_t)c.pend_site; gi[4] = (uint32_t)c.pend_lane; gi[5] = (uint32_t)c.pend_case;
         O.gen_c[slot] = c.gen.c;
-#pragma unroll(KOUT <= kLsegUnrollK ? (1 << KOUT) : 4)
-        for (uint32_t j = 0; j < (1u << KOUT); j++) O.amps[store_amp_index(slot, j, 1u << KOUT, O.shot_major)] = c.arr[j];
+        constexpr int KB = KOUT - NLAZY;  // array held at the save
+#pragma unroll(KOUT <= kLsegUnrollK ? (1 << NLAZY) : 1)
+        for (uint32_t hi = 0; hi < (1u << NLAZY); hi++) {
+#pragma unroll(KOUT <= kLsegUnrollK ? (1 << KB) : 4)
+          for (uint32_t j = 0; j < (1u << KB); j++) {
+            double2 v = c.arr[j];
+#pragma unroll
+            for (int t = 0; t < NLAZY; t++) v = cmul(v, ((hi >> t) & 1u) ? c.lz1[t] : c.lz0[t]);
+            O.amps[store_amp_index(slot, j | (hi << KB), 1u << KOUT, O.shot_major)] = v;
+          }
+        }
       }
     }
   }

@@ -114,7 +114,7 @@ struct EnvSwitches {
   bool no_affine = false;      // FS_NO_AFFINE: frame-only programs use the fault-list frame kernel
   bool block_no_jit = false;   // FS_BLOCK_NO_JIT: segmented engine interprets every segment
   bool block_jit_warp = false; // FS_BLOCK_JIT_WARP: also specialise warp-per-shot segments
-  bool block_no_wjit = false;  // FS_BLOCK_NO_WJIT: warp-per-shot segments keep the interpreter (no fs_wseg.cuh kernels)
+  bool block_no_wjit = false;  // FS_BLOCK_NO_WJIT: no packed-frame segment kernels (fs_wseg.cuh): warp-per-shot segments keep the interpreter, CTA-per-shot ones the shared-VM specialised form
   bool seg_no_ljit = false;    // FS_SEG_NO_LJIT: lane-per-shot segments keep the interpreter (no fs_lseg.cuh kernels)
   bool block_no_fuse = false;  // FS_BLOCK_NO_FUSE: block engine runs ArrayGates one sweep each (no star groups)
   int block_k = 0;             // FS_BLOCK_K: segment k at which a shot gets a warp / CTA (0 = default)
@@ -218,8 +218,9 @@ struct fs_prog {
   std::string pass_jit_err;
   // program-specialised segment kernels of the block engine (key: segment begin), Philox stream
   int seg_jit = 0;
+  std::map<int, int> seg_G;  // block segments in the packed-frame form (fs_wseg.cuh): threads per shot
   std::set<int> seg_lane;  // segment starts compiled as lane-per-shot kernels (fs_lseg.cuh)
-  std::map<int, int> seg_occ;  // their resident blocks per SM
+  std::map<int, int> seg_occ;  // resident blocks per SM of the specialised segment kernels
   std::vector<int32_t> h_next_array, h_frame_mat_off, h_fuse_at, h_fuse;
   std::map<int, fsjit::CUfunction> seg_fn;
   std::string seg_jit_err;
@@ -1072,11 +1073,16 @@ void gen_segment(std::ostringstream& o, const fs_prog* p, int b, int e, int karr
 
 // Warp-per-shot segments fully specialised (fs_wseg.cuh): scalar instructions included, the frame
 // bit-packed in registers.  Needs 2n <= 128 (frame matrices, case masks), <= 32 slots / observables.
+// threads of a CTA of G-thread shots: 16 warp shots, 15 two-warp shots (named barriers 1..15), one
+// CTA-wide shot
+int wseg_groups(int G) { return G == 32 ? fs::kBlockMaxGroups : (G == 256 ? 1 : 15); }
+int wseg_threads(int G) { return G * wseg_groups(G); }
+
 bool wseg_supported(const fs_prog* p) {
   return 2 * p->dp.n <= 128 && p->dp.num_slots <= 32 && p->dp.O <= 32 && p->dp.case_mask != nullptr;
 }
 
-void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int karr) {
+void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int karr, int G) {
   const int* IN = p->h_instrs.data();
   const int n = p->dp.n, R = p->dp.R;
   auto C = [&](int off) {
@@ -1098,11 +1104,29 @@ void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int ka
       case FS_G_H: o << "    c.g_h(" << va << ", " << n + va << ");\n"; break;
       case FS_G_CX: o << "    c.g_cx(" << va << ", " << n + va << ", " << vb << ", " << n + vb << ");\n"; break;
       case FS_G_CZ: o << "    c.g_cz(" << va << ", " << n + va << ", " << vb << ", " << n + vb << ");\n"; break;
+      case FS_G_SWAP: o << "    c.g_swap(" << va << ", " << n + va << ", " << vb << ", " << n + vb << ");\n"; break;
       default: break;
     }
   };
-  o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * fs::kBlockMaxGroups << ", 1) fs_seg_" << b
-    << "(DevProg P, RunArgs A, SegArgs S, int group_bytes) {\n  wseg_run(P, A, S, group_bytes, [&](WCtx& c) {\n";
+  // the frame side of instructions [i0, i1) gate by gate (wider groups have no warp to evaluate a
+  // frame matrix with)
+  auto frame_updates = [&](int i0, int i1) {
+    for (int i = i0; i < i1; i++) {
+      const int* I = IN + (size_t)i * FS_INS_WORDS;
+      const int op = FS_OPCODE(I[0]);
+      if (op == FS_OP_FRAME) {
+        for (int j = 0; j < I[2]; j++) {
+          const uint32_t g = p->h_gates[I[1] + j];
+          frame_gate(FS_GATE_G(g), FS_GATE_A(g), FS_GATE_B(g));
+        }
+      } else if (op == FS_OP_ARRAY_GATE) {
+        frame_gate(I[1], I[2], I[3]);
+      }
+    }
+  };
+  o << "extern \"C\" __global__ void __launch_bounds__(" << wseg_threads(G) << ", " << (G == 256 ? 3 : 1) << ") fs_seg_" << b
+    << "(DevProg P, RunArgs A, SegArgs S, int group_bytes) {\n  wseg_run<" << G << ", " << karr << ">(P, A, S, group_bytes, [&](WCtxT<" << G
+    << ">& c) {\n";
   for (int i = b; i < e;) {
     const int* I = IN + (size_t)i * FS_INS_WORDS;
     const int op = FS_OPCODE(I[0]), flip = FS_FLIP(I[0]);
@@ -1111,7 +1135,9 @@ void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int ka
     if (op == FS_OP_ARRAY_GATE && p->h_fuse_at[i] >= 0) {
       const int32_t* Dg = p->h_fuse.data() + (size_t)8 * p->h_fuse_at[i];
       const bool hasAR = (Dg[4] & 8) != 0;
-      o << "    c.frame_mat(" << Dg[7] << ");\n    {\n";
+      if (G == 32) o << "    c.frame_mat(" << Dg[7] << ");\n";
+      else frame_updates(i, i + Dg[0]);
+      o << "    {\n";
       if (hasAR) {
         const int virt = Dg[5] & 0xFFFF, fp = Dg[6];
         o << "      const uint32_t par = c.fbit(" << virt << ");\n      const double2 e0 = " << C(fp) << ", e1 = " << C(fp + 2)
@@ -1127,7 +1153,8 @@ void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int ka
     }
     switch (op) {
       case FS_OP_FRAME:
-        o << "    c.frame_mat(" << p->h_frame_mat_off[i] << ");\n";
+        if (G == 32) o << "    c.frame_mat(" << p->h_frame_mat_off[i] << ");\n";
+        else frame_updates(i, i + 1);
         break;
       case FS_OP_ARRAY_GATE:
         o << "    c.gate(" << I[1] << ", " << I[4] << ", " << I[5] << ", " << size << "u);\n";
@@ -1225,12 +1252,33 @@ void gen_segment_l(std::ostringstream& o, const fs_prog* p, int b, int e, int ka
       case FS_G_H: o << "    c.g_h(" << va << ", " << n + va << ");\n"; break;
       case FS_G_CX: o << "    c.g_cx(" << va << ", " << n + va << ", " << vb << ", " << n + vb << ");\n"; break;
       case FS_G_CZ: o << "    c.g_cz(" << va << ", " << n + va << ", " << vb << ", " << n + vb << ");\n"; break;
+      case FS_G_SWAP: o << "    c.g_swap(" << va << ", " << n + va << ", " << vb << ", " << n + vb << ");\n"; break;
       default: break;
     }
   };
+  // Expands after the last array-reading instruction are deferred to the save (fs_lseg.cuh)
+  int lazy_from = b;
+  for (int i = b; i < e; i++) {
+    const int op = FS_OPCODE(IN[(size_t)i * FS_INS_WORDS]);
+    if (op == FS_OP_ARRAY_GATE || op == FS_OP_ARRAY_ROT || op == FS_OP_MEAS_ACTIVE || op == FS_OP_MEAS_COLLAPSE || op == FS_OP_RETIRE)
+      lazy_from = i + 1;
+  }
+  int nlazy = 0, karr_eff = k_in;
+  for (int i = b; i < e; i++) {
+    const int op = FS_OPCODE(IN[(size_t)i * FS_INS_WORDS]);
+    if (i >= lazy_from && op == FS_OP_EXPAND) nlazy++;
+    else if (i < lazy_from) karr_eff = std::max(karr_eff, p->h_sched[i]);
+  }
+  if (nlazy > 6) {  // keep the pending phase pairs few: the earliest Expands run eagerly
+    int skip = nlazy - 6;
+    for (int i = lazy_from; i < e && skip > 0; i++)
+      if (FS_OPCODE(IN[(size_t)i * FS_INS_WORDS]) == FS_OP_EXPAND) { lazy_from = i + 1; karr_eff = std::max(karr_eff, p->h_sched[i]); skip--; nlazy--; }
+  }
+  (void)karr;
   o << "extern \"C\" __global__ void __launch_bounds__(128) fs_seg_" << b
-    << "(DevProg P, RunArgs A, SegArgs S, int group_bytes) {\n  lseg_run<" << karr << ", " << k_in << ", " << k_out
-    << ">(P, A, S, [&](LCtx<" << karr << ">& c) {\n";
+    << "(DevProg P, RunArgs A, SegArgs S, int group_bytes) {\n  lseg_run<" << karr_eff << ", " << k_in << ", " << k_out << ", " << nlazy
+    << ">(P, A, S, [&](LCtx<" << karr_eff << ", " << nlazy << ">& c) {\n";
+  int lz = 0;
   for (int i = b; i < e; i++) {
     const int* I = IN + (size_t)i * FS_INS_WORDS;
     const int op = FS_OPCODE(I[0]), flip = FS_FLIP(I[0]);
@@ -1247,6 +1295,12 @@ void gen_segment_l(std::ostringstream& o, const fs_prog* p, int b, int e, int ka
         frame_gate(I[1], I[2], I[3]);
         break;
       case FS_OP_EXPAND:
+        if (i >= lazy_from) {
+          o << "    { const uint32_t par = c.fbit(" << I[1] << "); c.lz0[" << lz << "] = par ? " << C(I[5] + 4) << " : " << C(I[5])
+            << "; c.lz1[" << lz << "] = par ? " << C(I[5] + 6) << " : " << C(I[5] + 2) << "; }\n";
+          lz++;
+          break;
+        }
         o << "    { const uint32_t par = c.fbit(" << I[1] << "); c.expand<" << I[6] << ">(par ? " << C(I[5] + 4) << " : " << C(I[5])
           << ", par ? " << C(I[5] + 6) << " : " << C(I[5] + 2) << "); }\n";
         break;
@@ -1329,13 +1383,17 @@ int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector
       if (karr > kLsegMaxK || !wseg_supported(p) || p->env.seg_no_ljit) continue;
       gen_segment_l(o, p, bounds[s], bounds[s + 1], karr, bounds[s] > 0 ? sched[bounds[s] - 1] : 0, sched[bounds[s + 1] - 1]);
       p->seg_lane.insert(bounds[s]);
-    } else if (karr <= 10 && wseg_supported(p) && !p->env.block_no_wjit) {
-      // warp-per-shot segments: fully specialised (fs_wseg.cuh)
-      gen_segment_w(o, p, bounds[s], bounds[s + 1], karr);
+    } else if (wseg_supported(p) && !p->env.block_no_wjit) {
+      // warp-per-shot (k <= 10) and CTA-per-shot segments fully specialised, packed frame in
+      // registers (fs_wseg.cuh); two warps per shot measured no faster than one at k = 9-10
+      const int G = karr <= 10 ? 32 : 256;
+      gen_segment_w(o, p, bounds[s], bounds[s + 1], karr, G);
+      p->seg_G[bounds[s]] = G;
     } else {
-      // CTA-per-shot segments: specialised sweeps around the shared scalar VM (measured 1.2-1.8x
-      // faster); warp-per-shot ones in that form ran ~2x slower than interpreted (instruction-fetch
-      // stalls) and keep the interpreter unless FS_BLOCK_JIT_WARP is set
+      // programs beyond the packed frame (2n > 128, > 32 slots) or FS_BLOCK_NO_WJIT: CTA-per-shot
+      // segments as specialised sweeps around the shared scalar VM (measured 1.2-1.8x faster than
+      // interpreted); warp-per-shot ones in that form ran ~2x slower than interpreted (instruction-
+      // fetch stalls) and keep the interpreter unless FS_BLOCK_JIT_WARP is set
       if (karr <= 10 && !p->env.block_jit_warp) continue;
       gen_segment(o, p, bounds[s], bounds[s + 1], karr, karr <= 10 ? 32 : 256);
     }
@@ -1375,27 +1433,37 @@ int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector
 
 int launch_block_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cudaStream_t stream) {
   const fs::DevProg& dp = p->dp;
-  const size_t group_bytes = align_up(((size_t)16 << karr) + (size_t)4 * (2 * dp.n + dp.num_slots + dp.O + 4), 16);
+  // per shot: the array, then the interpreter's frame words / the packed-frame kernels' scratch
+  const size_t group_bytes = align_up(((size_t)16 << karr) + std::max<size_t>(256, (size_t)4 * (2 * dp.n + dp.num_slots + dp.O + 4)), 16);
   if (group_bytes > kSmemBudget) return set_error(FS_ERR_ARG, "active array too large for the block engine");
+  const bool sm = a.flags & FS_RNG_SPLITMIX;
+  const bool trace = a.fault_modes || a.forced || a.t_fx || a.t_gamma || a.t_amps || a.t_draws || a.t_rec || a.ncp;
+  auto fit = p->seg_fn.find(S.seg_begin);
+  const bool jit = !sm && !trace && p->seg_jit == 1 && fit != p->seg_fn.end() && !p->env.block_no_jit;
   const bool warp_mode = karr <= 10;
-  // as many warp groups as fit next to the static shared arrays (a k = 10 shot is ~17 KB)
+  // threads per shot: the packed-frame kernels carry their own, else a warp (k <= 10) or a CTA
+  auto git = p->seg_G.find(S.seg_begin);
+  const int G = jit && git != p->seg_G.end() ? git->second : (warp_mode ? 32 : 256);
+  // as many shots per CTA as fit next to the static shared arrays (a k = 10 shot is ~17 KB)
   const size_t dyn_budget = 220 * 1024;
-  const int ngroups = warp_mode ? (int)std::max<size_t>(1, std::min<size_t>(fs::kBlockMaxGroups, dyn_budget / group_bytes)) : 1;
-  const int nt = warp_mode ? 32 * ngroups : 256;
+  const int ngroups = G == 256 ? 1 : (int)std::max<size_t>(1, std::min<size_t>(wseg_groups(G), dyn_budget / group_bytes));
+  const int nt = G * ngroups;
   const size_t smem = group_bytes * ngroups;
   void (*kern)(fs::DevProg, fs::RunArgs, fs::SegArgs, int, int);
-  const bool sm = a.flags & FS_RNG_SPLITMIX;
   if (warp_mode) kern = sm ? fs::block_kernel<true, 32> : fs::block_kernel<false, 32>;
   else kern = sm ? fs::block_kernel<true, 256> : fs::block_kernel<false, 256>;
-  FS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int occ = occupancy_blocks(kern, nt, smem);
   const size_t blocks_needed = (S.n_in + ngroups - 1) / ngroups;
-  const size_t grid = std::max<size_t>(1, std::min<size_t>(blocks_needed, (size_t)p->num_sms * occ));
-  auto fit = p->seg_fn.find(S.seg_begin);
-  const bool trace = a.fault_modes || a.forced || a.t_fx || a.t_gamma || a.t_amps || a.t_draws || a.t_rec || a.ncp;
-  if (!sm && !trace && p->seg_jit == 1 && fit != p->seg_fn.end() && !p->env.block_no_jit) {  // specialised kernel
+  if (jit) {  // specialised kernel
     fsjit::Api& J = fsjit::api();
     if (J.cuFuncSetAttribute(fit->second, 8, (int)smem) != 0) return set_error(FS_ERR_CUDA, "cuFuncSetAttribute(fs_seg)");
+    int occ = 0;
+    auto oit = p->seg_occ.find(S.seg_begin);  // threads and shared memory are fixed per segment
+    if (oit != p->seg_occ.end()) occ = oit->second;
+    else {
+      if (J.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fit->second, nt, smem) != 0 || occ < 1) occ = 1;
+      p->seg_occ[S.seg_begin] = occ;
+    }
+    const size_t grid = std::max<size_t>(1, std::min<size_t>(blocks_needed, (size_t)p->num_sms * occ));
     fs::DevProg dpv = dp;
     fs::RunArgs av = a;
     fs::SegArgs sv = S;
@@ -1408,6 +1476,9 @@ int launch_block_kernel(fs_prog* p, fs::RunArgs& a, fs::SegArgs& S, int karr, cu
     if (r != 0) return set_error(FS_ERR_CUDA, "cuLaunchKernel(fs_seg) failed: " + std::to_string(r));
     return FS_OK;
   }
+  FS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int occ = occupancy_blocks(kern, nt, smem);
+  const size_t grid = std::max<size_t>(1, std::min<size_t>(blocks_needed, (size_t)p->num_sms * occ));
   kt_begin(p, stream);
   kern<<<(unsigned)grid, nt, smem, stream>>>(dp, a, S, karr, (int)group_bytes);
   kt_end(p, stream);

@@ -37,7 +37,8 @@ struct SCtx {
   uint32_t slots, obs;  // packed record / detector slots, observables
   int alive, err;
   WordFaultGen gen;
-  int pend_site, pend_lane, pend_case;
+  int pend_site, pend_lane, pend_case, pend_certain;
+  double pend_x;
   int coin_blk;
   uint4 coin_b;
   int branch;
@@ -51,6 +52,8 @@ struct SCtx {
     pend_site = -1;
     pend_lane = 0;
     pend_case = 0;
+    pend_certain = 0;
+    pend_x = 0.0;
     branch = 0;
     coin_blk = -1;
     coin_b = make_uint4(0, 0, 0, 0);
@@ -77,6 +80,13 @@ struct SCtx {
   __device__ __forceinline__ void g_cz(int xa, int za, int xb, int zb) {
     fxor(zb, fbit(xa));
     fxor(za, fbit(xb));
+  }
+  __device__ __forceinline__ void g_swap(int xa, int za, int xb, int zb) {
+    const uint32_t tx = fbit(xa) ^ fbit(xb), tz = fbit(za) ^ fbit(zb);
+    fxor(xa, tx);
+    fxor(xb, tx);
+    fxor(za, tz);
+    fxor(zb, tz);
   }
   __device__ __forceinline__ void xor_mask(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
     F[0] ^= m0; F[1] ^= m1; F[2] ^= m2; F[3] ^= m3;
@@ -109,22 +119,39 @@ struct SCtx {
     if (sl >= 0) slots = (slots & ~(1u << sl)) | (v << sl);
   }
 
-  // NoiseBlock over sites < hi: the word's fault stream, this shot's lane (fs_block.cuh scalar_step)
+  // NoiseBlock over sites < hi: the word's fault stream, this shot's lane.  The same stream and the
+  // same faults as fs_block.cuh scalar_step, but a candidate is resolved (thinning test, case pick:
+  // dependent table loads) only if it is this shot's; another lane's candidate is just a place to
+  // stop at (pend_case == -2: unresolved)
   __device__ __forceinline__ void noise(int hi) {
     for (;;) {
       if (pend_site < 0) {
-        int st_, ln_, cs_;
-        const int r = gen.step(P, st_, ln_, cs_);
+        int st_, ln_, ce_;
+        double x_;
+        const int r = gen.step_cand(P, st_, ln_, x_, ce_);
         if (r == 2) { pend_site = 0x7FFFFFFF; break; }
         if (r == 0) continue;
-        pend_site = st_; pend_lane = ln_; pend_case = cs_;
+        pend_site = st_; pend_lane = ln_; pend_case = -2; pend_x = x_; pend_certain = ce_;
       }
       if (pend_site >= hi) break;
       if (pend_lane == mylane) {
-        const uint4 m = __ldg(P.case_mask + pend_case);
-        xor_mask(m.x, m.y, m.z, m.w);
+        const int cs = pend_case == -2 ? WordFaultGen::resolve(P, pend_site, pend_x, pend_certain) : pend_case;
+        if (cs >= 0) {
+          const uint4 m = __ldg(P.case_mask + cs);
+          xor_mask(m.x, m.y, m.z, m.w);
+        }
       }
       pend_site = -1;
+    }
+  }
+  // before the state goes to the survivor store: other engines expect a resolved pending fault; a
+  // candidate of another lane or one that thinning drops is no fault of this shot, the next
+  // NoiseBlock just goes on stepping
+  __device__ __forceinline__ void settle_pending() {
+    if (pend_site >= 0 && pend_site != 0x7FFFFFFF && pend_case == -2) {
+      const int cs = pend_lane == mylane ? WordFaultGen::resolve(P, pend_site, pend_x, pend_certain) : -1;
+      if (cs >= 0) pend_case = cs;
+      else { pend_site = -1; pend_case = 0; }
     }
   }
 
@@ -145,15 +172,27 @@ struct SCtx {
   }
 };
 
-struct WCtx : SCtx {
+// G threads per shot: 32 (one warp, warp barriers and shuffles), 64 .. 256 (warps of one CTA behind a
+// named barrier; per-warp partial sums and broadcast words go through the shot's scratch `scr`)
+template <int G>
+struct WCtxT : SCtx {
   double2* amp;
-  int tid;
+  double* scr;  // G > 32: 2 * (G / 32) doubles of partial sums, then 4 words
+  int tid, bar_id;
 
-  __device__ __forceinline__ WCtx(const DevProg& P_, const RunArgs& A_, const SegArgs& S_, double2* amp_, int tid_, uint64_t si_)
-      : SCtx(P_, A_, S_, si_, tid_ == 0), amp(amp_), tid(tid_) {}
+  __device__ __forceinline__ WCtxT(const DevProg& P_, const RunArgs& A_, const SegArgs& S_, double2* amp_, double* scr_, int tid_,
+                                   int bar_id_, uint64_t si_)
+      : SCtx(P_, A_, S_, si_, tid_ == 0), amp(amp_), scr(scr_), tid(tid_), bar_id(bar_id_) {}
+
+  // barrier of the shot's threads
+  __device__ __forceinline__ void sync() const {
+    if (G == 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(G) : "memory");
+  }
 
   // FrameGates (or a star group's frame side) as a GF(2) matrix: v'_r = parity(row_r & v)
   __device__ __forceinline__ void frame_mat(int mo) {
+    static_assert(G == 32, "frame matrices are evaluated by one warp; wider groups update the frame gate by gate");
     const int n2 = 2 * P.n;
     uint32_t o[4];
 #pragma unroll
@@ -174,13 +213,13 @@ struct WCtx : SCtx {
   __device__ __forceinline__ void gate(int g, int a, int b, uint32_t size) {
     if (g == FS_G_S || g == FS_G_SDAG) {
       const double2 ph = make_double2(0.0, g == FS_G_S ? 1.0 : -1.0);
-      for (uint32_t j = tid; j < size / 2; j += 32) {
+      for (uint32_t j = tid; j < size / 2; j += G) {
         const uint32_t id = ins0(j, a) | (1u << a);
         amp[id] = cmul(amp[id], ph);
       }
     } else if (g == FS_G_H) {
       const uint32_t st = 1u << a;
-      for (uint32_t j = tid; j < size / 2; j += 32) {
+      for (uint32_t j = tid; j < size / 2; j += G) {
         const uint32_t i0 = ins0(j, a);
         const double2 lo = amp[i0], hi = amp[i0 + st];
         amp[i0] = cscale(cadd(lo, hi), kInvSqrt2);
@@ -188,7 +227,7 @@ struct WCtx : SCtx {
       }
     } else {
       const int lo_ax = a < b ? a : b, hi_ax = a < b ? b : a;
-      for (uint32_t j = tid; j < size / 4; j += 32) {
+      for (uint32_t j = tid; j < size / 4; j += G) {
         const uint32_t id = ins0(ins0(j, lo_ax), hi_ax) | (1u << a);
         const uint32_t jd = id | (1u << b);
         if (g == FS_G_CX) {
@@ -201,21 +240,21 @@ struct WCtx : SCtx {
         }
       }
     }
-    __syncwarp();
+    sync();
   }
 
   __device__ __forceinline__ void expand(uint32_t size, double2 ph0, double2 ph1) {
-    for (uint32_t j = tid; j < size; j += 32) {
+    for (uint32_t j = tid; j < size; j += G) {
       const double2 v = amp[j];
       amp[j] = cmul(v, ph0);
       amp[size + j] = cmul(v, ph1);
     }
-    __syncwarp();
+    sync();
   }
 
   __device__ __forceinline__ void array_rot(int a, uint32_t size, double2 ph0, double2 ph1) {
-    for (uint32_t j = tid; j < size; j += 32) amp[j] = cmul(amp[j], ((j >> a) & 1) ? ph1 : ph0);
-    __syncwarp();
+    for (uint32_t j = tid; j < size; j += G) amp[j] = cmul(amp[j], ((j >> a) & 1) ? ph1 : ph0);
+    sync();
   }
 
   // star group (fs_block.cuh star_group_t); ph0 / ph1 = the closing ArrayRot's phases for bit 0 / 1
@@ -244,7 +283,7 @@ struct WCtx : SCtx {
     };
     const bool touch_lo = hasH || hasAR;
     if (M == 0u) {
-      for (uint32_t j = tid; j < size / 2; j += 32) {
+      for (uint32_t j = tid; j < size / 2; j += G) {
         const uint32_t i0 = ins0(j, a);
         const double2 hi = hiphase(i0 | A_, amp[i0 | A_]);
         if (touch_lo) finish(i0, amp[i0], hi);
@@ -253,7 +292,7 @@ struct WCtx : SCtx {
     } else {
       const int m = __ffs((int)M) - 1;
       const int lo_ax = a < m ? a : m, hi_ax = a < m ? m : a;
-      for (uint32_t j = tid; j < size / 4; j += 32) {
+      for (uint32_t j = tid; j < size / 4; j += G) {
         const uint32_t i0 = ins0(ins0(j, lo_ax), hi_ax), i1 = i0 ^ M;
         const double2 h0 = amp[i1 | A_], h1 = amp[i0 | A_];
         const double2 n0 = hiphase(i0 | A_, h0), n1 = hiphase(i1 | A_, h1);
@@ -266,7 +305,7 @@ struct WCtx : SCtx {
         }
       }
     }
-    __syncwarp();
+    sync();
   }
 
   // MeasActive / MeasCollapse (fs_block.cuh measure + meas_decide); xv = frame bit of the measured
@@ -277,7 +316,7 @@ struct WCtx : SCtx {
                                           double2 u01, double2 u10, double2 u11) {
     const uint32_t half = size >> 1, st = 1u << a;
     double s1 = 0.0, sa = 0.0;
-    for (uint32_t j = tid; j < half; j += 32) {
+    for (uint32_t j = tid; j < half; j += G) {
       const uint32_t i0 = ins0(j, a);
       const double2 a0 = amp[i0], a1 = amp[i0 + st];
       if (COLLAPSE) s1 = __dadd_rn(s1, cnorm2(cadd(cmul(a0, u10), cmul(u11, a1))));
@@ -287,13 +326,30 @@ struct WCtx : SCtx {
 #pragma unroll
     for (int w = 16; w; w >>= 1) {  // the block engine's tree: element t += element t + w
       const double o1 = __shfl_down_sync(0xFFFFFFFFu, s1, w), o2 = __shfl_down_sync(0xFFFFFFFFu, sa, w);
-      if (tid < w) {
+      if ((tid & 31) < w) {
         s1 = __dadd_rn(s1, o1);
         sa = __dadd_rn(sa, o2);
       }
     }
-    double p1 = __shfl_sync(0xFFFFFFFFu, s1, 0);
-    const double p_all = __shfl_sync(0xFFFFFFFFu, sa, 0);
+    double p1, p_all;
+    if (G == 32) {
+      p1 = __shfl_sync(0xFFFFFFFFu, s1, 0);
+      p_all = __shfl_sync(0xFFFFFFFFu, sa, 0);
+    } else {  // warp sums in warp order, by every thread
+      if ((tid & 31) == 0) {
+        scr[2 * (tid >> 5)] = s1;
+        scr[2 * (tid >> 5) + 1] = sa;
+      }
+      sync();
+      p1 = scr[0];
+      p_all = scr[1];
+#pragma unroll
+      for (int w = 1; w < G / 32; w++) {
+        p1 = __dadd_rn(p1, scr[2 * w]);
+        p_all = __dadd_rn(p_all, scr[2 * w + 1]);
+      }
+      sync();
+    }
     const uint32_t parity = fbit(xv);
     if (p1 != p1) {
       err = FS_ERR_SHOT_NAN;
@@ -315,38 +371,38 @@ struct WCtx : SCtx {
       const double2 k0 = br == 0 ? cscale(u00, scale) : cscale(u10, scale);
       const double2 k1 = br == 0 ? cscale(u01, scale) : cscale(u11, scale);
       fxor(xv, (uint32_t)br);
-      for (uint32_t b0 = 0; b0 < half; b0 += 32) {  // in place, strip by strip
+      for (uint32_t b0 = 0; b0 < half; b0 += G) {  // in place, strip by strip
         const uint32_t j = b0 + tid;
         double2 val = make_double2(0.0, 0.0);
         if (j < half) {
           const uint32_t i0 = ins0(j, a);
           val = cadd(cmul(k0, amp[i0]), cmul(k1, amp[i0 + st]));
         }
-        __syncwarp();
+        sync();
         if (j < half) amp[j] = val;
-        __syncwarp();
+        sync();
       }
     } else {
       const double s = renorm ? __ddiv_rn(1.0, __dsqrt_rn(pb)) : 1.0;
       const uint32_t dead = 1u - (uint32_t)br;
-      for (uint32_t j = tid; j < size; j += 32) {
+      for (uint32_t j = tid; j < size; j += G) {
         if (((j >> a) & 1) == dead) amp[j] = make_double2(0.0, 0.0);
         else if (renorm) amp[j] = cscale(amp[j], s);
       }
-      __syncwarp();
+      sync();
     }
     return true;
   }
 
   __device__ __forceinline__ void retire(int xv, int a, uint32_t size) {
     const uint32_t half = size >> 1;
-    for (uint32_t b0 = 0; b0 < half; b0 += 32) {
+    for (uint32_t b0 = 0; b0 < half; b0 += G) {
       const uint32_t j = b0 + tid;
       double2 val = make_double2(0.0, 0.0);
       if (j < half) val = amp[ins0(j, a) + ((uint32_t)branch << a)];
-      __syncwarp();
+      sync();
       if (j < half) amp[j] = val;
-      __syncwarp();
+      sync();
     }
     fxor(xv, (uint32_t)branch);
   }
@@ -354,23 +410,27 @@ struct WCtx : SCtx {
 
 // the shot loop of a specialised warp-per-shot segment (fs_block.cuh block_run without the shared
 // frame): one warp per shot, `group_bytes` of dynamic shared memory per warp for the array
-template <class Exec>
+template <int G, int KARR, class Exec>
 __device__ __forceinline__ void wseg_run(const DevProg& P, const RunArgs& A, const SegArgs& S, int group_bytes,
                                          Exec&& exec) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int group = threadIdx.x >> 5, ngroups = blockDim.x >> 5, tid = threadIdx.x & 31;
+  const int group = threadIdx.x / G, ngroups = blockDim.x / G, tid = threadIdx.x % G;
   double2* amp = reinterpret_cast<double2*>(smem_raw + (size_t)group * group_bytes);
+  // the shot's scratch follows its array (fs_sampler.cu launch_block_kernel leaves >= 256 bytes)
+  double* scr = reinterpret_cast<double*>(smem_raw + (size_t)group * group_bytes + ((size_t)16 << KARR));
+  uint32_t* scrw = reinterpret_cast<uint32_t*>(scr + 2 * (G / 32));
+  const int bar_id = ngroups == 1 ? 0 : group + 1;
   for (uint32_t idx = blockIdx.x * ngroups + group; idx < S.n_in; idx += gridDim.x * ngroups) {
     const uint64_t si = S.first ? S.chunk0 + idx : S.in.shot[idx];
     if (si >= A.nshots) continue;
-    WCtx c(P, A, S, amp, tid, si);
+    WCtxT<G> c(P, A, S, amp, scr, tid, bar_id, si);
     double2 gamma = make_double2(1.0, 0.0);
     if (S.first) {
       if (tid == 0) amp[0] = make_double2(1.0, 0.0);
     } else {
       const StateStore& I = S.in;
       const uint32_t sz = 1u << S.k_in;
-      for (uint32_t j = tid; j < sz; j += 32) {
+      for (uint32_t j = tid; j < sz; j += G) {
         const uint32_t d = (uint32_t)__cvta_generic_to_shared(amp + j);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(I.amps + store_amp_index(idx, j, sz, I.shot_major)) : "memory");
       }
@@ -379,9 +439,9 @@ __device__ __forceinline__ void wseg_run(const DevProg& P, const RunArgs& A, con
       gamma = I.gamma[idx];
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
-    __syncwarp();
+    c.sync();
     exec(c);
-    __syncwarp();
+    c.sync();
     const bool alive = c.alive != 0, errored = c.err != 0;
     if (tid == 0 && errored) {
       atomicOr(A.error + (si >> 5), 1u << (si & 31));
@@ -393,15 +453,21 @@ __device__ __forceinline__ void wseg_run(const DevProg& P, const RunArgs& A, con
       if (alive && !errored) c.out_bit(A.accepted);
     }
     if (!S.last && alive) {  // survivor: compact into the output store
+      c.settle_pending();
       uint32_t slot = 0;
       if (tid == 0) slot = atomicAdd(S.n_out, 1u);
-      slot = __shfl_sync(0xFFFFFFFFu, slot, 0);
+      if (G == 32) slot = __shfl_sync(0xFFFFFFFFu, slot, 0);
+      else {
+        if (tid == 0) scrw[0] = slot;
+        c.sync();
+        slot = scrw[0];
+      }
       const StateStore& O = S.out;
 #pragma unroll
       for (int k = 0; k < 4; k++)
         if (k < S.nfw && tid == k) O.frame[(size_t)slot * S.nfw + k] = c.F[k];
       const uint32_t sz = 1u << S.k_out;
-      for (uint32_t j = tid; j < sz; j += 32) O.amps[store_amp_index(slot, j, sz, O.shot_major)] = amp[j];
+      for (uint32_t j = tid; j < sz; j += G) O.amps[store_amp_index(slot, j, sz, O.shot_major)] = amp[j];
       if (tid == 0) {
         if (S.nsw) O.slotbits[(size_t)slot * S.nsw] = c.slots;
         if (S.now) O.obsbits[(size_t)slot * S.now] = c.obs;
@@ -413,7 +479,7 @@ __device__ __forceinline__ void wseg_run(const DevProg& P, const RunArgs& A, con
         O.gen_c[slot] = c.gen.c;
       }
     }
-    __syncwarp();
+    c.sync();
   }
 }
 

@@ -381,7 +381,7 @@ def test_gpu_block_engines_match_reference_and_oracle(cuda, name, env, monkeypat
 @pytest.mark.parametrize("env", [{"FS_BLOCK_K": "1"}, {"FS_BLOCK_K": "1", "FS_BLOCK_NO_JIT": "1"},
                                  {"FS_BLOCK_K": "1", "FS_BLOCK_NO_WJIT": "1"},
                                  {"FS_BLOCK_K": "1", "FS_BLOCK_NO_WJIT": "1", "FS_BLOCK_JIT_WARP": "1"},
-                                 {"FS_BLOCK_K": "1", "FS_BLOCK_NO_FUSE": "1"}])
+                                 {"FS_BLOCK_K": "1", "FS_BLOCK_NO_FUSE": "1"}, {}, {"FS_SEG_NO_LJIT": "1"}])
 def test_gpu_star_groups_match_oracle(cuda, k, seed, env, monkeypatch):
     """The block engine's fused ArrayGate runs (star groups: CX / CZ / S through one pivot axis,
     an optional H and ArrayRot, FrameGates in between; interpreter, specialised CTA-per-shot
@@ -401,8 +401,11 @@ def test_gpu_star_groups_match_oracle(cuda, k, seed, env, monkeypatch):
     np.testing.assert_array_equal(a.accepted_bits(), b.accepted_bits())
     assert a.accepted_bits().all()
     # the specialised segment kernel compiled (a failed compile would fall back to the interpreter)
-    interpreted = "FS_BLOCK_NO_JIT" in env or (k <= 10 and "FS_BLOCK_NO_WJIT" in env and "FS_BLOCK_JIT_WARP" not in env)
-    assert ("segments: ready kernels=1 " in dp.jit_status()) == (not interpreted), dp.jit_status()
+    if "FS_BLOCK_K" in env:
+        interpreted = "FS_BLOCK_NO_JIT" in env or (k <= 10 and "FS_BLOCK_NO_WJIT" in env and "FS_BLOCK_JIT_WARP" not in env)
+        assert ("segments: ready kernels=1 " in dp.jit_status()) == (not interpreted), dp.jit_status()
+    elif k < 9:  # default threshold: both segments are lane-per-shot (fs_lseg.cuh, FrameGates with SWAP gate by gate)
+        assert ("segments: ready kernels=0 lane=2" in dp.jit_status()) == ("FS_SEG_NO_LJIT" not in env), dp.jit_status()
     cuts = P.meta["cuts"]
     ns = 8
     _, g, tb = dp.sample_host(ns, seed=11, flags=FS_RNG_SPLITMIX | FS_FORCE_SEGMENTED, want_state=True,

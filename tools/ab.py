@@ -1,6 +1,6 @@
-"""A/B the affine frame kernel under generator switches: bit-equality with the first variant and
-device time per launch (CUDA events, 1e7 shots of a config).
-    python tools/aff_ab.py CFG "ENV=1,ENV2=3" "..."      ("" = defaults)"""
+"""A/B a config's kernels under generator / engine switches: bit-equality with the first variant and
+device time per launch (CUDA events; the config's shots, or AB_SHOTS; AB_REPS launches).
+    python tools/ab.py CFG "ENV=1,ENV2=3" "..."      ("" = defaults)"""
 import json
 import os
 import sys
@@ -15,7 +15,8 @@ from paper_2604_27058_b200.program import Program  # noqa: E402
 cfg = int(sys.argv[1])
 variants = sys.argv[2:] or [""]
 P = Program.load(f"paper_2604_27058_b200/programs/c{cfg}.npz")
-shots = CONFIGS[cfg]["shots"]
+shots = int(os.environ.get("AB_SHOTS", CONFIGS[cfg]["shots"]))
+reps = int(os.environ.get("AB_REPS", 12))
 ref = None
 for v in variants:
     env = dict(kv.split("=", 1) for kv in v.split(",") if kv)
@@ -36,7 +37,7 @@ for v in variants:
         ref = got
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ms = []
-    for s in range(12):
+    for s in range(reps):
         flush.fill_(s)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
