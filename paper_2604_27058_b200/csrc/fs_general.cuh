@@ -101,9 +101,15 @@ struct WordFaultGen {
   // loads, most of a step's latency) only for the candidates the consumer keeps (resolve)
   __device__ __forceinline__ int step_cand(const DevProg& P, int& site, int& lane, double& x, int& certain) {
     if (run >= P.num_runs) return 2;
+    const uint4 b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), 0u, (TAG_NOISE << 24) | step_no, seed);
+    return step_with(P, ln_unit(((uint64_t)b.y << 32) | b.x), u64_to_unit(((uint64_t)b.w << 32) | b.z), site, lane, x, certain);
+  }
+  // the stream-position half of step_cand, given the step's two draws (L = ln of the gap uniform,
+  // u2 = the thinning / case uniform): consumers that draw a batch of steps at once (fs_wseg.cuh)
+  __device__ __forceinline__ int step_with(const DevProg& P, double L, double u2, int& site, int& lane, double& x,
+                                           int& certain) {
     const int start = __ldg(P.run_start + run), len = __ldg(P.run_len + run);
-    const uint4 b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), 0u, (TAG_NOISE << 24) | step_no++, seed);
-    const double u2 = u64_to_unit(((uint64_t)b.w << 32) | b.z);
+    step_no++;
     if (len == 0) {
       site = start;
       lane = cl++;
@@ -112,7 +118,7 @@ struct WordFaultGen {
       certain = 1;
       return 1;
     }
-    const double g = floor(__dmul_rn(ln_unit(((uint64_t)b.y << 32) | b.x), __ldg(P.run_lp + run)));
+    const double g = floor(__dmul_rn(L, __ldg(P.run_lp + run)));
     c = __dadd_rn(__dadd_rn(c, 1.0), g);
     if (!(c < (double)(32 * len))) { run++; c = -1.0; return 0; }
     const long long ci = (long long)c;

@@ -184,6 +184,46 @@ struct WCtxT : SCtx {
                                    int bar_id_, uint64_t si_)
       : SCtx(P_, A_, S_, si_, tid_ == 0), amp(amp_), scr(scr_), tid(tid_), bar_id(bar_id_) {}
 
+  // NoiseBlock (SCtx::noise) with the draws of 32 consecutive steps of the word's stream made at
+  // once: lane j of each warp holds the two draws of step cb0 + j (one Philox block and one ln per
+  // lane instead of per step), the walk over the steps reads them by shuffles.  All lanes of a
+  // warp hold the same shot, so they walk in lockstep; the stream position that goes to the
+  // survivor store is the plain one (step_no, run, cl, c), the batch is dropped at the segment end.
+  uint32_t cb0 = 0u;
+  bool chave = false;
+  double cL = 0.0, cU = 0.0;
+  __device__ __forceinline__ void noise(int hi) {
+    const int ln = tid & 31;
+    for (;;) {
+      if (pend_site < 0) {
+        if (gen.run >= P.num_runs) { pend_site = 0x7FFFFFFF; break; }
+        if (!chave || gen.step_no - cb0 >= 32u) {
+          cb0 = gen.step_no;
+          const uint4 b = philox((uint32_t)wabs, (uint32_t)(wabs >> 32), 0u, (TAG_NOISE << 24) | (cb0 + (uint32_t)ln), A.seed);
+          cU = u64_to_unit(((uint64_t)b.w << 32) | b.z);
+          cL = ln_unit(((uint64_t)b.y << 32) | b.x);
+          chave = true;
+        }
+        const int src = (int)(gen.step_no - cb0);
+        const double L = __shfl_sync(0xFFFFFFFFu, cL, src), u2 = __shfl_sync(0xFFFFFFFFu, cU, src);
+        int st_, ln_, ce_;
+        double x_;
+        const int r = gen.step_with(P, L, u2, st_, ln_, x_, ce_);
+        if (r == 0) continue;
+        pend_site = st_; pend_lane = ln_; pend_case = -2; pend_x = x_; pend_certain = ce_;
+      }
+      if (pend_site >= hi) break;
+      if (pend_lane == mylane) {
+        const int cs = pend_case == -2 ? WordFaultGen::resolve(P, pend_site, pend_x, pend_certain) : pend_case;
+        if (cs >= 0) {
+          const uint4 m = __ldg(P.case_mask + cs);
+          xor_mask(m.x, m.y, m.z, m.w);
+        }
+      }
+      pend_site = -1;
+    }
+  }
+
   // barrier of the shot's threads
   __device__ __forceinline__ void sync() const {
     if (G == 32) __syncwarp();
