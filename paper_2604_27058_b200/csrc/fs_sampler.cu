@@ -1108,8 +1108,9 @@ void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int ka
       default: break;
     }
   };
-  // the frame side of instructions [i0, i1) gate by gate (wider groups have no warp to evaluate a
-  // frame matrix with)
+  // the frame side of instructions [i0, i1) gate by gate: register instructions at constant bit
+  // positions (the GF(2) frame matrices of the interpreter cost a row load per frame bit: measured
+  // 43.1 vs 41.5 ms per 16.8M shots of config 4)
   auto frame_updates = [&](int i0, int i1) {
     for (int i = i0; i < i1; i++) {
       const int* I = IN + (size_t)i * FS_INS_WORDS;
@@ -1135,8 +1136,7 @@ void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int ka
     if (op == FS_OP_ARRAY_GATE && p->h_fuse_at[i] >= 0) {
       const int32_t* Dg = p->h_fuse.data() + (size_t)8 * p->h_fuse_at[i];
       const bool hasAR = (Dg[4] & 8) != 0;
-      if (G == 32) o << "    c.frame_mat(" << Dg[7] << ");\n";
-      else frame_updates(i, i + Dg[0]);
+      frame_updates(i, i + Dg[0]);
       o << "    {\n";
       if (hasAR) {
         const int virt = Dg[5] & 0xFFFF, fp = Dg[6];
@@ -1153,8 +1153,7 @@ void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int ka
     }
     switch (op) {
       case FS_OP_FRAME:
-        if (G == 32) o << "    c.frame_mat(" << p->h_frame_mat_off[i] << ");\n";
-        else frame_updates(i, i + 1);
+        frame_updates(i, i + 1);
         break;
       case FS_OP_ARRAY_GATE:
         o << "    c.gate(" << I[1] << ", " << I[4] << ", " << I[5] << ", " << size << "u);\n";
@@ -1375,29 +1374,37 @@ int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector
   o << "#include \"fs_lseg.cuh\"\nusing namespace fs;\n";
   std::vector<int> begins;
   const int* sched = p->h_sched.data();
-  for (size_t s = 0; s + 1 < bounds.size(); s++) {
-    const int karr = karrs[s];
+  // One kernel per PostSelect segment.  (Measured and not adopted: runs of consecutive warp- or CTA-
+  // per-shot segments as ONE kernel, a shot staying in shared memory across its PostSelects -- 15 %
+  // fewer instructions and no survivor-store round trips, but 77 vs 41.6 ms per 16.8M shots of
+  // config 4: the warps of a CTA then sit in different segments' straight-line code and stall on
+  // instruction fetch.)
+  const bool packed = wseg_supported(p) && !p->env.block_no_wjit;
+  const std::vector<int>& fb = bounds;
+  const std::vector<int>& fk = karrs;
+  for (size_t s = 0; s + 1 < fb.size(); s++) {
+    const int karr = fk[s];
     if (karr < block_k) {
       // lane-per-shot segments: fully specialised (fs_lseg.cuh) while the array fits thread-local
       // memory; the interpreter otherwise
       if (karr > kLsegMaxK || !wseg_supported(p) || p->env.seg_no_ljit) continue;
-      gen_segment_l(o, p, bounds[s], bounds[s + 1], karr, bounds[s] > 0 ? sched[bounds[s] - 1] : 0, sched[bounds[s + 1] - 1]);
-      p->seg_lane.insert(bounds[s]);
-    } else if (wseg_supported(p) && !p->env.block_no_wjit) {
+      gen_segment_l(o, p, fb[s], fb[s + 1], karr, fb[s] > 0 ? sched[fb[s] - 1] : 0, sched[fb[s + 1] - 1]);
+      p->seg_lane.insert(fb[s]);
+    } else if (packed) {
       // warp-per-shot (k <= 10) and CTA-per-shot segments fully specialised, packed frame in
       // registers (fs_wseg.cuh); two warps per shot measured no faster than one at k = 9-10
       const int G = karr <= 10 ? 32 : 256;
-      gen_segment_w(o, p, bounds[s], bounds[s + 1], karr, G);
-      p->seg_G[bounds[s]] = G;
+      gen_segment_w(o, p, fb[s], fb[s + 1], karr, G);
+      p->seg_G[fb[s]] = G;
     } else {
       // programs beyond the packed frame (2n > 128, > 32 slots) or FS_BLOCK_NO_WJIT: CTA-per-shot
       // segments as specialised sweeps around the shared scalar VM (measured 1.2-1.8x faster than
       // interpreted); warp-per-shot ones in that form ran ~2x slower than interpreted (instruction-
       // fetch stalls) and keep the interpreter unless FS_BLOCK_JIT_WARP is set
       if (karr <= 10 && !p->env.block_jit_warp) continue;
-      gen_segment(o, p, bounds[s], bounds[s + 1], karr, karr <= 10 ? 32 : 256);
+      gen_segment(o, p, fb[s], fb[s + 1], karr, karr <= 10 ? 32 : 256);
     }
-    begins.push_back(bounds[s]);
+    begins.push_back(fb[s]);
   }
   if (begins.empty()) { p->seg_jit = 1; return FS_OK; }
   static std::mutex mu;  // modules belong to a context: key (current context, source)
@@ -1554,7 +1561,6 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   for (int i = 0; i < dp.num_instrs; i++)
     if (FS_OPCODE(I[(size_t)i * FS_INS_WORDS]) == FS_OP_POSTSELECT && i + 1 < dp.num_instrs) bounds.push_back(i + 1);
   bounds.push_back(dp.num_instrs);
-  const int nseg = (int)bounds.size() - 1;
   // outputs are OR-ed bit by bit once shots are compacted
   const size_t W = a.W;
   if (dp.U) FS_CUDA_TRY(cudaMemsetAsync(a.meas, 0, 4 * dp.U * W, stream));
@@ -1581,13 +1587,14 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
   if (p->env.block_k) block_k = p->env.block_k;  // experiments
   if (!(a.flags & FS_RNG_SPLITMIX) && !p->env.block_no_jit && p->seg_jit == 0) {
     std::vector<int> karrs;
-    for (int sgi = 0; sgi < nseg; sgi++) {
+    for (int sgi = 0; sgi + 1 < (int)bounds.size(); sgi++) {
       int kk = bounds[sgi] > 0 ? sched[bounds[sgi] - 1] : 0;
       for (int i = bounds[sgi]; i < bounds[sgi + 1]; i++) kk = std::max(kk, sched[i]);
       karrs.push_back(kk);
     }
     ensure_seg_jit(p, bounds, karrs, block_k);  // failure leaves the interpreter in place
   }
+  const int nseg = (int)bounds.size() - 1;
   for (uint64_t c0 = 0; c0 < a.nshots; c0 += chunk) {
     uint32_t n_in = (uint32_t)std::min<uint64_t>(chunk, a.nshots - c0);
     p->seg_counts.push_back(n_in);

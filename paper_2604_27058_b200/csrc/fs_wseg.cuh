@@ -10,8 +10,8 @@
 //     bit n + q -- the survivor store's own layout) that every lane holds: scalar instructions are
 //     executed redundantly by all 32 lanes, so there is no shared-memory frame, no barrier and no
 //     instruction decode; a CondFrame or a noise case is four XORs with a mask (immediates, or
-//     one 16-byte load from the host-built per-case table), FrameGates are their GF(2) matrix
-//     (lane r evaluates rows r, r + 32, .. and ballots assemble the new words);
+//     one 16-byte load from the host-built per-case table), a frame gate two or three register
+//     instructions at constant bit positions;
 //   * record / detector slots and observables are one register each;
 //   * array sweeps are the block engine's (same per-thread order of partial sums, same tree);
 //   * the measurement decision is taken by every lane from the broadcast sums.
@@ -228,25 +228,6 @@ struct WCtxT : SCtx {
   __device__ __forceinline__ void sync() const {
     if (G == 32) __syncwarp();
     else asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(G) : "memory");
-  }
-
-  // FrameGates (or a star group's frame side) as a GF(2) matrix: v'_r = parity(row_r & v)
-  __device__ __forceinline__ void frame_mat(int mo) {
-    static_assert(G == 32, "frame matrices are evaluated by one warp; wider groups update the frame gate by gate");
-    const int n2 = 2 * P.n;
-    uint32_t o[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const int r = tid + 32 * k;
-      uint32_t b = 0u;
-      if (r < n2) {
-        const uint4 row = __ldg(reinterpret_cast<const uint4*>(P.frame_mat + mo) + r);
-        b = (uint32_t)__popc((row.x & F[0]) ^ (row.y & F[1]) ^ (row.z & F[2]) ^ (row.w & F[3])) & 1u;
-      }
-      o[k] = __ballot_sync(0xFFFFFFFFu, b != 0u);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; k++) F[k] = o[k];
   }
 
   // sweeps ------------------------------------------------------------------------------------
