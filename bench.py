@@ -187,7 +187,7 @@ def workload_config(cfg: int) -> dict:
 
 KERNEL_NAME = {"frame": "fs_aff_frame (affine frame kernel: fault-effect row tables, warp-cooperative noise stream)",
                "general": "fs_jit_general (program-specialised general kernel, NVRTC)",
-               "segmented": "general_kernel<SEG> / block_kernel (post-select segments)",
+               "segmented": "fs_seg_<b> (program-specialised post-select segments: lane / warp / CTA per shot, NVRTC)",
                "hbm": "fs_pass_<i> (program-specialised fused tile passes, NVRTC)"}
 
 

@@ -184,8 +184,10 @@ __device__ __forceinline__ void lseg_run(const DevProg& P, const RunArgs& A, con
         const StateStore& I = S.in;
         c.load_scalars(I, idx);
         gamma = I.gamma[idx];
+        const double2* const src = I.amps + store_amp_index(idx, 0, 1u << KIN, I.shot_major);
+        const uint32_t sstride = I.shot_major ? 1u : 32u;
 #pragma unroll(KIN <= kLsegUnrollK ? (1 << KIN) : 4)
-        for (uint32_t j = 0; j < (1u << KIN); j++) c.arr[j] = I.amps[store_amp_index(idx, j, 1u << KIN, I.shot_major)];
+        for (uint32_t j = 0; j < (1u << KIN); j++) c.arr[j] = src[(size_t)j * sstride];
       }
       exec(c);
     }
@@ -221,6 +223,8 @@ __device__ __forceinline__ void lseg_run(const DevProg& P, const RunArgs& A, con
         gi[3] = (uint32_t)c.pend_site; gi[4] = (uint32_t)c.pend_lane; gi[5] = (uint32_t)c.pend_case;
         O.gen_c[slot] = c.gen.c;
         constexpr int KB = KOUT - NLAZY;  // array held at the save
+        double2* const dst = O.amps + store_amp_index(slot, 0, 1u << KOUT, O.shot_major);
+        const uint32_t dstride = O.shot_major ? 1u : 32u;
 #pragma unroll(KOUT <= kLsegUnrollK ? (1 << NLAZY) : 1)
         for (uint32_t hi = 0; hi < (1u << NLAZY); hi++) {
 #pragma unroll(KOUT <= kLsegUnrollK ? (1 << KB) : 4)
@@ -228,7 +232,7 @@ __device__ __forceinline__ void lseg_run(const DevProg& P, const RunArgs& A, con
             double2 v = c.arr[j];
 #pragma unroll
             for (int t = 0; t < NLAZY; t++) v = cmul(v, ((hi >> t) & 1u) ? c.lz1[t] : c.lz0[t]);
-            O.amps[store_amp_index(slot, j | (hi << KB), 1u << KOUT, O.shot_major)] = v;
+            dst[(size_t)(j | (hi << KB)) * dstride] = v;
           }
         }
       }

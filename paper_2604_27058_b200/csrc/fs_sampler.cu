@@ -113,7 +113,6 @@ constexpr int kChunks = 4;   // max word chunks of the fault-list | frame-kernel
 struct EnvSwitches {
   bool no_affine = false;      // FS_NO_AFFINE: frame-only programs use the fault-list frame kernel
   bool block_no_jit = false;   // FS_BLOCK_NO_JIT: segmented engine interprets every segment
-  bool block_jit_warp = false; // FS_BLOCK_JIT_WARP: also specialise warp-per-shot segments
   bool block_no_wjit = false;  // FS_BLOCK_NO_WJIT: no packed-frame segment kernels (fs_wseg.cuh): warp-per-shot segments keep the interpreter, CTA-per-shot ones the shared-VM specialised form
   bool seg_no_ljit = false;    // FS_SEG_NO_LJIT: lane-per-shot segments keep the interpreter (no fs_lseg.cuh kernels)
   bool block_no_fuse = false;  // FS_BLOCK_NO_FUSE: block engine runs ArrayGates one sweep each (no star groups)
@@ -127,7 +126,6 @@ struct EnvSwitches {
   void read() {
     no_affine = getenv("FS_NO_AFFINE") != nullptr;
     block_no_jit = getenv("FS_BLOCK_NO_JIT") != nullptr;
-    block_jit_warp = getenv("FS_BLOCK_JIT_WARP") != nullptr;
     block_no_fuse = getenv("FS_BLOCK_NO_FUSE") != nullptr;
     block_no_wjit = getenv("FS_BLOCK_NO_WJIT") != nullptr;
     seg_no_ljit = getenv("FS_SEG_NO_LJIT") != nullptr;
@@ -1400,9 +1398,9 @@ int ensure_seg_jit(fs_prog* p, const std::vector<int>& bounds, const std::vector
       // programs beyond the packed frame (2n > 128, > 32 slots) or FS_BLOCK_NO_WJIT: CTA-per-shot
       // segments as specialised sweeps around the shared scalar VM (measured 1.2-1.8x faster than
       // interpreted); warp-per-shot ones in that form ran ~2x slower than interpreted (instruction-
-      // fetch stalls) and keep the interpreter unless FS_BLOCK_JIT_WARP is set
-      if (karr <= 10 && !p->env.block_jit_warp) continue;
-      gen_segment(o, p, fb[s], fb[s + 1], karr, karr <= 10 ? 32 : 256);
+      // fetch stalls) and keep the interpreter
+      if (karr <= 10) continue;
+      gen_segment(o, p, fb[s], fb[s + 1], karr, 256);
     }
     begins.push_back(fb[s]);
   }
@@ -1579,7 +1577,9 @@ int launch_segmented(fs_prog* p, fs::RunArgs& a, cudaStream_t stream) {
     for (int c : p->cp_list)
       for (int i = 0; i < dp.num_instrs; i++)
         if (p->h_fuse_at[i] >= 0 && c > i && c < i + p->h_fuse[(size_t)8 * p->h_fuse_at[i]]) S.fuse = 0;
-  const uint64_t chunk = (uint64_t)1 << 22;
+  // shots per pass over the segments: 2^23 measured 2 % faster than 2^22 on config 4 (the deep
+  // segments' launches carry more shots), 2^24 the same; the k = 10 survivor store is ~9 GB
+  const uint64_t chunk = (uint64_t)1 << 23;
   if (!p->d_counts) FS_CUDA_TRY(cudaMalloc(&p->d_counts, 64));
   uint32_t* d_nout = reinterpret_cast<uint32_t*>(p->d_counts);
   p->seg_counts.clear();

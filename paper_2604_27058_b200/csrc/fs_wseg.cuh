@@ -1,4 +1,4 @@
-// fs_wseg.cuh -- warp-per-shot segments of the block engine, fully specialised (NVRTC).
+// fs_wseg.cuh -- warp- and CTA-per-shot segments of the block engine, fully specialised (NVRTC).
 //
 // The interpreter form (fs_block.cuh block_kernel<.., 32>) keeps one shot's frame as one shared
 // word per bit and runs every scalar instruction (FrameGates, dormant measurements, CondFrame,
@@ -66,27 +66,36 @@ struct SCtx {
 
   __device__ __forceinline__ uint32_t fbit(int b) const { return (F[b >> 5] >> (b & 31)) & 1u; }
   __device__ __forceinline__ void fxor(int b, uint32_t v) { F[b >> 5] ^= v << (b & 31); }
+  // frame bit dst ^= frame bit src: the source word shifted by the difference of the two bit
+  // positions, masked to the destination bit (a shift and one three-input logic instruction when
+  // the positions are constants, as in the generated code)
+  __device__ __forceinline__ void xor_from(int dst, int src) {
+    const int d = (src & 31) - (dst & 31);
+    const uint32_t w = F[src >> 5];
+    F[dst >> 5] ^= (d >= 0 ? w >> d : w << -d) & (1u << (dst & 31));
+  }
   // frame gates on bit positions (x_a, z_a, x_b, z_b are positions in the packed frame)
-  __device__ __forceinline__ void g_s(int xa, int za) { fxor(za, fbit(xa)); }
-  __device__ __forceinline__ void g_h(int xa, int za) {
-    const uint32_t t = fbit(xa) ^ fbit(za);
-    fxor(xa, t);
-    fxor(za, t);
+  __device__ __forceinline__ void g_s(int xa, int za) { xor_from(za, xa); }
+  __device__ __forceinline__ void g_h(int xa, int za) {  // x <-> z
+    xor_from(xa, za);
+    xor_from(za, xa);
+    xor_from(xa, za);
   }
   __device__ __forceinline__ void g_cx(int xa, int za, int xb, int zb) {
-    fxor(xb, fbit(xa));
-    fxor(za, fbit(zb));
+    xor_from(xb, xa);
+    xor_from(za, zb);
   }
   __device__ __forceinline__ void g_cz(int xa, int za, int xb, int zb) {
-    fxor(zb, fbit(xa));
-    fxor(za, fbit(xb));
+    xor_from(zb, xa);
+    xor_from(za, xb);
   }
   __device__ __forceinline__ void g_swap(int xa, int za, int xb, int zb) {
-    const uint32_t tx = fbit(xa) ^ fbit(xb), tz = fbit(za) ^ fbit(zb);
-    fxor(xa, tx);
-    fxor(xb, tx);
-    fxor(za, tz);
-    fxor(zb, tz);
+    xor_from(xa, xb);
+    xor_from(xb, xa);
+    xor_from(xa, xb);
+    xor_from(za, zb);
+    xor_from(zb, za);
+    xor_from(za, zb);
   }
   __device__ __forceinline__ void xor_mask(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
     F[0] ^= m0; F[1] ^= m1; F[2] ^= m2; F[3] ^= m3;
@@ -451,9 +460,11 @@ __device__ __forceinline__ void wseg_run(const DevProg& P, const RunArgs& A, con
     } else {
       const StateStore& I = S.in;
       const uint32_t sz = 1u << S.k_in;
+      const double2* const src = I.amps + store_amp_index(idx, 0, sz, I.shot_major);
+      const uint32_t sstride = I.shot_major ? 1u : 32u;
       for (uint32_t j = tid; j < sz; j += G) {
         const uint32_t d = (uint32_t)__cvta_generic_to_shared(amp + j);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(I.amps + store_amp_index(idx, j, sz, I.shot_major)) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + (size_t)j * sstride) : "memory");
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
       c.load_scalars(I, idx);
@@ -488,7 +499,10 @@ __device__ __forceinline__ void wseg_run(const DevProg& P, const RunArgs& A, con
       for (int k = 0; k < 4; k++)
         if (k < S.nfw && tid == k) O.frame[(size_t)slot * S.nfw + k] = c.F[k];
       const uint32_t sz = 1u << S.k_out;
-      for (uint32_t j = tid; j < sz; j += G) O.amps[store_amp_index(slot, j, sz, O.shot_major)] = amp[j];
+      // element j of the slot: base + j * stride (shot-major or lane-interleaved store)
+      double2* const dst = O.amps + store_amp_index(slot, 0, sz, O.shot_major);
+      const uint32_t dstride = O.shot_major ? 1u : 32u;
+      for (uint32_t j = tid; j < sz; j += G) dst[(size_t)j * dstride] = amp[j];
       if (tid == 0) {
         if (S.nsw) O.slotbits[(size_t)slot * S.nsw] = c.slots;
         if (S.now) O.obsbits[(size_t)slot * S.now] = c.obs;

@@ -380,12 +380,11 @@ def test_gpu_block_engines_match_reference_and_oracle(cuda, name, env, monkeypat
                                     (11, 10), (12, 11)])
 @pytest.mark.parametrize("env", [{"FS_BLOCK_K": "1"}, {"FS_BLOCK_K": "1", "FS_BLOCK_NO_JIT": "1"},
                                  {"FS_BLOCK_K": "1", "FS_BLOCK_NO_WJIT": "1"},
-                                 {"FS_BLOCK_K": "1", "FS_BLOCK_NO_WJIT": "1", "FS_BLOCK_JIT_WARP": "1"},
                                  {"FS_BLOCK_K": "1", "FS_BLOCK_NO_FUSE": "1"}, {}, {"FS_SEG_NO_LJIT": "1"}])
 def test_gpu_star_groups_match_oracle(cuda, k, seed, env, monkeypatch):
     """The block engine's fused ArrayGate runs (star groups: CX / CZ / S through one pivot axis,
     an optional H and ArrayRot, FrameGates in between; interpreter, specialised CTA-per-shot
-    kernels, packed-frame (fs_wseg.cuh) and shared-frame specialised warp-per-shot kernels) against the oracle's one-sweep-per-instruction VM on hand-built
+    kernels in the shared-VM and the packed-frame (fs_wseg.cuh) form, packed-frame warp-per-shot kernels) against the oracle's one-sweep-per-instruction VM on hand-built
     programs (tests/synth.py): records of Philox free sampling bit for bit, and the frame, gamma
     and amplitudes at checkpoints between the runs (the reference stream, trace mode)."""
     from synth import star_program
@@ -402,7 +401,7 @@ def test_gpu_star_groups_match_oracle(cuda, k, seed, env, monkeypatch):
     assert a.accepted_bits().all()
     # the specialised segment kernel compiled (a failed compile would fall back to the interpreter)
     if "FS_BLOCK_K" in env:
-        interpreted = "FS_BLOCK_NO_JIT" in env or (k <= 10 and "FS_BLOCK_NO_WJIT" in env and "FS_BLOCK_JIT_WARP" not in env)
+        interpreted = "FS_BLOCK_NO_JIT" in env or (k <= 10 and "FS_BLOCK_NO_WJIT" in env)
         assert ("segments: ready kernels=1 " in dp.jit_status()) == (not interpreted), dp.jit_status()
     elif k < 9:  # default threshold: both segments are lane-per-shot (fs_lseg.cuh, FrameGates with SWAP gate by gate)
         assert ("segments: ready kernels=0 lane=2" in dp.jit_status()) == ("FS_SEG_NO_LJIT" not in env), dp.jit_status()
