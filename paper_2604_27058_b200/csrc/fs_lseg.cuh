@@ -80,8 +80,8 @@ struct LCtx : SCtx {
 #pragma unroll(K < kLsegUnrollK ? (1 << K) : 4)
     for (uint32_t j = 0; j < size; j++) {
       const double2 v = arr[j];
-      arr[j] = cmul(v, ph0);
-      arr[size + j] = cmul(v, ph1);
+      arr[j] = FS_SEG_CMUL(v, ph0);
+      arr[size + j] = FS_SEG_CMUL(v, ph1);
     }
   }
 
@@ -89,7 +89,7 @@ struct LCtx : SCtx {
   __device__ __forceinline__ void array_rot(double2 ph0, double2 ph1) {
     constexpr uint32_t size = 1u << K;
 #pragma unroll(K <= kLsegUnrollK ? (1 << K) : 4)
-    for (uint32_t j = 0; j < size; j++) arr[j] = cmul(arr[j], ((j >> AX) & 1) ? ph1 : ph0);
+    for (uint32_t j = 0; j < size; j++) arr[j] = FS_SEG_CMUL(arr[j], ((j >> AX) & 1) ? ph1 : ph0);
   }
 
   // MeasActive / MeasCollapse (runtime.py:409-511; the interpreter's lane-per-shot form): false
@@ -103,7 +103,7 @@ struct LCtx : SCtx {
     for (uint32_t j = 0; j < half; j++) {
       const uint32_t i0 = ins0(j, AX);
       const double2 a0 = arr[i0], a1 = arr[i0 + st];
-      if (COLLAPSE) p1 = __dadd_rn(p1, cnorm2(cadd(cmul(a0, u10), cmul(u11, a1))));
+      if (COLLAPSE) p1 = __dadd_rn(p1, cnorm2(cadd(FS_SEG_CMUL(a0, u10), FS_SEG_CMUL(u11, a1))));
       else p1 = __dadd_rn(p1, cnorm2(a1));
       p_all = __dadd_rn(p_all, __dadd_rn(cnorm2(a0), cnorm2(a1)));
     }
@@ -132,7 +132,7 @@ struct LCtx : SCtx {
 #pragma unroll(K <= kLsegUnrollK ? (1 << K) : 4)
       for (uint32_t j = 0; j < half; j++) {
         const uint32_t i0 = ins0(j, AX);
-        arr[j] = cadd(cmul(k0, arr[i0]), cmul(k1, arr[i0 + st]));
+        arr[j] = cadd(FS_SEG_CMUL(k0, arr[i0]), FS_SEG_CMUL(k1, arr[i0 + st]));
       }
     } else {
       const double s = renorm ? __ddiv_rn(1.0, __dsqrt_rn(pb)) : 1.0;
@@ -231,7 +231,7 @@ __device__ __forceinline__ void lseg_run(const DevProg& P, const RunArgs& A, con
           for (uint32_t j = 0; j < (1u << KB); j++) {
             double2 v = c.arr[j];
 #pragma unroll
-            for (int t = 0; t < NLAZY; t++) v = cmul(v, ((hi >> t) & 1u) ? c.lz1[t] : c.lz0[t]);
+            for (int t = 0; t < NLAZY; t++) v = FS_SEG_CMUL(v, ((hi >> t) & 1u) ? c.lz1[t] : c.lz0[t]);
             dst[(size_t)(j | (hi << KB)) * dstride] = v;
           }
         }

@@ -21,6 +21,13 @@
 #pragma once
 #include "fs_block.cuh"
 
+// complex multiply of the specialised segment kernels: the fused form (as in fs_jit_general:
+// records unchanged, amplitudes within the last ulp of the interpreters') unless the including
+// source asks for the interpreters' own
+#ifndef FS_SEG_CMUL
+#define FS_SEG_CMUL cmul_f
+#endif
+
 namespace fs {
 
 // Scalar state of one shot and the scalar instructions on it (shared by the warp-per-shot segments
@@ -245,7 +252,7 @@ struct WCtxT : SCtx {
       const double2 ph = make_double2(0.0, g == FS_G_S ? 1.0 : -1.0);
       for (uint32_t j = tid; j < size / 2; j += G) {
         const uint32_t id = ins0(j, a) | (1u << a);
-        amp[id] = cmul(amp[id], ph);
+        amp[id] = FS_SEG_CMUL(amp[id], ph);
       }
     } else if (g == FS_G_H) {
       const uint32_t st = 1u << a;
@@ -276,14 +283,14 @@ struct WCtxT : SCtx {
   __device__ __forceinline__ void expand(uint32_t size, double2 ph0, double2 ph1) {
     for (uint32_t j = tid; j < size; j += G) {
       const double2 v = amp[j];
-      amp[j] = cmul(v, ph0);
-      amp[size + j] = cmul(v, ph1);
+      amp[j] = FS_SEG_CMUL(v, ph0);
+      amp[size + j] = FS_SEG_CMUL(v, ph1);
     }
     sync();
   }
 
   __device__ __forceinline__ void array_rot(int a, uint32_t size, double2 ph0, double2 ph1) {
-    for (uint32_t j = tid; j < size; j += G) amp[j] = cmul(amp[j], ((j >> a) & 1) ? ph1 : ph0);
+    for (uint32_t j = tid; j < size; j += G) amp[j] = FS_SEG_CMUL(amp[j], ((j >> a) & 1) ? ph1 : ph0);
     sync();
   }
 
@@ -305,8 +312,8 @@ struct WCtxT : SCtx {
         hi = d;
       }
       if (hasAR) {
-        lo = cmul(lo, ((i0 >> ar_axis) & 1u) ? ph1 : ph0);
-        hi = cmul(hi, (((i0 | A_) >> ar_axis) & 1u) ? ph1 : ph0);
+        lo = FS_SEG_CMUL(lo, ((i0 >> ar_axis) & 1u) ? ph1 : ph0);
+        hi = FS_SEG_CMUL(hi, (((i0 | A_) >> ar_axis) & 1u) ? ph1 : ph0);
       }
       amp[i0] = lo;
       amp[i0 | A_] = hi;
@@ -349,7 +356,7 @@ struct WCtxT : SCtx {
     for (uint32_t j = tid; j < half; j += G) {
       const uint32_t i0 = ins0(j, a);
       const double2 a0 = amp[i0], a1 = amp[i0 + st];
-      if (COLLAPSE) s1 = __dadd_rn(s1, cnorm2(cadd(cmul(a0, u10), cmul(u11, a1))));
+      if (COLLAPSE) s1 = __dadd_rn(s1, cnorm2(cadd(FS_SEG_CMUL(a0, u10), FS_SEG_CMUL(u11, a1))));
       else s1 = __dadd_rn(s1, cnorm2(a1));
       sa = __dadd_rn(sa, __dadd_rn(cnorm2(a0), cnorm2(a1)));
     }
@@ -406,7 +413,7 @@ struct WCtxT : SCtx {
         double2 val = make_double2(0.0, 0.0);
         if (j < half) {
           const uint32_t i0 = ins0(j, a);
-          val = cadd(cmul(k0, amp[i0]), cmul(k1, amp[i0 + st]));
+          val = cadd(FS_SEG_CMUL(k0, amp[i0]), FS_SEG_CMUL(k1, amp[i0 + st]));
         }
         sync();
         if (j < half) amp[j] = val;
