@@ -48,13 +48,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             if Path(cand).exists():
                 nvcc = cand
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc, *NVCC_FLAGS, "-Xptxas", "-v", "-o", str(tmp), str(CSRC / "fs_sampler.cu")]
+    cmd = [nvcc, *NVCC_FLAGS, "-Xptxas", "-v", "-I", str(INCLUDE), "-o", str(tmp), str(CSRC / "fs_sampler.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{res.stderr}")
     if verbose:
         print(res.stderr)
     (PKG / "_build" / "ptxas.log").write_text(res.stderr)
+    # the segment-kernel headers are compiled per program at run time (NVRTC): check them here with
+    # hand-written stand-ins for the generated kernels (csrc/fs_seg_check.cu), cubin only
+    chk = PKG / "_build" / "fs_seg_check.cubin"
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-cubin",
+           "-I", str(INCLUDE), "-o", str(chk), str(CSRC / "fs_seg_check.cu")]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed on the segment-kernel headers:\n{res.stderr}")
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

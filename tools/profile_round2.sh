@@ -12,6 +12,5 @@ python tools/one_call.py 3 1000 >/dev/null && \
   $M -k regex:fs_pass --log-file gpurun_out/r2_c3_passes.csv python tools/one_call.py 3 1000 >/dev/null 2>&1
 python tools/one_call.py 3 64 >/dev/null && \
   $N -k regex:fs_pass_42 -c 1 -o gpurun_out/r2_prof_c3_p42 python tools/one_call.py 3 64 >/dev/null 2>&1
-python tools/one_call.py 4 4000000 >/dev/null && \
-  $N -k regex:block_kernel -c 1 -o gpurun_out/r2_prof_c4_block python tools/one_call.py 4 4000000 >/dev/null 2>&1
+bash tools/profile_c4.sh   # config 4: launch list + one capture per specialised segment form
 ls -la gpurun_out/r2_prof_*.ncu-rep gpurun_out/r2_c3_passes.csv
