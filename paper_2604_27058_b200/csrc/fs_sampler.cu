@@ -1123,7 +1123,7 @@ void gen_segment_w(std::ostringstream& o, const fs_prog* p, int b, int e, int ka
       }
     }
   };
-  o << "extern \"C\" __global__ void __launch_bounds__(" << wseg_threads(G) << ", " << (G == 256 ? 3 : 1) << ") fs_seg_" << b
+  o << "extern \"C\" __global__ void __launch_bounds__(" << wseg_threads(G) << ", " << (G == 256 ? (karr <= 11 ? 4 : 3) : 1) << ") fs_seg_" << b
     << "(DevProg P, RunArgs A, SegArgs S, int group_bytes) {\n  wseg_run<" << G << ", " << karr << ">(P, A, S, group_bytes, [&](WCtxT<" << G
     << ">& c) {\n";
   for (int i = b; i < e;) {
